@@ -1,0 +1,261 @@
+"""Pins for the oracle's p-BiCGStab (§2 Algorithm 2) and plain
+BiCGStab (Algorithm 1).
+
+The oracle's floating-point Algorithm 2 is pinned to things it does not
+compute itself:
+* the textbook method: Algorithm 1 run in EXACT rational arithmetic gives the
+  scalars the fp trajectory must track to rounding error (a transposed operand,
+  wrong sign or index in any recurrence breaks this at the first iterations);
+* the reading of Algorithm 2 (R-1..R-3) is itself pinned: Algorithm 2
+  in exact rationals reproduces Algorithm 1's iterates exactly and terminates
+  in <= n steps;
+* definitional identities (S8/S4 products), auxiliary-vector
+  invariants (w ~ Ar, s ~ Ap, z ~ As, y ~ Aq, r ~ b - Ax);
+* closed forms (1x1 diag(2); a breakdown-at-init system);
+* a dense direct solve (numpy.linalg.solve) on 100 random systems.
+"""
+import math
+import struct
+from fractions import Fraction as F
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+
+def bits(v):
+    return struct.unpack("<Q", struct.pack("<d", v))[0]
+
+
+# ---------------------------------------------------------------- exact rational
+
+def _mv(M, v):
+    return [sum((M[i][j] * v[j] for j in range(len(v))), F(0)) for i in range(len(M))]
+
+
+def _dot(a, b):
+    return sum((x * y for x, y in zip(a, b)), F(0))
+
+
+def alg1_exact(M, b, iters):
+    """Algorithm 1 in exact rationals, x0 = 0."""
+    n = len(b)
+    x = [F(0)] * n
+    r = list(b)
+    r0 = list(r)
+    p = list(r)
+    out = []
+    for _ in range(iters):
+        s = _mv(M, p)
+        a = _dot(r0, r) / _dot(r0, s)
+        q = [ri - a * si for ri, si in zip(r, s)]
+        y = _mv(M, q)
+        yy = _dot(y, y)
+        if yy == 0:
+            x = [xi + a * pi for xi, pi in zip(x, p)]
+            out.append(dict(alpha=a, omega=F(0), x=list(x), r=[F(0)] * n))
+            break
+        w = _dot(q, y) / yy
+        x = [xi + a * pi + w * qi for xi, pi, qi in zip(x, p, q)]
+        rn = [qi - w * yi for qi, yi in zip(q, y)]
+        beta = (a / w) * _dot(r0, rn) / _dot(r0, r)
+        out.append(dict(alpha=a, omega=w, x=list(x), r=list(rn), beta=beta))
+        if all(v == 0 for v in rn):
+            break
+        p = [ri + beta * (pi - w * si) for ri, pi, si in zip(rn, p, s)]
+        r = rn
+    return out
+
+
+def alg2_exact(M, b, iters):
+    """Algorithm 2 in exact rationals, with readings
+    R-1 (w0 := A r0), R-2 (scalar omega vs vector w), R-3 (i=0 copies)."""
+    n = len(b)
+    x = [F(0)] * n
+    r = list(b)
+    r0 = list(r)
+    w = _mv(M, r)
+    t = _mv(M, w)
+    a = _dot(r0, r) / _dot(r0, w)
+    out = []
+    p = s = z = v = None
+    beta = om = None
+    for i in range(iters):
+        if i == 0:
+            p, s, z = list(r), list(w), list(t)
+        else:
+            p = [ri + beta * (pi - om * si) for ri, pi, si in zip(r, p, s)]
+            s = [wi + beta * (si - om * zi) for wi, si, zi in zip(w, s, z)]
+            z = [ti + beta * (zi - om * vi) for ti, zi, vi in zip(t, z, v)]
+        q = [ri - a * si for ri, si in zip(r, s)]
+        y = [wi - a * zi for wi, zi in zip(w, z)]
+        v = _mv(M, z)
+        yy = _dot(y, y)
+        om = F(0) if yy == 0 else _dot(q, y) / yy
+        x = [xi + a * pi + om * qi for xi, pi, qi in zip(x, p, q)]
+        rn = [qi - om * yi for qi, yi in zip(q, y)]
+        w = [yi - om * (ti - a * vi) for yi, ti, vi in zip(y, t, v)]
+        t = _mv(M, w)
+        out.append(dict(alpha=a, omega=om, x=list(x), r=list(rn)))
+        if all(vv == 0 for vv in rn):
+            break
+        beta = (a / om) * _dot(r0, rn) / _dot(r0, r)
+        a = _dot(r0, rn) / (_dot(r0, w) + beta * _dot(r0, s) - beta * om * _dot(r0, z))
+        out[-1]["beta"] = beta
+        r = rn
+    return out
+
+
+def _int_system(n, seed):
+    rng = np.random.default_rng(seed)
+    M = rng.integers(-3, 4, (n, n)).astype(float)
+    M[np.arange(n), np.arange(n)] = np.abs(M).sum(1) + 2
+    b = rng.integers(-5, 6, n).astype(float)
+    if not b.any():
+        b[0] = 1.0
+    return M, b
+
+
+def test_reading_alg2_equals_alg1_exactly():
+    # pins readings R-1..R-3 (SURVEY.md App. A check): identical iterates,
+    # exact zero residual after <= n steps
+    for seed in range(3):
+        M, b = _int_system(6, seed)
+        Mf = [[F(v) for v in row] for row in M]
+        bf = [F(v) for v in b]
+        t1 = alg1_exact(Mf, bf, 10)
+        t2 = alg2_exact(Mf, bf, 10)
+        assert len(t1) == len(t2) <= 6
+        for a1, a2 in zip(t1, t2):
+            assert a1["alpha"] == a2["alpha"] and a1["omega"] == a2["omega"] and a1["x"] == a2["x"]
+        assert all(v == 0 for v in t2[-1]["r"])
+        xs = np.linalg.solve(M, b)
+        assert np.allclose([float(v) for v in t2[-1]["x"]], xs, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fp_alg2_tracks_exact_alg1(seed):
+    # the oracle's fp trajectory agrees with exact Algorithm 1 to rounding error
+    n = 12
+    M, b = _int_system(n, 100 + seed)
+    A = gen.from_dense(M)
+    S = oracle.PBiCGStab(A, b=b, tol=0.0, max_iter=4)
+    S.run()
+    H = S.history()
+    ex = alg1_exact([[F(v) for v in row] for row in M], [F(v) for v in b], 4)
+    # row 0 holds alpha_0 in H_ALPHA; row i+1 holds omega_i, and alpha_{i+1}
+    assert math.isclose(H[0, oracle.H_ALPHA], float(ex[0]["alpha"]), rel_tol=1e-12)
+    for i in range(3):
+        assert math.isclose(H[i + 1, oracle.H_OMEGA], float(ex[i]["omega"]), rel_tol=1e-9), i
+        assert math.isclose(H[i + 1, oracle.H_ALPHA], float(ex[i + 1]["alpha"]), rel_tol=1e-9), i
+        assert math.isclose(H[i + 1, oracle.H_BETA], float(ex[i]["beta"]), rel_tol=1e-9), i
+        rr = float(_dot(ex[i]["r"], ex[i]["r"]))
+        assert math.isclose(H[i + 1, oracle.H_RR], rr, rel_tol=1e-8), i
+
+
+def test_diag2_one_step():
+    # SPEC.md l.243 / l.234: 1x1 diag(2), b=[2] -> converged in one step, x=[1]
+    A = gen.from_dense(np.array([[2.0]]))
+    S = oracle.PBiCGStab(A, b=[2.0], tol=1e-10, max_iter=10)
+    S.run()
+    assert S.status == oracle.CONVERGED and S.iterations == 1
+    assert S.vec("x")[0] == 1.0
+    assert S.history()[1, oracle.H_OMEGA] == 0.0  # (y,y) = 0 -> omega := 0 (R-12)
+
+
+def test_i0_identities_and_definitional_products():
+    # after i=0, s0 = A p0 and z0 = A s0 bitwise; v = A z and
+    # t = A w are SpMV outputs by definition (S4, S8).
+    M, b = _int_system(16, 7)
+    A = gen.from_dense(M)
+    S = oracle.PBiCGStab(A, b=b, tol=0.0, max_iter=1)
+    S.step()
+    p, s, z = S.vec("p"), S.vec("s"), S.vec("z")
+    assert np.array_equal(s, oracle.spmv(A, p))
+    assert np.array_equal(z, oracle.spmv(A, s))
+    assert np.array_equal(S.vec("v"), oracle.spmv(A, z))
+    assert np.array_equal(S.vec("t"), oracle.spmv(A, S.vec("w")))
+
+
+def test_auxiliary_vector_invariants():
+    # in exact arithmetic w = A r, s = A p, z = A s, y = A q, r = b - A x
+    A = gen.stencil(2, 16, 10.0)
+    S = oracle.PBiCGStab(A, tol=0.0, max_iter=8)
+    S.run(8)
+    v = {k: S.vec(k) for k in ("b", "x", "r", "p", "s", "z", "q", "y", "w")}
+    Av = lambda u: oracle.spmv(A, u)
+    nb = np.linalg.norm(v["b"])
+    for lhs, rhs in [("w", Av(v["r"])), ("s", Av(v["p"])), ("z", Av(v["s"]))]:
+        assert np.linalg.norm(v[lhs] - rhs) <= 1e-10 * nb, lhs
+    assert np.linalg.norm(v["r"] - (v["b"] - Av(v["x"]))) <= 1e-10 * nb
+
+
+def test_breakdown_init_closed_form():
+    # A = [[0,1],[1,0]], b = [1,0]: r0 = b, w0 = A r0 = [0,1], (r0,w0) = 0
+    A = gen.from_dense(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    S = oracle.PBiCGStab(A, b=[1.0, 0.0], tol=1e-10, max_iter=10)
+    assert S.rc == 0 and S.status == oracle.BREAKDOWN_INIT and S.iterations == 0
+
+
+def test_errors_and_degenerate():
+    A = gen.from_dense(np.eye(3))
+    assert oracle.PBiCGStab(A, b=[0.0, 0.0, 0.0]).rc == 1             # ||b|| = 0 -> EINVAL
+    assert oracle.PBiCGStab(A, b=[1.0, math.nan, 0.0]).rc == 5        # NaN -> ENONFINITE
+    B = gen.from_dense(np.array([[1.0, math.inf], [0.0, 1.0]]))
+    assert oracle.PBiCGStab(B, b=[1.0, 1.0]).rc == 5
+    S = oracle.PBiCGStab(A, b=[1.0, 2.0, 3.0], max_iter=0)
+    assert S.status == oracle.MAXITER and S.iterations == 0
+    S = oracle.PBiCGStab(A, b=[1.0, 2.0, 3.0], x0=[1.0, 2.0, 3.0])   # already solved
+    assert S.status == oracle.CONVERGED and S.iterations == 0
+
+
+def test_random_systems_vs_direct_solve():
+    # 100 random well-conditioned systems of size 4-64 at
+    # tol 1e-10, forward error <= 1e-6; l.380: true relres <= 10 tol
+    rng = np.random.default_rng(2024)
+    for k in range(100):
+        n = int(rng.integers(4, 65))
+        A = gen.dense_as_sparse(n, seed=k, density=0.5)
+        M = np.zeros((n, n))
+        for i in range(n):
+            M[i, A.col[A.row_ptr[i]:A.row_ptr[i + 1]]] = A.val[A.row_ptr[i]:A.row_ptr[i + 1]]
+        b = rng.uniform(-1, 1, n)
+        S = oracle.PBiCGStab(A, b=b, tol=1e-10, max_iter=1000)
+        S.run()
+        assert S.status == oracle.CONVERGED, (k, S.status)
+        xs = np.linalg.solve(M, b)
+        x = S.vec("x")
+        assert np.linalg.norm(x - xs) <= 1e-6 * np.linalg.norm(xs)
+        assert S.true_relres() <= 10 * 1e-10
+        st, it, xb, _ = oracle.bicgstab(A, b, tol=1e-10, max_iter=1000)
+        assert st == oracle.CONVERGED and np.linalg.norm(xb - xs) <= 1e-6 * np.linalg.norm(xs)
+
+
+def test_c1_converges_and_matches_plain_bicgstab():
+    # BASELINE.json configs[0]; north_star: final ||b-Ax||/||b|| agrees with a
+    # plain-double BiCGStab within 1e-10
+    A = gen.make_config("c1_2d64")
+    S = oracle.PBiCGStab(A, tol=1e-10, max_iter=500)
+    S.run()
+    assert S.status == oracle.CONVERGED and 0 < S.iterations < 500
+    H = S.history()
+    assert H[-1, oracle.H_RELRES] <= 1e-10 < H[-2, oracle.H_RELRES]
+    assert H[0, oracle.H_RELRES] == 1.0  # r0 = b (x0 = 0)
+    tr = S.true_relres()
+    b = S.vec("b")
+    st, it, xb, _ = oracle.bicgstab(A, b, tol=1e-10, max_iter=500)
+    assert st == oracle.CONVERGED
+    tb = oracle.true_relres(A, b, xb)[0]
+    assert abs(tr - tb) <= 1e-10
+    assert np.abs(S.vec("x") - 1.0).max() < 1e-6  # b = A*ones
+
+
+def test_deterministic():
+    A = gen.stencil(2, 20, 10.0)
+    S1 = oracle.PBiCGStab(A, tol=1e-10, max_iter=300)
+    S2 = oracle.PBiCGStab(A, tol=1e-10, max_iter=300)
+    S1.run(), S2.run()
+    assert np.array_equal(S1.history().view(np.uint64), S2.history().view(np.uint64))
+    assert np.array_equal(S1.vec("x").view(np.uint64), S2.vec("x").view(np.uint64))
