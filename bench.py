@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""bench.py -- p-BiCGStab (ExBLAS dots) iterations/s on B200, plus the
+per-kernel HBM roofline, the end-to-end (host buffers) rate and the CPU
+oracle baseline.  One JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5_3d256]
+  python bench.py --impl reference ...   (the CPU oracle on the same workload)
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
+
+A "step" is one p-BiCGStab iteration (§2 Alg. 2 l.70-82: K2, SpMV
+v=Az, K3, SpMV t=Aw with the six+1 ExBLAS dots) over the whole matrix.
+Workload: BASELINE.json configs[4] (3D convection-diffusion 256^3, Pe=200,
+synthetic, b = A*ones) at every N (strong scaling, rows split over ranks).
+Timing: W untimed iterations, then K iterations bracketed by barrier +
+synchronize, CUDA events on the solver stream, max over ranks.  The working
+set (6.6 GB/iteration) is 50x the 126 MB L2, so no flush is needed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "p-BiCGStab iter/s; SpMV/AXPY/ExBLAS-dot HBM GB/s vs 8 TB/s, 1/2/4/8 GPU"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ clocks --
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.p = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self):
+        return time.time()
+
+    def stop(self):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self, t0, t1):
+        rows = [l for (t, l) in self.lines if t0 <= t <= t1] or [l for (_, l) in self.lines][-5:]
+        if not rows:
+            return None
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            f = [x.strip() for x in r.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except Exception:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- workloads --
+def algorithmic_bytes(n: int, nnz: int):
+    """SpMV 12 nnz + 4 (n+1) + 16 n; K2 104 n; K3 80 n."""
+    spmv = 12 * nnz + 4 * (n + 1) + 16 * n
+    return {"k2": 104 * n, "spmv": spmv, "k3": 80 * n, "iteration": 2 * spmv + 184 * n}
+
+
+def local_rows(A, rank, world):
+    import paper_2404_13216_b200 as pb
+    b = pb.plan_partition(A.n, world)
+    return int(b[rank]), int(b[rank + 1])
+
+
+def run_gpu(args, rank, world, local_rank, dist):
+    import torch
+
+    import gen
+    import paper_2404_13216_b200 as pb
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    hbm, peak_src = peaks()
+    t_gen = time.time()
+    A = gen.make_config(args.workload)
+    t_gen = time.time() - t_gen
+    r0, r1 = local_rows(A, rank, world)
+    Al = A.rows(r0, r1)
+    uid = None
+    if world > 1:
+        obj = [pb.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    S = pb.Solver(Al.row_ptr, Al.col, Al.val, A.n, row_begin=r0, row_end=r1, rank=rank, nranks=world,
+                  nccl_uid=uid, history_capacity=16)
+    nloc = r1 - r0
+    # b = A*ones (configs: "b=A*ones") with the GPU SpMV; x0 = 0
+    if A.rhs == "given":
+        b = torch.from_numpy(A.b[r0:r1].copy()).to(dev)
+    else:
+        b = S.spmv(torch.ones(nloc, dtype=torch.float64, device=dev))
+    torch.cuda.synchronize()
+    K, W = args.steps, args.warmup
+    clocks = Clocks(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    # ---- timed region: K iterations replayed as CUDA-graph chunks ----
+    S.start(b, tol=0.0, max_iter=W + K + 8)  # tol 0: every timed iteration does full work
+    S.iterate(W)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tc0 = time.time()
+    e0.record(S.stream)
+    S.iterate(K)
+    e1.record(S.stream)
+    torch.cuda.synchronize()
+    tc1 = time.time()
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    res = S.finish(None)
+    ok = (res.iterations == W + K) and res.status == pb.MAXITER
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        okt = torch.tensor([1 if ok else 0], device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        ok = bool(okt.item())
+    clk = clocks.summary(tc0 - 0.05, tc1 + 0.05)
+    out = {"ms": ms, "ok": ok, "iters": res.iterations, "clocks": clk}
+    # ---- per-kernel times: a second timed pass over the same K steps with
+    # CUDA events around every launch (single rank) ----
+    by = algorithmic_bytes(nloc, Al.nnz)
+    kern = None
+    if world == 1:
+        S.start(b, tol=0.0, max_iter=W + K + 8)
+        S.iterate(W)
+        kms = S.profile(K)
+        res2 = S.finish(None)
+        names = ["k2", "spmv_z", "k3", "spmv_w"]
+        bytes_per = [by["k2"], by["spmv"], by["k3"], by["spmv"]]
+        kern = {}
+        for nm, t, bb in zip(names, kms, bytes_per):
+            avg = t / K * 1e-3
+            kern[nm] = {"avg_us": avg * 1e6, "alg_bytes": bb, "GBps": bb / avg / 1e9, "frac_hbm": bb / avg / 1e9 / hbm,
+                        "frac_8TBs": bb / avg / 1e9 / 8000.0}
+        kern["profile_iters_ok"] = res2.iterations == W + K
+        kern["iteration_sum_us"] = float(sum(kms) / K * 1e3)
+    clocks.stop()
+    # ---- end to end: host buffers through the C ABI (pinned), full solve ----
+    e2e = None
+    if not args.no_e2e:
+        bh = torch.empty(nloc, dtype=torch.float64, pin_memory=True)
+        bh.copy_(b.cpu())
+        xh = torch.zeros(nloc, dtype=torch.float64, pin_memory=True)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tw0 = time.time()
+        f0.record(S.stream)
+        x, r = S.solve(bh, x0=xh, tol=1e-10, max_iter=args.e2e_max_iter, poll_every=32)
+        f1.record(S.stream)
+        torch.cuda.synchronize()
+        tw1 = time.time()
+        ems = f0.elapsed_time(f1)
+        if dist:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        it = max(r.iterations, 1)
+        e2e = {"value": it / (ems * 1e-3), "unit": "iter/s", "iterations": r.iterations, "status": r.status_name,
+               "relres_true": r.relres_true, "solve_ms": ems, "wall_ms": (tw1 - tw0) * 1e3,
+               "h2d_bytes_per_step": (2 * nloc * 8 * world) / it, "d2h_bytes_per_step": (nloc * 8 * world) / it,
+               "h2d_bytes_per_solve": 2 * nloc * 8 * world, "d2h_bytes_per_solve": nloc * 8 * world,
+               "note": "pbicgstab_solve with pinned host b, x0 -> host x; copies, init, polls and true residual inside the timed region"}
+    S.close()
+    return out, kern, e2e, A, by, hbm, peak_src, t_gen
+
+
+def exdot_microbench(args, hbm):
+    """BASELINE.json configs[1]: EXDOT vs plain fp64 dot vs torch.dot, GB/s."""
+    import torch
+
+    import gen
+    import paper_2404_13216_b200 as pb
+    out = {}
+    n = 1 << args.dot_log2
+    for kind in ("well", "ill"):
+        if kind == "well":
+            x, y = gen.uniform(n, 1), gen.uniform(n, 2)
+        else:
+            x, y = gen.ill_pair(n, seed=3)
+        xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        del x, y
+        res = torch.zeros(1, dtype=torch.float64, device="cuda")
+        fl = torch.zeros(1, dtype=torch.int32, device="cuda")
+        st = torch.cuda.current_stream()
+        fns = {"exdot": lambda: pb.exdot(xt, yt, on_device=True, out=res, flags_out=fl),
+               "plain_dot": lambda: pb.dot_plain(xt, yt, out=res),
+               "torch_dot": lambda: torch.dot(xt, yt)}
+        row = {}
+        for nm, fn in fns.items():
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            reps = 10
+            es = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+            ts = []
+            for i in range(reps):
+                es[i].record(st)
+                fn()
+                es[i + 1].record(st)
+            torch.cuda.synchronize()
+            ts = [es[i].elapsed_time(es[i + 1]) for i in range(reps)]
+            med = float(np.median(ts))
+            row[nm] = {"median_us": med * 1e3, "min_us": float(min(ts)) * 1e3, "GBps": 16 * n / (med * 1e-3) / 1e9}
+            row[nm]["frac_hbm"] = row[nm]["GBps"] / hbm
+        row["exdot_vs_plain"] = row["exdot"]["GBps"] / row["plain_dot"]["GBps"]
+        row["flags"] = int(fl.item())
+        out[kind] = row
+        del xt, yt
+        torch.cuda.empty_cache()
+    out["n"] = n
+    return out
+
+
+def cpu_baseline(A, budget_s: float, max_iters: int):
+    """The oracle as it stands, single thread, a bounded number of iterations
+    of the same workload (its own b = A*ones)."""
+    import oracle
+    t0 = time.time()
+    O = oracle.PBiCGStab(A, b=A.b if A.rhs == "given" else None, tol=0.0, max_iter=max_iters, history=False)
+    t_init = time.time() - t0
+    done = 0
+    while done < max_iters and O.loop_seconds < budget_s:
+        O.step()
+        done += 1
+    secs = O.loop_seconds
+    O.close()
+    return {"value": done / secs if secs > 0 else None, "unit": "iter/s", "cores": 1, "kind": "oracle",
+            "iterations": done, "loop_s": secs, "init_s": t_init,
+            "sample": f"{done} oracle iterations (single thread, exact big-integer dots) of the same workload; init excluded",
+            "host": host_cpu()}
+
+
+def host_cpu():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        model = [l.split(":", 1)[1].strip() for l in out.splitlines() if l.startswith("Model name")]
+        return {"model": model[0] if model else "?", "nproc": os.cpu_count()}
+    except Exception:
+        return {"model": "?", "nproc": os.cpu_count()}
+
+
+def traffic_from_profiles(workload: str, kernel: str):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            t = json.load(f)
+        return t.get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- reference --
+def run_reference(args, rank, world):
+    import gen
+    if rank != 0:
+        return
+    A = gen.make_config(args.workload)
+    cb = cpu_baseline(A, budget_s=args.ref_budget, max_iters=args.warmup + args.steps)
+    value = cb["value"]
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": args.gpus,
+            "steps": cb["iterations"], "warmup": 0, "ms_per_step": 1e3 / value if value else None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(args, A),
+            "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "oracle", "sample": cb["sample"]},
+            "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "host": cb["host"]}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, A):
+    desc = {"c5_3d256": "BASELINE configs[4]: 3D convection-diffusion 7-pt upwind FD 256^3, Pe=200, b=A*ones, x0=0",
+            "c3_3d128": "BASELINE configs[2]: 3D convection-diffusion 7-pt upwind FD 128^3, Pe=100, b=A*ones, x0=0",
+            "c4_rand4m": "BASELINE configs[3]: random unsymmetric banded n=2^22, Poisson(27) row lengths",
+            "c1_2d64": "BASELINE configs[0]: 2D convection-diffusion 5-pt 64^2, Pe=10"}[args.workload]
+    return {"workload": args.workload, "description": desc, "n": A.n, "nnz": A.nnz,
+            "parallelism": f"rows/{args.gpus} (NCCL halo + int64 superaccumulator allreduce)" if args.gpus > 1 else "1 GPU",
+            "l2": "no flush: per-iteration working set far above the 126 MB L2" if A.nnz > 5e7 else "L2 may hold part of the working set",
+            "step": "one p-BiCGStab iteration (K2, SpMV v=Az, K3, SpMV t=Aw; 7 EXDOTs)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--workload", default="c5_3d256", choices=["c5_3d256", "c3_3d128", "c4_rand4m", "c1_2d64"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the exdot microbench and the CPU baseline")
+    ap.add_argument("--dot-log2", type=int, default=26)
+    ap.add_argument("--e2e-max-iter", type=int, default=2000)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--ref-budget", type=float, default=90.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local_rank)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist = tdist
+    args.gpus = world if world > 1 else args.gpus
+    if args.gpus > 1 and world == 1:
+        print(json.dumps({"error": "--gpus > 1 needs torchrun (one process per GPU)"}))
+        sys.exit(2)
+
+    out, kern, e2e, A, by, hbm, peak_src, t_gen = run_gpu(args, rank, world, local_rank, dist)
+    K = args.steps
+    ms_step = out["ms"] / K
+    value = K / (out["ms"] * 1e-3)
+    line = {"metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": args.gpus, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_config(args, A),
+            "valid": out["ok"], "gpu_launches": 4 * K if args.gpus == 1 else None}
+    if args.gpus > 1:
+        line["gpu_launches"] = 8 * K  # K2, finalize A, SpMV, K3, finalize B, SpMV per rank per iteration (+NCCL)
+    line["bytes_per_iteration_per_gpu"] = by["iteration"]
+    line["iteration_GBps_per_gpu"] = by["iteration"] / (ms_step * 1e-3) / 1e9
+    line["iteration_frac_hbm"] = line["iteration_GBps_per_gpu"] / hbm
+    if kern:
+        sp_us = (kern["spmv_z"]["avg_us"] + kern["spmv_w"]["avg_us"]) / 2
+        achieved = by["spmv"] / (sp_us * 1e-6) / 1e9
+        tr = traffic_from_profiles(args.workload, "spmv")
+        line["roofline"] = {"kernel": "spmv_sell (SpMV v=Az / t=Aw, 2 launches per step)", "bound": "hbm",
+                            "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                            "traffic": tr, "peak_source": peak_src,
+                            "alg_bytes_per_launch": by["spmv"],
+                            "share_of_step": 2 * sp_us / kern["iteration_sum_us"]}
+        line["kernels"] = kern
+    line["clocks"] = out["clocks"]
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0 and not args.no_extras and args.gpus == 1:
+        line["exdot_microbench"] = exdot_microbench(args, hbm)
+        line["cpu_baseline"] = cpu_baseline(A, budget_s=args.cpu_budget, max_iters=50)
+    elif rank == 0 and not args.no_extras:
+        line["cpu_baseline"] = cpu_baseline(A, budget_s=args.cpu_budget, max_iters=50)
+    line["gen_seconds"] = t_gen
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

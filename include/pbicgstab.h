@@ -1,0 +1,228 @@
+/*
+ * pbicgstab.h -- C ABI of the B200-native hot path of arXiv 2404.13216:
+ * pipelined BiCGStab (p-BiCGStab, §2 Algorithm 2, l.60-86) whose
+ * inner products are computed ExBLAS-style (§2 l.95: floating-point
+ * expansions + long accumulator, "independent of data partitioning, order of
+ * computations, thread scheduling, or reduction tree schemes").
+ *
+ * Library: paper_2404_13216_b200/libpbicgstab.so (sm_100a).  Plain pointers
+ * and sizes only; no C++ or torch types cross this boundary.  No function
+ * aborts or throws: each returns a pbcg_rc and leaves a thread-local message
+ * for pbicgstab_last_error().
+ *
+ * Conventions used below
+ *   EXDOT(u,v)  the binary64 nearest (ties-to-even) to the exact real
+ *               sum_k u_k v_k.  Exact zero -> +0.0.
+ *   NORM(u)     sqrt(EXDOT(u,u)) (IEEE sqrt, round-to-nearest).
+ *   SpMV        y_i = +0.0; for k in row i in ascending column order:
+ *               y_i = fma(a_ik, x_k, y_i)  (R-6).
+ *   Algorithm 2 is implemented with the readings R-1..R-15 of DESIGN.md
+ *   (w0 := A r0, scalar omega vs vector w, i=0 copies, FMA policy F, ...).
+ *   "device"    = CUDA global memory of the current device; "host" = CPU.
+ *
+ * Threading: a handle is used by one host thread at a time.  Collective
+ * calls (setup, solve, start/iterate/finish, spmv, distributed exdot) must be
+ * made by every rank with consistent arguments, as with MPI.
+ */
+#ifndef PBICGSTAB_H
+#define PBICGSTAB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PBCG_ABI_VERSION 1
+
+/* return codes of every entry point (never an abort across the ABI) */
+enum pbcg_rc {
+    PBCG_OK = 0,
+    PBCG_EINVAL = 1,     /* bad argument / dimension mismatch, ||b|| = 0 (l.259) */
+    PBCG_ECUDA = 2,      /* CUDA runtime error (message in pbicgstab_last_error) */
+    PBCG_ENCCL = 3,      /* NCCL error or NCCL unavailable for nranks > 1 */
+    PBCG_ENOMEM = 4,     /* workspace too small */
+    PBCG_ENONFINITE = 5, /* NaN/Inf in an input */
+    PBCG_ERANGE = 6      /* exdot: a product outside the exact zone (R-9) or overflow */
+};
+
+/* solve outcome (pbcg_result.status); an outcome is not an error */
+enum pbcg_status {
+    PBCG_CONVERGED = 0,       /* ||r_i||/||b|| <= tol (recursive residual, R-10) */
+    PBCG_MAXITER = 1,
+    PBCG_BREAKDOWN_INIT = 2,  /* (r0,w0) = 0 or alpha_0 not finite (l.67) */
+    PBCG_BREAKDOWN_RHO = 3,   /* |(r0,r_{i+1})| <= thr (R-11) */
+    PBCG_BREAKDOWN_OMEGA = 4, /* omega_i = 0 and not converged (R-12) */
+    PBCG_BREAKDOWN_ALPHA = 5, /* |alpha denominator| <= thr or not finite (R-11) */
+    PBCG_RANGE = 6,           /* an EXDOT left the exact zone (R-9) */
+    PBCG_RUNNING = -1
+};
+
+/* One rank's contiguous block of rows of the square global matrix, CSR.
+ * All three arrays are DEVICE pointers, borrowed only for the duration of
+ * pbicgstab_workspace_size / pbicgstab_setup (they are converted into the
+ * workspace; the caller may free them afterwards). */
+typedef struct {
+    int64_t n_global;         /* global order n (rows = columns) */
+    int64_t row_begin;        /* this rank owns global rows [row_begin, row_end) */
+    int64_t row_end;
+    int64_t nnz_local;        /* row_ptr[row_end-row_begin] */
+    const int32_t *row_ptr;   /* device, n_local+1 entries, row_ptr[0] = 0, non-decreasing */
+    const int32_t *col_idx;   /* device, GLOBAL column ids in [0,n_global), strictly increasing per row */
+    const double *values;     /* device, finite */
+} pbcg_csr_local;
+
+/* Distribution.  nranks > 1: one process per GPU, NCCL over NVLink; every rank
+ * passes its own contiguous row block (rank r owns the r-th block of any
+ * contiguous partition; blocks must tile [0,n) in rank order).
+ * virtual_ranks > 1 (requires nranks == 1 and the FULL matrix): the library
+ * splits the rows into that many balanced blocks and runs them
+ * as separate ranks inside this process on this GPU (halo exchange and
+ * superaccumulator allreduce done with device copies) -- a partition-invariance
+ * test vehicle on a single GPU. */
+typedef struct {
+    int32_t rank;
+    int32_t nranks;
+    const uint8_t *nccl_uid;  /* host, 128 bytes from pbcg_nccl_unique_id() on rank 0, same on all ranks; NULL if nranks == 1 */
+    int32_t virtual_ranks;    /* 0 or 1 = off */
+    int32_t history_capacity; /* rows of per-iteration scalar history kept on device; 0 -> 10001 */
+} pbcg_dist;
+
+/* Solver options (SPEC.md l.214-217 SolverConfig subset). */
+typedef struct {
+    double tol;               /* stop when ||r_{i+1}||/||b|| <= tol (>= 0; 0 never converges) */
+    int32_t max_iter;         /* >= 0 */
+    double breakdown_eps;     /* relative breakdown threshold, default 1e-30; <= 0 -> 1e-30 */
+    int32_t poll_every;       /* iterations per CUDA-graph chunk / host poll; <= 0 -> 16 */
+    int32_t use_graphs;       /* 1: replay captured CUDA graphs of poll_every iterations; 0: direct launches */
+} pbcg_opts;
+
+/* Solve result.  history row layout (12 doubles per row, row 0 = init, row
+ * i+1 = iteration i), identical to the oracle's:
+ *   0 theta=(q,y) 1 eta=(y,y) 2 sigma=(r0,s) 3 zeta=(r0,z) 4 omega
+ *   5 rho=(r0,r) 6 delta=(r0,w) 7 rr=(r,r) 8 relres=sqrt(rr)/||b||
+ *   9 beta 10 alpha (next) 11 reserved (0)                                   */
+typedef struct {
+    int32_t status;           /* enum pbcg_status */
+    int32_t iterations;       /* completed iterations */
+    double relres_recursive;  /* sqrt((r,r))/||b|| at the last completed iteration */
+    double relres_true;       /* NORM(b - A x)/NORM(b) */
+    double loop_seconds;      /* device time of the iteration loop (CUDA events) */
+    int32_t history_rows;     /* rows available via pbicgstab_history */
+    int32_t reserved;
+} pbcg_result;
+
+typedef struct pbcg_handle pbcg_handle;
+
+/* Bytes of device workspace pbicgstab_setup needs for A (A == NULL: a
+ * comm-only handle for distributed exdot).  Local (not collective); copies
+ * row_ptr to the host. */
+int pbicgstab_workspace_size(const pbcg_csr_local *A, const pbcg_dist *dist, size_t *bytes);
+
+/* Build a solver handle.  `stream` is the caller's cudaStream_t (NULL = legacy
+ * default stream) on which all work is ordered; `workspace` is caller-owned
+ * device memory of >= workspace_bytes that must outlive the handle (the
+ * library makes no cudaMalloc after setup).  Converts A to the internal
+ * sliced-ELL layout, plans the halo exchange, creates the NCCL communicators
+ * (nranks > 1), scans A for NaN/Inf (-> PBCG_ENONFINITE).  Collective. */
+int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *dist, void *stream, void *workspace,
+                    size_t workspace_bytes, pbcg_handle **out);
+
+/* Solve A x = b with Algorithm 2.  b_local/x_local hold this rank's rows
+ * (virtual ranks: the full vectors) and may be DEVICE or HOST pointers
+ * (host buffers are staged through the workspace inside the call: the
+ * "end-to-end" path).  x_local: in = x0, out = x.  Host-synchronous on
+ * return.  Breakdown / max-iter are outcomes in result->status with rc 0. */
+int pbicgstab_solve(pbcg_handle *h, const double *b_local, double *x_local, const pbcg_opts *opts,
+                    pbcg_result *result);
+
+/* Stepping interface (used by solve, bench and tracing):
+ *   start    lines I1-I4: r0 = b - A x0, r^ = r0, w0 = A r0, t0 = A w0, the
+ *            four initial EXDOTs and alpha_0; synchronises once to report
+ *            EINVAL (||b|| = 0) / ENONFINITE.
+ *   iterate  enqueue k more iterations on the stream (asynchronous; iterations
+ *            after convergence/breakdown are device-side no-ops).
+ *   finish   synchronise, true residual, copy x out (device or host pointer),
+ *            fill result. */
+int pbicgstab_start(pbcg_handle *h, const double *b_local, const double *x0_local, const pbcg_opts *opts);
+int pbicgstab_iterate(pbcg_handle *h, int32_t k);
+int pbicgstab_finish(pbcg_handle *h, double *x_local, pbcg_result *result);
+
+/* Copy up to max_rows rows (12 doubles each, layout above) of the scalar
+ * history of the last start/solve to host memory `out`; *rows = rows copied.
+ * Identical on every rank and every virtual rank. */
+int pbicgstab_history(pbcg_handle *h, double *out, int32_t max_rows, int32_t *rows);
+
+/* y = A x for this rank's rows (x_local, y_local: device, n_local each; the
+ * halo is exchanged internally).  Stream-ordered, asynchronous.  Virtual
+ * ranks: full vectors. */
+int pbicgstab_spmv(pbcg_handle *h, const double *x_local, double *y_local);
+
+/* EXDOT over n_local elements of device vectors x, y.  h == NULL: single
+ * GPU; otherwise the handle's ranks each pass their slice and the
+ * superaccumulators are allreduced (int64 sum) before the single rounding.
+ * result_on_device = 1: `result` (1 double) and `flags` (1 int32, may be
+ * NULL) are device pointers, the call is stream-ordered on `stream` and
+ * returns PBCG_OK; = 0: host pointers, the call synchronises and returns
+ * PBCG_ERANGE / PBCG_ENONFINITE when flagged (result still written).
+ * n_local = 0 gives +0.0. */
+int exdot(pbcg_handle *h, int64_t n_local, const double *x, const double *y, double *result, int32_t *flags,
+          int result_on_device, void *stream);
+
+/* Plain (non-reproducible, tree-ordered) fp64 dot -- the measurement
+ * baseline of BASELINE.json ("within 2x of a plain fp64 dot").  result is a
+ * device pointer; stream-ordered. */
+int pbcg_dot_plain(int64_t n, const double *x, const double *y, double *result, void *stream);
+
+/* Release the handle (communicators, events, graphs).  Workspace stays the
+ * caller's. */
+void pbicgstab_destroy(pbcg_handle *h);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char *pbicgstab_last_error(void);
+
+/* 128-byte NCCL unique id (rank 0 calls it; broadcast it to every rank). */
+int pbcg_nccl_unique_id(uint8_t *out128);
+
+int pbcg_abi_version(void);
+
+/* ---- measurement hooks (not part of the numerical contract) -------------- */
+
+/* Enqueue k more iterations of a started single-rank solve as direct launches
+ * bracketed by CUDA events on the handle's stream, synchronise, and return in
+ * ms[0..3] the summed device time of K2 (l.70-74 + phase-A dots), SpMV v=Az
+ * (l.75), K3 (l.77-79 + phase-B dots) and SpMV t=Aw (l.80). */
+int pbcg_profile_iterations(pbcg_handle *h, int32_t k, double *ms);
+
+/* Iterations per captured CUDA-graph chunk used by pbicgstab_iterate (>= 1). */
+int pbcg_set_chunk(int32_t iters);
+
+/* ---- host-only planning helpers (no GPU needed; CPU-testable) ------------ */
+
+/* Balanced contiguous partition of n rows over p ranks (SPEC.md l.148,
+ * l.185-187): the first n mod p ranks get one extra row.  begins: p+1 entries. */
+int pbcg_plan_partition(int64_t n, int32_t p, int64_t *begins);
+
+/* Halo plan for rank `me` given every rank's [row_begin,row_end) and the
+ * inclusive column hull [cmin,cmax] of its local rows (ranges: 4*p int64,
+ * cmax < cmin for a rank without nonzeros).  Outputs (p int64 each):
+ *   recv_lo/recv_hi  global rows [lo,hi) this rank receives from rank q
+ *   send_lo/send_hi  global rows [lo,hi) this rank sends to rank q
+ * (empty: lo == hi).  The x-buffer of rank `me` covers [*buf_lo, *buf_hi). */
+int pbcg_plan_halo(int32_t p, int32_t me, const int64_t *ranges, int64_t *recv_lo, int64_t *recv_hi,
+                   int64_t *send_lo, int64_t *send_hi, int64_t *buf_lo, int64_t *buf_hi);
+
+/* Host twin of the device superaccumulator (same source as the device
+ * normalise/round; CPU tests of the cross-rank merge path).  words: SACC
+ * words (pbcg_sacc_words(), int64, 32-bit digits, bit 0 = 2^-1074).
+ *   accumulate  words := normalised sum of x_k*y_k (TwoProd split; R-9 zone)
+ *   round       *out := RN-even(value(words)); PBCG_ERANGE on overflow */
+int pbcg_sacc_words(void);
+int pbcg_sacc_accumulate(int64_t n, const double *x, const double *y, int64_t *words);
+int pbcg_sacc_round(const int64_t *words, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PBICGSTAB_H */

@@ -1,0 +1,324 @@
+// exblas.cuh -- ExBLAS-style exactly rounded dot products on sm_100a.
+//
+// PAPER.md §2 l.95: "ExBLAS combines together long accumulator and
+// floating-point expansions"; results are "independent of data partitioning,
+// order of computations, thread scheduling, or reduction tree schemes".
+// SPEC.md l.116-117 fixes the two-level scheme (per-element TwoProd, an FPE of
+// doubles fed by TwoSum, spill into a Kulisch long accumulator, one rounding).
+//
+// B200 placement:
+//   registers  per thread and per dot, two FPEs: P (the rounded products
+//              p = fl(x*y)) and E (their exact errors e = x*y - p), NP/NE
+//              doubles each, fed by branch-free Knuth TwoSum;
+//   shared     a residual that falls out of an FPE is deposited into the
+//              CTA's superaccumulator with int64 shared atomics (rare);
+//   warp       at the end the lanes' FPEs are merged into lane 0 by a
+//              shuffle tree (TwoSum again; exact), lane 0 deposits its terms;
+//   CTA        the CTA normalises its superaccumulator and red.adds the
+//              nonzero words into a global one;
+//   grid       the last CTA (ticket) normalises and rounds once (or, with
+//              several ranks, leaves the normalised words for the int64
+//              allreduce).
+// Invariant: value(FPEs) + value(superaccumulators) + unread inputs = the
+// exact sum, at every point -- so the result is the exact sum rounded once,
+// whatever the grid, the thread order, NP/NE or the number of ranks.
+//
+// Superaccumulator geometry: SACC_L int64 words holding 32-bit digits, bit 0
+// of word 0 weighs 2^-1074 (the binary64 LSB), so any double deposits into at
+// most 3 words without carries; 31 spare bits per word absorb 2^31 deposits.
+// Normalised form: words 0..L-2 in [0,2^32), word L-1 signed.  Range: up to
+// 2^(32*66 - 1074 + 63) -- far beyond any sum of < 2^40 products < 2^1000.
+#pragma once
+#include <cstdint>
+#include <cstring>
+
+namespace pbcg {
+
+constexpr int SACC_L = 67;
+constexpr int SACC_FLAGW = 2;  // two trailing words: #CTAs with a range flag, with a non-finite flag
+
+enum : unsigned { FLAG_RANGE = 1u, FLAG_NONFINITE = 2u };
+
+__device__ __forceinline__ void two_sum(double a, double b, double &s, double &e) {
+    // Knuth TwoSum, 6 DADD, exact for all finite a, b without overflow.
+    s = __dadd_rn(a, b);
+    double bp = __dsub_rn(s, a);
+    double ap = __dsub_rn(s, bp);
+    e = __dadd_rn(__dsub_rn(a, ap), __dsub_rn(b, bp));
+}
+
+__device__ __forceinline__ bool is_nonzero(double v) { return (__double_as_longlong(v) << 1) != 0; }
+
+__host__ __device__ __forceinline__ double bits_to_double(unsigned long long b) {
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double((long long)b);
+#else
+    double d;
+    memcpy(&d, &b, 8);
+    return d;
+#endif
+}
+__host__ __device__ __forceinline__ int clz32(unsigned v) {
+#ifdef __CUDA_ARCH__
+    return __clz(v);
+#else
+    return __builtin_clz(v);
+#endif
+}
+
+__host__ __device__ __forceinline__ long long double_to_bits(double v) {
+#ifdef __CUDA_ARCH__
+    return __double_as_longlong(v);
+#else
+    long long b;
+    memcpy(&b, &v, 8);
+    return b;
+#endif
+}
+
+// Split a finite double into signed 32-bit-digit chunks (c0,c1,c2) for words
+// i, i+1, i+2 of the superaccumulator.  Returns false for NaN/Inf (which the
+// callers flag and never deposit).
+__host__ __device__ __forceinline__ bool sacc_split(double v, int &i, long long &c0, long long &c1, long long &c2) {
+    const long long bits = double_to_bits(v);
+    const unsigned E = (unsigned)(bits >> 52) & 0x7FFu;
+    if (E == 0x7FFu) return false;
+    unsigned long long m = (unsigned long long)bits & 0xFFFFFFFFFFFFFull;
+    int off = 0;
+    if (E) { m |= (1ull << 52); off = (int)E - 1; }  // LSB exponent E-1075 -> bit E-1 above 2^-1074
+    i = off >> 5;
+    const int s = off & 31;
+    const unsigned long long sh = m << s;
+    c0 = (long long)(sh & 0xFFFFFFFFull);
+    c1 = (long long)(sh >> 32);
+    c2 = s ? (long long)(m >> (64 - s)) : 0ll;
+    if (bits < 0) { c0 = -c0; c1 = -c1; c2 = -c2; }
+    return true;
+}
+
+// Deposit a finite double into a superaccumulator in shared memory.
+__device__ __forceinline__ void sacc_deposit(unsigned long long *acc, double v) {
+    int i;
+    long long c0, c1, c2;
+    if (!sacc_split(v, i, c0, c1, c2)) return;
+    if (c0) atomicAdd(&acc[i], (unsigned long long)c0);
+    if (c1) atomicAdd(&acc[i + 1], (unsigned long long)c1);
+    if (c2) atomicAdd(&acc[i + 2], (unsigned long long)c2);
+}
+
+// Host twin (CPU-side tests of the rounding path and of cross-rank merging).
+inline void sacc_deposit_host(long long *acc, double v) {
+    int i;
+    long long c0, c1, c2;
+    if (!sacc_split(v, i, c0, c1, c2)) return;
+    acc[i] += c0;
+    acc[i + 1] += c1;
+    acc[i + 2] += c2;
+}
+
+// Carry-normalise (one thread): words 0..L-2 -> [0,2^32), carry into word L-1.
+__host__ __device__ __forceinline__ void sacc_normalize(long long *w) {
+    long long carry = 0;
+    for (int i = 0; i < SACC_L - 1; ++i) {
+        long long v = w[i] + carry;
+        carry = v >> 32;  // arithmetic shift = floor division
+        w[i] = v & 0xFFFFFFFFll;
+    }
+    w[SACC_L - 1] += carry;
+}
+
+// bit `k` of a little-endian array of 32-bit digits
+__host__ __device__ __forceinline__ unsigned dig_bit(const unsigned *d, int k) { return (d[k >> 5] >> (k & 31)) & 1u; }
+
+// Round a NORMALISED superaccumulator to the nearest binary64, ties to even.
+// Exact zero -> +0.0.  Overflow -> +-inf and *ovf = true.
+__host__ __device__ inline double sacc_round(const long long *w, bool *ovf) {
+    constexpr int ND = SACC_L + 1;  // digits 0..L-2 from words, L-1 and L from the signed top word
+    unsigned d[ND];
+    for (int i = 0; i < SACC_L - 1; ++i) d[i] = (unsigned)w[i];
+    const long long top = w[SACC_L - 1];
+    d[SACC_L - 1] = (unsigned)((unsigned long long)top & 0xFFFFFFFFull);
+    d[SACC_L] = (unsigned)((unsigned long long)top >> 32);
+    const bool neg = top < 0;
+    if (neg) {  // two's complement negation of the ND-digit number
+        unsigned long long c = 1;
+        for (int i = 0; i < ND; ++i) {
+            unsigned long long t = (unsigned long long)(~d[i]) + c;
+            d[i] = (unsigned)t;
+            c = t >> 32;
+        }
+    }
+    int hi = ND - 1;
+    while (hi >= 0 && d[hi] == 0) --hi;
+    if (hi < 0) return 0.0;
+    const int B = hi * 32 + 31 - clz32(d[hi]);  // index of the most significant bit (bit 0 = 2^-1074)
+    double r;
+    if (B < 52) {  // subnormal range: every multiple of 2^-1074 below 2^-1022 is exact
+        unsigned long long m = 0;
+        for (int k = B; k >= 0; --k) m = (m << 1) | dig_bit(d, k);
+        r = bits_to_double(m);  // subnormal encoding = integer multiple of 2^-1074
+    } else {
+        int k0 = B - 52;  // kept LSB
+        unsigned long long m = 0;
+        for (int k = B; k >= k0; --k) m = (m << 1) | dig_bit(d, k);
+        unsigned rb = (k0 >= 1) ? dig_bit(d, k0 - 1) : 0u;
+        bool sticky = false;
+        if (k0 >= 2) {
+            const int lim = k0 - 1;  // bits [0, lim) below the round bit
+            for (int i = 0; i < (lim >> 5) && !sticky; ++i) sticky = d[i] != 0;
+            if (!sticky && (lim & 31)) sticky = (d[lim >> 5] & ((1u << (lim & 31)) - 1u)) != 0;
+        }
+        if (rb && (sticky || (m & 1ull))) {
+            m += 1;
+            if (m == (1ull << 53)) { m >>= 1; k0 += 1; }
+        }
+        // value = m * 2^(k0 - 1074), m in [2^52, 2^53): biased exponent = k0 + 1
+        const long long be = (long long)k0 + 1;
+        if (be >= 2047) {
+            *ovf = true;
+            r = bits_to_double(0x7FF0000000000000ull);
+        } else {
+            r = bits_to_double(((unsigned long long)be << 52) | (m & 0xFFFFFFFFFFFFFull));
+        }
+    }
+    return neg ? -r : r;
+}
+
+template <int N>
+struct Fpe {
+    double a[N];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int i = 0; i < N; ++i) a[i] = 0.0;
+    }
+    // cascade v through the expansion; returns what did not fit (exactly)
+    __device__ __forceinline__ double add(double v) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            double s, e;
+            two_sum(a[i], v, s, e);
+            a[i] = s;
+            v = e;
+        }
+        return v;
+    }
+};
+
+// Range rule (R-9): with x,y != 0, flag when |fl(x*y)| < 2^-960 or
+// >= 2^1000 (TwoProd is exact outside that zone); NaN/Inf flagged non-finite.
+__device__ __noinline__ unsigned range_class(double x, double y) {
+    const bool xz = (__double_as_longlong(x) << 1) == 0, yz = (__double_as_longlong(y) << 1) == 0;
+    const unsigned ex = (unsigned)(__double_as_longlong(x) >> 52) & 0x7FFu;
+    const unsigned ey = (unsigned)(__double_as_longlong(y) >> 52) & 0x7FFu;
+    if (ex == 0x7FFu || ey == 0x7FFu) return FLAG_NONFINITE;
+    if (xz || yz) return 0u;
+    return FLAG_RANGE;
+}
+
+template <int NP, int NE>
+struct ExAcc {
+    Fpe<NP> P;
+    Fpe<NE> E;
+    __device__ __forceinline__ void zero() {
+        P.zero();
+        E.zero();
+    }
+    // acc += x*y exactly; residuals go to the shared superaccumulator `sacc`
+    __device__ __forceinline__ void add(double x, double y, unsigned long long *sacc, unsigned &flags) {
+        const double p = __dmul_rn(x, y);
+        const double e = __fma_rn(x, y, -p);
+        const unsigned ep = (unsigned)(__double2hiint(p) >> 20) & 0x7FFu;
+        if (ep - 63u >= 1960u) flags |= range_class(x, y);
+        double r = P.add(p);
+        if (is_nonzero(r)) sacc_deposit(sacc, r);
+        r = E.add(e);
+        if (is_nonzero(r)) sacc_deposit(sacc, r);
+    }
+    // merge the lanes of the warp into lane 0 (tree: at step `off` lanes
+    // [0,off) absorb lanes [off,2off); the senders' terms are then dead)
+    __device__ __forceinline__ void warp_merge(unsigned long long *sacc) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            double ip[NP], ie[NE];
+#pragma unroll
+            for (int j = 0; j < NP; ++j) ip[j] = __shfl_down_sync(0xFFFFFFFFu, P.a[j], off);
+#pragma unroll
+            for (int j = 0; j < NE; ++j) ie[j] = __shfl_down_sync(0xFFFFFFFFu, E.a[j], off);
+            if (lane < off) {
+#pragma unroll
+                for (int j = 0; j < NP; ++j) {
+                    double r = P.add(ip[j]);
+                    if (is_nonzero(r)) sacc_deposit(sacc, r);
+                }
+#pragma unroll
+                for (int j = 0; j < NE; ++j) {
+                    double r = E.add(ie[j]);
+                    if (is_nonzero(r)) sacc_deposit(sacc, r);
+                }
+            }
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int j = 0; j < NP; ++j)
+                if (is_nonzero(P.a[j])) sacc_deposit(sacc, P.a[j]);
+#pragma unroll
+            for (int j = 0; j < NE; ++j)
+                if (is_nonzero(E.a[j])) sacc_deposit(sacc, E.a[j]);
+        }
+    }
+};
+
+// Shared-memory state of a CTA computing ND dots.
+template <int ND>
+struct CtaSacc {
+    unsigned long long w[ND][SACC_L];
+    unsigned flags;
+    int last;
+    double rounded[ND];
+};
+
+template <int ND>
+__device__ __forceinline__ void cta_sacc_zero(CtaSacc<ND> &S) {
+    for (int i = threadIdx.x; i < ND * SACC_L; i += blockDim.x) (&S.w[0][0])[i] = 0ull;
+    if (threadIdx.x == 0) S.flags = 0u;
+}
+
+// After every thread has merged its FPEs: normalise the CTA superaccumulators,
+// red.add them into gacc[ND*L + FLAGW], take a ticket; returns true in the
+// last CTA of the grid (whose threads then see the complete gacc).
+template <int ND>
+__device__ bool cta_sacc_publish(CtaSacc<ND> &S, unsigned flags, long long *gacc, unsigned *ticket) {
+    if (flags) atomicOr(&S.flags, flags);
+    __syncthreads();
+    if (threadIdx.x < ND) sacc_normalize((long long *)S.w[threadIdx.x]);
+    __syncthreads();
+    for (int i = threadIdx.x; i < ND * SACC_L; i += blockDim.x) {
+        const long long v = (long long)(&S.w[0][0])[i];
+        if (v) atomicAdd((unsigned long long *)&gacc[i], (unsigned long long)v);
+    }
+    if (threadIdx.x == 0) {
+        if (S.flags & FLAG_RANGE) atomicAdd((unsigned long long *)&gacc[ND * SACC_L], 1ull);
+        if (S.flags & FLAG_NONFINITE) atomicAdd((unsigned long long *)&gacc[ND * SACC_L + 1], 1ull);
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) S.last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (S.last) __threadfence();
+    return S.last != 0;
+}
+
+// In the last CTA: pull gacc into shared memory and normalise it.
+template <int ND>
+__device__ void cta_sacc_collect(CtaSacc<ND> &S, long long *gacc, unsigned &gflags) {
+    long long *w = (long long *)&S.w[0][0];
+    for (int i = threadIdx.x; i < ND * SACC_L; i += blockDim.x) w[i] = __ldcg(&gacc[i]);
+    __syncthreads();
+    if (threadIdx.x < ND) sacc_normalize(w + threadIdx.x * SACC_L);
+    __syncthreads();
+    const long long fr = __ldcg(&gacc[ND * SACC_L]), fn = __ldcg(&gacc[ND * SACC_L + 1]);
+    gflags = (fr ? FLAG_RANGE : 0u) | (fn ? FLAG_NONFINITE : 0u);
+}
+
+}  // namespace pbcg

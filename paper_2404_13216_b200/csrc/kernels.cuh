@@ -1,0 +1,516 @@
+// kernels.cuh -- the sm_100a kernels of the p-BiCGStab + ExBLAS hot path.
+//
+//   k2_kernel     Alg. 2 l.70-74 (p,s,z,q,y) + phase-A EXDOT partials
+//                 (q,y),(y,y),(r0,s),(r0,z)              [SURVEY §8(a) a2-a4, a6]
+//   spmv_sell     l.75 v = A z and l.80 t = A w, per-row ordered FMA chain
+//                 on a sliced-ELL (C = 32) layout         [a5, a10; reading R-6]
+//   k3_kernel     l.77-79 (x,r,w) + phase-B EXDOT partials
+//                 (r0,r'),(r0,w'),(r',r')                 [a7-a9, a11]
+//   multidot      generic fused EXDOTs (init, true residual, standalone exdot)
+//   finalize      normalise+round+scalars after a cross-rank allreduce
+//
+// Every floating-point value op is an explicit __fma_rn/__dmul_rn/__dadd_rn or
+// an IEEE division/sqrt; the library is compiled with -fmad=false.
+#pragma once
+#include <cstdint>
+
+#include "exblas.cuh"
+
+namespace pbcg {
+
+// history row layout (identical to the oracle's, include/pbicgstab.h)
+enum { H_THETA = 0, H_ETA, H_SIGMA, H_ZETA, H_OMEGA, H_RHO, H_DELTA, H_RR, H_RELRES, H_BETA, H_ALPHA, H_COLS = 12 };
+enum { ST_CONVERGED = 0, ST_MAXITER = 1, ST_BD_INIT = 2, ST_BD_RHO = 3, ST_BD_OMEGA = 4, ST_BD_ALPHA = 5,
+       ST_RANGE = 6, ST_RUNNING = -1 };
+enum Phase { PH_INIT = 0, PH_A = 1, PH_B = 2, PH_TRUE = 3, PH_EXDOT = 4 };
+
+// device-resident solver scalars (one copy per rank; identical on all ranks)
+struct Scalars {
+    double alpha, beta, omega, rho, sigma, zeta;
+    double nb, epsn, tol, eps;
+    double relres, relres_true;
+    int32_t it, done, status, max_iter;
+    int32_t hist_cap, err;
+    int32_t pad0, pad1;
+};
+
+// ------------------------------------------------------------------------
+// phase finalisation (one thread): the scalar part of Algorithm 2
+// ------------------------------------------------------------------------
+__device__ __forceinline__ void hist_put(double *hist, const Scalars *sc, int row, int col, double v) {
+    if (hist && row < sc->hist_cap) hist[(int64_t)row * H_COLS + col] = v;
+}
+
+__device__ void phase_finalize(int phase, Scalars *sc, const double *d, unsigned flags, double *hist,
+                               double *out, int32_t *out_flags) {
+    if (phase == PH_EXDOT) {
+        if (out) *out = d[0];
+        if (out_flags) *out_flags = (int32_t)flags;
+        return;
+    }
+    if (phase == PH_TRUE) {  // NORM(b - A x)/NORM(b)
+        sc->relres_true = __ddiv_rn(__dsqrt_rn(d[0]), sc->nb);
+        return;
+    }
+    if (phase == PH_INIT) {  // lines I2-I4
+        const double bb = d[0], rho = d[1], delta = d[2], rr = d[3];
+        sc->it = 0;
+        sc->nb = __dsqrt_rn(bb);
+        if (sc->nb == 0.0) { sc->err = 1; sc->done = 1; sc->status = ST_MAXITER; return; }  // EINVAL
+        const double relres = __ddiv_rn(__dsqrt_rn(rr), sc->nb);
+        sc->epsn = __dmul_rn(sc->eps, __dsqrt_rn(rho));  // eps * NORM(r^), (r^,r^) = (r^,r0) = rho
+        sc->rho = rho;
+        sc->relres = relres;
+        hist_put(hist, sc, 0, H_RHO, rho);
+        hist_put(hist, sc, 0, H_DELTA, delta);
+        hist_put(hist, sc, 0, H_RR, rr);
+        hist_put(hist, sc, 0, H_RELRES, relres);
+        if (flags) { sc->status = ST_RANGE; sc->done = 1; return; }
+        if (relres <= sc->tol) { sc->status = ST_CONVERGED; sc->done = 1; return; }
+        const double a0 = __ddiv_rn(rho, delta);
+        if (delta == 0.0 || !isfinite(a0)) { sc->status = ST_BD_INIT; sc->done = 1; return; }
+        sc->alpha = a0;
+        hist_put(hist, sc, 0, H_ALPHA, a0);
+        if (sc->max_iter == 0) { sc->status = ST_MAXITER; sc->done = 1; return; }
+        sc->status = ST_RUNNING;
+        return;
+    }
+    if (phase == PH_A) {  // l.76: omega := (q,y)/(y,y); omega := 0 when (y,y) = 0 (R-12)
+        const int i = sc->it;
+        const double theta = d[0], eta = d[1], sigma = d[2], zeta = d[3];
+        const double om = (eta == 0.0) ? 0.0 : __ddiv_rn(theta, eta);
+        hist_put(hist, sc, i + 1, H_THETA, theta);
+        hist_put(hist, sc, i + 1, H_ETA, eta);
+        hist_put(hist, sc, i + 1, H_SIGMA, sigma);
+        hist_put(hist, sc, i + 1, H_ZETA, zeta);
+        hist_put(hist, sc, i + 1, H_OMEGA, om);
+        if (flags) { sc->status = ST_RANGE; sc->done = 1; return; }
+        sc->omega = om;
+        sc->sigma = sigma;
+        sc->zeta = zeta;
+        return;
+    }
+    // PH_B: l.81-82 and the stopping / breakdown rules (R-10, R-11)
+    const int i = sc->it;
+    const double rhon = d[0], deltan = d[1], rr = d[2];
+    const double relres = __ddiv_rn(__dsqrt_rn(rr), sc->nb);
+    hist_put(hist, sc, i + 1, H_RHO, rhon);
+    hist_put(hist, sc, i + 1, H_DELTA, deltan);
+    hist_put(hist, sc, i + 1, H_RR, rr);
+    hist_put(hist, sc, i + 1, H_RELRES, relres);
+    sc->it = i + 1;
+    sc->relres = relres;
+    if (flags) { sc->status = ST_RANGE; sc->done = 1; return; }
+    if (relres <= sc->tol) { sc->status = ST_CONVERGED; sc->done = 1; return; }
+    const double thr = fmax(__dmul_rn(sc->epsn, __dsqrt_rn(rr)), 1e-300);
+    const double om = sc->omega, al = sc->alpha;
+    if (om == 0.0) { sc->status = ST_BD_OMEGA; sc->done = 1; return; }
+    if (fabs(rhon) <= thr) { sc->status = ST_BD_RHO; sc->done = 1; return; }
+    const double ben = __ddiv_rn(__dmul_rn(__ddiv_rn(al, om), rhon), sc->rho);  // ((a/w) rho')/rho
+    const double dd = __fma_rn(-__dmul_rn(ben, om), sc->zeta, __fma_rn(ben, sc->sigma, deltan));
+    hist_put(hist, sc, i + 1, H_BETA, ben);
+    if (!(fabs(dd) > thr) || !isfinite(dd)) { sc->status = ST_BD_ALPHA; sc->done = 1; return; }
+    const double aln = __ddiv_rn(rhon, dd);
+    if (!isfinite(aln)) { sc->status = ST_BD_ALPHA; sc->done = 1; return; }
+    hist_put(hist, sc, i + 1, H_ALPHA, aln);
+    sc->beta = ben;
+    sc->alpha = aln;
+    sc->rho = rhon;
+    if (sc->it >= sc->max_iter) { sc->status = ST_MAXITER; sc->done = 1; }
+}
+
+// Last CTA of a dot kernel: collect + normalise gacc; then either round and
+// finalise (single rank) or leave normalised words for the allreduce.
+template <int ND>
+__device__ void last_cta_finish(CtaSacc<ND> &S, long long *gacc, unsigned *ticket, int phase, int finalize,
+                                Scalars *sc, double *hist, double *out, int32_t *out_flags) {
+    unsigned gflags;
+    cta_sacc_collect<ND>(S, gacc, gflags);
+    long long *w = (long long *)&S.w[0][0];
+    if (finalize) {
+        if (threadIdx.x < ND) {
+            bool ovf = false;
+            S.rounded[threadIdx.x] = sacc_round(w + threadIdx.x * SACC_L, &ovf);
+            if (ovf) atomicOr(&S.flags, FLAG_RANGE);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned f = gflags | (S.flags & FLAG_RANGE);
+            phase_finalize(phase, sc, S.rounded, f, hist, out, out_flags);
+        }
+        for (int i = threadIdx.x; i < ND * SACC_L + SACC_FLAGW; i += blockDim.x) gacc[i] = 0;
+    } else {
+        for (int i = threadIdx.x; i < ND * SACC_L; i += blockDim.x) gacc[i] = w[i];
+    }
+    if (threadIdx.x == 0) *ticket = 0u;
+}
+
+// ------------------------------------------------------------------------
+// K2: p,s,z,q,y + phase-A partial dots
+// ------------------------------------------------------------------------
+struct K2Args {
+    int64_t n;
+    const double *r, *rh, *w, *t, *v;
+    double *p, *s, *z, *q, *y;
+    Scalars *sc;
+    long long *gacc;
+    unsigned *ticket;
+    double *hist;
+    int finalize;
+};
+
+template <int NP, int NE, int BS>
+__global__ void __launch_bounds__(BS) k2_kernel(K2Args a) {
+    __shared__ CtaSacc<4> S;
+    Scalars *sc = a.sc;
+    if (sc->done) return;
+    cta_sacc_zero<4>(S);
+    __syncthreads();
+    const bool first = (sc->it == 0);
+    const double al = sc->alpha, be = sc->beta, om = sc->omega;
+    const double nal = -al, nom = -om;
+    ExAcc<NP, NE> dqy, dyy, drs, drz;
+    dqy.zero(); dyy.zero(); drs.zero(); drz.zero();
+    unsigned flags = 0;
+    unsigned long long *s0 = S.w[0], *s1 = S.w[1], *s2 = S.w[2], *s3 = S.w[3];
+    const int64_t n = a.n;
+    const int64_t npair = n >> 1;
+    const int64_t stride = (int64_t)gridDim.x * BS;
+    const double2 *r2 = (const double2 *)a.r, *rh2 = (const double2 *)a.rh, *w2 = (const double2 *)a.w,
+                  *t2 = (const double2 *)a.t, *v2 = (const double2 *)a.v;
+    double2 *p2 = (double2 *)a.p, *ss2 = (double2 *)a.s, *z2 = (double2 *)a.z, *q2 = (double2 *)a.q,
+            *y2 = (double2 *)a.y;
+    auto row = [&](double r, double rh, double w, double t, double v, double &p, double &s, double &z,
+                   double &q, double &y) {
+        if (first) {  // beta_{-1} = 0: exact copies (R-3)
+            p = r; s = w; z = t;
+        } else {
+            p = __fma_rn(be, __fma_rn(nom, s, p), r);
+            s = __fma_rn(be, __fma_rn(nom, z, s), w);
+            z = __fma_rn(be, __fma_rn(nom, v, z), t);
+        }
+        q = __fma_rn(nal, s, r);
+        y = __fma_rn(nal, z, w);
+        dqy.add(q, y, s0, flags);
+        dyy.add(y, y, s1, flags);
+        drs.add(rh, s, s2, flags);
+        drz.add(rh, z, s3, flags);
+    };
+    for (int64_t k = (int64_t)blockIdx.x * BS + threadIdx.x; k < npair; k += stride) {
+        const double2 r = r2[k], rh = rh2[k], w = w2[k], t = t2[k];
+        double2 p, s, z, v;
+        if (!first) { p = p2[k]; s = ss2[k]; z = z2[k]; v = v2[k]; }
+        double2 q, y;
+        row(r.x, rh.x, w.x, t.x, v.x, p.x, s.x, z.x, q.x, y.x);
+        row(r.y, rh.y, w.y, t.y, v.y, p.y, s.y, z.y, q.y, y.y);
+        p2[k] = p; ss2[k] = s; z2[k] = z; q2[k] = q; y2[k] = y;
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int64_t k = n - 1;
+        double p = 0, s = 0, z = 0, v = 0, q, y;
+        if (!first) { p = a.p[k]; s = a.s[k]; z = a.z[k]; v = a.v[k]; }
+        row(a.r[k], a.rh[k], a.w[k], a.t[k], v, p, s, z, q, y);
+        a.p[k] = p; a.s[k] = s; a.z[k] = z; a.q[k] = q; a.y[k] = y;
+    }
+    dqy.warp_merge(s0); dyy.warp_merge(s1); drs.warp_merge(s2); drz.warp_merge(s3);
+    if (cta_sacc_publish<4>(S, flags, a.gacc, a.ticket))
+        last_cta_finish<4>(S, a.gacc, a.ticket, PH_A, a.finalize, sc, a.hist, nullptr, nullptr);
+}
+
+// ------------------------------------------------------------------------
+// K3: x,r,w + phase-B partial dots
+// ------------------------------------------------------------------------
+struct K3Args {
+    int64_t n;
+    const double *rh, *p, *q, *y, *t, *v;
+    double *x, *r, *w;
+    Scalars *sc;
+    long long *gacc;
+    unsigned *ticket;
+    double *hist;
+    int finalize;
+};
+
+template <int NP, int NE, int BS>
+__global__ void __launch_bounds__(BS) k3_kernel(K3Args a) {
+    __shared__ CtaSacc<3> S;
+    Scalars *sc = a.sc;
+    if (sc->done) return;
+    cta_sacc_zero<3>(S);
+    __syncthreads();
+    const double al = sc->alpha, om = sc->omega;
+    const double nal = -al, nom = -om;
+    ExAcc<NP, NE> drr, drw, dnn;
+    drr.zero(); drw.zero(); dnn.zero();
+    unsigned flags = 0;
+    unsigned long long *s0 = S.w[0], *s1 = S.w[1], *s2 = S.w[2];
+    const int64_t n = a.n;
+    const int64_t npair = n >> 1;
+    const int64_t stride = (int64_t)gridDim.x * BS;
+    const double2 *rh2 = (const double2 *)a.rh, *p2 = (const double2 *)a.p, *q2 = (const double2 *)a.q,
+                  *y2 = (const double2 *)a.y, *t2 = (const double2 *)a.t, *v2 = (const double2 *)a.v;
+    double2 *x2 = (double2 *)a.x, *rr2 = (double2 *)a.r, *w2 = (double2 *)a.w;
+    auto row = [&](double rh, double p, double q, double y, double t, double v, double &x, double &r,
+                   double &w) {
+        x = __fma_rn(om, q, __fma_rn(al, p, x));   // x + alpha p + omega q (l.77)
+        r = __fma_rn(nom, y, q);                   // q - omega y           (l.78)
+        w = __fma_rn(nom, __fma_rn(nal, v, t), y); // y - omega (t - alpha v) (l.79)
+        drr.add(rh, r, s0, flags);
+        drw.add(rh, w, s1, flags);
+        dnn.add(r, r, s2, flags);
+    };
+    for (int64_t k = (int64_t)blockIdx.x * BS + threadIdx.x; k < npair; k += stride) {
+        const double2 rh = rh2[k], p = p2[k], q = q2[k], y = y2[k], t = t2[k], v = v2[k];
+        double2 x = x2[k], r, w;
+        row(rh.x, p.x, q.x, y.x, t.x, v.x, x.x, r.x, w.x);
+        row(rh.y, p.y, q.y, y.y, t.y, v.y, x.y, r.y, w.y);
+        x2[k] = x; rr2[k] = r; w2[k] = w;
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int64_t k = n - 1;
+        double x = a.x[k], r, w;
+        row(a.rh[k], a.p[k], a.q[k], a.y[k], a.t[k], a.v[k], x, r, w);
+        a.x[k] = x; a.r[k] = r; a.w[k] = w;
+    }
+    drr.warp_merge(s0); drw.warp_merge(s1); dnn.warp_merge(s2);
+    if (cta_sacc_publish<3>(S, flags, a.gacc, a.ticket))
+        last_cta_finish<3>(S, a.gacc, a.ticket, PH_B, a.finalize, sc, a.hist, nullptr, nullptr);
+}
+
+// ------------------------------------------------------------------------
+// multidot: up to 4 fused EXDOTs (init, true residual, standalone exdot)
+// ------------------------------------------------------------------------
+struct MultiDotArgs {
+    int64_t n;
+    const double *x[4], *y[4];
+    Scalars *sc;  // may be null for standalone exdot
+    long long *gacc;
+    unsigned *ticket;
+    double *hist;
+    int phase, finalize;
+    double *out;
+    int32_t *out_flags;
+};
+
+template <int ND, int NP, int NE, int BS>
+__global__ void __launch_bounds__(BS) multidot_kernel(MultiDotArgs a) {
+    __shared__ CtaSacc<ND> S;
+    if (a.sc && a.sc->done && a.phase != PH_TRUE) return;
+    cta_sacc_zero<ND>(S);
+    __syncthreads();
+    ExAcc<NP, NE> acc[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) acc[d].zero();
+    unsigned flags = 0;
+    const int64_t n = a.n;
+    const int64_t npair = n >> 1;
+    const int64_t stride = (int64_t)gridDim.x * BS;
+    bool aligned = true;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) aligned &= ((((uintptr_t)a.x[d]) | ((uintptr_t)a.y[d])) & 15) == 0;
+    if (aligned) {
+        for (int64_t k = (int64_t)blockIdx.x * BS + threadIdx.x; k < npair; k += stride) {
+            double2 xv[ND], yv[ND];
+#pragma unroll
+            for (int d = 0; d < ND; ++d) {
+                xv[d] = ((const double2 *)a.x[d])[k];
+                yv[d] = ((const double2 *)a.y[d])[k];
+            }
+#pragma unroll
+            for (int d = 0; d < ND; ++d) {
+                acc[d].add(xv[d].x, yv[d].x, S.w[d], flags);
+                acc[d].add(xv[d].y, yv[d].y, S.w[d], flags);
+            }
+        }
+        if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+#pragma unroll
+            for (int d = 0; d < ND; ++d) acc[d].add(a.x[d][n - 1], a.y[d][n - 1], S.w[d], flags);
+        }
+    } else {
+        for (int64_t k = (int64_t)blockIdx.x * BS + threadIdx.x; k < n; k += stride) {
+#pragma unroll
+            for (int d = 0; d < ND; ++d) acc[d].add(a.x[d][k], a.y[d][k], S.w[d], flags);
+        }
+    }
+#pragma unroll
+    for (int d = 0; d < ND; ++d) acc[d].warp_merge(S.w[d]);
+    if (cta_sacc_publish<ND>(S, flags, a.gacc, a.ticket))
+        last_cta_finish<ND>(S, a.gacc, a.ticket, a.phase, a.finalize, a.sc, a.hist, a.out, a.out_flags);
+}
+
+// After an allreduce of normalised words: normalise, round, finalise (1 CTA).
+template <int ND>
+__global__ void finalize_kernel(long long *gacc, int phase, Scalars *sc, double *hist, double *out,
+                                int32_t *out_flags) {
+    __shared__ CtaSacc<ND> S;
+    if (sc && sc->done && phase != PH_TRUE && phase != PH_EXDOT) {
+        for (int i = threadIdx.x; i < ND * SACC_L + SACC_FLAGW; i += blockDim.x) gacc[i] = 0;
+        return;
+    }
+    if (threadIdx.x == 0) S.flags = 0u;
+    unsigned gflags;
+    cta_sacc_collect<ND>(S, gacc, gflags);
+    long long *w = (long long *)&S.w[0][0];
+    if (threadIdx.x < ND) {
+        bool ovf = false;
+        S.rounded[threadIdx.x] = sacc_round(w + threadIdx.x * SACC_L, &ovf);
+        if (ovf) atomicOr(&S.flags, FLAG_RANGE);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) phase_finalize(phase, sc, S.rounded, gflags | (S.flags & FLAG_RANGE), hist, out, out_flags);
+    __syncthreads();
+    for (int i = threadIdx.x; i < ND * SACC_L + SACC_FLAGW; i += blockDim.x) gacc[i] = 0;
+}
+
+// Virtual-rank "allreduce": every rank's gacc := sum over ranks (int64).
+__global__ void vallreduce_kernel(long long **gaccs, int nr, int words) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < words; i += gridDim.x * blockDim.x) {
+        long long s = 0;
+        for (int r = 0; r < nr; ++r) s += gaccs[r][i];
+        for (int r = 0; r < nr; ++r) gaccs[r][i] = s;
+    }
+}
+
+// ------------------------------------------------------------------------
+// SpMV on sliced ELL (C = 32 rows per slice, slot-major), one thread per row.
+// The per-row chain is left to right in ascending column order starting from
+// +0.0, one fma per nonzero; padding slots are never folded (R-6).
+// ------------------------------------------------------------------------
+struct SellMat {
+    int64_t n;
+    const int64_t *slice_off;  // nslices+1, element offsets of each slice
+    const int32_t *row_len;
+    const double *val;
+    const int32_t *col;        // indices into the rank's padded x buffer
+};
+
+enum { SPMV_PLAIN = 0, SPMV_RESID = 1 };
+
+template <int MODE, int UNR>
+__global__ void __launch_bounds__(256) spmv_sell_kernel(SellMat A, const double *__restrict__ x,
+                                                        double *__restrict__ y, const double *__restrict__ b,
+                                                        double *__restrict__ y2, const Scalars *sc) {
+    if (sc && sc->done) return;
+    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= A.n) return;
+    const int64_t base = __ldg(&A.slice_off[row >> 5]) + (row & 31);
+    const int len = __ldg(&A.row_len[row]);
+    const double *vp = A.val + base;
+    const int32_t *cp = A.col + base;
+    double acc = 0.0;
+    for (int k = 0; k < len; k += UNR) {
+        double v[UNR], xv[UNR];
+        int c[UNR];
+#pragma unroll
+        for (int j = 0; j < UNR; ++j) {
+            if (k + j < len) {
+                v[j] = __ldcs(vp + 32 * (k + j));
+                c[j] = __ldcs(cp + 32 * (k + j));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < UNR; ++j)
+            if (k + j < len) xv[j] = __ldg(x + c[j]);
+#pragma unroll
+        for (int j = 0; j < UNR; ++j)
+            if (k + j < len) acc = __fma_rn(v[j], xv[j], acc);
+    }
+    if (MODE == SPMV_PLAIN) {
+        y[row] = acc;
+    } else {
+        const double r = __dsub_rn(b[row], acc);  // r0 := b - A x0 (l.64), one rounding
+        y[row] = r;
+        if (y2) y2[row] = r;
+    }
+}
+
+// ------------------------------------------------------------------------
+// setup helpers
+// ------------------------------------------------------------------------
+// per-row column hull: out[2v] = min col, out[2v+1] = max col over rank v's rows
+__global__ void row_hull_kernel(int64_t nrows, const int32_t *rp, const int32_t *col, const int64_t *begins,
+                                int nr, long long *out) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t s = rp[r], e = rp[r + 1];
+        if (e <= s) continue;
+        int v = 0;
+        while (v + 1 < nr && r >= begins[v + 1]) ++v;
+        atomicMin(&out[2 * v], (long long)col[s]);
+        atomicMax(&out[2 * v + 1], (long long)col[e - 1]);
+    }
+}
+
+// CSR rows -> sliced ELL.  rp is indexed by local row and holds absolute
+// offsets into col/val.  Checks: finite values, strictly increasing columns in
+// [0, ncols), row pointer monotone.
+__global__ void csr_to_sell_kernel(int64_t n, const int32_t *rp, const int32_t *col, const double *val,
+                                   int64_t ncols, int64_t col_shift, const int64_t *slice_off, int32_t *row_len,
+                                   double *sval, int32_t *scol, int *bad) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t s = rp[r], e = rp[r + 1];
+        const int len = e - s;
+        if (len < 0) { atomicOr(bad, 1); continue; }
+        row_len[r] = len;
+        const int64_t base = slice_off[r >> 5] + (r & 31);
+        int32_t prev = -1;
+        for (int k = 0; k < len; ++k) {
+            const int32_t c = col[s + k];
+            const double v = val[s + k];
+            if (c <= prev || c < 0 || (int64_t)c >= ncols) atomicOr(bad, 1);
+            if (!isfinite(v)) atomicOr(bad, 2);
+            prev = c;
+            sval[base + 32 * k] = v;
+            scol[base + 32 * k] = (int32_t)((int64_t)c - col_shift);
+        }
+        const int64_t width = (slice_off[(r >> 5) + 1] - slice_off[r >> 5]) >> 5;
+        for (int64_t k = len; k < width; ++k) {  // padding: never folded, kept addressable
+            sval[base + 32 * k] = 0.0;
+            scol[base + 32 * k] = 0;
+        }
+    }
+}
+
+__global__ void nonfinite_scan_kernel(int64_t n, const double *v, int *bad) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(v[i])) atomicOr(bad, 2);
+}
+
+// ------------------------------------------------------------------------
+// plain fp64 dot (measurement baseline, BASELINE.json north_star): grid-stride
+// + warp shuffle tree + CTA partials, last CTA sums the partials in order.
+// ------------------------------------------------------------------------
+template <int BS>
+__global__ void __launch_bounds__(BS) plain_dot_kernel(int64_t n, const double *x, const double *y,
+                                                        double *partials, unsigned *ticket, double *out) {
+    __shared__ double red[BS / 32];
+    __shared__ int last;
+    double s = 0.0;
+    const int64_t npair = n >> 1;
+    const int64_t stride = (int64_t)gridDim.x * BS;
+    for (int64_t k = (int64_t)blockIdx.x * BS + threadIdx.x; k < npair; k += stride) {
+        const double2 a = ((const double2 *)x)[k], b = ((const double2 *)y)[k];
+        s = __fma_rn(a.x, b.x, s);
+        s = __fma_rn(a.y, b.y, s);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) s = __fma_rn(x[n - 1], y[n - 1], s);
+    for (int o = 16; o; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xFFFFFFFFu, s, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < BS / 32; ++i) t = __dadd_rn(t, red[i]);
+        partials[blockIdx.x] = t;
+        __threadfence();
+        last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double t = 0.0;
+        for (unsigned i = 0; i < gridDim.x; ++i) t = __dadd_rn(t, __ldcg(&partials[i]));
+        *out = t;
+        *ticket = 0u;
+    }
+}
+
+}  // namespace pbcg

@@ -1,0 +1,1121 @@
+// runtime.cu -- host runtime and C ABI (include/pbicgstab.h) of the B200
+// p-BiCGStab + ExBLAS hot path.
+//
+// Layers:
+//   setup    partition / halo plan / sliced-ELL conversion / workspace carve /
+//            NCCL communicators (dlopen'ed libnccl.so.2, the copy torch loads)
+//   solve    I1-I4 once, then the Algorithm 2 loop replayed as CUDA-graph
+//            chunks of `poll_every` iterations; the host polls a device done
+//            flag between chunks, later iterations are device-side no-ops
+//   ranks    1 rank: K2 -> SpMV(z) -> K3 -> SpMV(w), each dot kernel rounds
+//            in its last CTA (no extra launch);
+//            P real ranks: phase-A/B superaccumulators allreduced (int64 sum)
+//            by NCCL on a side stream while the halo exchange + SpMV run on
+//            the main stream (§2 l.90, "communication hiding");
+//            V virtual ranks: the same dataflow emulated in one process on
+//            one GPU with device copies (partition-invariance test vehicle).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <nccl.h>
+
+#include "../../include/pbicgstab.h"
+#include "kernels.cuh"
+
+using namespace pbcg;
+
+// ----------------------------------------------------------------------------
+// errors
+// ----------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static int fail(int rc, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return rc;
+}
+
+#define CUDA_TRY(x)                                                                                      \
+    do {                                                                                                 \
+        cudaError_t e_ = (x);                                                                            \
+        if (e_ != cudaSuccess)                                                                           \
+            return fail(PBCG_ECUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, __LINE__);    \
+    } while (0)
+
+#define RC_TRY(x)                  \
+    do {                           \
+        int rc_ = (x);             \
+        if (rc_ != PBCG_OK) return rc_; \
+    } while (0)
+
+// ----------------------------------------------------------------------------
+// NCCL (resolved at run time: the library works without NCCL on one GPU)
+// ----------------------------------------------------------------------------
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi g_nccl;
+static std::once_flag g_nccl_once;
+
+static void nccl_load() {
+    const char *names[] = {getenv("PBCG_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+    void *h = nullptr;
+    for (const char *nm : names) {
+        if (!nm) continue;
+        h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        if (!h) h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+        if (h) break;
+    }
+    if (!h) return;
+#define SYM(f, s) g_nccl.f = (decltype(g_nccl.f))dlsym(h, s)
+    SYM(GetUniqueId, "ncclGetUniqueId");
+    SYM(CommInitRank, "ncclCommInitRank");
+    SYM(CommDestroy, "ncclCommDestroy");
+    SYM(AllReduce, "ncclAllReduce");
+    SYM(AllGather, "ncclAllGather");
+    SYM(Send, "ncclSend");
+    SYM(Recv, "ncclRecv");
+    SYM(GroupStart, "ncclGroupStart");
+    SYM(GroupEnd, "ncclGroupEnd");
+    SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllReduce &&
+                g_nccl.AllGather && g_nccl.Send && g_nccl.Recv && g_nccl.GroupStart && g_nccl.GroupEnd;
+}
+
+static bool nccl_available() {
+    std::call_once(g_nccl_once, nccl_load);
+    return g_nccl.ok;
+}
+
+#define NCCL_TRY(x)                                                                                          \
+    do {                                                                                                     \
+        ncclResult_t e_ = (x);                                                                               \
+        if (e_ != ncclSuccess)                                                                               \
+            return fail(PBCG_ENCCL, "%s: %s", #x, g_nccl.GetErrorString ? g_nccl.GetErrorString(e_) : "?"); \
+    } while (0)
+
+// ----------------------------------------------------------------------------
+// host-only planning (exported; CPU-testable)
+// ----------------------------------------------------------------------------
+extern "C" int pbcg_plan_partition(int64_t n, int32_t p, int64_t *begins) {
+    if (n < 0 || p < 1 || !begins) return fail(PBCG_EINVAL, "plan_partition: bad arguments");
+    const int64_t q = n / p, rem = n % p;
+    begins[0] = 0;
+    for (int32_t k = 0; k < p; ++k) begins[k + 1] = begins[k] + q + (k < rem ? 1 : 0);
+    return PBCG_OK;
+}
+
+static void buf_range(const int64_t *rg, int64_t &lo, int64_t &hi) {
+    const int64_t rb = rg[0], re = rg[1], cmin = rg[2], cmax = rg[3];
+    lo = rb;
+    hi = re;
+    if (cmax >= cmin) {
+        lo = std::min(lo, cmin);
+        hi = std::max(hi, cmax + 1);
+    }
+}
+
+extern "C" int pbcg_plan_halo(int32_t p, int32_t me, const int64_t *ranges, int64_t *recv_lo, int64_t *recv_hi,
+                              int64_t *send_lo, int64_t *send_hi, int64_t *buf_lo, int64_t *buf_hi) {
+    if (p < 1 || me < 0 || me >= p || !ranges) return fail(PBCG_EINVAL, "plan_halo: bad arguments");
+    for (int32_t q = 0; q < p; ++q) {
+        if (ranges[4 * q] > ranges[4 * q + 1]) return fail(PBCG_EINVAL, "plan_halo: rank %d has row_begin > row_end", q);
+        if (q > 0 && ranges[4 * q] != ranges[4 * (q - 1) + 1])
+            return fail(PBCG_EINVAL, "plan_halo: row blocks do not tile in rank order at rank %d", q);
+    }
+    int64_t mlo, mhi;
+    buf_range(ranges + 4 * me, mlo, mhi);
+    if (buf_lo) *buf_lo = mlo;
+    if (buf_hi) *buf_hi = mhi;
+    const int64_t mrb = ranges[4 * me], mre = ranges[4 * me + 1];
+    for (int32_t q = 0; q < p; ++q) {
+        int64_t rl = 0, rh = 0, sl = 0, sh = 0;
+        if (q != me) {
+            const int64_t qrb = ranges[4 * q], qre = ranges[4 * q + 1];
+            rl = std::max(mlo, qrb);
+            rh = std::min(mhi, qre);
+            if (rh <= rl) rl = rh = 0;
+            int64_t qlo, qhi;
+            buf_range(ranges + 4 * q, qlo, qhi);
+            sl = std::max(qlo, mrb);
+            sh = std::min(qhi, mre);
+            if (sh <= sl) sl = sh = 0;
+        }
+        if (recv_lo) recv_lo[q] = rl;
+        if (recv_hi) recv_hi[q] = rh;
+        if (send_lo) send_lo[q] = sl;
+        if (send_hi) send_hi[q] = sh;
+    }
+    return PBCG_OK;
+}
+
+// host twins of the device superaccumulator (CPU tests of the merge + round
+// path used after the cross-rank allreduce)
+extern "C" int pbcg_sacc_accumulate(int64_t n, const double *x, const double *y, int64_t *words) {
+    if (n < 0 || !words) return fail(PBCG_EINVAL, "sacc_accumulate: bad arguments");
+    long long *w = (long long *)words;
+    for (int64_t k = 0; k < n; ++k) {
+        const double p = x[k] * y[k];
+        const double e = std::fma(x[k], y[k], -p);  // exact in the R-9 zone
+        sacc_deposit_host(w, p);
+        sacc_deposit_host(w, e);
+    }
+    sacc_normalize(w);
+    return PBCG_OK;
+}
+
+extern "C" int pbcg_sacc_round(const int64_t *words, double *out) {
+    if (!words || !out) return fail(PBCG_EINVAL, "sacc_round: bad arguments");
+    long long w[SACC_L];
+    memcpy(w, words, sizeof(w));
+    sacc_normalize(w);
+    bool ovf = false;
+    *out = sacc_round(w, &ovf);
+    return ovf ? PBCG_ERANGE : PBCG_OK;
+}
+
+extern "C" int pbcg_sacc_words(void) { return SACC_L; }
+
+// ----------------------------------------------------------------------------
+// handle
+// ----------------------------------------------------------------------------
+static constexpr int GW4 = 4 * SACC_L + SACC_FLAGW;  // words of a 4-dot reduction buffer
+static constexpr int NPH = 5;                        // reduction buffers: init, A, B, true, exdot
+static constexpr int K_BS = 256;
+static constexpr int K_NP = 2, K_NE = 2;             // FPE depth for products / errors (performance only, R-16)
+
+struct Rank {
+    int id = 0;
+    int64_t rb = 0, re = 0, n = 0;
+    int64_t buf_lo = 0, buf_hi = 0, own_off = 0;  // padded x-buffer covers global [buf_lo, buf_hi)
+    std::vector<int64_t> recv_lo, recv_hi, send_lo, send_hi;
+    int64_t nslices = 0, sell_nnz = 0;
+    std::vector<int64_t> h_slice_off;
+    // device
+    int64_t *slice_off = nullptr;
+    int32_t *row_len = nullptr;
+    double *sval = nullptr;
+    int32_t *scol = nullptr;
+    double *x = nullptr, *r = nullptr, *rh = nullptr, *p = nullptr, *s = nullptr, *q = nullptr, *y = nullptr,
+           *t = nullptr, *v = nullptr, *b = nullptr, *tmp = nullptr;
+    double *zpad = nullptr, *wpad = nullptr, *xpad = nullptr;
+    long long *gacc[NPH] = {};
+    unsigned *tickets = nullptr;
+    Scalars *sc = nullptr;
+    double *hist = nullptr;
+    int *bad = nullptr;
+    double *z() const { return zpad + own_off; }
+    double *w() const { return wpad + own_off; }
+    SellMat mat() const { return SellMat{n, slice_off, row_len, sval, scol}; }
+};
+
+struct pbcg_handle {
+    int dev = 0, nsm = 148;
+    cudaStream_t stream = nullptr, side = nullptr;
+    int nranks = 1, rank = 0, V = 1;  // real ranks, this rank, virtual ranks
+    int64_t n_global = 0;
+    bool comm_only = false;
+    std::vector<Rank> R;
+    ncclComm_t comm_halo = nullptr, comm_red = nullptr;
+    long long **vgacc = nullptr;  // device array [NPH][V] of gacc pointers (virtual ranks)
+    int hist_cap = 10001;
+    Scalars *h_sc = nullptr;      // pinned mirror of rank 0's scalars
+    int grid_k2 = 0, grid_k3 = 0, grid_md = 0;
+    cudaGraphExec_t gexec = nullptr;
+    int g_iters = 0;
+    cudaEvent_t ev[8] = {};
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    bool started = false;
+    int max_iter = 0;
+    size_t ws_need = 0;
+    // scratch for exdot on a handle
+    double *xd_out = nullptr;
+    int32_t *xd_flags = nullptr;
+};
+
+// workspace carving (dry run computes the size)
+struct Carver {
+    char *base;
+    size_t off = 0;
+    template <class T>
+    T *take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        T *p = base ? (T *)(base + off) : nullptr;
+        off += std::max<size_t>(count, 1) * sizeof(T);
+        return p;
+    }
+};
+
+static void carve_rank(Carver &C, Rank &R, int hist_cap, bool comm_only) {
+    if (!comm_only) {
+        R.slice_off = C.take<int64_t>(R.nslices + 1);
+        R.row_len = C.take<int32_t>(R.n);
+        R.sval = C.take<double>(R.sell_nnz);
+        R.scol = C.take<int32_t>(R.sell_nnz);
+        const size_t n = (size_t)R.n + 2;
+        R.x = C.take<double>(n); R.r = C.take<double>(n); R.rh = C.take<double>(n); R.p = C.take<double>(n);
+        R.s = C.take<double>(n); R.q = C.take<double>(n); R.y = C.take<double>(n); R.t = C.take<double>(n);
+        R.v = C.take<double>(n); R.b = C.take<double>(n); R.tmp = C.take<double>(n);
+        const size_t nb = (size_t)(R.buf_hi - R.buf_lo) + 2;
+        R.zpad = C.take<double>(nb); R.wpad = C.take<double>(nb); R.xpad = C.take<double>(nb);
+        R.hist = C.take<double>((size_t)hist_cap * H_COLS);
+    }
+    for (int k = 0; k < NPH; ++k) R.gacc[k] = C.take<long long>(GW4);
+    R.tickets = C.take<unsigned>(16);
+    R.sc = C.take<Scalars>(1);
+    R.bad = C.take<int>(4);
+}
+
+static size_t carve_handle_extra(Carver &C, pbcg_handle *h) {
+    h->vgacc = C.take<long long *>((size_t)NPH * h->V);
+    h->xd_out = C.take<double>(4);
+    h->xd_flags = C.take<int32_t>(4);
+    return C.off;
+}
+
+// Plan ranks: row ranges, hulls, halo, slices.  h_rp: host row_ptr of the rows
+// passed in (full matrix for virtual ranks).  hulls: 2 per rank (min,max col).
+static int plan_ranks(pbcg_handle *h, const pbcg_csr_local *A, const std::vector<int32_t> &h_rp,
+                      const std::vector<long long> &hulls, const std::vector<int64_t> &all_ranges) {
+    const int P = h->V > 1 ? h->V : 1;
+    h->R.assign(P, Rank());
+    std::vector<int64_t> begins(P + 1);
+    if (h->V > 1) pbcg_plan_partition(A->n_global, P, begins.data());
+    else { begins[0] = A->row_begin; begins[1] = A->row_end; }
+    // ranges of every (virtual or real) rank
+    const int PR = h->V > 1 ? P : h->nranks;
+    std::vector<int64_t> ranges(4 * PR);
+    if (h->V > 1) {
+        for (int v = 0; v < P; ++v) {
+            ranges[4 * v] = begins[v];
+            ranges[4 * v + 1] = begins[v + 1];
+            ranges[4 * v + 2] = hulls[2 * v];
+            ranges[4 * v + 3] = hulls[2 * v + 1];
+        }
+    } else {
+        ranges = all_ranges;
+    }
+    for (int v = 0; v < P; ++v) {
+        Rank &R = h->R[v];
+        const int me = h->V > 1 ? v : h->rank;
+        R.id = me;
+        R.rb = begins[v];
+        R.re = begins[v + 1];
+        R.n = R.re - R.rb;
+        R.recv_lo.resize(PR); R.recv_hi.resize(PR); R.send_lo.resize(PR); R.send_hi.resize(PR);
+        int64_t blo, bhi;
+        RC_TRY(pbcg_plan_halo(PR, me, ranges.data(), R.recv_lo.data(), R.recv_hi.data(), R.send_lo.data(),
+                              R.send_hi.data(), &blo, &bhi));
+        // align so that the owned part starts on a 32-byte boundary
+        const int64_t lead = R.rb - blo;
+        const int64_t lead_al = (lead + 3) & ~int64_t(3);
+        R.buf_lo = R.rb - lead_al;
+        R.buf_hi = bhi;
+        R.own_off = lead_al;
+        // sliced ELL: 32 rows per slice, width = longest row of the slice
+        R.nslices = (R.n + 31) / 32;
+        R.h_slice_off.assign(R.nslices + 1, 0);
+        const int64_t r0 = (h->V > 1) ? R.rb : 0;  // index into h_rp
+        for (int64_t sl = 0; sl < R.nslices; ++sl) {
+            int32_t wmax = 0;
+            const int64_t a = sl * 32, e = std::min<int64_t>(a + 32, R.n);
+            for (int64_t r = a; r < e; ++r) wmax = std::max(wmax, h_rp[r0 + r + 1] - h_rp[r0 + r]);
+            R.h_slice_off[sl + 1] = R.h_slice_off[sl] + 32 * (int64_t)wmax;
+        }
+        R.sell_nnz = R.h_slice_off[R.nslices];
+    }
+    return PBCG_OK;
+}
+
+static int compute_hulls(const pbcg_csr_local *A, int P, const std::vector<int64_t> &begins_local,
+                         std::vector<long long> &hulls) {
+    const int64_t nloc = A->row_end - A->row_begin;
+    hulls.assign(2 * P, 0);
+    for (int v = 0; v < P; ++v) { hulls[2 * v] = INT64_MAX; hulls[2 * v + 1] = INT64_MIN; }
+    if (nloc == 0) return PBCG_OK;
+    long long *d_h = nullptr;
+    int64_t *d_b = nullptr;
+    CUDA_TRY(cudaMalloc(&d_h, sizeof(long long) * 2 * P));
+    CUDA_TRY(cudaMalloc(&d_b, sizeof(int64_t) * (P + 1)));
+    CUDA_TRY(cudaMemcpy(d_h, hulls.data(), sizeof(long long) * 2 * P, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d_b, begins_local.data(), sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice));
+    const int grid = (int)std::min<int64_t>((nloc + 255) / 256, 4096);
+    row_hull_kernel<<<grid, 256>>>(nloc, A->row_ptr, A->col_idx, d_b, P, d_h);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpy(hulls.data(), d_h, sizeof(long long) * 2 * P, cudaMemcpyDeviceToHost));
+    cudaFree(d_h);
+    cudaFree(d_b);
+    return PBCG_OK;
+}
+
+static int validate_csr(const pbcg_csr_local *A, const pbcg_dist *d) {
+    if (!A) return PBCG_OK;
+    if (A->n_global < 1 || A->row_begin < 0 || A->row_end < A->row_begin || A->row_end > A->n_global)
+        return fail(PBCG_EINVAL, "csr: bad dimensions (n=%lld rows [%lld,%lld))", (long long)A->n_global,
+                    (long long)A->row_begin, (long long)A->row_end);
+    if (A->n_global > INT32_MAX) return fail(PBCG_EINVAL, "csr: n_global exceeds int32 column ids");
+    if ((A->row_end > A->row_begin) && (!A->row_ptr || (A->nnz_local > 0 && (!A->col_idx || !A->values))))
+        return fail(PBCG_EINVAL, "csr: null array");
+    if (d && d->virtual_ranks > 1 && (A->row_begin != 0 || A->row_end != A->n_global))
+        return fail(PBCG_EINVAL, "virtual ranks need the full matrix");
+    return PBCG_OK;
+}
+
+// Everything workspace_size and setup share: host row_ptr, hulls, plan.
+static int prepare(pbcg_handle *h, const pbcg_csr_local *A, const pbcg_dist *d, std::vector<int32_t> &h_rp,
+                   const std::vector<int64_t> *all_ranges) {
+    h->nranks = d ? std::max(1, d->nranks) : 1;
+    h->rank = d ? d->rank : 0;
+    h->V = (d && d->virtual_ranks > 1) ? d->virtual_ranks : 1;
+    h->hist_cap = (d && d->history_capacity > 0) ? d->history_capacity : 10001;
+    if (h->nranks > 1 && h->V > 1) return fail(PBCG_EINVAL, "virtual ranks need nranks == 1");
+    if (h->rank < 0 || h->rank >= h->nranks) return fail(PBCG_EINVAL, "bad rank");
+    if (!A) {
+        h->comm_only = true;
+        h->R.assign(h->V, Rank());
+        return PBCG_OK;
+    }
+    RC_TRY(validate_csr(A, d));
+    h->n_global = A->n_global;
+    const int64_t nloc = A->row_end - A->row_begin;
+    if (h->V > nloc) return fail(PBCG_EINVAL, "more virtual ranks than rows");
+    h_rp.resize(nloc + 1);
+    CUDA_TRY(cudaMemcpy(h_rp.data(), A->row_ptr, sizeof(int32_t) * (nloc + 1), cudaMemcpyDeviceToHost));
+    if (h_rp[0] != 0) return fail(PBCG_EINVAL, "csr: row_ptr[0] != 0");
+    for (int64_t r = 0; r < nloc; ++r)
+        if (h_rp[r + 1] < h_rp[r]) return fail(PBCG_EINVAL, "csr: row_ptr decreases at row %lld", (long long)r);
+    if (h_rp[nloc] != A->nnz_local) return fail(PBCG_EINVAL, "csr: nnz_local != row_ptr[n]");
+    const int P = h->V;
+    std::vector<int64_t> begins(P + 1);
+    if (P > 1) pbcg_plan_partition(nloc, P, begins.data());
+    else { begins[0] = 0; begins[1] = nloc; }
+    std::vector<long long> hulls;
+    RC_TRY(compute_hulls(A, P, begins, hulls));
+    std::vector<int64_t> ranges;
+    if (h->V == 1) {
+        if (all_ranges) ranges = *all_ranges;
+        else ranges = {A->row_begin, A->row_end, hulls[0], hulls[1]};  // local-only view (size query)
+    }
+    if (h->V == 1 && !all_ranges) {
+        // size query for one real rank: the buffer hull only depends on local rows
+        h->nranks = 1;
+        h->rank = 0;
+    }
+    return plan_ranks(h, A, h_rp, hulls, ranges);
+}
+
+static size_t total_size(pbcg_handle *h) {
+    Carver C{nullptr};
+    for (auto &R : h->R) carve_rank(C, R, h->hist_cap, h->comm_only);
+    return carve_handle_extra(C, h) + 256;
+}
+
+extern "C" int pbicgstab_workspace_size(const pbcg_csr_local *A, const pbcg_dist *d, size_t *bytes) {
+    if (!bytes) return fail(PBCG_EINVAL, "bytes == NULL");
+    pbcg_handle tmp;
+    std::vector<int32_t> h_rp;
+    RC_TRY(prepare(&tmp, A, d, h_rp, nullptr));
+    *bytes = total_size(&tmp);
+    return PBCG_OK;
+}
+
+static int grid_for(const void *kern, int bs, int nsm, size_t smem = 0) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, bs, smem) != cudaSuccess || occ < 1) occ = 1;
+    return occ * nsm;
+}
+
+// ----------------------------------------------------------------------------
+// halo exchange and cross-rank reduction
+// ----------------------------------------------------------------------------
+// padded buffer selector: 0 = z, 1 = w, 2 = x scratch
+static double *padbuf(Rank &R, int which) { return which == 0 ? R.zpad : which == 1 ? R.wpad : R.xpad; }
+
+static int halo(pbcg_handle *h, int which) {
+    const int P = (int)h->R.size();
+    if (h->V > 1) {
+        for (int me = 0; me < P; ++me) {
+            Rank &R = h->R[me];
+            for (int q = 0; q < P; ++q) {
+                const int64_t lo = R.recv_lo[q], hi = R.recv_hi[q];
+                if (hi <= lo) continue;
+                Rank &Q = h->R[q];
+                CUDA_TRY(cudaMemcpyAsync(padbuf(R, which) + (lo - R.buf_lo), padbuf(Q, which) + (lo - Q.buf_lo),
+                                         sizeof(double) * (hi - lo), cudaMemcpyDeviceToDevice, h->stream));
+            }
+        }
+        return PBCG_OK;
+    }
+    if (h->nranks == 1) return PBCG_OK;
+    Rank &R = h->R[0];
+    NCCL_TRY(g_nccl.GroupStart());
+    for (int q = 0; q < h->nranks; ++q) {
+        if (R.send_hi[q] > R.send_lo[q])
+            NCCL_TRY(g_nccl.Send(padbuf(R, which) + (R.send_lo[q] - R.buf_lo), (size_t)(R.send_hi[q] - R.send_lo[q]),
+                                 ncclFloat64, q, h->comm_halo, h->stream));
+        if (R.recv_hi[q] > R.recv_lo[q])
+            NCCL_TRY(g_nccl.Recv(padbuf(R, which) + (R.recv_lo[q] - R.buf_lo), (size_t)(R.recv_hi[q] - R.recv_lo[q]),
+                                 ncclFloat64, q, h->comm_halo, h->stream));
+    }
+    NCCL_TRY(g_nccl.GroupEnd());
+    return PBCG_OK;
+}
+
+// sum the phase-`ph` superaccumulators over ranks, then round + finalise
+template <int ND>
+static int reduce_finalize(pbcg_handle *h, int ph, int phase, cudaStream_t st, double *out, int32_t *oflags) {
+    const int words = ND * SACC_L + SACC_FLAGW;
+    if (h->V > 1) {
+        vallreduce_kernel<<<(words + 127) / 128, 128, 0, st>>>(h->vgacc + (size_t)ph * h->V, h->V, words);
+        CUDA_TRY(cudaGetLastError());
+    } else if (h->nranks > 1) {
+        NCCL_TRY(g_nccl.AllReduce(h->R[0].gacc[ph], h->R[0].gacc[ph], (size_t)words, ncclInt64, ncclSum, h->comm_red, st));
+    }
+    for (auto &R : h->R) {
+        finalize_kernel<ND><<<1, 128, 0, st>>>(R.gacc[ph], phase, R.sc, R.hist, out, oflags);
+        CUDA_TRY(cudaGetLastError());
+        out = nullptr;  // only the first (virtual) rank writes the exdot result
+        oflags = nullptr;
+    }
+    return PBCG_OK;
+}
+
+static bool multi(const pbcg_handle *h) { return h->V > 1 || h->nranks > 1; }
+
+static int launch_spmv(pbcg_handle *h, Rank &R, int mode, const double *xpad, double *y, const double *b, double *y2,
+                       bool predicated, cudaStream_t st) {
+    if (R.n == 0) return PBCG_OK;
+    const int grid = (int)((R.n + 255) / 256);
+    const Scalars *sc = predicated ? R.sc : nullptr;
+    if (mode == SPMV_PLAIN)
+        spmv_sell_kernel<SPMV_PLAIN, 8><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
+    else
+        spmv_sell_kernel<SPMV_RESID, 8><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
+    CUDA_TRY(cudaGetLastError());
+    return PBCG_OK;
+}
+
+// up-to-4 fused EXDOTs over every rank's rows (phase PH_INIT / PH_TRUE)
+static int multidot(pbcg_handle *h, int ph, int phase, int nd, const double *const *xs_per_rank[4],
+                    const double *const *ys_per_rank[4]) {
+    const bool fin = !multi(h);
+    for (size_t v = 0; v < h->R.size(); ++v) {
+        Rank &R = h->R[v];
+        MultiDotArgs a{};
+        a.n = R.n;
+        for (int d = 0; d < 4; ++d) {
+            a.x[d] = d < nd ? xs_per_rank[d][v] : nullptr;
+            a.y[d] = d < nd ? ys_per_rank[d][v] : nullptr;
+        }
+        a.sc = R.sc;
+        a.gacc = R.gacc[ph];
+        a.ticket = R.tickets + ph;
+        a.hist = R.hist;
+        a.phase = phase;
+        a.finalize = fin;
+        const int grid = std::max(1, std::min<int>(h->grid_md, (int)((R.n / 2 + K_BS - 1) / K_BS)));
+        if (nd == 4) multidot_kernel<4, K_NP, K_NE, K_BS><<<grid, K_BS, 0, h->stream>>>(a);
+        else multidot_kernel<1, K_NP, K_NE, K_BS><<<grid, K_BS, 0, h->stream>>>(a);
+        CUDA_TRY(cudaGetLastError());
+    }
+    if (!fin) {
+        if (nd == 4) RC_TRY(reduce_finalize<4>(h, ph, phase, h->stream, nullptr, nullptr));
+        else RC_TRY(reduce_finalize<1>(h, ph, phase, h->stream, nullptr, nullptr));
+    }
+    return PBCG_OK;
+}
+
+// ----------------------------------------------------------------------------
+// one iteration of Algorithm 2 (enqueue only)
+// ----------------------------------------------------------------------------
+static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
+    K2Args a{R.n, R.r, R.rh, R.w(), R.t, R.v, R.p, R.s, R.z(), R.q, R.y, R.sc, R.gacc[1], R.tickets + 1, R.hist, fin};
+    const int grid = std::max(1, std::min<int>(h->grid_k2, (int)((R.n / 2 + K_BS - 1) / K_BS)));
+    k2_kernel<K_NP, K_NE, K_BS><<<grid, K_BS, 0, st>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    return PBCG_OK;
+}
+
+static int launch_k3(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
+    K3Args a{R.n, R.rh, R.p, R.q, R.y, R.t, R.v, R.x, R.r, R.w(), R.sc, R.gacc[2], R.tickets + 2, R.hist, fin};
+    const int grid = std::max(1, std::min<int>(h->grid_k3, (int)((R.n / 2 + K_BS - 1) / K_BS)));
+    k3_kernel<K_NP, K_NE, K_BS><<<grid, K_BS, 0, st>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    return PBCG_OK;
+}
+
+static int enqueue_iteration(pbcg_handle *h) {
+    cudaStream_t st = h->stream;
+    if (!multi(h)) {  // single rank: 4 launches, dots rounded in the last CTA
+        Rank &R = h->R[0];
+        RC_TRY(launch_k2(h, R, 1, st));
+        RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.zpad, R.v, nullptr, nullptr, true, st));
+        RC_TRY(launch_k3(h, R, 1, st));
+        RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, true, st));
+        return PBCG_OK;
+    }
+    if (h->V > 1) {  // virtual ranks: same dataflow, serialised on one stream
+        for (auto &R : h->R) RC_TRY(launch_k2(h, R, 0, st));
+        RC_TRY(reduce_finalize<4>(h, 1, PH_A, st, nullptr, nullptr));
+        RC_TRY(halo(h, 0));
+        for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.zpad, R.v, nullptr, nullptr, true, st));
+        for (auto &R : h->R) RC_TRY(launch_k3(h, R, 0, st));
+        RC_TRY(reduce_finalize<3>(h, 2, PH_B, st, nullptr, nullptr));
+        RC_TRY(halo(h, 1));
+        for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, true, st));
+        return PBCG_OK;
+    }
+    // real ranks: phase allreduce on the side stream overlaps halo + SpMV (l.90)
+    Rank &R = h->R[0];
+    RC_TRY(launch_k2(h, R, 0, st));
+    CUDA_TRY(cudaEventRecord(h->ev[0], st));
+    CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev[0], 0));
+    RC_TRY(reduce_finalize<4>(h, 1, PH_A, h->side, nullptr, nullptr));
+    CUDA_TRY(cudaEventRecord(h->ev[1], h->side));
+    RC_TRY(halo(h, 0));
+    RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.zpad, R.v, nullptr, nullptr, true, st));
+    CUDA_TRY(cudaStreamWaitEvent(st, h->ev[1], 0));
+    RC_TRY(launch_k3(h, R, 0, st));
+    CUDA_TRY(cudaEventRecord(h->ev[2], st));
+    CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev[2], 0));
+    RC_TRY(reduce_finalize<3>(h, 2, PH_B, h->side, nullptr, nullptr));
+    CUDA_TRY(cudaEventRecord(h->ev[3], h->side));
+    RC_TRY(halo(h, 1));
+    RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, true, st));
+    CUDA_TRY(cudaStreamWaitEvent(st, h->ev[3], 0));
+    return PBCG_OK;
+}
+
+// ----------------------------------------------------------------------------
+// setup / destroy
+// ----------------------------------------------------------------------------
+extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void *stream, void *workspace,
+                               size_t workspace_bytes, pbcg_handle **out) {
+    if (!out) return fail(PBCG_EINVAL, "out == NULL");
+    *out = nullptr;
+    auto *h = new pbcg_handle();
+    std::unique_ptr<pbcg_handle> guard(h);
+    h->stream = (cudaStream_t)stream;
+    CUDA_TRY(cudaGetDevice(&h->dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->dev));
+    const int nranks = d ? std::max(1, d->nranks) : 1;
+    // communicators first: real ranks need the allgathered row ranges + hulls
+    std::vector<int64_t> all_ranges;
+    std::vector<int32_t> h_rp;
+    if (nranks > 1) {
+        if (!nccl_available()) return fail(PBCG_ENCCL, "nranks > 1 but libnccl.so.2 could not be loaded");
+        if (!d->nccl_uid) return fail(PBCG_EINVAL, "nranks > 1 needs nccl_uid");
+        ncclUniqueId uid;
+        memcpy(&uid, d->nccl_uid, sizeof(uid));
+        NCCL_TRY(g_nccl.CommInitRank(&h->comm_halo, nranks, uid, d->rank));
+        NCCL_TRY(g_nccl.CommInitRank(&h->comm_red, nranks, uid, d->rank));
+        // hull of my rows, then allgather (rb, re, cmin, cmax) of every rank
+        RC_TRY(validate_csr(A, d));
+        if (!A) return fail(PBCG_EINVAL, "nranks > 1 needs a matrix (comm-only handles are single-rank)");
+        int64_t mine[4] = {A->row_begin, A->row_end, 0, -1};
+        {
+            std::vector<int64_t> b1 = {0, A->row_end - A->row_begin};
+            std::vector<long long> hull;
+            RC_TRY(compute_hulls(A, 1, b1, hull));
+            if (hull[1] >= hull[0]) { mine[2] = hull[0]; mine[3] = hull[1]; }
+        }
+        int64_t *dbuf = nullptr;
+        CUDA_TRY(cudaMalloc(&dbuf, sizeof(int64_t) * 4 * (nranks + 1)));
+        CUDA_TRY(cudaMemcpy(dbuf, mine, sizeof(mine), cudaMemcpyHostToDevice));
+        NCCL_TRY(g_nccl.AllGather(dbuf, dbuf + 4, 4, ncclInt64, h->comm_red, h->stream));
+        CUDA_TRY(cudaStreamSynchronize(h->stream));
+        all_ranges.resize(4 * nranks);
+        CUDA_TRY(cudaMemcpy(all_ranges.data(), dbuf + 4, sizeof(int64_t) * 4 * nranks, cudaMemcpyDeviceToHost));
+        cudaFree(dbuf);
+        if (all_ranges[0] != 0 || all_ranges[4 * (nranks - 1) + 1] != A->n_global)
+            return fail(PBCG_EINVAL, "row blocks of the ranks do not cover [0, n_global)");
+    }
+    RC_TRY(prepare(h, A, d, h_rp, nranks > 1 ? &all_ranges : nullptr));
+    h->nranks = nranks;
+    h->rank = d ? d->rank : 0;
+    const size_t need = total_size(h);
+    h->ws_need = need;
+    if (!workspace || workspace_bytes < need)
+        return fail(PBCG_ENOMEM, "workspace too small: need %zu bytes, got %zu", need, workspace_bytes);
+    Carver C{(char *)(((uintptr_t)workspace + 255) & ~uintptr_t(255))};
+    for (auto &R : h->R) carve_rank(C, R, h->hist_cap, h->comm_only);
+    carve_handle_extra(C, h);
+    // zero reduction state
+    for (auto &R : h->R) {
+        for (int k = 0; k < NPH; ++k) CUDA_TRY(cudaMemsetAsync(R.gacc[k], 0, sizeof(long long) * GW4, h->stream));
+        CUDA_TRY(cudaMemsetAsync(R.tickets, 0, sizeof(unsigned) * 16, h->stream));
+        CUDA_TRY(cudaMemsetAsync(R.sc, 0, sizeof(Scalars), h->stream));
+        CUDA_TRY(cudaMemsetAsync(R.bad, 0, sizeof(int) * 4, h->stream));
+    }
+    {
+        std::vector<long long *> vg((size_t)NPH * h->V);
+        for (int ph = 0; ph < NPH; ++ph)
+            for (int v = 0; v < h->V; ++v) vg[(size_t)ph * h->V + v] = h->R[v].gacc[ph];
+        CUDA_TRY(cudaMemcpyAsync(h->vgacc, vg.data(), sizeof(long long *) * vg.size(), cudaMemcpyHostToDevice, h->stream));
+        CUDA_TRY(cudaStreamSynchronize(h->stream));
+    }
+    if (!h->comm_only) {
+        for (size_t v = 0; v < h->R.size(); ++v) {
+            Rank &R = h->R[v];
+            CUDA_TRY(cudaMemcpyAsync(R.slice_off, R.h_slice_off.data(), sizeof(int64_t) * (R.nslices + 1),
+                                     cudaMemcpyHostToDevice, h->stream));
+            CUDA_TRY(cudaMemsetAsync(R.zpad, 0, sizeof(double) * (R.buf_hi - R.buf_lo), h->stream));
+            CUDA_TRY(cudaMemsetAsync(R.wpad, 0, sizeof(double) * (R.buf_hi - R.buf_lo), h->stream));
+            CUDA_TRY(cudaMemsetAsync(R.xpad, 0, sizeof(double) * (R.buf_hi - R.buf_lo), h->stream));
+            if (R.n > 0) {
+                const int32_t *rp = A->row_ptr + (h->V > 1 ? R.rb : 0);
+                const int grid = (int)std::min<int64_t>((R.n + 255) / 256, 65535);
+                csr_to_sell_kernel<<<grid, 256, 0, h->stream>>>(R.n, rp, A->col_idx, A->values, A->n_global, R.buf_lo,
+                                                                R.slice_off, R.row_len, R.sval, R.scol, R.bad);
+                CUDA_TRY(cudaGetLastError());
+            }
+        }
+        CUDA_TRY(cudaStreamSynchronize(h->stream));
+        for (auto &R : h->R) {
+            int bad = 0;
+            CUDA_TRY(cudaMemcpy(&bad, R.bad, sizeof(int), cudaMemcpyDeviceToHost));
+            if (bad & 1) return fail(PBCG_EINVAL, "csr: column ids not strictly increasing / out of range");
+            if (bad & 2) return fail(PBCG_ENONFINITE, "csr: NaN/Inf value");
+        }
+    }
+    h->grid_k2 = grid_for((const void *)k2_kernel<K_NP, K_NE, K_BS>, K_BS, h->nsm);
+    h->grid_k3 = grid_for((const void *)k3_kernel<K_NP, K_NE, K_BS>, K_BS, h->nsm);
+    h->grid_md = grid_for((const void *)multidot_kernel<4, K_NP, K_NE, K_BS>, K_BS, h->nsm);
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    for (auto &e : h->ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreate(&h->t0));
+    CUDA_TRY(cudaEventCreate(&h->t1));
+    CUDA_TRY(cudaMallocHost(&h->h_sc, sizeof(Scalars)));
+    *out = guard.release();
+    return PBCG_OK;
+}
+
+extern "C" void pbicgstab_destroy(pbcg_handle *h) {
+    if (!h) return;
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    for (auto &e : h->ev)
+        if (e) cudaEventDestroy(e);
+    if (h->t0) cudaEventDestroy(h->t0);
+    if (h->t1) cudaEventDestroy(h->t1);
+    if (h->side) cudaStreamDestroy(h->side);
+    if (h->h_sc) cudaFreeHost(h->h_sc);
+    if (h->comm_halo && g_nccl.CommDestroy) g_nccl.CommDestroy(h->comm_halo);
+    if (h->comm_red && g_nccl.CommDestroy) g_nccl.CommDestroy(h->comm_red);
+    delete h;
+}
+
+// ----------------------------------------------------------------------------
+// vectors in/out (device or host pointers; virtual ranks: full vectors)
+// ----------------------------------------------------------------------------
+static bool is_host_ptr(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+}
+
+static int scatter_in(pbcg_handle *h, const double *src, double *Rank::*dst_member, bool host) {
+    for (auto &R : h->R) {
+        const int64_t off = h->V > 1 ? R.rb : 0;
+        CUDA_TRY(cudaMemcpyAsync(R.*dst_member, src + off, sizeof(double) * R.n,
+                                 host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, h->stream));
+    }
+    return PBCG_OK;
+}
+
+static int copy_own_to_pad(pbcg_handle *h, double *Rank::*src_member, int which) {
+    for (auto &R : h->R)
+        CUDA_TRY(cudaMemcpyAsync(padbuf(R, which) + R.own_off, R.*src_member, sizeof(double) * R.n,
+                                 cudaMemcpyDeviceToDevice, h->stream));
+    return PBCG_OK;
+}
+
+static void opts_defaults(const pbcg_opts *o, pbcg_opts &e) {
+    e.tol = 1e-10;
+    e.max_iter = 10000;
+    e.breakdown_eps = 1e-30;
+    e.poll_every = 16;
+    e.use_graphs = 1;
+    if (o) {
+        e = *o;
+        if (!(e.breakdown_eps > 0.0)) e.breakdown_eps = 1e-30;
+        if (e.poll_every <= 0) e.poll_every = 16;
+    }
+}
+
+// ----------------------------------------------------------------------------
+// start / iterate / finish / solve
+// ----------------------------------------------------------------------------
+extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0, const pbcg_opts *o) {
+    if (!h || h->comm_only) return fail(PBCG_EINVAL, "start: no matrix on this handle");
+    if (!b || !x0) return fail(PBCG_EINVAL, "start: b and x0 are required");
+    pbcg_opts op;
+    opts_defaults(o, op);
+    if (!(op.tol >= 0.0) || op.max_iter < 0) return fail(PBCG_EINVAL, "start: bad tol / max_iter");
+    h->max_iter = op.max_iter;
+    Scalars s0{};
+    s0.tol = op.tol;
+    s0.eps = op.breakdown_eps;
+    s0.max_iter = op.max_iter;
+    s0.hist_cap = h->hist_cap;
+    s0.status = ST_RUNNING;
+    for (auto &R : h->R) {
+        CUDA_TRY(cudaMemcpyAsync(R.sc, &s0, sizeof(Scalars), cudaMemcpyHostToDevice, h->stream));
+        CUDA_TRY(cudaMemsetAsync(R.hist, 0, sizeof(double) * (size_t)h->hist_cap * H_COLS, h->stream));
+        CUDA_TRY(cudaMemsetAsync(R.bad, 0, sizeof(int) * 4, h->stream));
+    }
+    RC_TRY(scatter_in(h, b, &Rank::b, is_host_ptr(b)));
+    RC_TRY(scatter_in(h, x0, &Rank::x, is_host_ptr(x0)));
+    for (auto &R : h->R) {
+        if (R.n == 0) continue;
+        const int grid = (int)std::min<int64_t>((R.n + 255) / 256, 4096);
+        nonfinite_scan_kernel<<<grid, 256, 0, h->stream>>>(R.n, R.b, R.bad);
+        nonfinite_scan_kernel<<<grid, 256, 0, h->stream>>>(R.n, R.x, R.bad);
+        CUDA_TRY(cudaGetLastError());
+    }
+    // I1: r0 := b - A x0 ; r^ := r0 ; w0 := A r0 ; t0 := A w0   (R-1)
+    RC_TRY(copy_own_to_pad(h, &Rank::x, 2));
+    RC_TRY(halo(h, 2));
+    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_RESID, R.xpad, R.r, R.b, R.rh, false, h->stream));
+    RC_TRY(copy_own_to_pad(h, &Rank::r, 2));
+    RC_TRY(halo(h, 2));
+    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.xpad, R.w(), nullptr, nullptr, false, h->stream));
+    RC_TRY(halo(h, 1));
+    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, false, h->stream));
+    // I2-I4: ||b||, rho0 = (r^,r0), delta0 = (r^,w0), (r0,r0); alpha0
+    std::vector<const double *> xb, yb, xr, yr, xw, yw, xn, yn;
+    for (auto &R : h->R) {
+        xb.push_back(R.b); yb.push_back(R.b);
+        xr.push_back(R.rh); yr.push_back(R.r);
+        xw.push_back(R.rh); yw.push_back(R.w());
+        xn.push_back(R.r); yn.push_back(R.r);
+    }
+    const double *const *xs[4] = {xb.data(), xr.data(), xw.data(), xn.data()};
+    const double *const *ys[4] = {yb.data(), yr.data(), yw.data(), yn.data()};
+    RC_TRY(multidot(h, 0, PH_INIT, 4, xs, ys));
+    CUDA_TRY(cudaMemcpyAsync(h->h_sc, h->R[0].sc, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    int bad = 0;
+    for (auto &R : h->R) {
+        int bb = 0;
+        CUDA_TRY(cudaMemcpy(&bb, R.bad, sizeof(int), cudaMemcpyDeviceToHost));
+        bad |= bb;
+    }
+    h->started = true;
+    if (bad & 2) return fail(PBCG_ENONFINITE, "start: NaN/Inf in b or x0");
+    if (h->h_sc->err) return fail(PBCG_EINVAL, "start: ||b|| = 0");
+    return PBCG_OK;
+}
+
+static int capture_chunk(pbcg_handle *h, int iters) {
+    if (h->gexec && h->g_iters == iters) return PBCG_OK;
+    if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+    cudaGraph_t g;
+    CUDA_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
+    int rc = PBCG_OK;
+    for (int k = 0; k < iters && rc == PBCG_OK; ++k) rc = enqueue_iteration(h);
+    cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    if (rc != PBCG_OK) return rc;
+    if (e != cudaSuccess) return fail(PBCG_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+    CUDA_TRY(cudaGraphInstantiate(&h->gexec, g, 0));
+    cudaGraphDestroy(g);
+    h->g_iters = iters;
+    return PBCG_OK;
+}
+
+static int iterate_impl(pbcg_handle *h, int32_t k, int chunk, bool graphs) {
+    if (graphs && h->stream == nullptr) graphs = false;  // cannot capture the legacy stream
+    while (k > 0) {
+        if (graphs && k >= chunk) {
+            RC_TRY(capture_chunk(h, chunk));
+            CUDA_TRY(cudaGraphLaunch(h->gexec, h->stream));
+            k -= chunk;
+        } else {
+            RC_TRY(enqueue_iteration(h));
+            k -= 1;
+        }
+    }
+    return PBCG_OK;
+}
+
+static int g_default_chunk = 16;
+
+extern "C" int pbicgstab_iterate(pbcg_handle *h, int32_t k) {
+    if (!h || !h->started) return fail(PBCG_EINVAL, "iterate before start");
+    if (k < 0) return fail(PBCG_EINVAL, "iterate: k < 0");
+    return iterate_impl(h, k, g_default_chunk, true);
+}
+
+static int true_residual(pbcg_handle *h) {
+    RC_TRY(copy_own_to_pad(h, &Rank::x, 2));
+    RC_TRY(halo(h, 2));
+    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_RESID, R.xpad, R.tmp, R.b, nullptr, false, h->stream));
+    std::vector<const double *> xt;
+    for (auto &R : h->R) xt.push_back(R.tmp);
+    const double *const *xs[4] = {xt.data(), nullptr, nullptr, nullptr};
+    const double *const *ys[4] = {xt.data(), nullptr, nullptr, nullptr};
+    return multidot(h, 3, PH_TRUE, 1, xs, ys);
+}
+
+extern "C" int pbicgstab_finish(pbcg_handle *h, double *x, pbcg_result *res) {
+    if (!h || !h->started) return fail(PBCG_EINVAL, "finish before start");
+    if (h->h_sc->err == 0) RC_TRY(true_residual(h));
+    CUDA_TRY(cudaMemcpyAsync(h->h_sc, h->R[0].sc, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
+    if (x) {
+        const bool host = is_host_ptr(x);
+        for (auto &R : h->R) {
+            const int64_t off = h->V > 1 ? R.rb : 0;
+            CUDA_TRY(cudaMemcpyAsync(x + off, R.x, sizeof(double) * R.n,
+                                     host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, h->stream));
+        }
+    }
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (res) {
+        const Scalars &s = *h->h_sc;
+        res->status = s.status == ST_RUNNING ? PBCG_MAXITER : s.status;
+        res->iterations = s.it;
+        res->relres_recursive = s.relres;
+        res->relres_true = s.relres_true;
+        res->history_rows = std::min(s.it + 1, h->hist_cap);
+        res->loop_seconds = 0.0;
+    }
+    return PBCG_OK;
+}
+
+extern "C" int pbicgstab_solve(pbcg_handle *h, const double *b, double *x, const pbcg_opts *o, pbcg_result *res) {
+    if (!h || h->comm_only) return fail(PBCG_EINVAL, "solve: no matrix on this handle");
+    if (!x) return fail(PBCG_EINVAL, "solve: x is required (in: x0)");
+    pbcg_opts op;
+    opts_defaults(o, op);
+    RC_TRY(pbicgstab_start(h, b, x, &op));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventRecord(h->t0, h->stream));
+    int done_iters = 0;
+    while (!h->h_sc->done && done_iters <= op.max_iter) {
+        const int chunk = op.poll_every;
+        RC_TRY(iterate_impl(h, chunk, chunk, op.use_graphs != 0));
+        done_iters += chunk;
+        CUDA_TRY(cudaMemcpyAsync(h->h_sc, h->R[0].sc, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_TRY(cudaStreamSynchronize(h->stream));
+    }
+    CUDA_TRY(cudaEventRecord(h->t1, h->stream));
+    CUDA_TRY(cudaEventSynchronize(h->t1));
+    CUDA_TRY(cudaEventElapsedTime(&ms, h->t0, h->t1));
+    RC_TRY(pbicgstab_finish(h, x, res));
+    if (res) res->loop_seconds = ms * 1e-3;
+    return PBCG_OK;
+}
+
+extern "C" int pbicgstab_history(pbcg_handle *h, double *out, int32_t max_rows, int32_t *rows) {
+    if (!h || h->comm_only || !out) return fail(PBCG_EINVAL, "history: bad arguments");
+    Scalars s;
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    CUDA_TRY(cudaMemcpy(&s, h->R[0].sc, sizeof(Scalars), cudaMemcpyDeviceToHost));
+    int nrow = std::min(std::min(s.it + 1, h->hist_cap), std::max(0, max_rows));
+    if (nrow > 0)
+        CUDA_TRY(cudaMemcpy(out, h->R[0].hist, sizeof(double) * H_COLS * nrow, cudaMemcpyDeviceToHost));
+    if (rows) *rows = nrow;
+    return PBCG_OK;
+}
+
+extern "C" int pbicgstab_spmv(pbcg_handle *h, const double *x, double *y) {
+    if (!h || h->comm_only || !x || !y) return fail(PBCG_EINVAL, "spmv: bad arguments");
+    for (auto &R : h->R) {
+        const int64_t off = h->V > 1 ? R.rb : 0;
+        CUDA_TRY(cudaMemcpyAsync(R.xpad + R.own_off, x + off, sizeof(double) * R.n, cudaMemcpyDeviceToDevice, h->stream));
+    }
+    RC_TRY(halo(h, 2));
+    for (auto &R : h->R) {
+        const int64_t off = h->V > 1 ? R.rb : 0;
+        RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.xpad, y + off, nullptr, nullptr, false, h->stream));
+    }
+    return PBCG_OK;
+}
+
+// ----------------------------------------------------------------------------
+// standalone EXDOT and the plain baseline dot
+// ----------------------------------------------------------------------------
+struct Scratch {
+    long long *gacc = nullptr;
+    unsigned *ticket = nullptr;
+    double *out = nullptr;
+    int32_t *flags = nullptr;
+    double *partials = nullptr;
+    unsigned *pticket = nullptr;
+    int grid1 = 0, gridp = 0;
+};
+static std::mutex g_scr_mu;
+static Scratch g_scr[64];
+
+static int scratch(Scratch **out) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_scr_mu);
+    Scratch &S = g_scr[dev & 63];
+    if (!S.gacc) {
+        int nsm = 148;
+        CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        S.grid1 = grid_for((const void *)multidot_kernel<1, K_NP, K_NE, K_BS>, K_BS, nsm);
+        S.gridp = grid_for((const void *)plain_dot_kernel<K_BS>, K_BS, nsm);
+        CUDA_TRY(cudaMalloc(&S.gacc, sizeof(long long) * (SACC_L + SACC_FLAGW)));
+        CUDA_TRY(cudaMalloc(&S.ticket, 64));
+        CUDA_TRY(cudaMalloc(&S.out, 64));
+        CUDA_TRY(cudaMalloc(&S.flags, 64));
+        CUDA_TRY(cudaMalloc(&S.partials, sizeof(double) * (S.gridp + 1)));
+        CUDA_TRY(cudaMalloc(&S.pticket, 64));
+        CUDA_TRY(cudaMemset(S.gacc, 0, sizeof(long long) * (SACC_L + SACC_FLAGW)));
+        CUDA_TRY(cudaMemset(S.ticket, 0, 64));
+        CUDA_TRY(cudaMemset(S.pticket, 0, 64));
+        CUDA_TRY(cudaDeviceSynchronize());
+    }
+    *out = &S;
+    return PBCG_OK;
+}
+
+extern "C" int exdot(pbcg_handle *h, int64_t n, const double *x, const double *y, double *result, int32_t *flags,
+                     int on_device, void *stream) {
+    if (n < 0 || !result || (n > 0 && (!x || !y))) return fail(PBCG_EINVAL, "exdot: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch *S = nullptr;
+    RC_TRY(scratch(&S));
+    double *out = on_device ? result : S->out;
+    int32_t *ofl = on_device ? flags : S->flags;
+    if (!h || (h->V == 1 && h->nranks == 1)) {
+        MultiDotArgs a{};
+        a.n = n;
+        a.x[0] = x;
+        a.y[0] = y;
+        a.sc = nullptr;
+        a.gacc = (h && !h->R.empty()) ? h->R[0].gacc[4] : S->gacc;
+        a.ticket = (h && !h->R.empty()) ? h->R[0].tickets + 4 : S->ticket;
+        a.phase = PH_EXDOT;
+        a.finalize = 1;
+        a.out = out;
+        a.out_flags = ofl;
+        const int grid = std::max(1, std::min<int>(S->grid1, (int)((n / 2 + K_BS - 1) / K_BS)));
+        multidot_kernel<1, K_NP, K_NE, K_BS><<<grid, K_BS, 0, st>>>(a);
+        CUDA_TRY(cudaGetLastError());
+    } else {
+        // distributed: each (virtual) rank reduces its slice, int64 allreduce, round once
+        const int P = (int)h->R.size();
+        for (int v = 0; v < P; ++v) {
+            const int64_t lo = (h->V > 1) ? n * v / P : 0, hi = (h->V > 1) ? n * (v + 1) / P : n;
+            MultiDotArgs a{};
+            a.n = hi - lo;
+            a.x[0] = x + lo;
+            a.y[0] = y + lo;
+            a.gacc = h->R[v].gacc[4];
+            a.ticket = h->R[v].tickets + 4;
+            a.phase = PH_EXDOT;
+            a.finalize = 0;
+            const int grid = std::max(1, std::min<int>(S->grid1, (int)(((hi - lo) / 2 + K_BS - 1) / K_BS)));
+            multidot_kernel<1, K_NP, K_NE, K_BS><<<grid, K_BS, 0, st>>>(a);
+            CUDA_TRY(cudaGetLastError());
+        }
+        RC_TRY(reduce_finalize<1>(h, 4, PH_EXDOT, st, out, ofl));
+    }
+    if (on_device) return PBCG_OK;
+    int32_t fl = 0;
+    CUDA_TRY(cudaMemcpyAsync(result, S->out, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&fl, S->flags, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (flags) *flags = fl;
+    if (fl & FLAG_NONFINITE) return fail(PBCG_ENONFINITE, "exdot: NaN/Inf input");
+    if (fl & FLAG_RANGE) return fail(PBCG_ERANGE, "exdot: product outside the exact zone (R-9) or overflow");
+    return PBCG_OK;
+}
+
+extern "C" int pbcg_dot_plain(int64_t n, const double *x, const double *y, double *result, void *stream) {
+    if (n < 0 || !result) return fail(PBCG_EINVAL, "dot_plain: bad arguments");
+    Scratch *S = nullptr;
+    RC_TRY(scratch(&S));
+    const int grid = std::max(1, std::min<int>(S->gridp, (int)((n / 2 + K_BS - 1) / K_BS)));
+    plain_dot_kernel<K_BS><<<grid, K_BS, 0, (cudaStream_t)stream>>>(n, x, y, S->partials, S->pticket, result);
+    CUDA_TRY(cudaGetLastError());
+    return PBCG_OK;
+}
+
+extern "C" const char *pbicgstab_last_error(void) { return g_err.c_str(); }
+
+extern "C" int pbcg_nccl_unique_id(uint8_t *out128) {
+    if (!out128) return fail(PBCG_EINVAL, "null");
+    if (!nccl_available()) return fail(PBCG_ENCCL, "libnccl.so.2 could not be loaded");
+    ncclUniqueId id;
+    NCCL_TRY(g_nccl.GetUniqueId(&id));
+    memcpy(out128, &id, sizeof(id));
+    return PBCG_OK;
+}
+
+extern "C" int pbcg_abi_version(void) { return PBCG_ABI_VERSION; }
+
+// Per-kernel device time of k more iterations (single rank): direct launches
+// bracketed by CUDA events on the handle's stream.  ms[0..3] = summed ms of
+// K2, SpMV(v=Az), K3, SpMV(t=Aw).  Same kernels and arguments as iterate().
+extern "C" int pbcg_profile_iterations(pbcg_handle *h, int32_t k, double *ms) {
+    if (!h || !h->started || k < 1 || !ms) return fail(PBCG_EINVAL, "profile: bad arguments");
+    if (multi(h)) return fail(PBCG_EINVAL, "profile: single-rank handles only");
+    std::vector<cudaEvent_t> ev((size_t)5 * k);
+    for (auto &e : ev) CUDA_TRY(cudaEventCreate(&e));
+    Rank &R = h->R[0];
+    cudaStream_t st = h->stream;
+    int rc = PBCG_OK;
+    for (int i = 0; i < k && rc == PBCG_OK; ++i) {
+        cudaEvent_t *e = &ev[(size_t)5 * i];
+        cudaEventRecord(e[0], st);
+        rc = launch_k2(h, R, 1, st);
+        cudaEventRecord(e[1], st);
+        if (rc == PBCG_OK) rc = launch_spmv(h, R, SPMV_PLAIN, R.zpad, R.v, nullptr, nullptr, true, st);
+        cudaEventRecord(e[2], st);
+        if (rc == PBCG_OK) rc = launch_k3(h, R, 1, st);
+        cudaEventRecord(e[3], st);
+        if (rc == PBCG_OK) rc = launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, true, st);
+        cudaEventRecord(e[4], st);
+    }
+    cudaError_t se = cudaStreamSynchronize(st);
+    for (int j = 0; j < 4; ++j) ms[j] = 0.0;
+    for (int i = 0; i < k && rc == PBCG_OK && se == cudaSuccess; ++i)
+        for (int j = 0; j < 4; ++j) {
+            float t = 0.f;
+            cudaEventElapsedTime(&t, ev[(size_t)5 * i + j], ev[(size_t)5 * i + j + 1]);
+            ms[j] += t;
+        }
+    for (auto &e : ev) cudaEventDestroy(e);
+    if (se != cudaSuccess) return fail(PBCG_ECUDA, "profile: %s", cudaGetErrorString(se));
+    return rc;
+}
+
+// kernel tuning knobs for benchmarks (not part of the numerical contract)
+extern "C" int pbcg_set_chunk(int32_t iters) {
+    if (iters < 1) return fail(PBCG_EINVAL, "chunk < 1");
+    g_default_chunk = iters;
+    return PBCG_OK;
+}

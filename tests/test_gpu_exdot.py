@@ -1,0 +1,147 @@
+"""GPU parity: the CUDA ExBLAS dot (through the C ABI `exdot`) against the
+oracle's EXDOT, bit for bit (BASELINE.json north_star: "The GPU ExBLAS dots
+must match it bit-exactly")."""
+import math
+import struct
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(v):
+    return struct.unpack("<Q", struct.pack("<d", v))[0]
+
+
+@pytest.fixture(scope="module")
+def pb():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_2404_13216_b200 as pb
+    return pb
+
+
+def gpu_exdot(pb, x, y, handle=None):
+    import torch
+    xt = torch.from_numpy(np.ascontiguousarray(x, np.float64)).cuda()
+    yt = torch.from_numpy(np.ascontiguousarray(y, np.float64)).cuda()
+    return pb.exdot(xt, yt, handle=handle)
+
+
+def check(pb, x, y, handle=None):
+    want, wf = oracle.exdot(x, y)
+    got, gf = gpu_exdot(pb, x, y, handle)
+    assert bool(wf & oracle.F_NONFINITE) == bool(gf & pb.FLAG_NONFINITE)
+    assert bool(wf & oracle.F_RANGE) == bool(gf & pb.FLAG_RANGE), (wf, gf)
+    if wf == 0:
+        assert bits(got) == bits(want), (len(x), got, want)
+    return got
+
+
+def test_spec_examples(pb):
+    assert gpu_exdot(pb, [1e16, 1.0, -1e16], [1, 1, 1]) == (1.0, 0)
+    v, f = gpu_exdot(pb, [], [])
+    assert bits(v) == bits(0.0) and f == 0
+    v, _ = gpu_exdot(pb, [-0.0, 3.0, -3.0], [1.0, 1.0, 1.0])
+    assert bits(v) == bits(0.0)
+    assert gpu_exdot(pb, np.full(10 ** 6, 0.1), np.ones(10 ** 6))[0] == 100000.0
+    assert gpu_exdot(pb, [1.0, 2.0 ** -53], [1, 1])[0] == 1.0
+    assert gpu_exdot(pb, [1.0 + 2.0 ** -52, 2.0 ** -53], [1, 1])[0] == 1.0 + 2.0 ** -51
+    for i in range(5):
+        for j in range(5):
+            assert gpu_exdot(pb, np.eye(5)[i], np.eye(5)[j])[0] == (1.0 if i == j else 0.0)
+
+
+def test_edge_values(pb):
+    u = 2.0 ** -52
+    check(pb, [(1 + u) * 2.0 ** -480, -(1 + 2 * u) * 2.0 ** -480], [(1 + u) * 2.0 ** -480, 2.0 ** -480])
+    # range zone and non-finite flags mirror the oracle (R-9)
+    check(pb, [2.0 ** -1074], [1.0])
+    check(pb, [2.0 ** -480], [2.0 ** -481])
+    check(pb, [2.0 ** 500], [2.0 ** 500])
+    check(pb, [0.0, 2.0 ** -1074], [2.0 ** -1074, 0.0])
+    check(pb, [1.0, math.nan], [1.0, 1.0])
+    check(pb, [math.inf, 1.0], [0.0, 1.0])
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 32, 33, 255, 256, 257, 511, 1000, 4097, 65537, 1 << 18, (1 << 20) + 3])
+def test_sizes_ragged(pb, n):
+    # spans several tiles, odd lengths exercise the scalar tail and the
+    # unaligned path
+    x = gen.uniform(n, 1)
+    y = gen.uniform(n, 2)
+    check(pb, x, y)
+    check(pb, x[1:], y[1:])  # 8-byte misaligned start
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_distributions(pb, seed):
+    n = 5000 + 777 * seed
+    kind = seed % 4
+    if kind == 0:
+        x, y = gen.loguniform(n, seed, -100, 100), gen.loguniform(n, seed + 99, -100, 100)
+    elif kind == 1:
+        x, y = gen.ill_pair(n - n % 2, seed=seed, block=1024)
+    elif kind == 2:  # heavy cancellation
+        x = gen.uniform(n, seed) * 2.0 ** 40
+        x = np.concatenate([x, -x, gen.uniform(7, seed)])
+        y = np.concatenate([gen.uniform(n, seed + 1), gen.uniform(n, seed + 1), gen.uniform(7, seed + 3)])
+    else:  # sparse-ish vectors with exact zeros (like r0 of the stencil configs)
+        x = gen.uniform(n, seed)
+        x[::3] = 0.0
+        y = gen.uniform(n, seed + 5)
+    check(pb, x, y)
+
+
+def test_permutation_invariance(pb):
+    x, y = gen.ill_pair(1 << 16, seed=21, block=1 << 14)
+    ref = bits(gpu_exdot(pb, x, y)[0])
+    rng = np.random.default_rng(0)
+    for _ in range(5):
+        p = rng.permutation(x.size)
+        assert bits(gpu_exdot(pb, x[p], y[p])[0]) == ref
+
+
+@pytest.mark.parametrize("kind", ["well", "ill"])
+def test_full_size_2_26(pb, kind):
+    # BASELINE.json configs[1] at n = 2^26, in the launch configuration bench.py times
+    n = 1 << 26
+    if kind == "well":
+        x, y = gen.uniform(n, 1), gen.uniform(n, 2)
+    else:
+        x, y = gen.ill_pair(n, seed=3)
+    check(pb, x, y)
+
+
+def test_virtual_rank_partition_invariance(pb):
+    # the cross-rank path (per-rank superaccumulators, int64 sum, one rounding)
+    # on one GPU: identical bits for 1..8 virtual ranks
+    import torch
+    x, y = gen.ill_pair(1 << 17, seed=5, block=1 << 12)
+    want = oracle.exdot(x, y)[0]
+    A = gen.stencil(2, 16, 10.0)
+    for V in (2, 3, 4, 8):
+        S = pb.Solver(A.row_ptr, A.col, A.val, A.n, virtual_ranks=V)
+        got, f = gpu_exdot(pb, x, y, handle=S)
+        assert f == 0 and bits(got) == bits(want), V
+        S.close()
+
+
+def test_on_device_result_and_plain_dot(pb):
+    import torch
+    n = 1 << 20
+    x = torch.from_numpy(gen.uniform(n, 7)).cuda()
+    y = torch.from_numpy(gen.uniform(n, 8)).cuda()
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    fl = torch.zeros(1, dtype=torch.int32, device="cuda")
+    pb.exdot(x, y, on_device=True, out=out, flags_out=fl)
+    torch.cuda.synchronize()
+    want = oracle.exdot(x.cpu().numpy(), y.cpu().numpy())[0]
+    assert bits(out.item()) == bits(want) and fl.item() == 0
+    p = pb.dot_plain(x, y)
+    torch.cuda.synchronize()
+    assert abs(p.item() - want) <= 1e-12 * float(torch.sum(torch.abs(x * y)))

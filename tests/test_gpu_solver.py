@@ -1,0 +1,221 @@
+"""GPU parity of SpMV and of the whole p-BiCGStab trajectory against the
+oracle (BASELINE.json north_star: "The full p-BiCGStab iterate trajectory must
+be bit-exact against the oracle and identical at 1/2/4/8 GPUs")."""
+import struct
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def u64(a):
+    return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+@pytest.fixture(scope="module")
+def pb():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_2404_13216_b200 as pb
+    return pb
+
+
+def solver(pb, A, **kw):
+    return pb.Solver(A.row_ptr, A.col, A.val, A.n, **kw)
+
+
+def gpu_b(pb, S, A):
+    """b := A*ones with the GPU SpMV (stencils), or the generated b."""
+    import torch
+    if A.rhs == "given":
+        return torch.from_numpy(A.b).cuda()
+    return S.spmv(torch.ones(A.n, dtype=torch.float64, device="cuda"))
+
+
+# ------------------------------------------------------------------- SpMV ---
+
+@pytest.mark.parametrize("name", ["c1_2d64", "small3d", "rand", "dense", "c3_3d128"])
+def test_spmv_bitwise(pb, name):
+    import torch
+    A = {"c1_2d64": lambda: gen.make_config("c1_2d64"),
+         "small3d": lambda: gen.stencil(3, 21, 100.0),
+         "rand": lambda: gen.random_banded(50_001, seed=3, band=2000),
+         "dense": lambda: gen.dense_as_sparse(97, seed=4, density=0.3),
+         "c3_3d128": lambda: gen.make_config("c3_3d128")}[name]()
+    S = solver(pb, A)
+    for seed in (1, 2):
+        x = gen.loguniform(A.n, seed, -20, 20)
+        y = S.spmv(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert np.array_equal(u64(y), u64(oracle.spmv(A, x))), name
+    ones = S.spmv(torch.ones(A.n, dtype=torch.float64, device="cuda")).cpu().numpy()
+    assert np.array_equal(u64(ones), u64(oracle.spmv(A, np.ones(A.n))))
+    S.close()
+
+
+def test_spmv_virtual_ranks(pb):
+    import torch
+    A = gen.random_banded(30_000, seed=8, band=3000)
+    x = gen.uniform(A.n, 5)
+    want = u64(oracle.spmv(A, x))
+    for V in (2, 3, 8):
+        S = solver(pb, A, virtual_ranks=V)
+        y = S.spmv(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert np.array_equal(u64(y), want), V
+        S.close()
+
+
+def test_spmv_empty_rows_and_signed_zero(pb):
+    import torch
+    A = gen.CSR(40, np.array([0] + [1] * 20 + [2] * 20, np.int32), np.array([0, 39], np.int32),
+                np.array([1.0, -1.0]))
+    S = solver(pb, A)
+    x = np.zeros(40)
+    x[0] = -0.0
+    y = S.spmv(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(u64(y), u64(oracle.spmv(A, x)))
+    S.close()
+
+
+def test_setup_rejects_bad_csr(pb):
+    A = gen.from_dense(np.eye(4))
+    bad = gen.CSR(4, A.row_ptr.copy(), A.col.copy(), A.val.copy())
+    bad.val[2] = np.nan
+    with pytest.raises(pb.PbcgError) as e:
+        solver(pb, bad)
+    assert e.value.rc == 5
+    bad = gen.CSR(4, np.array([0, 2, 3, 4, 5], np.int32), np.array([1, 0, 2, 3, 3], np.int32), np.ones(5))
+    with pytest.raises(pb.PbcgError) as e:
+        solver(pb, bad)
+    assert e.value.rc == 1
+
+
+# ------------------------------------------------------------- trajectory ---
+
+def run_both(pb, A, tol, max_iter, steps=None, **kw):
+    import torch
+    S = solver(pb, A, history_capacity=max_iter + 1, **{k: v for k, v in kw.items() if k == "virtual_ranks"})
+    b = gpu_b(pb, S, A)
+    O = oracle.PBiCGStab(A, b=None if A.rhs != "given" else A.b, tol=tol, max_iter=max_iter)
+    assert O.rc == 0
+    assert np.array_equal(u64(b.cpu().numpy()), u64(O.vec("b")))
+    O.run(steps)
+    if steps is None:
+        x, r = S.solve(b, tol=tol, max_iter=max_iter, poll_every=kw.get("poll_every", 16),
+                       use_graphs=kw.get("use_graphs", True))
+    else:
+        S.start(b, tol=tol, max_iter=max_iter)
+        S.iterate(steps)
+        x = torch.zeros(A.n_local if hasattr(A, "n_local") else A.n, dtype=torch.float64, device="cuda")
+        r = S.finish(x)
+    H = S.history()
+    S.close()
+    return S, O, x.cpu().numpy(), r, H
+
+
+def assert_same(O, x, r, H, A):
+    Ho = O.history()
+    assert r.iterations == O.iterations, (r.iterations, O.iterations)
+    st = O.status if O.status != oracle.RUNNING else oracle.MAXITER
+    assert r.status == st, (r.status, O.status)
+    assert H.shape == Ho.shape
+    bad = np.argwhere(u64(H) != u64(Ho))
+    assert bad.size == 0, f"first differing (row, col): {bad[:5].tolist()} gpu={H[tuple(bad[0])]!r} oracle={Ho[tuple(bad[0])]!r}"
+    assert np.array_equal(u64(x), u64(O.vec("x")))
+
+
+def test_c1_to_convergence(pb):
+    # BASELINE.json configs[0], full trajectory, final x bits, true residual
+    A = gen.make_config("c1_2d64")
+    S, O, x, r, H = run_both(pb, A, tol=1e-10, max_iter=500)
+    assert r.status == pb.CONVERGED
+    assert_same(O, x, r, H, A)
+    tr, _ = oracle.true_relres(A, O.vec("b"), O.vec("x"))
+    assert struct.pack("<d", r.relres_true) == struct.pack("<d", tr)
+    # north_star: agrees with a plain-double BiCGStab within 1e-10
+    st, it, xb, _ = oracle.bicgstab(A, O.vec("b"), tol=1e-10, max_iter=500)
+    assert st == oracle.CONVERGED
+    assert abs(r.relres_true - oracle.true_relres(A, O.vec("b"), xb)[0]) <= 1e-10
+
+
+@pytest.mark.parametrize("V", [2, 3, 4, 8])
+def test_c1_virtual_ranks_identical(pb, V):
+    A = gen.make_config("c1_2d64")
+    S, O, x, r, H = run_both(pb, A, tol=1e-10, max_iter=500, virtual_ranks=V)
+    assert_same(O, x, r, H, A)
+
+
+def test_graphs_and_chunking_do_not_change_bits(pb):
+    A = gen.stencil(3, 20, 100.0)
+    ref = None
+    for use_graphs, poll in [(True, 16), (False, 1), (True, 7)]:
+        S, O, x, r, H = run_both(pb, A, tol=1e-10, max_iter=2000, use_graphs=use_graphs, poll_every=poll)
+        assert_same(O, x, r, H, A)
+        if ref is None:
+            ref = (x, H)
+        assert np.array_equal(u64(ref[0]), u64(x)) and np.array_equal(u64(ref[1]), u64(H))
+
+
+def test_small3d_and_random_to_convergence(pb):
+    for A in (gen.stencil(3, 24, 100.0), gen.random_banded(20_000, seed=9, band=1500)):
+        S, O, x, r, H = run_both(pb, A, tol=1e-10, max_iter=3000)
+        assert r.status == pb.CONVERGED, A.name
+        assert_same(O, x, r, H, A)
+
+
+@pytest.mark.parametrize("name,steps", [("c3_3d128", 6), ("c4_small", 4)])
+def test_full_size_first_iterations(pb, name, steps):
+    # full-size configs: first K iterations bit-exact plus the state after them
+    A = gen.make_config("c3_3d128") if name == "c3_3d128" else gen.random_banded(1 << 19, seed=42)
+    S, O, x, r, H = run_both(pb, A, tol=1e-10, max_iter=10000, steps=steps)
+    assert r.iterations == steps
+    assert_same(O, x, r, H, A)
+
+
+def test_diag2_and_breakdowns(pb):
+    import torch
+    # 1x1 diag(2), b = [2] -> one step, x = [1]
+    A = gen.from_dense(np.array([[2.0]]))
+    S = solver(pb, A)
+    x, r = S.solve(torch.tensor([2.0], dtype=torch.float64, device="cuda"), tol=1e-10, max_iter=10)
+    assert r.status == pb.CONVERGED and r.iterations == 1 and x.item() == 1.0
+    S.close()
+    # breakdown at init: (r0, A r0) = 0
+    A = gen.from_dense(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    S = solver(pb, A)
+    x, r = S.solve(torch.tensor([1.0, 0.0], dtype=torch.float64, device="cuda"), tol=1e-10, max_iter=10)
+    assert r.status == pb.BREAKDOWN_INIT and r.iterations == 0
+    # ||b|| = 0 -> EINVAL; NaN in b -> ENONFINITE
+    with pytest.raises(pb.PbcgError) as e:
+        S.solve(torch.zeros(2, dtype=torch.float64, device="cuda"))
+    assert e.value.rc == 1
+    with pytest.raises(pb.PbcgError) as e:
+        S.solve(torch.tensor([1.0, float("nan")], dtype=torch.float64, device="cuda"))
+    assert e.value.rc == 5
+    S.close()
+
+
+def test_random_small_systems_match_oracle(pb):
+    for k in range(12):
+        n = 4 + 5 * k
+        A = gen.dense_as_sparse(n, seed=100 + k, density=0.5)
+        A.rhs = "given"
+        A.b = gen.uniform(n, 200 + k)
+        S, O, x, r, H = run_both(pb, A, tol=1e-10, max_iter=500)
+        assert_same(O, x, r, H, A)
+
+
+def test_host_buffers_end_to_end(pb):
+    # the e2e path: host b/x through the C ABI (staged inside the call)
+    import torch
+    A = gen.make_config("c1_2d64")
+    S = solver(pb, A)
+    b = S.spmv(torch.ones(A.n, dtype=torch.float64, device="cuda"))
+    xd, rd = S.solve(b, tol=1e-10, max_iter=500)
+    xh, rh = S.solve(b.cpu().numpy(), tol=1e-10, max_iter=500)
+    assert isinstance(xh, np.ndarray)
+    assert rd.iterations == rh.iterations and np.array_equal(u64(xd.cpu().numpy()), u64(xh))
+    S.close()
