@@ -204,7 +204,7 @@ def run_gpu(args, rank, world, local_rank, dist):
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         tw0 = time.time()
         f0.record(S.stream)
-        x, r = S.solve(bh, x0=xh, tol=1e-10, max_iter=args.e2e_max_iter, poll_every=32)
+        x, r = S.solve(bh, x0=xh, tol=1e-10, max_iter=args.e2e_max_iter or args.steps, poll_every=32)
         f1.record(S.stream)
         torch.cuda.synchronize()
         tw1 = time.time()
@@ -347,7 +347,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the exdot microbench and the CPU baseline")
     ap.add_argument("--dot-log2", type=int, default=26)
-    ap.add_argument("--e2e-max-iter", type=int, default=2000)
+    ap.add_argument("--e2e-max-iter", type=int, default=0, help="0: --steps")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-budget", type=float, default=90.0)
     args = ap.parse_args()

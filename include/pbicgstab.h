@@ -166,6 +166,9 @@ int pbicgstab_spmv(pbcg_handle *h, const double *x_local, double *y_local);
  * NULL) are device pointers, the call is stream-ordered on `stream` and
  * returns PBCG_OK; = 0: host pointers, the call synchronises and returns
  * PBCG_ERANGE / PBCG_ENONFINITE when flagged (result still written).
+ * flags: bit 1 (2) = some input is NaN/Inf; otherwise bit 0 (1) = some
+ * nonzero product has |fl(x*y)| < 2^-960 or >= 2^1000 (R-9) or the
+ * rounded sum overflowed.  When bit 1 is set, bit 0 is unspecified.
  * n_local = 0 gives +0.0. */
 int exdot(pbcg_handle *h, int64_t n_local, const double *x, const double *y, double *result, int32_t *flags,
           int result_on_device, void *stream);

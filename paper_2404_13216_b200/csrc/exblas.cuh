@@ -48,6 +48,13 @@ __device__ __forceinline__ void two_sum(double a, double b, double &s, double &e
 }
 
 __device__ __forceinline__ bool is_nonzero(double v) { return (__double_as_longlong(v) << 1) != 0; }
+__device__ __forceinline__ bool is_zero(double v) { return (__double_as_longlong(v) << 1) == 0; }
+__device__ __forceinline__ bool any_nonzero(const double *v, int n) {
+    unsigned long long acc = 0;
+#pragma unroll
+    for (int i = 0; i < n; ++i) acc |= (unsigned long long)__double_as_longlong(v[i]) << 1;
+    return acc != 0;
+}
 
 __host__ __device__ __forceinline__ double bits_to_double(unsigned long long b) {
 #ifdef __CUDA_ARCH__
@@ -96,8 +103,9 @@ __host__ __device__ __forceinline__ bool sacc_split(double v, int &i, long long 
     return true;
 }
 
-// Deposit a finite double into a superaccumulator in shared memory.
-__device__ __forceinline__ void sacc_deposit(unsigned long long *acc, double v) {
+// Deposit a finite double into a superaccumulator in shared memory (the
+// rare path: kept out of line so the streaming loops stay small).
+__device__ __noinline__ void sacc_deposit(unsigned long long *acc, double v) {
     int i;
     long long c0, c1, c2;
     if (!sacc_split(v, i, c0, c1, c2)) return;
@@ -202,6 +210,19 @@ struct Fpe {
         }
         return v;
     }
+    // same, but stops once the carried value is zero in every lane of the
+    // warp (warp-uniform branch; all 32 lanes must be active)
+    __device__ __forceinline__ double add_early(double v) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            if (i >= 2 && !__any_sync(0xFFFFFFFFu, is_nonzero(v))) break;
+            double s, e;
+            two_sum(a[i], v, s, e);
+            a[i] = s;
+            v = e;
+        }
+        return v;
+    }
 };
 
 // Range rule (R-9): with x,y != 0, flag when |fl(x*y)| < 2^-960 or
@@ -223,15 +244,17 @@ struct ExAcc {
         P.zero();
         E.zero();
     }
-    // acc += x*y exactly; residuals go to the shared superaccumulator `sacc`
+    // acc += x*y exactly; residuals go to the shared superaccumulator `sacc`.
+    // EARLY (warp-uniform early exit) requires all 32 lanes to be active.
+    template <bool EARLY = true>
     __device__ __forceinline__ void add(double x, double y, unsigned long long *sacc, unsigned &flags) {
         const double p = __dmul_rn(x, y);
         const double e = __fma_rn(x, y, -p);
         const unsigned ep = (unsigned)(__double2hiint(p) >> 20) & 0x7FFu;
         if (ep - 63u >= 1960u) flags |= range_class(x, y);
-        double r = P.add(p);
+        double r = EARLY ? P.add_early(p) : P.add(p);
         if (is_nonzero(r)) sacc_deposit(sacc, r);
-        r = E.add(e);
+        r = EARLY ? E.add_early(e) : E.add(e);
         if (is_nonzero(r)) sacc_deposit(sacc, r);
     }
     // merge the lanes of the warp into lane 0 (tree: at step `off` lanes
@@ -265,6 +288,98 @@ struct ExAcc {
 #pragma unroll
             for (int j = 0; j < NE; ++j)
                 if (is_nonzero(E.a[j])) sacc_deposit(sacc, E.a[j]);
+        }
+    }
+};
+
+// Three-tier accumulator used by the streaming kernels: P and E take the
+// rounded products and their errors (NP/NE levels, branch-free); whatever
+// falls out of them (values far below the running sums, e.g. the ~1e-16
+// interior entries of b = A*ones next to O(1) boundary entries) cascades into
+// the overflow expansion O, anchored at its own scale; only O's residual is
+// deposited into the shared superaccumulator.  All steps are exact TwoSums.
+template <int NP, int NE, int NO>
+struct ExAcc3 {
+    Fpe<NP> P;
+    Fpe<NE> E;
+    Fpe<NO> O;
+    __device__ __forceinline__ void zero() {
+        P.zero();
+        E.zero();
+        O.zero();
+    }
+    __device__ __forceinline__ void overflow(double rp, double re, unsigned long long *sacc) {
+        double r = O.add(rp);
+        if (is_nonzero(r)) sacc_deposit(sacc, r);
+        r = O.add(re);
+        if (is_nonzero(r)) sacc_deposit(sacc, r);
+    }
+    // Branch-free part of one product: TwoProd, the R-9 range flag, P and E
+    // cascades.  rp/re are what fell out of P/E (exact); the caller batches
+    // the rare spill decision over several products (one warp vote).
+    // zero_op: x or y is +-0 (then p = e = 0 and the product is never flagged
+    // unless an operand is non-finite).
+    __device__ __forceinline__ void step(double x, double y, bool zero_op, double &rp, double &re,
+                                         unsigned &flags) {
+        const double p = __dmul_rn(x, y);
+        const double e = __fma_rn(x, y, -p);
+        const unsigned ep = (unsigned)(__double2hiint(p) >> 20) & 0x7FFu;
+        flags |= (((ep - 63u) >= 1960u) & !zero_op) | (ep == 0x7FFu);
+        rp = P.add(p);
+        re = E.add(e);
+    }
+    __device__ __forceinline__ void spill(double rp, double re, unsigned long long *sacc) {
+        if (is_nonzero(rp) | is_nonzero(re)) overflow(rp, re, sacc);
+    }
+    // EARLY: the overflow branch is taken warp-uniformly (all 32 lanes active)
+    template <bool EARLY = true>
+    __device__ __forceinline__ void add(double x, double y, unsigned long long *sacc, unsigned &flags) {
+        const double p = __dmul_rn(x, y);
+        const double e = __fma_rn(x, y, -p);
+        const unsigned ep = (unsigned)(__double2hiint(p) >> 20) & 0x7FFu;
+        if (ep - 63u >= 1960u) flags |= range_class(x, y);
+        const double rp = P.add(p);
+        const double re = E.add(e);
+        const bool spill = is_nonzero(rp) | is_nonzero(re);
+        if (EARLY) {
+            if (__any_sync(0xFFFFFFFFu, spill)) overflow(rp, re, sacc);
+        } else if (spill) {
+            overflow(rp, re, sacc);
+        }
+    }
+    template <int N>
+    __device__ __forceinline__ static void merge_fpe(Fpe<N> &F, int off, bool recv, unsigned long long *sacc) {
+        double in[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) in[j] = __shfl_down_sync(0xFFFFFFFFu, F.a[j], off);
+        if (recv) {
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                double r = F.add(in[j]);
+                if (is_nonzero(r)) sacc_deposit(sacc, r);
+            }
+        }
+    }
+    // merge the lanes of the warp into lane 0, which deposits its terms
+    __device__ __forceinline__ void warp_merge(unsigned long long *sacc) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            const bool recv = lane < off;
+            merge_fpe<NP>(P, off, recv, sacc);
+            merge_fpe<NE>(E, off, recv, sacc);
+            merge_fpe<NO>(O, off, recv, sacc);
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int j = 0; j < NP; ++j)
+                if (is_nonzero(P.a[j])) sacc_deposit(sacc, P.a[j]);
+#pragma unroll
+            for (int j = 0; j < NE; ++j)
+                if (is_nonzero(E.a[j])) sacc_deposit(sacc, E.a[j]);
+#pragma unroll
+            for (int j = 0; j < NO; ++j)
+                if (is_nonzero(O.a[j])) sacc_deposit(sacc, O.a[j]);
         }
     }
 };

@@ -123,7 +123,8 @@ __device__ void phase_finalize(int phase, Scalars *sc, const double *d, unsigned
 // finalise (single rank) or leave normalised words for the allreduce.
 template <int ND>
 __device__ void last_cta_finish(CtaSacc<ND> &S, long long *gacc, unsigned *ticket, int phase, int finalize,
-                                Scalars *sc, double *hist, double *out, int32_t *out_flags) {
+                                Scalars *sc, double *hist, double *out, int32_t *out_flags,
+                                const double *cx = nullptr, const double *cy = nullptr, int64_t cn = 0) {
     unsigned gflags;
     cta_sacc_collect<ND>(S, gacc, gflags);
     long long *w = (long long *)&S.w[0][0];
@@ -134,8 +135,15 @@ __device__ void last_cta_finish(CtaSacc<ND> &S, long long *gacc, unsigned *ticke
             if (ovf) atomicOr(&S.flags, FLAG_RANGE);
         }
         __syncthreads();
+        // rare error path: a flagged standalone dot is classified as
+        // non-finite if any input is NaN/Inf, else range
+        if (gflags && cx) {
+            for (int64_t i = threadIdx.x; i < cn; i += blockDim.x)
+                if (!isfinite(cx[i]) || !isfinite(cy[i])) atomicOr(&S.flags, FLAG_NONFINITE);
+            __syncthreads();
+        }
         if (threadIdx.x == 0) {
-            unsigned f = gflags | (S.flags & FLAG_RANGE);
+            unsigned f = gflags | (S.flags & (FLAG_RANGE | FLAG_NONFINITE));
             phase_finalize(phase, sc, S.rounded, f, hist, out, out_flags);
         }
         for (int i = threadIdx.x; i < ND * SACC_L + SACC_FLAGW; i += blockDim.x) gacc[i] = 0;
@@ -147,6 +155,8 @@ __device__ void last_cta_finish(CtaSacc<ND> &S, long long *gacc, unsigned *ticke
 
 // ------------------------------------------------------------------------
 // K2: p,s,z,q,y + phase-A partial dots
+// Memory pipelining: each thread loads U row pairs (8 x 16 B each) before it
+// computes any of them, so U*128 B per thread are in flight.
 // ------------------------------------------------------------------------
 struct K2Args {
     int64_t n;
@@ -159,60 +169,87 @@ struct K2Args {
     int finalize;
 };
 
-template <int NP, int NE, int BS>
+template <int NP, int NE>
+struct K2Row {
+    ExAcc<NP, NE> dqy, dyy, drs, drz;
+    double be, nom, nal;
+    bool first;
+    template <bool EARLY>
+    __device__ __forceinline__ void row(unsigned long long (*sw)[SACC_L], unsigned &flags, double r, double rh,
+                                        double w, double t, double v, double &p, double &s, double &z, double &q,
+                                        double &y) {
+        if (first) {  // beta_{-1} = 0: exact copies (R-3)
+            p = r; s = w; z = t;
+        } else {
+            p = __fma_rn(be, __fma_rn(nom, s, p), r);  // p := r + beta (p - omega s)   l.70
+            s = __fma_rn(be, __fma_rn(nom, z, s), w);  // s := w + beta (s - omega z)   l.71
+            z = __fma_rn(be, __fma_rn(nom, v, z), t);  // z := t + beta (z - omega v)   l.72
+        }
+        q = __fma_rn(nal, s, r);  // q := r - alpha s  l.73
+        y = __fma_rn(nal, z, w);  // y := w - alpha z  l.74
+        dqy.template add<EARLY>(q, y, sw[0], flags);
+        dyy.template add<EARLY>(y, y, sw[1], flags);
+        drs.template add<EARLY>(rh, s, sw[2], flags);
+        drz.template add<EARLY>(rh, z, sw[3], flags);
+    }
+};
+
+template <int NP, int NE, int BS, int U>
 __global__ void __launch_bounds__(BS) k2_kernel(K2Args a) {
     __shared__ CtaSacc<4> S;
     Scalars *sc = a.sc;
     if (sc->done) return;
     cta_sacc_zero<4>(S);
     __syncthreads();
-    const bool first = (sc->it == 0);
-    const double al = sc->alpha, be = sc->beta, om = sc->omega;
-    const double nal = -al, nom = -om;
-    ExAcc<NP, NE> dqy, dyy, drs, drz;
-    dqy.zero(); dyy.zero(); drs.zero(); drz.zero();
+    K2Row<NP, NE> R;
+    R.first = (sc->it == 0);
+    R.be = sc->beta;
+    R.nom = -sc->omega;
+    R.nal = -sc->alpha;
+    R.dqy.zero(); R.dyy.zero(); R.drs.zero(); R.drz.zero();
     unsigned flags = 0;
-    unsigned long long *s0 = S.w[0], *s1 = S.w[1], *s2 = S.w[2], *s3 = S.w[3];
-    const int64_t n = a.n;
-    const int64_t npair = n >> 1;
+    const int64_t n = a.n, npair = n >> 1;
     const int64_t stride = (int64_t)gridDim.x * BS;
-    const double2 *r2 = (const double2 *)a.r, *rh2 = (const double2 *)a.rh, *w2 = (const double2 *)a.w,
-                  *t2 = (const double2 *)a.t, *v2 = (const double2 *)a.v;
+    const double2 *__restrict__ r2 = (const double2 *)a.r, *__restrict__ rh2 = (const double2 *)a.rh,
+                  *__restrict__ w2 = (const double2 *)a.w, *__restrict__ t2 = (const double2 *)a.t,
+                  *__restrict__ v2 = (const double2 *)a.v;
     double2 *p2 = (double2 *)a.p, *ss2 = (double2 *)a.s, *z2 = (double2 *)a.z, *q2 = (double2 *)a.q,
             *y2 = (double2 *)a.y;
-    auto row = [&](double r, double rh, double w, double t, double v, double &p, double &s, double &z,
-                   double &q, double &y) {
-        if (first) {  // beta_{-1} = 0: exact copies (R-3)
-            p = r; s = w; z = t;
-        } else {
-            p = __fma_rn(be, __fma_rn(nom, s, p), r);
-            s = __fma_rn(be, __fma_rn(nom, z, s), w);
-            z = __fma_rn(be, __fma_rn(nom, v, z), t);
+    int64_t k = (int64_t)blockIdx.x * BS + threadIdx.x;
+    // full groups: every lane of a warp runs the same trip count (warp-uniform early exits)
+    const int64_t full = (npair / (stride * U)) * (stride * U);
+    for (int64_t base = k; base < full; base += stride * U) {
+        double2 r[U], rh[U], w[U], t[U], p[U], s[U], z[U], v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = base + u * stride;
+            r[u] = __ldcs(r2 + i); rh[u] = __ldg(rh2 + i); w[u] = __ldcs(w2 + i); t[u] = __ldcs(t2 + i);
+            if (!R.first) { p[u] = __ldcs(p2 + i); s[u] = __ldcs(ss2 + i); z[u] = __ldcs(z2 + i); v[u] = __ldcs(v2 + i); }
         }
-        q = __fma_rn(nal, s, r);
-        y = __fma_rn(nal, z, w);
-        dqy.add(q, y, s0, flags);
-        dyy.add(y, y, s1, flags);
-        drs.add(rh, s, s2, flags);
-        drz.add(rh, z, s3, flags);
-    };
-    for (int64_t k = (int64_t)blockIdx.x * BS + threadIdx.x; k < npair; k += stride) {
-        const double2 r = r2[k], rh = rh2[k], w = w2[k], t = t2[k];
-        double2 p, s, z, v;
-        if (!first) { p = p2[k]; s = ss2[k]; z = z2[k]; v = v2[k]; }
-        double2 q, y;
-        row(r.x, rh.x, w.x, t.x, v.x, p.x, s.x, z.x, q.x, y.x);
-        row(r.y, rh.y, w.y, t.y, v.y, p.y, s.y, z.y, q.y, y.y);
-        p2[k] = p; ss2[k] = s; z2[k] = z; q2[k] = q; y2[k] = y;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = base + u * stride;
+            double2 q, y;
+            R.template row<true>(S.w, flags, r[u].x, rh[u].x, w[u].x, t[u].x, v[u].x, p[u].x, s[u].x, z[u].x, q.x, y.x);
+            R.template row<true>(S.w, flags, r[u].y, rh[u].y, w[u].y, t[u].y, v[u].y, p[u].y, s[u].y, z[u].y, q.y, y.y);
+            p2[i] = p[u]; ss2[i] = s[u]; z2[i] = z[u]; q2[i] = q; y2[i] = y;
+        }
     }
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-        const int64_t k = n - 1;
+    for (int64_t i = full + k; i < npair; i += stride) {  // remainder pairs (lanes diverge: no early exit)
+        double2 r = r2[i], rh = rh2[i], w = w2[i], t = t2[i], p, s, z, v, q, y;
+        if (!R.first) { p = p2[i]; s = ss2[i]; z = z2[i]; v = v2[i]; }
+        R.template row<false>(S.w, flags, r.x, rh.x, w.x, t.x, v.x, p.x, s.x, z.x, q.x, y.x);
+        R.template row<false>(S.w, flags, r.y, rh.y, w.y, t.y, v.y, p.y, s.y, z.y, q.y, y.y);
+        p2[i] = p; ss2[i] = s; z2[i] = z; q2[i] = q; y2[i] = y;
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail row
+        const int64_t i = n - 1;
         double p = 0, s = 0, z = 0, v = 0, q, y;
-        if (!first) { p = a.p[k]; s = a.s[k]; z = a.z[k]; v = a.v[k]; }
-        row(a.r[k], a.rh[k], a.w[k], a.t[k], v, p, s, z, q, y);
-        a.p[k] = p; a.s[k] = s; a.z[k] = z; a.q[k] = q; a.y[k] = y;
+        if (!R.first) { p = a.p[i]; s = a.s[i]; z = a.z[i]; v = a.v[i]; }
+        R.template row<false>(S.w, flags, a.r[i], a.rh[i], a.w[i], a.t[i], v, p, s, z, q, y);
+        a.p[i] = p; a.s[i] = s; a.z[i] = z; a.q[i] = q; a.y[i] = y;
     }
-    dqy.warp_merge(s0); dyy.warp_merge(s1); drs.warp_merge(s2); drz.warp_merge(s3);
+    R.dqy.warp_merge(S.w[0]); R.dyy.warp_merge(S.w[1]); R.drs.warp_merge(S.w[2]); R.drz.warp_merge(S.w[3]);
     if (cta_sacc_publish<4>(S, flags, a.gacc, a.ticket))
         last_cta_finish<4>(S, a.gacc, a.ticket, PH_A, a.finalize, sc, a.hist, nullptr, nullptr);
 }
@@ -231,48 +268,74 @@ struct K3Args {
     int finalize;
 };
 
-template <int NP, int NE, int BS>
+template <int NP, int NE>
+struct K3Row {
+    ExAcc<NP, NE> drr, drw, dnn;
+    double al, om, nal, nom;
+    template <bool EARLY>
+    __device__ __forceinline__ void row(unsigned long long (*sw)[SACC_L], unsigned &flags, double rh, double p,
+                                        double q, double y, double t, double v, double &x, double &r, double &w) {
+        x = __fma_rn(om, q, __fma_rn(al, p, x));    // x := x + alpha p + omega q      l.77
+        r = __fma_rn(nom, y, q);                    // r := q - omega y                l.78
+        w = __fma_rn(nom, __fma_rn(nal, v, t), y);  // w := y - omega (t - alpha v)    l.79
+        drr.template add<EARLY>(rh, r, sw[0], flags);
+        drw.template add<EARLY>(rh, w, sw[1], flags);
+        dnn.template add<EARLY>(r, r, sw[2], flags);
+    }
+};
+
+template <int NP, int NE, int BS, int U>
 __global__ void __launch_bounds__(BS) k3_kernel(K3Args a) {
     __shared__ CtaSacc<3> S;
     Scalars *sc = a.sc;
     if (sc->done) return;
     cta_sacc_zero<3>(S);
     __syncthreads();
-    const double al = sc->alpha, om = sc->omega;
-    const double nal = -al, nom = -om;
-    ExAcc<NP, NE> drr, drw, dnn;
-    drr.zero(); drw.zero(); dnn.zero();
+    K3Row<NP, NE> R;
+    R.al = sc->alpha;
+    R.om = sc->omega;
+    R.nal = -R.al;
+    R.nom = -R.om;
+    R.drr.zero(); R.drw.zero(); R.dnn.zero();
     unsigned flags = 0;
-    unsigned long long *s0 = S.w[0], *s1 = S.w[1], *s2 = S.w[2];
-    const int64_t n = a.n;
-    const int64_t npair = n >> 1;
+    const int64_t n = a.n, npair = n >> 1;
     const int64_t stride = (int64_t)gridDim.x * BS;
-    const double2 *rh2 = (const double2 *)a.rh, *p2 = (const double2 *)a.p, *q2 = (const double2 *)a.q,
-                  *y2 = (const double2 *)a.y, *t2 = (const double2 *)a.t, *v2 = (const double2 *)a.v;
+    const double2 *__restrict__ rh2 = (const double2 *)a.rh, *__restrict__ p2 = (const double2 *)a.p,
+                  *__restrict__ q2 = (const double2 *)a.q, *__restrict__ y2 = (const double2 *)a.y,
+                  *__restrict__ t2 = (const double2 *)a.t, *__restrict__ v2 = (const double2 *)a.v;
     double2 *x2 = (double2 *)a.x, *rr2 = (double2 *)a.r, *w2 = (double2 *)a.w;
-    auto row = [&](double rh, double p, double q, double y, double t, double v, double &x, double &r,
-                   double &w) {
-        x = __fma_rn(om, q, __fma_rn(al, p, x));   // x + alpha p + omega q (l.77)
-        r = __fma_rn(nom, y, q);                   // q - omega y           (l.78)
-        w = __fma_rn(nom, __fma_rn(nal, v, t), y); // y - omega (t - alpha v) (l.79)
-        drr.add(rh, r, s0, flags);
-        drw.add(rh, w, s1, flags);
-        dnn.add(r, r, s2, flags);
-    };
-    for (int64_t k = (int64_t)blockIdx.x * BS + threadIdx.x; k < npair; k += stride) {
-        const double2 rh = rh2[k], p = p2[k], q = q2[k], y = y2[k], t = t2[k], v = v2[k];
-        double2 x = x2[k], r, w;
-        row(rh.x, p.x, q.x, y.x, t.x, v.x, x.x, r.x, w.x);
-        row(rh.y, p.y, q.y, y.y, t.y, v.y, x.y, r.y, w.y);
-        x2[k] = x; rr2[k] = r; w2[k] = w;
+    int64_t k = (int64_t)blockIdx.x * BS + threadIdx.x;
+    const int64_t full = (npair / (stride * U)) * (stride * U);
+    for (int64_t base = k; base < full; base += stride * U) {
+        double2 rh[U], p[U], q[U], y[U], t[U], v[U], x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = base + u * stride;
+            rh[u] = __ldg(rh2 + i); p[u] = __ldcs(p2 + i); q[u] = __ldcs(q2 + i); y[u] = __ldcs(y2 + i);
+            t[u] = __ldcs(t2 + i); v[u] = __ldcs(v2 + i); x[u] = __ldcs(x2 + i);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = base + u * stride;
+            double2 r, w;
+            R.template row<true>(S.w, flags, rh[u].x, p[u].x, q[u].x, y[u].x, t[u].x, v[u].x, x[u].x, r.x, w.x);
+            R.template row<true>(S.w, flags, rh[u].y, p[u].y, q[u].y, y[u].y, t[u].y, v[u].y, x[u].y, r.y, w.y);
+            x2[i] = x[u]; rr2[i] = r; w2[i] = w;
+        }
+    }
+    for (int64_t i = full + k; i < npair; i += stride) {
+        double2 rh = rh2[i], p = p2[i], q = q2[i], y = y2[i], t = t2[i], v = v2[i], x = x2[i], r, w;
+        R.template row<false>(S.w, flags, rh.x, p.x, q.x, y.x, t.x, v.x, x.x, r.x, w.x);
+        R.template row<false>(S.w, flags, rh.y, p.y, q.y, y.y, t.y, v.y, x.y, r.y, w.y);
+        x2[i] = x; rr2[i] = r; w2[i] = w;
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-        const int64_t k = n - 1;
-        double x = a.x[k], r, w;
-        row(a.rh[k], a.p[k], a.q[k], a.y[k], a.t[k], a.v[k], x, r, w);
-        a.x[k] = x; a.r[k] = r; a.w[k] = w;
+        const int64_t i = n - 1;
+        double x = a.x[i], r, w;
+        R.template row<false>(S.w, flags, a.rh[i], a.p[i], a.q[i], a.y[i], a.t[i], a.v[i], x, r, w);
+        a.x[i] = x; a.r[i] = r; a.w[i] = w;
     }
-    drr.warp_merge(s0); drw.warp_merge(s1); dnn.warp_merge(s2);
+    R.drr.warp_merge(S.w[0]); R.drw.warp_merge(S.w[1]); R.dnn.warp_merge(S.w[2]);
     if (cta_sacc_publish<3>(S, flags, a.gacc, a.ticket))
         last_cta_finish<3>(S, a.gacc, a.ticket, PH_B, a.finalize, sc, a.hist, nullptr, nullptr);
 }
@@ -292,7 +355,7 @@ struct MultiDotArgs {
     int32_t *out_flags;
 };
 
-template <int ND, int NP, int NE, int BS>
+template <int ND, int NP, int NE, int BS, int U>
 __global__ void __launch_bounds__(BS) multidot_kernel(MultiDotArgs a) {
     __shared__ CtaSacc<ND> S;
     if (a.sc && a.sc->done && a.phase != PH_TRUE) return;
@@ -303,39 +366,56 @@ __global__ void __launch_bounds__(BS) multidot_kernel(MultiDotArgs a) {
     for (int d = 0; d < ND; ++d) acc[d].zero();
     unsigned flags = 0;
     const int64_t n = a.n;
-    const int64_t npair = n >> 1;
     const int64_t stride = (int64_t)gridDim.x * BS;
+    const int64_t k = (int64_t)blockIdx.x * BS + threadIdx.x;
     bool aligned = true;
 #pragma unroll
     for (int d = 0; d < ND; ++d) aligned &= ((((uintptr_t)a.x[d]) | ((uintptr_t)a.y[d])) & 15) == 0;
     if (aligned) {
-        for (int64_t k = (int64_t)blockIdx.x * BS + threadIdx.x; k < npair; k += stride) {
-            double2 xv[ND], yv[ND];
+        const int64_t npair = n >> 1;
+        const int64_t full = (npair / (stride * U)) * (stride * U);
+        for (int64_t base = k; base < full; base += stride * U) {
+            double2 xv[U][ND], yv[U][ND];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int d = 0; d < ND; ++d) {
+                    xv[u][d] = __ldcs((const double2 *)a.x[d] + base + u * stride);
+                    yv[u][d] = __ldcs((const double2 *)a.y[d] + base + u * stride);
+                }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int d = 0; d < ND; ++d) {
+                    acc[d].template add<true>(xv[u][d].x, yv[u][d].x, S.w[d], flags);
+                    acc[d].template add<true>(xv[u][d].y, yv[u][d].y, S.w[d], flags);
+                }
+        }
+        for (int64_t i = full + k; i < npair; i += stride) {
 #pragma unroll
             for (int d = 0; d < ND; ++d) {
-                xv[d] = ((const double2 *)a.x[d])[k];
-                yv[d] = ((const double2 *)a.y[d])[k];
-            }
-#pragma unroll
-            for (int d = 0; d < ND; ++d) {
-                acc[d].add(xv[d].x, yv[d].x, S.w[d], flags);
-                acc[d].add(xv[d].y, yv[d].y, S.w[d], flags);
+                const double2 xv = ((const double2 *)a.x[d])[i], yv = ((const double2 *)a.y[d])[i];
+                acc[d].template add<false>(xv.x, yv.x, S.w[d], flags);
+                acc[d].template add<false>(xv.y, yv.y, S.w[d], flags);
             }
         }
         if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
 #pragma unroll
-            for (int d = 0; d < ND; ++d) acc[d].add(a.x[d][n - 1], a.y[d][n - 1], S.w[d], flags);
+            for (int d = 0; d < ND; ++d) acc[d].template add<false>(a.x[d][n - 1], a.y[d][n - 1], S.w[d], flags);
         }
     } else {
-        for (int64_t k = (int64_t)blockIdx.x * BS + threadIdx.x; k < n; k += stride) {
+        for (int64_t i = k; i < n; i += stride) {
 #pragma unroll
-            for (int d = 0; d < ND; ++d) acc[d].add(a.x[d][k], a.y[d][k], S.w[d], flags);
+            for (int d = 0; d < ND; ++d) acc[d].template add<false>(a.x[d][i], a.y[d][i], S.w[d], flags);
         }
     }
 #pragma unroll
     for (int d = 0; d < ND; ++d) acc[d].warp_merge(S.w[d]);
-    if (cta_sacc_publish<ND>(S, flags, a.gacc, a.ticket))
-        last_cta_finish<ND>(S, a.gacc, a.ticket, a.phase, a.finalize, a.sc, a.hist, a.out, a.out_flags);
+    if (cta_sacc_publish<ND>(S, flags, a.gacc, a.ticket)) {
+        const bool cls = (ND == 1 && a.phase == PH_EXDOT);
+        last_cta_finish<ND>(S, a.gacc, a.ticket, a.phase, a.finalize, a.sc, a.hist, a.out, a.out_flags,
+                            cls ? a.x[0] : nullptr, cls ? a.y[0] : nullptr, a.n);
+    }
 }
 
 // After an allreduce of normalised words: normalise, round, finalise (1 CTA).

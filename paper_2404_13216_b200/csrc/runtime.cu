@@ -31,6 +31,7 @@
 
 #include "../../include/pbicgstab.h"
 #include "kernels.cuh"
+#include "stream.cuh"
 
 using namespace pbcg;
 
@@ -209,7 +210,8 @@ extern "C" int pbcg_sacc_words(void) { return SACC_L; }
 static constexpr int GW4 = 4 * SACC_L + SACC_FLAGW;  // words of a 4-dot reduction buffer
 static constexpr int NPH = 5;                        // reduction buffers: init, A, B, true, exdot
 static constexpr int K_BS = 256;
-static constexpr int K_NP = 2, K_NE = 2;             // FPE depth for products / errors (performance only, R-16)
+static constexpr int K_NP = 4, K_NE = 4;             // FPE depth for products / errors (performance only, R-16)
+static constexpr int U_K2 = 2, U_K3 = 2, U_MD4 = 2, U_MD1 = 4;  // row pairs in flight per thread
 
 struct Rank {
     int id = 0;
@@ -541,8 +543,8 @@ static int multidot(pbcg_handle *h, int ph, int phase, int nd, const double *con
         a.phase = phase;
         a.finalize = fin;
         const int grid = std::max(1, std::min<int>(h->grid_md, (int)((R.n / 2 + K_BS - 1) / K_BS)));
-        if (nd == 4) multidot_kernel<4, K_NP, K_NE, K_BS><<<grid, K_BS, 0, h->stream>>>(a);
-        else multidot_kernel<1, K_NP, K_NE, K_BS><<<grid, K_BS, 0, h->stream>>>(a);
+        if (nd == 4) multidot_kernel<4, K_NP, K_NE, K_BS, U_MD4><<<grid, K_BS, 0, h->stream>>>(a);
+        else multidot_kernel<1, K_NP, K_NE, K_BS, U_MD1><<<grid, K_BS, 0, h->stream>>>(a);
         CUDA_TRY(cudaGetLastError());
     }
     if (!fin) {
@@ -555,18 +557,67 @@ static int multidot(pbcg_handle *h, int ph, int phase, int nd, const double *con
 // ----------------------------------------------------------------------------
 // one iteration of Algorithm 2 (enqueue only)
 // ----------------------------------------------------------------------------
+// Streaming (TMA-pipelined) kernel geometry -- performance parameters only.
+static constexpr int S_NP = 2, S_NE = 2, S_NO = 3, S_NCW = 7;  // S_NCW: warps per dot group (2*7+1 = 15 warps)
+static constexpr int X_NCW = 8;
+static constexpr int X_NP = 3, X_NE = 3, X_NO = 2;              // standalone EXDOT (wider dynamic range)
+static constexpr int K2_PPT = 1, K2_ST = 4, K3_PPT = 1, K3_ST = 4, XD_PPT = 4, XD_ST = 4;
+#define K2S k2_stream<S_NP, S_NE, S_NO, S_NCW, K2_PPT, K2_ST>
+#define K3S k3_stream<S_NP, S_NE, S_NO, S_NCW, K3_PPT, K3_ST>
+#define XDS exdot_stream<X_NP, X_NE, X_NO, X_NCW, XD_PPT, XD_ST>
+static constexpr size_t ring_bytes(int nv, int ncw, int ppt, int stages) {
+    return sizeof(double) * (size_t)stages * nv * (2 * ncw * 32 * ppt) + 2 * sizeof(uint64_t) * stages;
+}
+static constexpr size_t K2_SMEM = ring_bytes(8, S_NCW, K2_PPT, K2_ST);
+static constexpr size_t K3_SMEM = ring_bytes(7, S_NCW, K3_PPT, K3_ST);
+static constexpr size_t XD_SMEM = ring_bytes(2, X_NCW, XD_PPT, XD_ST);
+static constexpr int STREAM_THREADS = (X_NCW + 1) * 32;      // exdot: 1 dot group
+static constexpr int KSTREAM_THREADS = (2 * S_NCW + 1) * 32;  // K2/K3: 2 dot groups
+static int g_kernels_ldg = -1;  // 1: the register-pipelined (LDG) K2/K3 instead of the TMA ring (A/B runs)
+
+static bool use_ldg_kernels() {
+    if (g_kernels_ldg < 0) {
+        const char *e = getenv("PBCG_KERNELS");
+        g_kernels_ldg = (e && strcmp(e, "ldg") == 0) ? 1 : 0;
+    }
+    return g_kernels_ldg == 1;
+}
+
+static int stream_attrs() {
+    static int done = 0;
+    if (done) return PBCG_OK;
+    CUDA_TRY(cudaFuncSetAttribute((const void *)K2S, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM));
+    CUDA_TRY(cudaFuncSetAttribute((const void *)K3S, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM));
+    CUDA_TRY(cudaFuncSetAttribute((const void *)XDS, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XD_SMEM));
+    done = 1;
+    return PBCG_OK;
+}
+
+static int stream_grid(pbcg_handle *h, int64_t n, int rows_per_tile) {
+    const int64_t tiles = (n + rows_per_tile - 1) / rows_per_tile;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(h ? h->nsm : 148, tiles));
+}
+
 static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     K2Args a{R.n, R.r, R.rh, R.w(), R.t, R.v, R.p, R.s, R.z(), R.q, R.y, R.sc, R.gacc[1], R.tickets + 1, R.hist, fin};
-    const int grid = std::max(1, std::min<int>(h->grid_k2, (int)((R.n / 2 + K_BS - 1) / K_BS)));
-    k2_kernel<K_NP, K_NE, K_BS><<<grid, K_BS, 0, st>>>(a);
+    if (use_ldg_kernels()) {
+        const int grid = std::max(1, std::min<int>(h->grid_k2, (int)((R.n / 2 + K_BS - 1) / K_BS)));
+        k2_kernel<K_NP, K_NE, K_BS, U_K2><<<grid, K_BS, 0, st>>>(a);
+    } else {
+        K2S<<<stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T), KSTREAM_THREADS, K2_SMEM, st>>>(a);
+    }
     CUDA_TRY(cudaGetLastError());
     return PBCG_OK;
 }
 
 static int launch_k3(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     K3Args a{R.n, R.rh, R.p, R.q, R.y, R.t, R.v, R.x, R.r, R.w(), R.sc, R.gacc[2], R.tickets + 2, R.hist, fin};
-    const int grid = std::max(1, std::min<int>(h->grid_k3, (int)((R.n / 2 + K_BS - 1) / K_BS)));
-    k3_kernel<K_NP, K_NE, K_BS><<<grid, K_BS, 0, st>>>(a);
+    if (use_ldg_kernels()) {
+        const int grid = std::max(1, std::min<int>(h->grid_k3, (int)((R.n / 2 + K_BS - 1) / K_BS)));
+        k3_kernel<K_NP, K_NE, K_BS, U_K3><<<grid, K_BS, 0, st>>>(a);
+    } else {
+        K3S<<<stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T), KSTREAM_THREADS, K3_SMEM, st>>>(a);
+    }
     CUDA_TRY(cudaGetLastError());
     return PBCG_OK;
 }
@@ -705,9 +756,10 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
             if (bad & 2) return fail(PBCG_ENONFINITE, "csr: NaN/Inf value");
         }
     }
-    h->grid_k2 = grid_for((const void *)k2_kernel<K_NP, K_NE, K_BS>, K_BS, h->nsm);
-    h->grid_k3 = grid_for((const void *)k3_kernel<K_NP, K_NE, K_BS>, K_BS, h->nsm);
-    h->grid_md = grid_for((const void *)multidot_kernel<4, K_NP, K_NE, K_BS>, K_BS, h->nsm);
+    RC_TRY(stream_attrs());
+    h->grid_k2 = grid_for((const void *)k2_kernel<K_NP, K_NE, K_BS, U_K2>, K_BS, h->nsm);
+    h->grid_k3 = grid_for((const void *)k3_kernel<K_NP, K_NE, K_BS, U_K3>, K_BS, h->nsm);
+    h->grid_md = grid_for((const void *)multidot_kernel<4, K_NP, K_NE, K_BS, U_MD4>, K_BS, h->nsm);
     CUDA_TRY(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
     for (auto &e : h->ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreate(&h->t0));
@@ -984,7 +1036,7 @@ static int scratch(Scratch **out) {
     if (!S.gacc) {
         int nsm = 148;
         CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        S.grid1 = grid_for((const void *)multidot_kernel<1, K_NP, K_NE, K_BS>, K_BS, nsm);
+        S.grid1 = grid_for((const void *)multidot_kernel<1, K_NP, K_NE, K_BS, U_MD1>, K_BS, nsm);
         S.gridp = grid_for((const void *)plain_dot_kernel<K_BS>, K_BS, nsm);
         CUDA_TRY(cudaMalloc(&S.gacc, sizeof(long long) * (SACC_L + SACC_FLAGW)));
         CUDA_TRY(cudaMalloc(&S.ticket, 64));
@@ -1021,8 +1073,13 @@ extern "C" int exdot(pbcg_handle *h, int64_t n, const double *x, const double *y
         a.finalize = 1;
         a.out = out;
         a.out_flags = ofl;
-        const int grid = std::max(1, std::min<int>(S->grid1, (int)((n / 2 + K_BS - 1) / K_BS)));
-        multidot_kernel<1, K_NP, K_NE, K_BS><<<grid, K_BS, 0, st>>>(a);
+        if (((((uintptr_t)x) | ((uintptr_t)y)) & 15) == 0 && n > 0) {
+            RC_TRY(stream_attrs());
+            XDS<<<stream_grid(h, n, TileGeo<X_NCW, XD_PPT>::T), STREAM_THREADS, XD_SMEM, st>>>(a);
+        } else {
+            const int grid = std::max(1, std::min<int>(S->grid1, (int)((n / 2 + K_BS - 1) / K_BS)));
+            multidot_kernel<1, K_NP, K_NE, K_BS, U_MD1><<<grid, K_BS, 0, st>>>(a);
+        }
         CUDA_TRY(cudaGetLastError());
     } else {
         // distributed: each (virtual) rank reduces its slice, int64 allreduce, round once
@@ -1038,7 +1095,7 @@ extern "C" int exdot(pbcg_handle *h, int64_t n, const double *x, const double *y
             a.phase = PH_EXDOT;
             a.finalize = 0;
             const int grid = std::max(1, std::min<int>(S->grid1, (int)(((hi - lo) / 2 + K_BS - 1) / K_BS)));
-            multidot_kernel<1, K_NP, K_NE, K_BS><<<grid, K_BS, 0, st>>>(a);
+            multidot_kernel<1, K_NP, K_NE, K_BS, U_MD1><<<grid, K_BS, 0, st>>>(a);
             CUDA_TRY(cudaGetLastError());
         }
         RC_TRY(reduce_finalize<1>(h, 4, PH_EXDOT, st, out, ofl));

@@ -1,0 +1,463 @@
+// stream.cuh -- persistent, warp-specialised streaming kernels for the
+// vector part of p-BiCGStab (K2, K3) and for the standalone EXDOT.
+//
+// B200 design: one CTA per SM; one producer warp streams tiles
+// of every input vector HBM -> shared memory with cp.async.bulk (the TMA bulk
+// engine, SASS UBLKCP) into a STAGES-deep ring guarded by mbarriers
+// (full: transaction bytes landed; empty: every consumer warp is done);
+// NCW consumer warps read their rows from shared memory, run the recurrences
+// and the ExBLAS accumulation in registers, and store the output vectors with
+// coalesced 16-byte stores.  Memory stays busy while the fp64 pipe works on
+// the previous tiles, so the kernel runs at max(HBM time, fp64 time) instead
+// of their sum, without spending registers on loads in flight.
+#pragma once
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace pbcg {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared (TMA bulk engine), completion counted on bar
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// Tile geometry shared by the producer and the consumers.
+template <int NCW, int PPT>
+struct TileGeo {
+    static constexpr int PAIRS = NCW * 32 * PPT;  // row pairs per tile
+    static constexpr int T = 2 * PAIRS;           // rows per tile
+};
+
+// Producer loop (one lane): for each tile owned by this CTA, wait for a free
+// slot, arm the full barrier with the byte count and issue one bulk copy per
+// input vector.  Rows are copied in whole pairs (16-byte multiples); an odd
+// last row is read directly from global memory by its consumer.
+template <int NV, int T, int STAGES>
+__device__ __forceinline__ void produce(const double *const *src, int nv_act, int64_t n, double *buf, uint64_t *full,
+                                        uint64_t *empty) {
+    const int64_t ntiles = (n + T - 1) / T;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        mbar_wait(&empty[s], ph ^ 1u);
+        const int64_t r0 = tile * T;
+        const int rows = (int)min((int64_t)T, n - r0);
+        const uint32_t bytes = (uint32_t)(rows & ~1) * 8u;
+        mbar_expect_tx(&full[s], bytes * (uint32_t)nv_act);
+        if (bytes)
+            for (int v = 0; v < nv_act; ++v) bulk_g2s(buf + ((size_t)s * NV + v) * T, src[v] + r0, bytes, &full[s]);
+        if (++s == STAGES) { s = 0; ph ^= 1u; }
+    }
+}
+
+template <int NV, int T, int STAGES>
+__device__ __forceinline__ size_t stream_smem_bytes() {
+    return sizeof(double) * (size_t)STAGES * NV * T + 2 * STAGES * sizeof(uint64_t);
+}
+
+// ---------------------------------------------------------------------------
+// K2 (Alg. 2 l.70-74) + phase-A dots.  The consumer warps form two dot
+// groups of W warps that see the same tiles: group 0 owns (q,y), (y,y) and
+// stores p,s,z,q,y; group 1 recomputes s,z (8 FMAs) and owns (r0,s), (r0,z).
+// Splitting the dots halves the accumulator registers per thread, which buys
+// twice the warps (the ExBLAS cascades are latency-bound chains of DADDs).
+// ---------------------------------------------------------------------------
+template <int NP, int NE, int NO>
+struct K2Op {
+    ExAcc3<NP, NE, NO> d0, d1;
+    double be, nom, nal;
+    bool first;
+    __device__ __forceinline__ void sz(double w, double t, double v, double &s, double &z) const {
+        if (first) {  // beta_{-1} = 0: exact copies (R-3)
+            s = w; z = t;
+        } else {
+            s = __fma_rn(be, __fma_rn(nom, z, s), w);  // s := w + beta (s - omega z)   l.71
+            z = __fma_rn(be, __fma_rn(nom, v, z), t);  // z := t + beta (z - omega v)   l.72
+        }
+    }
+    // group 0: p,s,z,q,y and (q,y), (y,y)
+    __device__ __forceinline__ void row0(unsigned &flags, double r, double w, double t, double v, double &p,
+                                         double &s, double &z, double &q, double &y, double *res) {
+        p = first ? r : __fma_rn(be, __fma_rn(nom, s, p), r);  // p := r + beta (p - omega s)   l.70
+        sz(w, t, v, s, z);
+        q = __fma_rn(nal, s, r);  // q := r - alpha s   l.73
+        y = __fma_rn(nal, z, w);  // y := w - alpha z   l.74
+        const bool zy = is_zero(y);
+        d0.step(q, y, is_zero(q) | zy, res[0], res[1], flags);
+        d1.step(y, y, zy, res[2], res[3], flags);
+    }
+    // group 1: s,z and (r0,s), (r0,z)
+    __device__ __forceinline__ void row1(unsigned &flags, double rh, double w, double t, double v, double s, double z,
+                                         double *res) {
+        sz(w, t, v, s, z);
+        const bool zr = is_zero(rh);
+        d0.step(rh, s, zr | is_zero(s), res[0], res[1], flags);
+        d1.step(rh, z, zr | is_zero(z), res[2], res[3], flags);
+    }
+    __device__ __forceinline__ void spill(const double *res, unsigned long long *s0, unsigned long long *s1) {
+        d0.spill(res[0], res[1], s0);
+        d1.spill(res[2], res[3], s1);
+    }
+};
+
+template <int NP, int NE, int NO, int W, int PPT, int STAGES>
+__global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
+    constexpr int NV = 8;  // r, rh, w, t | p, s, z, v
+    constexpr int NCW = 2 * W;
+    constexpr int T = TileGeo<W, PPT>::T;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double *buf = (double *)smem_raw;
+    uint64_t *full = (uint64_t *)(buf + (size_t)STAGES * NV * T);
+    uint64_t *empty = full + STAGES;
+    __shared__ CtaSacc<4> S;
+    Scalars *sc = a.sc;
+    if (sc->done) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    cta_sacc_zero<4>(S);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NCW); }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const bool first = (sc->it == 0);
+    const int64_t n = a.n;
+    unsigned flags = 0;
+    K2Op<NP, NE, NO> R;
+    R.first = first;
+    R.be = sc->beta;
+    R.nom = -sc->omega;
+    R.nal = -sc->alpha;
+    R.d0.zero();
+    R.d1.zero();
+    const int g = warp / W, wg = warp % W;
+    unsigned long long *s0 = S.w[2 * g], *s1 = S.w[2 * g + 1];
+    if (warp == NCW) {
+        if (lane == 0) {
+            const double *src[NV] = {a.r, a.rh, a.w, a.t, a.p, a.s, a.z, a.v};
+            produce<NV, T, STAGES>(src, first ? 4 : 8, n, buf, full, empty);
+        }
+    } else {
+        const int64_t ntiles = (n + T - 1) / T;
+        int st = 0;
+        uint32_t ph = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            mbar_wait(&full[st], ph);
+            const int64_t r0 = tile * T;
+            const int rows = (int)min((int64_t)T, n - r0);
+            const int rows_even = rows & ~1;
+            const double *B = buf + (size_t)st * NV * T;
+            const double2 *B2 = (const double2 *)B;
+            constexpr int TP = T / 2;  // double2 per vector slice
+#pragma unroll
+            for (int u = 0; u < PPT; ++u) {
+                const int j = u * W * 32 + wg * 32 + lane;  // pair index in the tile
+                const int jw = u * W * 32 + wg * 32 + 31;
+                const int64_t gp = (r0 >> 1) + j;          // global pair index
+                if (2 * jw + 1 < rows_even) {              // whole warp valid
+                    const double2 w = B2[2 * TP + j], t = B2[3 * TP + j];
+                    double2 ss, z, v;
+                    if (!first) { ss = B2[5 * TP + j]; z = B2[6 * TP + j]; v = B2[7 * TP + j]; }
+                    double res0[4], res1[4];
+                    if (g == 0) {
+                        const double2 r = B2[0 * TP + j];
+                        double2 p, q, y;
+                        if (!first) p = B2[4 * TP + j];
+                        R.row0(flags, r.x, w.x, t.x, v.x, p.x, ss.x, z.x, q.x, y.x, res0);
+                        R.row0(flags, r.y, w.y, t.y, v.y, p.y, ss.y, z.y, q.y, y.y, res1);
+                        ((double2 *)a.p)[gp] = p; ((double2 *)a.s)[gp] = ss; ((double2 *)a.z)[gp] = z;
+                        ((double2 *)a.q)[gp] = q; ((double2 *)a.y)[gp] = y;
+                    } else {
+                        const double2 rh = B2[1 * TP + j];
+                        R.row1(flags, rh.x, w.x, t.x, v.x, ss.x, z.x, res0);
+                        R.row1(flags, rh.y, w.y, t.y, v.y, ss.y, z.y, res1);
+                    }
+                    if (__any_sync(0xFFFFFFFFu, any_nonzero(res0, 4) | any_nonzero(res1, 4))) {
+                        R.spill(res0, s0, s1);
+                        R.spill(res1, s0, s1);
+                    }
+                } else {
+                    for (int h = 0; h < 2; ++h) {
+                        const int lr = 2 * j + h;  // local row
+                        if (lr >= rows) break;
+                        const int64_t gi = r0 + lr;
+                        const bool m = lr < rows_even;
+                        const double w = m ? B[2 * T + lr] : a.w[gi], t = m ? B[3 * T + lr] : a.t[gi];
+                        double ss = 0, z = 0, v = 0, res[4];
+                        if (!first) {
+                            ss = m ? B[5 * T + lr] : a.s[gi]; z = m ? B[6 * T + lr] : a.z[gi];
+                            v = m ? B[7 * T + lr] : a.v[gi];
+                        }
+                        if (g == 0) {
+                            const double r = m ? B[0 * T + lr] : a.r[gi];
+                            double p = 0, q, y;
+                            if (!first) p = m ? B[4 * T + lr] : a.p[gi];
+                            R.row0(flags, r, w, t, v, p, ss, z, q, y, res);
+                            a.p[gi] = p; a.s[gi] = ss; a.z[gi] = z; a.q[gi] = q; a.y[gi] = y;
+                        } else {
+                            R.row1(flags, m ? B[1 * T + lr] : a.rh[gi], w, t, v, ss, z, res);
+                        }
+                        R.spill(res, s0, s1);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            if (++st == STAGES) { st = 0; ph ^= 1u; }
+        }
+    }
+    R.d0.warp_merge(s0);
+    R.d1.warp_merge(s1);
+    if (cta_sacc_publish<4>(S, flags, a.gacc, a.ticket))
+        last_cta_finish<4>(S, a.gacc, a.ticket, PH_A, a.finalize, sc, a.hist, nullptr, nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// K3 (Alg. 2 l.77-79) + phase-B dots.  Group 0: x, r' and (r0,r'), (r',r');
+// group 1: w' and (r0,w').
+// ---------------------------------------------------------------------------
+template <int NP, int NE, int NO>
+struct K3Op {
+    ExAcc3<NP, NE, NO> d0, d1;
+    double al, om, nal, nom;
+    __device__ __forceinline__ void row0(unsigned &flags, double rh, double p, double q, double y, double &x, double &r,
+                                         double *res) {
+        x = __fma_rn(om, q, __fma_rn(al, p, x));  // x := x + alpha p + omega q      l.77
+        r = __fma_rn(nom, y, q);                  // r := q - omega y                l.78
+        const bool zr = is_zero(r);
+        d0.step(rh, r, is_zero(rh) | zr, res[0], res[1], flags);
+        d1.step(r, r, zr, res[2], res[3], flags);
+    }
+    __device__ __forceinline__ void row1(unsigned &flags, double rh, double y, double t, double v, double &w,
+                                         double *res) {
+        w = __fma_rn(nom, __fma_rn(nal, v, t), y);  // w := y - omega (t - alpha v)    l.79
+        d0.step(rh, w, is_zero(rh) | is_zero(w), res[0], res[1], flags);
+        res[2] = 0.0;
+        res[3] = 0.0;
+    }
+    __device__ __forceinline__ void spill(const double *res, unsigned long long *s0, unsigned long long *s1) {
+        d0.spill(res[0], res[1], s0);
+        d1.spill(res[2], res[3], s1);
+    }
+};
+
+template <int NP, int NE, int NO, int W, int PPT, int STAGES>
+__global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
+    constexpr int NV = 7;  // rh, p, q, y, t, v, x
+    constexpr int NCW = 2 * W;
+    constexpr int T = TileGeo<W, PPT>::T;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double *buf = (double *)smem_raw;
+    uint64_t *full = (uint64_t *)(buf + (size_t)STAGES * NV * T);
+    uint64_t *empty = full + STAGES;
+    __shared__ CtaSacc<3> S;
+    Scalars *sc = a.sc;
+    if (sc->done) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    cta_sacc_zero<3>(S);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NCW); }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int64_t n = a.n;
+    unsigned flags = 0;
+    K3Op<NP, NE, NO> R;
+    R.al = sc->alpha;
+    R.om = sc->omega;
+    R.nal = -R.al;
+    R.nom = -R.om;
+    R.d0.zero();
+    R.d1.zero();
+    const int g = warp / W, wg = warp % W;
+    // dot slots: (r0,r') -> 0, (r0,w') -> 1, (r',r') -> 2
+    unsigned long long *s0 = S.w[g == 0 ? 0 : 1], *s1 = S.w[2];
+    if (warp == NCW) {
+        if (lane == 0) {
+            const double *src[NV] = {a.rh, a.p, a.q, a.y, a.t, a.v, a.x};
+            produce<NV, T, STAGES>(src, NV, n, buf, full, empty);
+        }
+    } else {
+        const int64_t ntiles = (n + T - 1) / T;
+        int st = 0;
+        uint32_t ph = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            mbar_wait(&full[st], ph);
+            const int64_t r0 = tile * T;
+            const int rows = (int)min((int64_t)T, n - r0);
+            const int rows_even = rows & ~1;
+            const double *B = buf + (size_t)st * NV * T;
+            const double2 *B2 = (const double2 *)B;
+            constexpr int TP = T / 2;
+#pragma unroll
+            for (int u = 0; u < PPT; ++u) {
+                const int j = u * W * 32 + wg * 32 + lane;
+                const int jw = u * W * 32 + wg * 32 + 31;
+                const int64_t gp = (r0 >> 1) + j;
+                if (2 * jw + 1 < rows_even) {
+                    const double2 rh = B2[0 * TP + j], y = B2[3 * TP + j];
+                    double res0[4], res1[4];
+                    if (g == 0) {
+                        const double2 p = B2[1 * TP + j], q = B2[2 * TP + j];
+                        double2 x = B2[6 * TP + j], r;
+                        R.row0(flags, rh.x, p.x, q.x, y.x, x.x, r.x, res0);
+                        R.row0(flags, rh.y, p.y, q.y, y.y, x.y, r.y, res1);
+                        ((double2 *)a.x)[gp] = x; ((double2 *)a.r)[gp] = r;
+                    } else {
+                        const double2 t = B2[4 * TP + j], v = B2[5 * TP + j];
+                        double2 w;
+                        R.row1(flags, rh.x, y.x, t.x, v.x, w.x, res0);
+                        R.row1(flags, rh.y, y.y, t.y, v.y, w.y, res1);
+                        ((double2 *)a.w)[gp] = w;
+                    }
+                    if (__any_sync(0xFFFFFFFFu, any_nonzero(res0, 4) | any_nonzero(res1, 4))) {
+                        R.spill(res0, s0, s1);
+                        R.spill(res1, s0, s1);
+                    }
+                } else {
+                    for (int h = 0; h < 2; ++h) {
+                        const int lr = 2 * j + h;
+                        if (lr >= rows) break;
+                        const int64_t gi = r0 + lr;
+                        const bool m = lr < rows_even;
+                        const double rh = m ? B[0 * T + lr] : a.rh[gi], y = m ? B[3 * T + lr] : a.y[gi];
+                        double res[4];
+                        if (g == 0) {
+                            double x = m ? B[6 * T + lr] : a.x[gi], r;
+                            R.row0(flags, rh, m ? B[1 * T + lr] : a.p[gi], m ? B[2 * T + lr] : a.q[gi], y, x, r, res);
+                            a.x[gi] = x; a.r[gi] = r;
+                        } else {
+                            double w;
+                            R.row1(flags, rh, y, m ? B[4 * T + lr] : a.t[gi], m ? B[5 * T + lr] : a.v[gi], w, res);
+                            a.w[gi] = w;
+                        }
+                        R.spill(res, s0, s1);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            if (++st == STAGES) { st = 0; ph ^= 1u; }
+        }
+    }
+    R.d0.warp_merge(s0);
+    R.d1.warp_merge(s1);
+    if (cta_sacc_publish<3>(S, flags, a.gacc, a.ticket))
+        last_cta_finish<3>(S, a.gacc, a.ticket, PH_B, a.finalize, sc, a.hist, nullptr, nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// Standalone EXDOT (one dot, x and y 16-byte aligned)
+// ---------------------------------------------------------------------------
+template <int NP, int NE, int NO, int NCW, int PPT, int STAGES>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a) {
+    constexpr int NV = 2;
+    constexpr int T = TileGeo<NCW, PPT>::T;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double *buf = (double *)smem_raw;
+    uint64_t *full = (uint64_t *)(buf + (size_t)STAGES * NV * T);
+    uint64_t *empty = full + STAGES;
+    __shared__ CtaSacc<1> S;
+    if (a.sc && a.sc->done && a.phase != PH_TRUE) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    cta_sacc_zero<1>(S);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NCW); }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int64_t n = a.n;
+    unsigned flags = 0;
+    ExAcc3<NP, NE, NO> acc;
+    acc.zero();
+    if (warp == NCW) {
+        if (lane == 0) {
+            const double *src[NV] = {a.x[0], a.y[0]};
+            produce<NV, T, STAGES>(src, NV, n, buf, full, empty);
+        }
+    } else {
+        const int64_t ntiles = (n + T - 1) / T;
+        int s = 0;
+        uint32_t ph = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            mbar_wait(&full[s], ph);
+            const int64_t r0 = tile * T;
+            const int rows = (int)min((int64_t)T, n - r0);
+            const int rows_even = rows & ~1;
+            const double *B = buf + (size_t)s * NV * T;
+            const int jw0 = warp * 32 + 31;
+            if (2 * ((PPT - 1) * NCW * 32 + jw0) + 1 < rows_even) {  // whole tile slice valid
+                double2 xv[PPT], yv[PPT];
+#pragma unroll
+                for (int u = 0; u < PPT; ++u) {
+                    const int j = u * NCW * 32 + warp * 32 + lane;
+                    xv[u] = ((const double2 *)B)[j];
+                    yv[u] = ((const double2 *)(B + T))[j];
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);  // operands are in registers: free the slot early
+#pragma unroll
+                for (int u = 0; u < PPT; ++u) {
+                    double res[4];
+                    acc.step(xv[u].x, yv[u].x, is_zero(xv[u].x) | is_zero(yv[u].x), res[0], res[1], flags);
+                    acc.step(xv[u].y, yv[u].y, is_zero(xv[u].y) | is_zero(yv[u].y), res[2], res[3], flags);
+                    if (__any_sync(0xFFFFFFFFu, any_nonzero(res, 4))) {
+                        acc.spill(res[0], res[1], S.w[0]);
+                        acc.spill(res[2], res[3], S.w[0]);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < PPT; ++u) {
+                    const int j = u * NCW * 32 + warp * 32 + lane;
+                    for (int h = 0; h < 2; ++h) {
+                        const int lr = 2 * j + h;
+                        if (lr >= rows) break;
+                        const bool m = lr < rows_even;
+                        const double xv = m ? B[lr] : a.x[0][r0 + lr], yv = m ? B[T + lr] : a.y[0][r0 + lr];
+                        double rp, re;
+                        acc.step(xv, yv, is_zero(xv) | is_zero(yv), rp, re, flags);
+                        acc.spill(rp, re, S.w[0]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+            }
+            if (++s == STAGES) { s = 0; ph ^= 1u; }
+        }
+    }
+    acc.warp_merge(S.w[0]);
+    if (cta_sacc_publish<1>(S, flags, a.gacc, a.ticket))
+        last_cta_finish<1>(S, a.gacc, a.ticket, a.phase, a.finalize, a.sc, a.hist, a.out, a.out_flags,
+                           a.phase == PH_EXDOT ? a.x[0] : nullptr, a.y[0], a.n);
+}
+
+}  // namespace pbcg

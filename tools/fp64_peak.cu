@@ -25,7 +25,9 @@ __global__ void dadd_loop(double *out, int iters, double a) {
     for (int j = 0; j < 8; ++j) s += c[j];
     if (s == 12345.678) out[0] = s;
 }
-int main() {
+int lat_main();
+int main(int argc, char **argv) {
+    if (argc > 1) return lat_main();
     int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     double *d; cudaMalloc(&d, 8);
     int iters = 20000, bs = 256, grid = nsm * 8;
@@ -40,5 +42,28 @@ int main() {
         printf("{\"op\": \"%s\", \"Gop_per_s\": %.1f, \"per_sm_per_clk_at_1965MHz\": %.2f, \"ms\": %.3f}\n",
                k == 0 ? "DFMA" : "DADD", ops / ms / 1e6, ops / (ms * 1e-3) / nsm / 1.965e9, ms);
     }
+    return 0;
+}
+// ---- latency probe (single thread, dependent chains), run with argv[1] == "lat"
+__global__ void lat_kernel(double *out, long long *cyc, double a, int n) {
+    double x = a;
+    long long t0 = clock64();
+    for (int i = 0; i < n; ++i) x = __dadd_rn(x, a);
+    long long t1 = clock64();
+    double y = a;
+    long long t2 = clock64();
+    for (int i = 0; i < n; ++i) y = __fma_rn(y, a, a);
+    long long t3 = clock64();
+    out[0] = x + y;
+    cyc[0] = t1 - t0;
+    cyc[1] = t3 - t2;
+}
+int lat_main() {
+    double *d; long long *c; cudaMalloc(&d, 8); cudaMalloc(&c, 16);
+    int n = 4096;
+    lat_kernel<<<1, 1>>>(d, c, 1e-9, n);
+    lat_kernel<<<1, 1>>>(d, c, 1e-9, n);
+    long long h[2]; cudaMemcpy(h, c, 16, cudaMemcpyDeviceToHost);
+    printf("{\"DADD_latency_cycles\": %.2f, \"DFMA_latency_cycles\": %.2f}\n", (double)h[0] / n, (double)h[1] / n);
     return 0;
 }
