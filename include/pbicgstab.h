@@ -201,6 +201,16 @@ int pbcg_profile_iterations(pbcg_handle *h, int32_t k, double *ms);
 /* Iterations per captured CUDA-graph chunk used by pbicgstab_iterate (>= 1). */
 int pbcg_set_chunk(int32_t iters);
 
+/* Copy internal vector `which` (0 b, 1 x, 2 r, 3 r^, 4 p, 5 s, 6 z, 7 q,
+ * 8 y, 9 w, 10 t, 11 v; this rank's rows, virtual ranks: all rows) to `out`
+ * (device or host, n_local doubles).  Synchronises.  Tests and diagnostics. */
+int pbcg_get_vector(pbcg_handle *h, int32_t which, double *out);
+
+/* Spill counters of a -DPBCG_DEBUG_COUNTERS build (16 uint64; zeros in the
+ * release build): [1] warp spill votes, [2] overflow-tier entries, [3]
+ * superaccumulator deposits.  reset != 0 clears them. */
+int pbcg_debug_counters(uint64_t *out16, int32_t reset);
+
 /* ---- host-only planning helpers (no GPU needed; CPU-testable) ------------ */
 
 /* Balanced contiguous partition of n rows over p ranks (SPEC.md l.148,

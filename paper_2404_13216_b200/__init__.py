@@ -65,7 +65,7 @@ def lib(build_if_missing: bool = True) -> ctypes.CDLL:
     """Load the in-tree CUDA library (building it with nvcc if it is missing)."""
     global _lib
     if _lib is None:
-        if build_if_missing and _build.needs_build():
+        if build_if_missing and not os.environ.get("PBCG_LIB") and _build.needs_build():
             _build.build()
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} is missing: run paper_2404_13216_b200/build.py (no CPU fallback)")
@@ -92,6 +92,8 @@ def lib(build_if_missing: bool = True) -> ctypes.CDLL:
         L.pbcg_sacc_round.argtypes = [vp, vp]
         L.pbcg_set_chunk.argtypes = [i32]
         L.pbcg_profile_iterations.argtypes = [vp, i32, vp]
+        L.pbcg_debug_counters.argtypes = [vp, i32]
+        L.pbcg_get_vector.argtypes = [vp, i32, vp]
         _lib = L
     return _lib
 
@@ -252,6 +254,14 @@ class Solver:
         _check(lib().pbcg_profile_iterations(self._h, int(k), ctypes.c_void_p(ms.ctypes.data)))
         return ms
 
+    VEC = dict(b=0, x=1, r=2, rh=3, p=4, s=5, z=6, q=7, y=8, w=9, t=10, v=11)
+
+    def vec(self, name: str) -> np.ndarray:
+        """Host copy of an internal vector (the oracle's names)."""
+        out = np.empty(self.n_local_vec, np.float64)
+        _check(lib().pbcg_get_vector(self._h, self.VEC[name], ctypes.c_void_p(out.ctypes.data)))
+        return out
+
     def history(self, max_rows: int = 1 << 20) -> np.ndarray:
         buf = np.zeros((max_rows, H_COLS), np.float64)
         rows = ctypes.c_int32(0)
@@ -368,3 +378,11 @@ def sacc_round(words: np.ndarray) -> float:
     if rc not in (0, 6):
         _check(rc)
     return out.value
+
+
+def debug_counters(reset: bool = True) -> np.ndarray:
+    """Spill counters of a -DPBCG_DEBUG_COUNTERS build (zeros otherwise):
+    [1] warp spill votes taken (K2/K3), [2] lane overflow() calls, [3] deposits."""
+    out = np.zeros(16, np.uint64)
+    _check(lib().pbcg_debug_counters(ctypes.c_void_p(out.ctypes.data), int(reset)))
+    return out

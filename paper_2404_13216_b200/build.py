@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libpbicgstab.so")
+LIB = os.environ.get("PBCG_LIB") or os.path.join(HERE, "libpbicgstab.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
@@ -44,20 +44,28 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    target = out or LIB
+    if out is None and not force and not needs_build():
         return LIB
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-fmad=false", "-Xcompiler", "-fPIC,-O2", "-shared",
            "-I", os.path.join(ROOT, "include"), "-I", nccl_include(),
-           "-o", LIB + ".tmp", os.path.join(CSRC, "runtime.cu"), "-ldl", "-lcudart"]
+           "-o", target + ".tmp", os.path.join(CSRC, "runtime.cu"), "-ldl", "-lcudart"] + [f"-D{d}" for d in defines]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     print("[build]", " ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    if "--variant" in sys.argv:  # python build.py --variant NAME DEFINE...
+        i = sys.argv.index("--variant")
+        build(force=True, out=os.path.join(HERE, f"libpbicgstab_{sys.argv[i + 1]}.so"), defines=tuple(sys.argv[i + 2:]))
+    elif "--debug-counters" in sys.argv:
+        build(force=True, verbose="-v" in sys.argv, out=os.path.join(HERE, "libpbicgstab_dbg.so"),
+              defines=("PBCG_DEBUG_COUNTERS",))
+    else:
+        build(force="--force" in sys.argv, verbose="-v" in sys.argv)

@@ -39,6 +39,15 @@ constexpr int SACC_FLAGW = 2;  // two trailing words: #CTAs with a range flag, w
 
 enum : unsigned { FLAG_RANGE = 1u, FLAG_NONFINITE = 2u };
 
+// Diagnostic counters (built only with -DPBCG_DEBUG_COUNTERS): spill events
+// per kernel family, read back with pbcg_debug_counters().
+__device__ unsigned long long g_dbg[16];
+#ifdef PBCG_DEBUG_COUNTERS
+#define PBCG_COUNT(i) atomicAdd(&g_dbg[(i)], 1ull)
+#else
+#define PBCG_COUNT(i) ((void)0)
+#endif
+
 __device__ __forceinline__ void two_sum(double a, double b, double &s, double &e) {
     // Knuth TwoSum, 6 DADD, exact for all finite a, b without overflow.
     s = __dadd_rn(a, b);
@@ -106,6 +115,7 @@ __host__ __device__ __forceinline__ bool sacc_split(double v, int &i, long long 
 // Deposit a finite double into a superaccumulator in shared memory (the
 // rare path: kept out of line so the streaming loops stay small).
 __device__ __noinline__ void sacc_deposit(unsigned long long *acc, double v) {
+    PBCG_COUNT(3);
     int i;
     long long c0, c1, c2;
     if (!sacc_split(v, i, c0, c1, c2)) return;
@@ -309,6 +319,7 @@ struct ExAcc3 {
         O.zero();
     }
     __device__ __forceinline__ void overflow(double rp, double re, unsigned long long *sacc) {
+        PBCG_COUNT(2);
         double r = O.add(rp);
         if (is_nonzero(r)) sacc_deposit(sacc, r);
         r = O.add(re);
@@ -383,6 +394,123 @@ struct ExAcc3 {
         }
     }
 };
+
+// Two-tier accumulator used by the streaming kernels.  Each product p and its
+// TwoProd error e enter short hot expansions P, E (NH levels each, branch
+// free).  What falls out of them -- values far below this thread's running
+// sums, e.g. the 1e-16 interior residue of b = A*ones next to O(1) boundary
+// entries, whose products spread over 150-200 bits -- continues into the
+// cold levels CP, CE (NC levels each; independent chains for p and e).  One
+// warp vote per batch of products decides whether the cold levels run, and a
+// second one whether anything fell out of them into the shared
+// superaccumulator.  Together the tiers are one exact cascade of NH+NC
+// levels per stream; all steps are TwoSums, so tiering only affects speed.
+struct Prod {
+    double p, e;
+};
+
+template <int NH, int NC>
+struct ExAccT {
+    Fpe<NH> P, E;
+    Fpe<NC> CP, CE;
+    __device__ __forceinline__ void zero() {
+        P.zero(); E.zero(); CP.zero(); CE.zero();
+    }
+    // TwoProd + the R-9 range flag (branch free).  zero_op: x or y is +-0.
+    __device__ __forceinline__ Prod prep(double x, double y, bool zero_op, unsigned &flags) const {
+        Prod r;
+        r.p = __dmul_rn(x, y);
+        r.e = __fma_rn(x, y, -r.p);
+        const unsigned ep = (unsigned)(__double2hiint(r.p) >> 20) & 0x7FFu;
+        flags |= (((ep - 63u) >= 1960u) & !zero_op) | (ep == 0x7FFu);
+        return r;
+    }
+    __device__ __forceinline__ void hot(const Prod &q, double *res) {
+        res[0] = P.add(q.p);
+        res[1] = E.add(q.e);
+    }
+    __device__ __forceinline__ void cold(const double *in, double *res) {
+        res[0] = CP.add(in[0]);
+        res[1] = CE.add(in[1]);
+    }
+    template <int N>
+    __device__ __forceinline__ static void merge_fpe(Fpe<N> &F, int off, bool recv, unsigned long long *sacc) {
+        double in[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) in[j] = __shfl_down_sync(0xFFFFFFFFu, F.a[j], off);
+        if (recv) {
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                double r = F.add(in[j]);
+                if (is_nonzero(r)) sacc_deposit(sacc, r);
+            }
+        }
+    }
+    template <int N>
+    __device__ __forceinline__ static void drain(Fpe<N> &F, unsigned long long *sacc) {
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+            if (is_nonzero(F.a[j])) sacc_deposit(sacc, F.a[j]);
+    }
+    // merge the lanes of the warp into lane 0, which deposits its terms
+    __device__ __forceinline__ void warp_merge(unsigned long long *sacc) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            const bool recv = lane < off;
+            merge_fpe<NH>(P, off, recv, sacc);
+            merge_fpe<NH>(E, off, recv, sacc);
+            merge_fpe<NC>(CP, off, recv, sacc);
+            merge_fpe<NC>(CE, off, recv, sacc);
+        }
+        if (lane == 0) {
+            drain<NH>(P, sacc); drain<NH>(E, sacc); drain<NC>(CP, sacc); drain<NC>(CE, sacc);
+        }
+    }
+};
+
+// Deposit every nonzero residual of a batch (the rare path).
+__device__ __forceinline__ void deposit_residuals(const double *res, int n, unsigned long long *sacc) {
+#pragma unroll
+    for (int i = 0; i < n; ++i)
+        if (is_nonzero(res[i])) sacc_deposit(sacc, res[i]);
+}
+
+// Accumulate a batch of K prepared products with one vote per tier.  Product
+// k goes to d1 when ALT and k is odd, else to d0 (s0/s1: their shared
+// superaccumulators).  All 32 lanes must be active.
+template <int K, bool ALT, class A>
+__device__ __forceinline__ void cascade_batch(A &d0, A &d1, const Prod (&P)[K], unsigned long long *s0,
+                                              unsigned long long *s1) {
+    double r[2 * K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        if (ALT && (k & 1)) d1.hot(P[k], r + 2 * k); else d0.hot(P[k], r + 2 * k);
+    }
+    if (__any_sync(0xFFFFFFFFu, any_nonzero(r, 2 * K))) {
+        PBCG_COUNT(1);
+        double c[2 * K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (ALT && (k & 1)) d1.cold(r + 2 * k, c + 2 * k); else d0.cold(r + 2 * k, c + 2 * k);
+        }
+        if (__any_sync(0xFFFFFFFFu, any_nonzero(c, 2 * K))) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) deposit_residuals(c + 2 * k, 2, (ALT && (k & 1)) ? s1 : s0);
+        }
+    }
+}
+
+// Same, for lanes that may be inactive or diverged (tails): no votes.
+template <class A>
+__device__ __forceinline__ void cascade_one(A &d, const Prod &q, unsigned long long *s) {
+    double r[2], c[2];
+    d.hot(q, r);
+    if (any_nonzero(r, 2)) {
+        d.cold(r, c);
+        deposit_residuals(c, 2, s);
+    }
+}
 
 // Shared-memory state of a CTA computing ND dots.
 template <int ND>

@@ -558,13 +558,19 @@ static int multidot(pbcg_handle *h, int ph, int phase, int nd, const double *con
 // one iteration of Algorithm 2 (enqueue only)
 // ----------------------------------------------------------------------------
 // Streaming (TMA-pipelined) kernel geometry -- performance parameters only.
-static constexpr int S_NP = 2, S_NE = 2, S_NO = 3, S_NCW = 7;  // S_NCW: warps per dot group (2*7+1 = 15 warps)
+#ifndef PBCG_S_NC
+#define PBCG_S_NC 3
+#endif
+static constexpr int S_NH = 2, S_NL = PBCG_S_NC, S_NCW = 7;  // hot/cold levels; S_NCW warps per dot group (2*7+1 = 15 warps)
 static constexpr int X_NCW = 8;
-static constexpr int X_NP = 3, X_NE = 3, X_NO = 2;              // standalone EXDOT (wider dynamic range)
+#ifndef PBCG_X_NH
+#define PBCG_X_NH 2
+#endif
+static constexpr int X_NH = PBCG_X_NH, X_NL = 2;  // standalone EXDOT: hot / cold levels
 static constexpr int K2_PPT = 1, K2_ST = 4, K3_PPT = 1, K3_ST = 4, XD_PPT = 4, XD_ST = 4;
-#define K2S k2_stream<S_NP, S_NE, S_NO, S_NCW, K2_PPT, K2_ST>
-#define K3S k3_stream<S_NP, S_NE, S_NO, S_NCW, K3_PPT, K3_ST>
-#define XDS exdot_stream<X_NP, X_NE, X_NO, X_NCW, XD_PPT, XD_ST>
+#define K2S k2_stream<S_NH, S_NL, S_NCW, K2_PPT, K2_ST>
+#define K3S k3_stream<S_NH, S_NL, S_NCW, K3_PPT, K3_ST>
+#define XDS exdot_stream<X_NH, X_NL, X_NCW, XD_PPT, XD_ST>
 static constexpr size_t ring_bytes(int nv, int ncw, int ppt, int stages) {
     return sizeof(double) * (size_t)stages * nv * (2 * ncw * 32 * ppt) + 2 * sizeof(uint64_t) * stages;
 }
@@ -1168,6 +1174,33 @@ extern "C" int pbcg_profile_iterations(pbcg_handle *h, int32_t k, double *ms) {
     for (auto &e : ev) cudaEventDestroy(e);
     if (se != cudaSuccess) return fail(PBCG_ECUDA, "profile: %s", cudaGetErrorString(se));
     return rc;
+}
+
+// Copy an internal solver vector (this rank's rows; virtual ranks: all rows)
+// to `out` (device or host): 0 b, 1 x, 2 r, 3 r^, 4 p, 5 s, 6 z, 7 q, 8 y,
+// 9 w, 10 t, 11 v -- the oracle's numbering.  Synchronises the stream.
+extern "C" int pbcg_get_vector(pbcg_handle *h, int32_t which, double *out) {
+    if (!h || h->comm_only || !out || which < 0 || which > 11) return fail(PBCG_EINVAL, "get_vector: bad arguments");
+    const bool host = is_host_ptr(out);
+    for (auto &R : h->R) {
+        double *tab[12] = {R.b, R.x, R.r, R.rh, R.p, R.s, R.z(), R.q, R.y, R.w(), R.t, R.v};
+        const int64_t off = h->V > 1 ? R.rb : 0;
+        CUDA_TRY(cudaMemcpyAsync(out + off, tab[which], sizeof(double) * R.n,
+                                 host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, h->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    return PBCG_OK;
+}
+
+// Diagnostic spill counters (non-zero only in a -DPBCG_DEBUG_COUNTERS build).
+extern "C" int pbcg_debug_counters(uint64_t *out16, int32_t reset) {
+    if (!out16) return fail(PBCG_EINVAL, "null");
+    CUDA_TRY(cudaMemcpyFromSymbol(out16, g_dbg, sizeof(unsigned long long) * 16));
+    if (reset) {
+        unsigned long long z[16] = {};
+        CUDA_TRY(cudaMemcpyToSymbol(g_dbg, z, sizeof(z)));
+    }
+    return PBCG_OK;
 }
 
 // kernel tuning knobs for benchmarks (not part of the numerical contract)

@@ -91,9 +91,9 @@ __device__ __forceinline__ size_t stream_smem_bytes() {
 // Splitting the dots halves the accumulator registers per thread, which buys
 // twice the warps (the ExBLAS cascades are latency-bound chains of DADDs).
 // ---------------------------------------------------------------------------
-template <int NP, int NE, int NO>
+template <int NH, int NL>
 struct K2Op {
-    ExAcc3<NP, NE, NO> d0, d1;
+    ExAccT<NH, NL> d0, d1;
     double be, nom, nal;
     bool first;
     __device__ __forceinline__ void sz(double w, double t, double v, double &s, double &z) const {
@@ -104,32 +104,28 @@ struct K2Op {
             z = __fma_rn(be, __fma_rn(nom, v, z), t);  // z := t + beta (z - omega v)   l.72
         }
     }
-    // group 0: p,s,z,q,y and (q,y), (y,y)
+    // group 0: p,s,z,q,y and the products of (q,y), (y,y)
     __device__ __forceinline__ void row0(unsigned &flags, double r, double w, double t, double v, double &p,
-                                         double &s, double &z, double &q, double &y, double *res) {
+                                         double &s, double &z, double &q, double &y, Prod &P0, Prod &P1) {
         p = first ? r : __fma_rn(be, __fma_rn(nom, s, p), r);  // p := r + beta (p - omega s)   l.70
         sz(w, t, v, s, z);
         q = __fma_rn(nal, s, r);  // q := r - alpha s   l.73
         y = __fma_rn(nal, z, w);  // y := w - alpha z   l.74
         const bool zy = is_zero(y);
-        d0.step(q, y, is_zero(q) | zy, res[0], res[1], flags);
-        d1.step(y, y, zy, res[2], res[3], flags);
+        P0 = d0.prep(q, y, is_zero(q) | zy, flags);
+        P1 = d1.prep(y, y, zy, flags);
     }
-    // group 1: s,z and (r0,s), (r0,z)
+    // group 1: s,z and the products of (r0,s), (r0,z)
     __device__ __forceinline__ void row1(unsigned &flags, double rh, double w, double t, double v, double s, double z,
-                                         double *res) {
+                                         Prod &P0, Prod &P1) {
         sz(w, t, v, s, z);
         const bool zr = is_zero(rh);
-        d0.step(rh, s, zr | is_zero(s), res[0], res[1], flags);
-        d1.step(rh, z, zr | is_zero(z), res[2], res[3], flags);
-    }
-    __device__ __forceinline__ void spill(const double *res, unsigned long long *s0, unsigned long long *s1) {
-        d0.spill(res[0], res[1], s0);
-        d1.spill(res[2], res[3], s1);
+        P0 = d0.prep(rh, s, zr | is_zero(s), flags);
+        P1 = d1.prep(rh, z, zr | is_zero(z), flags);
     }
 };
 
-template <int NP, int NE, int NO, int W, int PPT, int STAGES>
+template <int NH, int NL, int W, int PPT, int STAGES>
 __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
     constexpr int NV = 8;  // r, rh, w, t | p, s, z, v
     constexpr int NCW = 2 * W;
@@ -151,7 +147,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
     const bool first = (sc->it == 0);
     const int64_t n = a.n;
     unsigned flags = 0;
-    K2Op<NP, NE, NO> R;
+    K2Op<NH, NL> R;
     R.first = first;
     R.be = sc->beta;
     R.nom = -sc->omega;
@@ -186,24 +182,21 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
                     const double2 w = B2[2 * TP + j], t = B2[3 * TP + j];
                     double2 ss, z, v;
                     if (!first) { ss = B2[5 * TP + j]; z = B2[6 * TP + j]; v = B2[7 * TP + j]; }
-                    double res0[4], res1[4];
+                    Prod P[4];
                     if (g == 0) {
                         const double2 r = B2[0 * TP + j];
                         double2 p, q, y;
                         if (!first) p = B2[4 * TP + j];
-                        R.row0(flags, r.x, w.x, t.x, v.x, p.x, ss.x, z.x, q.x, y.x, res0);
-                        R.row0(flags, r.y, w.y, t.y, v.y, p.y, ss.y, z.y, q.y, y.y, res1);
+                        R.row0(flags, r.x, w.x, t.x, v.x, p.x, ss.x, z.x, q.x, y.x, P[0], P[1]);
+                        R.row0(flags, r.y, w.y, t.y, v.y, p.y, ss.y, z.y, q.y, y.y, P[2], P[3]);
                         ((double2 *)a.p)[gp] = p; ((double2 *)a.s)[gp] = ss; ((double2 *)a.z)[gp] = z;
                         ((double2 *)a.q)[gp] = q; ((double2 *)a.y)[gp] = y;
                     } else {
                         const double2 rh = B2[1 * TP + j];
-                        R.row1(flags, rh.x, w.x, t.x, v.x, ss.x, z.x, res0);
-                        R.row1(flags, rh.y, w.y, t.y, v.y, ss.y, z.y, res1);
+                        R.row1(flags, rh.x, w.x, t.x, v.x, ss.x, z.x, P[0], P[1]);
+                        R.row1(flags, rh.y, w.y, t.y, v.y, ss.y, z.y, P[2], P[3]);
                     }
-                    if (__any_sync(0xFFFFFFFFu, any_nonzero(res0, 4) | any_nonzero(res1, 4))) {
-                        R.spill(res0, s0, s1);
-                        R.spill(res1, s0, s1);
-                    }
+                    cascade_batch<4, true>(R.d0, R.d1, P, s0, s1);
                 } else {
                     for (int h = 0; h < 2; ++h) {
                         const int lr = 2 * j + h;  // local row
@@ -211,7 +204,8 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
                         const int64_t gi = r0 + lr;
                         const bool m = lr < rows_even;
                         const double w = m ? B[2 * T + lr] : a.w[gi], t = m ? B[3 * T + lr] : a.t[gi];
-                        double ss = 0, z = 0, v = 0, res[4];
+                        double ss = 0, z = 0, v = 0;
+                        Prod P0, P1;
                         if (!first) {
                             ss = m ? B[5 * T + lr] : a.s[gi]; z = m ? B[6 * T + lr] : a.z[gi];
                             v = m ? B[7 * T + lr] : a.v[gi];
@@ -220,12 +214,13 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
                             const double r = m ? B[0 * T + lr] : a.r[gi];
                             double p = 0, q, y;
                             if (!first) p = m ? B[4 * T + lr] : a.p[gi];
-                            R.row0(flags, r, w, t, v, p, ss, z, q, y, res);
+                            R.row0(flags, r, w, t, v, p, ss, z, q, y, P0, P1);
                             a.p[gi] = p; a.s[gi] = ss; a.z[gi] = z; a.q[gi] = q; a.y[gi] = y;
                         } else {
-                            R.row1(flags, m ? B[1 * T + lr] : a.rh[gi], w, t, v, ss, z, res);
+                            R.row1(flags, m ? B[1 * T + lr] : a.rh[gi], w, t, v, ss, z, P0, P1);
                         }
-                        R.spill(res, s0, s1);
+                        cascade_one(R.d0, P0, s0);
+                        cascade_one(R.d1, P1, s1);
                     }
                 }
             }
@@ -244,32 +239,28 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
 // K3 (Alg. 2 l.77-79) + phase-B dots.  Group 0: x, r' and (r0,r'), (r',r');
 // group 1: w' and (r0,w').
 // ---------------------------------------------------------------------------
-template <int NP, int NE, int NO>
+template <int NH, int NL>
 struct K3Op {
-    ExAcc3<NP, NE, NO> d0, d1;
+    ExAccT<NH, NL> d0, d1;
     double al, om, nal, nom;
+    // group 0: x, r' and the products of (r0,r'), (r',r')
     __device__ __forceinline__ void row0(unsigned &flags, double rh, double p, double q, double y, double &x, double &r,
-                                         double *res) {
+                                         Prod &P0, Prod &P1) {
         x = __fma_rn(om, q, __fma_rn(al, p, x));  // x := x + alpha p + omega q      l.77
         r = __fma_rn(nom, y, q);                  // r := q - omega y                l.78
         const bool zr = is_zero(r);
-        d0.step(rh, r, is_zero(rh) | zr, res[0], res[1], flags);
-        d1.step(r, r, zr, res[2], res[3], flags);
+        P0 = d0.prep(rh, r, is_zero(rh) | zr, flags);
+        P1 = d1.prep(r, r, zr, flags);
     }
+    // group 1: w' and the product of (r0,w')
     __device__ __forceinline__ void row1(unsigned &flags, double rh, double y, double t, double v, double &w,
-                                         double *res) {
+                                         Prod &P0) {
         w = __fma_rn(nom, __fma_rn(nal, v, t), y);  // w := y - omega (t - alpha v)    l.79
-        d0.step(rh, w, is_zero(rh) | is_zero(w), res[0], res[1], flags);
-        res[2] = 0.0;
-        res[3] = 0.0;
-    }
-    __device__ __forceinline__ void spill(const double *res, unsigned long long *s0, unsigned long long *s1) {
-        d0.spill(res[0], res[1], s0);
-        d1.spill(res[2], res[3], s1);
+        P0 = d0.prep(rh, w, is_zero(rh) | is_zero(w), flags);
     }
 };
 
-template <int NP, int NE, int NO, int W, int PPT, int STAGES>
+template <int NH, int NL, int W, int PPT, int STAGES>
 __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
     constexpr int NV = 7;  // rh, p, q, y, t, v, x
     constexpr int NCW = 2 * W;
@@ -290,7 +281,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
     __syncthreads();
     const int64_t n = a.n;
     unsigned flags = 0;
-    K3Op<NP, NE, NO> R;
+    K3Op<NH, NL> R;
     R.al = sc->alpha;
     R.om = sc->omega;
     R.nal = -R.al;
@@ -324,23 +315,22 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
                 const int64_t gp = (r0 >> 1) + j;
                 if (2 * jw + 1 < rows_even) {
                     const double2 rh = B2[0 * TP + j], y = B2[3 * TP + j];
-                    double res0[4], res1[4];
                     if (g == 0) {
                         const double2 p = B2[1 * TP + j], q = B2[2 * TP + j];
                         double2 x = B2[6 * TP + j], r;
-                        R.row0(flags, rh.x, p.x, q.x, y.x, x.x, r.x, res0);
-                        R.row0(flags, rh.y, p.y, q.y, y.y, x.y, r.y, res1);
+                        Prod P[4];
+                        R.row0(flags, rh.x, p.x, q.x, y.x, x.x, r.x, P[0], P[1]);
+                        R.row0(flags, rh.y, p.y, q.y, y.y, x.y, r.y, P[2], P[3]);
                         ((double2 *)a.x)[gp] = x; ((double2 *)a.r)[gp] = r;
+                        cascade_batch<4, true>(R.d0, R.d1, P, s0, s1);
                     } else {
                         const double2 t = B2[4 * TP + j], v = B2[5 * TP + j];
                         double2 w;
-                        R.row1(flags, rh.x, y.x, t.x, v.x, w.x, res0);
-                        R.row1(flags, rh.y, y.y, t.y, v.y, w.y, res1);
+                        Prod P[2];
+                        R.row1(flags, rh.x, y.x, t.x, v.x, w.x, P[0]);
+                        R.row1(flags, rh.y, y.y, t.y, v.y, w.y, P[1]);
                         ((double2 *)a.w)[gp] = w;
-                    }
-                    if (__any_sync(0xFFFFFFFFu, any_nonzero(res0, 4) | any_nonzero(res1, 4))) {
-                        R.spill(res0, s0, s1);
-                        R.spill(res1, s0, s1);
+                        cascade_batch<2, false>(R.d0, R.d1, P, s0, s1);
                     }
                 } else {
                     for (int h = 0; h < 2; ++h) {
@@ -349,17 +339,20 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
                         const int64_t gi = r0 + lr;
                         const bool m = lr < rows_even;
                         const double rh = m ? B[0 * T + lr] : a.rh[gi], y = m ? B[3 * T + lr] : a.y[gi];
-                        double res[4];
                         if (g == 0) {
                             double x = m ? B[6 * T + lr] : a.x[gi], r;
-                            R.row0(flags, rh, m ? B[1 * T + lr] : a.p[gi], m ? B[2 * T + lr] : a.q[gi], y, x, r, res);
+                            Prod P0, P1;
+                            R.row0(flags, rh, m ? B[1 * T + lr] : a.p[gi], m ? B[2 * T + lr] : a.q[gi], y, x, r, P0, P1);
                             a.x[gi] = x; a.r[gi] = r;
+                            cascade_one(R.d0, P0, s0);
+                            cascade_one(R.d1, P1, s1);
                         } else {
                             double w;
-                            R.row1(flags, rh, y, m ? B[4 * T + lr] : a.t[gi], m ? B[5 * T + lr] : a.v[gi], w, res);
+                            Prod P0;
+                            R.row1(flags, rh, y, m ? B[4 * T + lr] : a.t[gi], m ? B[5 * T + lr] : a.v[gi], w, P0);
                             a.w[gi] = w;
+                            cascade_one(R.d0, P0, s0);
                         }
-                        R.spill(res, s0, s1);
                     }
                 }
             }
@@ -377,7 +370,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
 // ---------------------------------------------------------------------------
 // Standalone EXDOT (one dot, x and y 16-byte aligned)
 // ---------------------------------------------------------------------------
-template <int NP, int NE, int NO, int NCW, int PPT, int STAGES>
+template <int NH, int NL, int NCW, int PPT, int STAGES>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a) {
     constexpr int NV = 2;
     constexpr int T = TileGeo<NCW, PPT>::T;
@@ -396,7 +389,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a
     __syncthreads();
     const int64_t n = a.n;
     unsigned flags = 0;
-    ExAcc3<NP, NE, NO> acc;
+    ExAccT<NH, NL> acc;
     acc.zero();
     if (warp == NCW) {
         if (lane == 0) {
@@ -425,14 +418,14 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);  // operands are in registers: free the slot early
 #pragma unroll
-                for (int u = 0; u < PPT; ++u) {
-                    double res[4];
-                    acc.step(xv[u].x, yv[u].x, is_zero(xv[u].x) | is_zero(yv[u].x), res[0], res[1], flags);
-                    acc.step(xv[u].y, yv[u].y, is_zero(xv[u].y) | is_zero(yv[u].y), res[2], res[3], flags);
-                    if (__any_sync(0xFFFFFFFFu, any_nonzero(res, 4))) {
-                        acc.spill(res[0], res[1], S.w[0]);
-                        acc.spill(res[2], res[3], S.w[0]);
+                for (int u = 0; u < PPT; u += 2) {
+                    Prod P[4];
+#pragma unroll
+                    for (int h = 0; h < 2 && u + h < PPT; ++h) {
+                        P[2 * h] = acc.prep(xv[u + h].x, yv[u + h].x, is_zero(xv[u + h].x) | is_zero(yv[u + h].x), flags);
+                        P[2 * h + 1] = acc.prep(xv[u + h].y, yv[u + h].y, is_zero(xv[u + h].y) | is_zero(yv[u + h].y), flags);
                     }
+                    cascade_batch<4, false>(acc, acc, P, S.w[0], S.w[0]);
                 }
             } else {
 #pragma unroll
@@ -443,9 +436,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a
                         if (lr >= rows) break;
                         const bool m = lr < rows_even;
                         const double xv = m ? B[lr] : a.x[0][r0 + lr], yv = m ? B[T + lr] : a.y[0][r0 + lr];
-                        double rp, re;
-                        acc.step(xv, yv, is_zero(xv) | is_zero(yv), rp, re, flags);
-                        acc.spill(rp, re, S.w[0]);
+                        cascade_one(acc, acc.prep(xv, yv, is_zero(xv) | is_zero(yv), flags), S.w[0]);
                     }
                 }
                 __syncwarp();
