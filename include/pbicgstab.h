@@ -193,9 +193,11 @@ int pbcg_abi_version(void);
 /* ---- measurement hooks (not part of the numerical contract) -------------- */
 
 /* Enqueue k more iterations of a started single-rank solve as direct launches
- * bracketed by CUDA events on the handle's stream, synchronise, and return in
- * ms[0..3] the summed device time of K2 (l.70-74 + phase-A dots), SpMV v=Az
- * (l.75), K3 (l.77-79 + phase-B dots) and SpMV t=Aw (l.80). */
+ * serialised on the handle's stream and bracketed by CUDA events, synchronise,
+ * and return in ms[0..5] the summed device time of K2 (l.70-74 + phase-A dot
+ * partials), finalize A (round, omega: l.76), SpMV v=Az (l.75), K3 (l.77-79 +
+ * phase-B partials), finalize B (round, beta/alpha/stop: l.81-82) and SpMV
+ * t=Aw (l.80).  (In iterate() the finalizes overlap the SpMVs.) */
 int pbcg_profile_iterations(pbcg_handle *h, int32_t k, double *ms);
 
 /* Iterations per captured CUDA-graph chunk used by pbicgstab_iterate (>= 1). */

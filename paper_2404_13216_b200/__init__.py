@@ -248,9 +248,10 @@ class Solver:
         return self._result(res)
 
     def profile(self, k: int) -> np.ndarray:
-        """Summed ms of [K2, SpMV v=Az, K3, SpMV t=Aw] over k more iterations
-        (direct launches bracketed by CUDA events on the solver stream)."""
-        ms = np.zeros(4, np.float64)
+        """Summed ms of [K2, finalize A, SpMV v=Az, K3, finalize B, SpMV t=Aw]
+        over k more iterations (direct launches serialised and bracketed by
+        CUDA events on the solver stream)."""
+        ms = np.zeros(6, np.float64)
         _check(lib().pbcg_profile_iterations(self._h, int(k), ctypes.c_void_p(ms.ctypes.data)))
         return ms
 

@@ -44,8 +44,18 @@ enum : unsigned { FLAG_RANGE = 1u, FLAG_NONFINITE = 2u };
 __device__ unsigned long long g_dbg[16];
 #ifdef PBCG_DEBUG_COUNTERS
 #define PBCG_COUNT(i) atomicAdd(&g_dbg[(i)], 1ull)
+// phase timestamps (globaltimer, ns) of thread 0 of block 0: slots 8..12
+#define PBCG_TS(k)                                                                     \
+    do {                                                                               \
+        if ((threadIdx.x & 31) == 0) {                                                 \
+            unsigned long long t_;                                                     \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                     \
+            atomicMax(&g_dbg[8 + (k)], t_);                                            \
+        }                                                                              \
+    } while (0)
 #else
 #define PBCG_COUNT(i) ((void)0)
+#define PBCG_TS(k) ((void)0)
 #endif
 
 __device__ __forceinline__ void two_sum(double a, double b, double &s, double &e) {
@@ -112,6 +122,20 @@ __host__ __device__ __forceinline__ bool sacc_split(double v, int &i, long long 
     return true;
 }
 
+// Add a signed 64-bit value c to a 64-bit shared word using native 32-bit
+// shared atomics (sm_100 has no 64-bit shared atomic add; atomicAdd(u64*) on
+// shared memory compiles to a CAS loop).  The word is (lo, hi) little-endian;
+// the carry/borrow out of lo is derived from the value the atomic returned,
+// so concurrent additions stay exact (mod 2^64, i.e. two's complement).
+__device__ __forceinline__ void sacc_add_shared(unsigned long long *word, long long c) {
+    unsigned *p = reinterpret_cast<unsigned *>(word);
+    const unsigned lo_add = (unsigned)(unsigned long long)c;
+    const unsigned old = atomicAdd(p, lo_add);
+    const unsigned carry = ((unsigned long long)old + lo_add) >> 32;  // 0 or 1
+    const unsigned hi_add = (unsigned)(c >> 32) + carry;                  // -1, 0 or 1 (mod 2^32)
+    if (hi_add) atomicAdd(p + 1, hi_add);
+}
+
 // Deposit a finite double into a superaccumulator in shared memory (the
 // rare path: kept out of line so the streaming loops stay small).
 __device__ __noinline__ void sacc_deposit(unsigned long long *acc, double v) {
@@ -119,9 +143,9 @@ __device__ __noinline__ void sacc_deposit(unsigned long long *acc, double v) {
     int i;
     long long c0, c1, c2;
     if (!sacc_split(v, i, c0, c1, c2)) return;
-    if (c0) atomicAdd(&acc[i], (unsigned long long)c0);
-    if (c1) atomicAdd(&acc[i + 1], (unsigned long long)c1);
-    if (c2) atomicAdd(&acc[i + 2], (unsigned long long)c2);
+    if (c0) sacc_add_shared(&acc[i], c0);
+    if (c1) sacc_add_shared(&acc[i + 1], c1);
+    if (c2) sacc_add_shared(&acc[i + 2], c2);
 }
 
 // Host twin (CPU-side tests of the rounding path and of cross-rank merging).
@@ -302,98 +326,51 @@ struct ExAcc {
     }
 };
 
-// Three-tier accumulator used by the streaming kernels: P and E take the
-// rounded products and their errors (NP/NE levels, branch-free); whatever
-// falls out of them (values far below the running sums, e.g. the ~1e-16
-// interior entries of b = A*ones next to O(1) boundary entries) cascades into
-// the overflow expansion O, anchored at its own scale; only O's residual is
-// deposited into the shared superaccumulator.  All steps are exact TwoSums.
-template <int NP, int NE, int NO>
-struct ExAcc3 {
-    Fpe<NP> P;
-    Fpe<NE> E;
-    Fpe<NO> O;
-    __device__ __forceinline__ void zero() {
-        P.zero();
-        E.zero();
-        O.zero();
-    }
-    __device__ __forceinline__ void overflow(double rp, double re, unsigned long long *sacc) {
-        PBCG_COUNT(2);
-        double r = O.add(rp);
-        if (is_nonzero(r)) sacc_deposit(sacc, r);
-        r = O.add(re);
-        if (is_nonzero(r)) sacc_deposit(sacc, r);
-    }
-    // Branch-free part of one product: TwoProd, the R-9 range flag, P and E
-    // cascades.  rp/re are what fell out of P/E (exact); the caller batches
-    // the rare spill decision over several products (one warp vote).
-    // zero_op: x or y is +-0 (then p = e = 0 and the product is never flagged
-    // unless an operand is non-finite).
-    __device__ __forceinline__ void step(double x, double y, bool zero_op, double &rp, double &re,
-                                         unsigned &flags) {
-        const double p = __dmul_rn(x, y);
-        const double e = __fma_rn(x, y, -p);
-        const unsigned ep = (unsigned)(__double2hiint(p) >> 20) & 0x7FFu;
-        flags |= (((ep - 63u) >= 1960u) & !zero_op) | (ep == 0x7FFu);
-        rp = P.add(p);
-        re = E.add(e);
-    }
-    __device__ __forceinline__ void spill(double rp, double re, unsigned long long *sacc) {
-        if (is_nonzero(rp) | is_nonzero(re)) overflow(rp, re, sacc);
-    }
-    // EARLY: the overflow branch is taken warp-uniformly (all 32 lanes active)
-    template <bool EARLY = true>
-    __device__ __forceinline__ void add(double x, double y, unsigned long long *sacc, unsigned &flags) {
-        const double p = __dmul_rn(x, y);
-        const double e = __fma_rn(x, y, -p);
-        const unsigned ep = (unsigned)(__double2hiint(p) >> 20) & 0x7FFu;
-        if (ep - 63u >= 1960u) flags |= range_class(x, y);
-        const double rp = P.add(p);
-        const double re = E.add(e);
-        const bool spill = is_nonzero(rp) | is_nonzero(re);
-        if (EARLY) {
-            if (__any_sync(0xFFFFFFFFu, spill)) overflow(rp, re, sacc);
-        } else if (spill) {
-            overflow(rp, re, sacc);
+// Deposit every nonzero residual of a batch (the rare path).
+__device__ __forceinline__ void deposit_residuals(const double *res, int n, unsigned long long *sacc) {
+#pragma unroll
+    for (int i = 0; i < n; ++i)
+        if (is_nonzero(res[i])) sacc_deposit(sacc, res[i]);
+}
+
+// int64 sum over the warp with 4 REDUX.SUM on 16-bit limbs (exact mod 2^64;
+// each limb sum is < 32 * 2^16).  Result valid in every lane.
+__device__ __forceinline__ long long warp_sum_i64(long long v) {
+    const unsigned long long u = (unsigned long long)v;
+    const unsigned long long l0 = __reduce_add_sync(0xFFFFFFFFu, (unsigned)(u & 0xFFFFu));
+    const unsigned long long l1 = __reduce_add_sync(0xFFFFFFFFu, (unsigned)((u >> 16) & 0xFFFFu));
+    const unsigned long long l2 = __reduce_add_sync(0xFFFFFFFFu, (unsigned)((u >> 32) & 0xFFFFu));
+    const unsigned long long l3 = __reduce_add_sync(0xFFFFFFFFu, (unsigned)(u >> 48));
+    return (long long)(l0 + (l1 << 16) + (l2 << 32) + (l3 << 48));
+}
+
+// Deposit one double per lane (zeros allowed) into a shared superaccumulator.
+// When the warp's values touch at most 4 consecutive words (the usual case:
+// the lanes' expansion terms have similar exponents), the chunks are summed
+// across the warp first and lane 0 adds 4 words -- no same-address atomic
+// storms; otherwise every lane deposits its own value.  All 32 lanes active.
+__device__ __forceinline__ void warp_deposit(double v, unsigned long long *sacc) {
+    int i = 0;
+    long long c0 = 0, c1 = 0, c2 = 0;
+    const bool nz = is_nonzero(v) && sacc_split(v, i, c0, c1, c2);
+    const unsigned imin = __reduce_min_sync(0xFFFFFFFFu, nz ? (unsigned)i : 0xFFFFFFFFu);
+    if (imin == 0xFFFFFFFFu) return;  // all lanes zero
+    const unsigned imax = __reduce_max_sync(0xFFFFFFFFu, nz ? (unsigned)i : 0u);
+    if (imax - imin <= 1u && imin + 3u < (unsigned)SACC_L) {
+        const bool sh = nz && ((unsigned)i != imin);
+        if (!nz) { c0 = 0; c1 = 0; c2 = 0; }
+        const long long d0 = sh ? 0 : c0, d1 = sh ? c0 : c1, d2 = sh ? c1 : c2, d3 = sh ? c2 : 0;
+        const long long s0 = warp_sum_i64(d0), s1 = warp_sum_i64(d1), s2 = warp_sum_i64(d2), s3 = warp_sum_i64(d3);
+        if ((threadIdx.x & 31) == 0) {
+            if (s0) sacc_add_shared(&sacc[imin], s0);
+            if (s1) sacc_add_shared(&sacc[imin + 1], s1);
+            if (s2) sacc_add_shared(&sacc[imin + 2], s2);
+            if (s3) sacc_add_shared(&sacc[imin + 3], s3);
         }
+    } else if (nz) {
+        sacc_deposit(sacc, v);
     }
-    template <int N>
-    __device__ __forceinline__ static void merge_fpe(Fpe<N> &F, int off, bool recv, unsigned long long *sacc) {
-        double in[N];
-#pragma unroll
-        for (int j = 0; j < N; ++j) in[j] = __shfl_down_sync(0xFFFFFFFFu, F.a[j], off);
-        if (recv) {
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-                double r = F.add(in[j]);
-                if (is_nonzero(r)) sacc_deposit(sacc, r);
-            }
-        }
-    }
-    // merge the lanes of the warp into lane 0, which deposits its terms
-    __device__ __forceinline__ void warp_merge(unsigned long long *sacc) {
-        const int lane = threadIdx.x & 31;
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) {
-            const bool recv = lane < off;
-            merge_fpe<NP>(P, off, recv, sacc);
-            merge_fpe<NE>(E, off, recv, sacc);
-            merge_fpe<NO>(O, off, recv, sacc);
-        }
-        if (lane == 0) {
-#pragma unroll
-            for (int j = 0; j < NP; ++j)
-                if (is_nonzero(P.a[j])) sacc_deposit(sacc, P.a[j]);
-#pragma unroll
-            for (int j = 0; j < NE; ++j)
-                if (is_nonzero(E.a[j])) sacc_deposit(sacc, E.a[j]);
-#pragma unroll
-            for (int j = 0; j < NO; ++j)
-                if (is_nonzero(O.a[j])) sacc_deposit(sacc, O.a[j]);
-        }
-    }
-};
+}
 
 // Two-tier accumulator used by the streaming kernels.  Each product p and its
 // TwoProd error e enter short hot expansions P, E (NH levels each, branch
@@ -433,48 +410,22 @@ struct ExAccT {
         res[0] = CP.add(in[0]);
         res[1] = CE.add(in[1]);
     }
+    // End of kernel: deposit every expansion term of every lane with one
+    // warp-aggregated deposit per term slot (see warp_deposit).
     template <int N>
-    __device__ __forceinline__ static void merge_fpe(Fpe<N> &F, int off, bool recv, unsigned long long *sacc) {
-        double in[N];
+    __device__ __forceinline__ static void drain_fpe(const Fpe<N> &F, unsigned long long *sacc) {
 #pragma unroll
-        for (int j = 0; j < N; ++j) in[j] = __shfl_down_sync(0xFFFFFFFFu, F.a[j], off);
-        if (recv) {
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-                double r = F.add(in[j]);
-                if (is_nonzero(r)) sacc_deposit(sacc, r);
-            }
-        }
+        for (int j = 0; j < N; ++j) warp_deposit(F.a[j], sacc);
     }
-    template <int N>
-    __device__ __forceinline__ static void drain(Fpe<N> &F, unsigned long long *sacc) {
-#pragma unroll
-        for (int j = 0; j < N; ++j)
-            if (is_nonzero(F.a[j])) sacc_deposit(sacc, F.a[j]);
-    }
-    // merge the lanes of the warp into lane 0, which deposits its terms
+    // all 32 lanes of the warp, converged (callers __syncwarp() first)
     __device__ __forceinline__ void warp_merge(unsigned long long *sacc) {
-        const int lane = threadIdx.x & 31;
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) {
-            const bool recv = lane < off;
-            merge_fpe<NH>(P, off, recv, sacc);
-            merge_fpe<NH>(E, off, recv, sacc);
-            merge_fpe<NC>(CP, off, recv, sacc);
-            merge_fpe<NC>(CE, off, recv, sacc);
-        }
-        if (lane == 0) {
-            drain<NH>(P, sacc); drain<NH>(E, sacc); drain<NC>(CP, sacc); drain<NC>(CE, sacc);
-        }
+        drain_fpe<NH>(P, sacc);
+        drain_fpe<NH>(E, sacc);
+        drain_fpe<NC>(CP, sacc);
+        drain_fpe<NC>(CE, sacc);
     }
 };
 
-// Deposit every nonzero residual of a batch (the rare path).
-__device__ __forceinline__ void deposit_residuals(const double *res, int n, unsigned long long *sacc) {
-#pragma unroll
-    for (int i = 0; i < n; ++i)
-        if (is_nonzero(res[i])) sacc_deposit(sacc, res[i]);
-}
 
 // Accumulate a batch of K prepared products with one vote per tier.  Product
 // k goes to d1 when ALT and k is odd, else to d0 (s0/s1: their shared
@@ -482,21 +433,41 @@ __device__ __forceinline__ void deposit_residuals(const double *res, int n, unsi
 template <int K, bool ALT, class A>
 __device__ __forceinline__ void cascade_batch(A &d0, A &d1, const Prod (&P)[K], unsigned long long *s0,
                                               unsigned long long *s1) {
-    double r[2 * K];
+    double rp[K], re[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        if (ALT && (k & 1)) d1.hot(P[k], r + 2 * k); else d0.hot(P[k], r + 2 * k);
+        double r[2];
+        if (ALT && (k & 1)) d1.hot(P[k], r); else d0.hot(P[k], r);
+        rp[k] = r[0];
+        re[k] = r[1];
     }
-    if (__any_sync(0xFFFFFFFFu, any_nonzero(r, 2 * K))) {
+    // the p and e streams spill independently (e usually more often: it sits
+    // 53 bits below p), so each gets its own vote for its cold levels
+    const bool cold_p = __any_sync(0xFFFFFFFFu, any_nonzero(rp, K));
+    const bool cold_e = __any_sync(0xFFFFFFFFu, any_nonzero(re, K));
+    if (cold_p | cold_e) {
         PBCG_COUNT(1);
-        double c[2 * K];
+        double cp[K], ce[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            if (ALT && (k & 1)) d1.cold(r + 2 * k, c + 2 * k); else d0.cold(r + 2 * k, c + 2 * k);
+            cp[k] = 0.0;
+            ce[k] = 0.0;
         }
-        if (__any_sync(0xFFFFFFFFu, any_nonzero(c, 2 * K))) {
+        if (cold_p) {
 #pragma unroll
-            for (int k = 0; k < K; ++k) deposit_residuals(c + 2 * k, 2, (ALT && (k & 1)) ? s1 : s0);
+            for (int k = 0; k < K; ++k) cp[k] = (ALT && (k & 1)) ? d1.CP.add(rp[k]) : d0.CP.add(rp[k]);
+        }
+        if (cold_e) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) ce[k] = (ALT && (k & 1)) ? d1.CE.add(re[k]) : d0.CE.add(re[k]);
+        }
+        if (__any_sync(0xFFFFFFFFu, any_nonzero(cp, K) | any_nonzero(ce, K))) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                unsigned long long *sk = (ALT && (k & 1)) ? s1 : s0;
+                if (is_nonzero(cp[k])) sacc_deposit(sk, cp[k]);
+                if (is_nonzero(ce[k])) sacc_deposit(sk, ce[k]);
+            }
         }
     }
 }
@@ -544,6 +515,7 @@ __device__ bool cta_sacc_publish(CtaSacc<ND> &S, unsigned flags, long long *gacc
         if (S.flags & FLAG_RANGE) atomicAdd((unsigned long long *)&gacc[ND * SACC_L], 1ull);
         if (S.flags & FLAG_NONFINITE) atomicAdd((unsigned long long *)&gacc[ND * SACC_L + 1], 1ull);
     }
+    if (!ticket) return false;  // reduced later by finalize_kernel (stream order makes the reds visible)
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) S.last = (atomicAdd(ticket, 1u) == gridDim.x - 1);

@@ -507,16 +507,21 @@ __global__ void __launch_bounds__(256) spmv_sell_kernel(SellMat A, const double 
 // ------------------------------------------------------------------------
 // setup helpers
 // ------------------------------------------------------------------------
-// per-row column hull: out[2v] = min col, out[2v+1] = max col over rank v's rows
-__global__ void row_hull_kernel(int64_t nrows, const int32_t *rp, const int32_t *col, const int64_t *begins,
-                                int nr, long long *out) {
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+// column hull of rows [r0,r1): out[0] = min col, out[1] = max col (unchanged if no nonzeros)
+__global__ void row_hull_kernel(int64_t r0, int64_t r1, const int32_t *rp, const int32_t *col, long long *out) {
+    int lo = INT32_MAX, hi = INT32_MIN;
+    for (int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < r1; r += (int64_t)gridDim.x * blockDim.x) {
         const int32_t s = rp[r], e = rp[r + 1];
-        if (e <= s) continue;
-        int v = 0;
-        while (v + 1 < nr && r >= begins[v + 1]) ++v;
-        atomicMin(&out[2 * v], (long long)col[s]);
-        atomicMax(&out[2 * v + 1], (long long)col[e - 1]);
+        if (e > s) {
+            lo = min(lo, col[s]);
+            hi = max(hi, col[e - 1]);
+        }
+    }
+    lo = __reduce_min_sync(0xFFFFFFFFu, lo);
+    hi = __reduce_max_sync(0xFFFFFFFFu, hi);
+    if ((threadIdx.x & 31) == 0 && lo <= hi) {
+        atomicMin(&out[0], (long long)lo);
+        atomicMax(&out[1], (long long)hi);
     }
 }
 

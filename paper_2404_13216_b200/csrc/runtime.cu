@@ -363,17 +363,17 @@ static int compute_hulls(const pbcg_csr_local *A, int P, const std::vector<int64
     for (int v = 0; v < P; ++v) { hulls[2 * v] = INT64_MAX; hulls[2 * v + 1] = INT64_MIN; }
     if (nloc == 0) return PBCG_OK;
     long long *d_h = nullptr;
-    int64_t *d_b = nullptr;
     CUDA_TRY(cudaMalloc(&d_h, sizeof(long long) * 2 * P));
-    CUDA_TRY(cudaMalloc(&d_b, sizeof(int64_t) * (P + 1)));
     CUDA_TRY(cudaMemcpy(d_h, hulls.data(), sizeof(long long) * 2 * P, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(d_b, begins_local.data(), sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice));
-    const int grid = (int)std::min<int64_t>((nloc + 255) / 256, 4096);
-    row_hull_kernel<<<grid, 256>>>(nloc, A->row_ptr, A->col_idx, d_b, P, d_h);
-    CUDA_TRY(cudaGetLastError());
+    for (int v = 0; v < P; ++v) {
+        const int64_t rows = begins_local[v + 1] - begins_local[v];
+        if (rows <= 0) continue;
+        const int grid = (int)std::min<int64_t>((rows + 255) / 256, 1184);
+        row_hull_kernel<<<grid, 256>>>(begins_local[v], begins_local[v + 1], A->row_ptr, A->col_idx, d_h + 2 * v);
+        CUDA_TRY(cudaGetLastError());
+    }
     CUDA_TRY(cudaMemcpy(hulls.data(), d_h, sizeof(long long) * 2 * P, cudaMemcpyDeviceToHost));
     cudaFree(d_h);
-    cudaFree(d_b);
     return PBCG_OK;
 }
 
@@ -605,7 +605,8 @@ static int stream_grid(pbcg_handle *h, int64_t n, int rows_per_tile) {
 }
 
 static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
-    K2Args a{R.n, R.r, R.rh, R.w(), R.t, R.v, R.p, R.s, R.z(), R.q, R.y, R.sc, R.gacc[1], R.tickets + 1, R.hist, fin};
+    // fin = 1: the last CTA rounds and runs the scalar step; fin = 0: publish only (finalize_kernel follows)
+    K2Args a{R.n, R.r, R.rh, R.w(), R.t, R.v, R.p, R.s, R.z(), R.q, R.y, R.sc, R.gacc[1], fin ? R.tickets + 1 : nullptr, R.hist, fin};
     if (use_ldg_kernels()) {
         const int grid = std::max(1, std::min<int>(h->grid_k2, (int)((R.n / 2 + K_BS - 1) / K_BS)));
         k2_kernel<K_NP, K_NE, K_BS, U_K2><<<grid, K_BS, 0, st>>>(a);
@@ -617,7 +618,7 @@ static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
 }
 
 static int launch_k3(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
-    K3Args a{R.n, R.rh, R.p, R.q, R.y, R.t, R.v, R.x, R.r, R.w(), R.sc, R.gacc[2], R.tickets + 2, R.hist, fin};
+    K3Args a{R.n, R.rh, R.p, R.q, R.y, R.t, R.v, R.x, R.r, R.w(), R.sc, R.gacc[2], fin ? R.tickets + 2 : nullptr, R.hist, fin};
     if (use_ldg_kernels()) {
         const int grid = std::max(1, std::min<int>(h->grid_k3, (int)((R.n / 2 + K_BS - 1) / K_BS)));
         k3_kernel<K_NP, K_NE, K_BS, U_K3><<<grid, K_BS, 0, st>>>(a);
@@ -630,12 +631,28 @@ static int launch_k3(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
 
 static int enqueue_iteration(pbcg_handle *h) {
     cudaStream_t st = h->stream;
-    if (!multi(h)) {  // single rank: 4 launches, dots rounded in the last CTA
+    if (!multi(h)) {
+        // single rank: the rounding + scalar step of each phase (finalize_kernel,
+        // 1 CTA) runs on the side stream while the SpMV that does not need
+        // its scalars runs on the main stream -- the same fork/join as the
+        // multi-rank allreduce, minus the communication.
         Rank &R = h->R[0];
-        RC_TRY(launch_k2(h, R, 1, st));
+        RC_TRY(launch_k2(h, R, 0, st));
+        CUDA_TRY(cudaEventRecord(h->ev[4], st));
+        CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev[4], 0));
+        finalize_kernel<4><<<1, 128, 0, h->side>>>(R.gacc[1], PH_A, R.sc, R.hist, nullptr, nullptr);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaEventRecord(h->ev[5], h->side));
         RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.zpad, R.v, nullptr, nullptr, true, st));
-        RC_TRY(launch_k3(h, R, 1, st));
+        CUDA_TRY(cudaStreamWaitEvent(st, h->ev[5], 0));
+        RC_TRY(launch_k3(h, R, 0, st));
+        CUDA_TRY(cudaEventRecord(h->ev[6], st));
+        CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev[6], 0));
+        finalize_kernel<3><<<1, 128, 0, h->side>>>(R.gacc[2], PH_B, R.sc, R.hist, nullptr, nullptr);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaEventRecord(h->ev[7], h->side));
         RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, true, st));
+        CUDA_TRY(cudaStreamWaitEvent(st, h->ev[7], 0));
         return PBCG_OK;
     }
     if (h->V > 1) {  // virtual ranks: same dataflow, serialised on one stream
@@ -833,6 +850,9 @@ static void opts_defaults(const pbcg_opts *o, pbcg_opts &e) {
 // ----------------------------------------------------------------------------
 // start / iterate / finish / solve
 // ----------------------------------------------------------------------------
+static int capture_chunk(pbcg_handle *h, int iters);
+static int g_default_chunk = 16;
+
 extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0, const pbcg_opts *o) {
     if (!h || h->comm_only) return fail(PBCG_EINVAL, "start: no matrix on this handle");
     if (!b || !x0) return fail(PBCG_EINVAL, "start: b and x0 are required");
@@ -891,6 +911,9 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
     h->started = true;
     if (bad & 2) return fail(PBCG_ENONFINITE, "start: NaN/Inf in b or x0");
     if (h->h_sc->err) return fail(PBCG_EINVAL, "start: ||b|| = 0");
+    // capture the iteration graph now (nothing runs), so that the first
+    // iterate()/solve() chunk does not pay for capture + instantiation
+    if (op.use_graphs && h->stream) RC_TRY(capture_chunk(h, o ? op.poll_every : g_default_chunk));
     return PBCG_OK;
 }
 
@@ -924,8 +947,6 @@ static int iterate_impl(pbcg_handle *h, int32_t k, int chunk, bool graphs) {
     }
     return PBCG_OK;
 }
-
-static int g_default_chunk = 16;
 
 extern "C" int pbicgstab_iterate(pbcg_handle *h, int32_t k) {
     if (!h || !h->started) return fail(PBCG_EINVAL, "iterate before start");
@@ -1146,29 +1167,34 @@ extern "C" int pbcg_abi_version(void) { return PBCG_ABI_VERSION; }
 extern "C" int pbcg_profile_iterations(pbcg_handle *h, int32_t k, double *ms) {
     if (!h || !h->started || k < 1 || !ms) return fail(PBCG_EINVAL, "profile: bad arguments");
     if (multi(h)) return fail(PBCG_EINVAL, "profile: single-rank handles only");
-    std::vector<cudaEvent_t> ev((size_t)5 * k);
+    constexpr int NK = 6;  // K2, finalize A, SpMV z, K3, finalize B, SpMV w (serialised here)
+    std::vector<cudaEvent_t> ev((size_t)(NK + 1) * k);
     for (auto &e : ev) CUDA_TRY(cudaEventCreate(&e));
     Rank &R = h->R[0];
     cudaStream_t st = h->stream;
     int rc = PBCG_OK;
     for (int i = 0; i < k && rc == PBCG_OK; ++i) {
-        cudaEvent_t *e = &ev[(size_t)5 * i];
+        cudaEvent_t *e = &ev[(size_t)(NK + 1) * i];
         cudaEventRecord(e[0], st);
-        rc = launch_k2(h, R, 1, st);
+        rc = launch_k2(h, R, 0, st);
         cudaEventRecord(e[1], st);
-        if (rc == PBCG_OK) rc = launch_spmv(h, R, SPMV_PLAIN, R.zpad, R.v, nullptr, nullptr, true, st);
+        finalize_kernel<4><<<1, 128, 0, st>>>(R.gacc[1], PH_A, R.sc, R.hist, nullptr, nullptr);
         cudaEventRecord(e[2], st);
-        if (rc == PBCG_OK) rc = launch_k3(h, R, 1, st);
+        if (rc == PBCG_OK) rc = launch_spmv(h, R, SPMV_PLAIN, R.zpad, R.v, nullptr, nullptr, true, st);
         cudaEventRecord(e[3], st);
-        if (rc == PBCG_OK) rc = launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, true, st);
+        if (rc == PBCG_OK) rc = launch_k3(h, R, 0, st);
         cudaEventRecord(e[4], st);
+        finalize_kernel<3><<<1, 128, 0, st>>>(R.gacc[2], PH_B, R.sc, R.hist, nullptr, nullptr);
+        cudaEventRecord(e[5], st);
+        if (rc == PBCG_OK) rc = launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, true, st);
+        cudaEventRecord(e[6], st);
     }
     cudaError_t se = cudaStreamSynchronize(st);
-    for (int j = 0; j < 4; ++j) ms[j] = 0.0;
+    for (int j = 0; j < NK; ++j) ms[j] = 0.0;
     for (int i = 0; i < k && rc == PBCG_OK && se == cudaSuccess; ++i)
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < NK; ++j) {
             float t = 0.f;
-            cudaEventElapsedTime(&t, ev[(size_t)5 * i + j], ev[(size_t)5 * i + j + 1]);
+            cudaEventElapsedTime(&t, ev[(size_t)(NK + 1) * i + j], ev[(size_t)(NK + 1) * i + j + 1]);
             ms[j] += t;
         }
     for (auto &e : ev) cudaEventDestroy(e);

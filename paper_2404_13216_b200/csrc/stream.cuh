@@ -137,6 +137,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
     __shared__ CtaSacc<4> S;
     Scalars *sc = a.sc;
     if (sc->done) return;
+    PBCG_TS(0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     cta_sacc_zero<4>(S);
     if (threadIdx.x == 0) {
@@ -229,10 +230,16 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
             if (++st == STAGES) { st = 0; ph ^= 1u; }
         }
     }
+    PBCG_TS(1);
+    __syncwarp();
     R.d0.warp_merge(s0);
     R.d1.warp_merge(s1);
-    if (cta_sacc_publish<4>(S, flags, a.gacc, a.ticket))
+    PBCG_TS(2);
+    if (cta_sacc_publish<4>(S, flags, a.gacc, a.ticket)) {
+        PBCG_TS(3);
         last_cta_finish<4>(S, a.gacc, a.ticket, PH_A, a.finalize, sc, a.hist, nullptr, nullptr);
+        PBCG_TS(4);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -361,6 +368,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
             if (++st == STAGES) { st = 0; ph ^= 1u; }
         }
     }
+    __syncwarp();
     R.d0.warp_merge(s0);
     R.d1.warp_merge(s1);
     if (cta_sacc_publish<3>(S, flags, a.gacc, a.ticket))
@@ -445,6 +453,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a
             if (++s == STAGES) { s = 0; ph ^= 1u; }
         }
     }
+    __syncwarp();
     acc.warp_merge(S.w[0]);
     if (cta_sacc_publish<1>(S, flags, a.gacc, a.ticket))
         last_cta_finish<1>(S, a.gacc, a.ticket, a.phase, a.finalize, a.sc, a.hist, a.out, a.out_flags,
