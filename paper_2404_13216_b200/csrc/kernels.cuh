@@ -459,9 +459,10 @@ __global__ void vallreduce_kernel(long long **gaccs, int nr, int words) {
 struct SellMat {
     int64_t n;
     const int64_t *slice_off;  // nslices+1, element offsets of each slice
-    const int32_t *row_len;
+    const int32_t *row_len;    // by position
     const double *val;
     const int32_t *col;        // indices into the rank's padded x buffer
+    const int32_t *perm;       // position -> row (sigma-sorted windows), or null (identity)
 };
 
 enum { SPMV_PLAIN = 0, SPMV_RESID = 1 };
@@ -471,10 +472,11 @@ __global__ void __launch_bounds__(256) spmv_sell_kernel(SellMat A, const double 
                                                         double *__restrict__ y, const double *__restrict__ b,
                                                         double *__restrict__ y2, const Scalars *sc) {
     if (sc && sc->done) return;
-    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (row >= A.n) return;
-    const int64_t base = __ldg(&A.slice_off[row >> 5]) + (row & 31);
-    const int len = __ldg(&A.row_len[row]);
+    const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos >= A.n) return;
+    const int64_t base = __ldg(&A.slice_off[pos >> 5]) + (pos & 31);
+    const int len = __ldg(&A.row_len[pos]);
+    const int64_t row = A.perm ? (int64_t)__ldg(&A.perm[pos]) : pos;
     const double *vp = A.val + base;
     const int32_t *cp = A.col + base;
     double acc = 0.0;
@@ -530,9 +532,10 @@ __global__ void row_hull_kernel(int64_t r0, int64_t r1, const int32_t *rp, const
 // [0, ncols), row pointer monotone.
 __global__ void csr_to_sell_kernel(int64_t n, const int32_t *rp, const int32_t *col, const double *val,
                                    int64_t ncols, int64_t col_shift, const int64_t *slice_off, int32_t *row_len,
-                                   double *sval, int32_t *scol, int *bad) {
+                                   double *sval, int32_t *scol, const int32_t *perm, int *bad) {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t s = rp[r], e = rp[r + 1];
+        const int64_t src = perm ? perm[r] : r;  // r is the SELL position
+        const int32_t s = rp[src], e = rp[src + 1];
         const int len = e - s;
         if (len < 0) { atomicOr(bad, 1); continue; }
         row_len[r] = len;

@@ -235,7 +235,9 @@ struct Rank {
     int *bad = nullptr;
     double *z() const { return zpad + own_off; }
     double *w() const { return wpad + own_off; }
-    SellMat mat() const { return SellMat{n, slice_off, row_len, sval, scol}; }
+    std::vector<int32_t> h_perm;  // SELL position -> local row (empty: identity)
+    int32_t *perm = nullptr;
+    SellMat mat() const { return SellMat{n, slice_off, row_len, sval, scol, h_perm.empty() ? nullptr : perm}; }
 };
 
 struct pbcg_handle {
@@ -262,6 +264,8 @@ struct pbcg_handle {
     int32_t *xd_flags = nullptr;
 };
 
+static constexpr int64_t SELL_SIGMA = 256;  // sorting window (rows) for irregular matrices
+
 // workspace carving (dry run computes the size)
 struct Carver {
     char *base;
@@ -281,6 +285,7 @@ static void carve_rank(Carver &C, Rank &R, int hist_cap, bool comm_only) {
         R.row_len = C.take<int32_t>(R.n);
         R.sval = C.take<double>(R.sell_nnz);
         R.scol = C.take<int32_t>(R.sell_nnz);
+        R.perm = C.take<int32_t>(R.h_perm.size());
         const size_t n = (size_t)R.n + 2;
         R.x = C.take<double>(n); R.r = C.take<double>(n); R.rh = C.take<double>(n); R.p = C.take<double>(n);
         R.s = C.take<double>(n); R.q = C.take<double>(n); R.y = C.take<double>(n); R.t = C.take<double>(n);
@@ -343,15 +348,34 @@ static int plan_ranks(pbcg_handle *h, const pbcg_csr_local *A, const std::vector
         R.own_off = lead_al;
         // sliced ELL: 32 rows per slice, width = longest row of the slice
         R.nslices = (R.n + 31) / 32;
-        R.h_slice_off.assign(R.nslices + 1, 0);
         const int64_t r0 = (h->V > 1) ? R.rb : 0;  // index into h_rp
-        for (int64_t sl = 0; sl < R.nslices; ++sl) {
-            int32_t wmax = 0;
-            const int64_t a = sl * 32, e = std::min<int64_t>(a + 32, R.n);
-            for (int64_t r = a; r < e; ++r) wmax = std::max(wmax, h_rp[r0 + r + 1] - h_rp[r0 + r]);
-            R.h_slice_off[sl + 1] = R.h_slice_off[sl] + 32 * (int64_t)wmax;
+        auto rowlen = [&](int64_t r) { return h_rp[r0 + r + 1] - h_rp[r0 + r]; };
+        auto slices = [&](const int32_t *perm) {
+            R.h_slice_off.assign(R.nslices + 1, 0);
+            for (int64_t sl = 0; sl < R.nslices; ++sl) {
+                int32_t wmax = 0;
+                const int64_t a = sl * 32, e = std::min<int64_t>(a + 32, R.n);
+                for (int64_t q = a; q < e; ++q) wmax = std::max(wmax, rowlen(perm ? perm[q] : q));
+                R.h_slice_off[sl + 1] = R.h_slice_off[sl] + 32 * (int64_t)wmax;
+            }
+            R.sell_nnz = R.h_slice_off[R.nslices];
+        };
+        slices(nullptr);
+        const int64_t nnz = (int64_t)h_rp[r0 + R.n] - h_rp[r0];
+        R.h_perm.clear();
+        if (R.sell_nnz > nnz + nnz / 16) {
+            // sigma-sorting (sliced ELL-C-sigma, C = 32, sigma = SELL_SIGMA): rows
+            // of each window sorted by length so that a slice holds rows of
+            // similar length -- the per-row summation order is unchanged
+            R.h_perm.resize(R.n);
+            for (int64_t q = 0; q < R.n; ++q) R.h_perm[q] = (int32_t)q;
+            for (int64_t w0 = 0; w0 < R.n; w0 += SELL_SIGMA) {
+                const int64_t w1 = std::min<int64_t>(w0 + SELL_SIGMA, R.n);
+                std::stable_sort(R.h_perm.begin() + w0, R.h_perm.begin() + w1,
+                                 [&](int32_t a, int32_t b) { return rowlen(a) > rowlen(b); });
+            }
+            slices(R.h_perm.data());
         }
-        R.sell_nnz = R.h_slice_off[R.nslices];
     }
     return PBCG_OK;
 }
@@ -760,6 +784,9 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
             Rank &R = h->R[v];
             CUDA_TRY(cudaMemcpyAsync(R.slice_off, R.h_slice_off.data(), sizeof(int64_t) * (R.nslices + 1),
                                      cudaMemcpyHostToDevice, h->stream));
+            if (!R.h_perm.empty())
+                CUDA_TRY(cudaMemcpyAsync(R.perm, R.h_perm.data(), sizeof(int32_t) * R.h_perm.size(),
+                                         cudaMemcpyHostToDevice, h->stream));
             CUDA_TRY(cudaMemsetAsync(R.zpad, 0, sizeof(double) * (R.buf_hi - R.buf_lo), h->stream));
             CUDA_TRY(cudaMemsetAsync(R.wpad, 0, sizeof(double) * (R.buf_hi - R.buf_lo), h->stream));
             CUDA_TRY(cudaMemsetAsync(R.xpad, 0, sizeof(double) * (R.buf_hi - R.buf_lo), h->stream));
@@ -767,7 +794,8 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
                 const int32_t *rp = A->row_ptr + (h->V > 1 ? R.rb : 0);
                 const int grid = (int)std::min<int64_t>((R.n + 255) / 256, 65535);
                 csr_to_sell_kernel<<<grid, 256, 0, h->stream>>>(R.n, rp, A->col_idx, A->values, A->n_global, R.buf_lo,
-                                                                R.slice_off, R.row_len, R.sval, R.scol, R.bad);
+                                                                R.slice_off, R.row_len, R.sval, R.scol,
+                                                                R.h_perm.empty() ? nullptr : R.perm, R.bad);
                 CUDA_TRY(cudaGetLastError());
             }
         }
