@@ -467,42 +467,64 @@ struct SellMat {
 
 enum { SPMV_PLAIN = 0, SPMV_RESID = 1 };
 
-template <int MODE, int UNR>
+template <int MODE, int UNR, int RPT>
 __global__ void __launch_bounds__(256) spmv_sell_kernel(SellMat A, const double *__restrict__ x,
                                                         double *__restrict__ y, const double *__restrict__ b,
                                                         double *__restrict__ y2, const Scalars *sc) {
+    // RPT positions per thread (pos0 + 256*u), loads of all of them in flight
+    // before any fold: more memory-level parallelism per thread.
     if (sc && sc->done) return;
-    const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (pos >= A.n) return;
-    const int64_t base = __ldg(&A.slice_off[pos >> 5]) + (pos & 31);
-    const int len = __ldg(&A.row_len[pos]);
-    const int64_t row = A.perm ? (int64_t)__ldg(&A.perm[pos]) : pos;
-    const double *vp = A.val + base;
-    const int32_t *cp = A.col + base;
-    double acc = 0.0;
-    for (int k = 0; k < len; k += UNR) {
-        double v[UNR], xv[UNR];
-        int c[UNR];
+    const int64_t pos0 = (int64_t)blockIdx.x * (256 * RPT) + threadIdx.x;
+    int64_t base[RPT];
+    int len[RPT], lmax = 0;
 #pragma unroll
-        for (int j = 0; j < UNR; ++j) {
-            if (k + j < len) {
-                v[j] = __ldcs(vp + 32 * (k + j));
-                c[j] = __ldcs(cp + 32 * (k + j));
-            }
+    for (int u = 0; u < RPT; ++u) {
+        const int64_t pos = pos0 + 256 * u;
+        base[u] = 0;
+        len[u] = 0;
+        if (pos < A.n) {
+            base[u] = __ldg(&A.slice_off[pos >> 5]) + (pos & 31);
+            len[u] = __ldg(&A.row_len[pos]);
         }
-#pragma unroll
-        for (int j = 0; j < UNR; ++j)
-            if (k + j < len) xv[j] = __ldg(x + c[j]);
-#pragma unroll
-        for (int j = 0; j < UNR; ++j)
-            if (k + j < len) acc = __fma_rn(v[j], xv[j], acc);
+        lmax = max(lmax, len[u]);
     }
-    if (MODE == SPMV_PLAIN) {
-        y[row] = acc;
-    } else {
-        const double r = __dsub_rn(b[row], acc);  // r0 := b - A x0 (l.64), one rounding
-        y[row] = r;
-        if (y2) y2[row] = r;
+    double acc[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) acc[u] = 0.0;
+    for (int k = 0; k < lmax; k += UNR) {
+        double v[RPT][UNR], xv[RPT][UNR];
+        int c[RPT][UNR];
+#pragma unroll
+        for (int u = 0; u < RPT; ++u)
+#pragma unroll
+            for (int j = 0; j < UNR; ++j)
+                if (k + j < len[u]) {
+                    v[u][j] = __ldcs(A.val + base[u] + 32 * (k + j));
+                    c[u][j] = __ldcs(A.col + base[u] + 32 * (k + j));
+                }
+#pragma unroll
+        for (int u = 0; u < RPT; ++u)
+#pragma unroll
+            for (int j = 0; j < UNR; ++j)
+                if (k + j < len[u]) xv[u][j] = __ldg(x + c[u][j]);
+#pragma unroll
+        for (int u = 0; u < RPT; ++u)
+#pragma unroll
+            for (int j = 0; j < UNR; ++j)
+                if (k + j < len[u]) acc[u] = __fma_rn(v[u][j], xv[u][j], acc[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+        const int64_t pos = pos0 + 256 * u;
+        if (pos >= A.n) continue;
+        const int64_t row = A.perm ? (int64_t)__ldg(&A.perm[pos]) : pos;
+        if (MODE == SPMV_PLAIN) {
+            y[row] = acc[u];
+        } else {
+            const double r = __dsub_rn(b[row], acc[u]);  // r0 := b - A x0 (l.64), one rounding
+            y[row] = r;
+            if (y2) y2[row] = r;
+        }
     }
 }
 

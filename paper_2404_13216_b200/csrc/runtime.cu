@@ -535,15 +535,28 @@ static int reduce_finalize(pbcg_handle *h, int ph, int phase, cudaStream_t st, d
 
 static bool multi(const pbcg_handle *h) { return h->V > 1 || h->nranks > 1; }
 
+static int g_spmv_rpt = 0;
+static int spmv_rpt() {  // rows per thread of the SELL SpMV (PBCG_SPMV_RPT = 1 | 2)
+    if (!g_spmv_rpt) {
+        const char *e = getenv("PBCG_SPMV_RPT");
+        g_spmv_rpt = (e && atoi(e) == 2) ? 2 : 1;
+    }
+    return g_spmv_rpt;
+}
+
 static int launch_spmv(pbcg_handle *h, Rank &R, int mode, const double *xpad, double *y, const double *b, double *y2,
                        bool predicated, cudaStream_t st) {
     if (R.n == 0) return PBCG_OK;
-    const int grid = (int)((R.n + 255) / 256);
     const Scalars *sc = predicated ? R.sc : nullptr;
-    if (mode == SPMV_PLAIN)
-        spmv_sell_kernel<SPMV_PLAIN, 8><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
-    else
-        spmv_sell_kernel<SPMV_RESID, 8><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
+    const int rpt = spmv_rpt();
+    const int grid = (int)((R.n + 256 * rpt - 1) / (256 * rpt));
+    if (rpt == 2) {
+        if (mode == SPMV_PLAIN) spmv_sell_kernel<SPMV_PLAIN, 8, 2><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
+        else spmv_sell_kernel<SPMV_RESID, 8, 2><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
+    } else {
+        if (mode == SPMV_PLAIN) spmv_sell_kernel<SPMV_PLAIN, 8, 1><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
+        else spmv_sell_kernel<SPMV_RESID, 8, 1><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
+    }
     CUDA_TRY(cudaGetLastError());
     return PBCG_OK;
 }
