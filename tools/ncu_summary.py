@@ -1,0 +1,58 @@
+"""Summaries of ncu output for profiles/:
+  python tools/ncu_summary.py launches <launches.csv>          -> per-kernel launch table (shares)
+  python tools/ncu_summary.py full <report.ncu-rep> [alg.json] -> per-kernel DRAM/pipe metrics (JSON lines)
+"""
+import csv, collections, io, json, subprocess, sys
+
+def launches(path):
+    rows = [r for r in csv.reader(open(path)) if len(r) > 5]
+    h = rows[0]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    agg = collections.OrderedDict()
+    tot = 0.0
+    for r in rows[1:]:
+        if r[ki] == "Kernel Name":
+            continue
+        name = r[ki].split("(")[0].replace("void ", "").split("<")[0].replace("pbcg::", "")
+        v = float(r[vi].replace(",", ""))
+        v = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0) * v
+        a = agg.setdefault(name, [0, 0.0])
+        a[0] += 1
+        a[1] += v
+        tot += v
+    out = ["| kernel | launches | total us | avg us | share |", "|---|---|---|---|---|"]
+    for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        out.append(f"| {k} | {c} | {t:.1f} | {t / c:.1f} | {t / tot:.3f} |")
+    return "\n".join(out)
+
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread", "launch__grid_size",
+        "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+        "l1tex__t_sector_hit_rate.pct", "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
+
+def full(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = {"kernel": r[h.index("Kernel Name")].split("(")[0].replace("void ", "")}
+        for w in WANT:
+            if w in h:
+                i = h.index(w)
+                try:
+                    d[w] = float(r[i].replace(",", ""))
+                except ValueError:
+                    d[w] = r[i]
+                d[w + ".unit"] = units[i]
+        res.append(d)
+    return res
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        print(launches(sys.argv[2]))
+    else:
+        for d in full(sys.argv[2]):
+            print(json.dumps(d))
