@@ -87,6 +87,9 @@ typedef struct {
     const uint8_t *nccl_uid;  /* host, 128 bytes from pbcg_nccl_unique_id() on rank 0, same on all ranks; NULL if nranks == 1 */
     int32_t virtual_ranks;    /* 0 or 1 = off */
     int32_t history_capacity; /* rows of per-iteration scalar history kept on device; 0 -> 10001 */
+    int32_t comm_mode;        /* 0 = auto; 1 = use the NCCL dataflow even with nranks == 1 (a 1-rank
+                                 communicator: halo no-ops, allreduce = identity) -- test vehicle for the
+                                 multi-GPU code path on one GPU */
 } pbcg_dist;
 
 /* Solver options (SPEC.md l.214-217 SolverConfig subset). */

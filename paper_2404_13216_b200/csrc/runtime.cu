@@ -71,6 +71,7 @@ struct NcclApi {
     ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
     ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t *, ncclConfig_t *) = nullptr;
     ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
@@ -98,6 +99,7 @@ static void nccl_load() {
     SYM(GetUniqueId, "ncclGetUniqueId");
     SYM(CommInitRank, "ncclCommInitRank");
     SYM(CommDestroy, "ncclCommDestroy");
+    SYM(CommSplit, "ncclCommSplit");
     SYM(AllReduce, "ncclAllReduce");
     SYM(AllGather, "ncclAllGather");
     SYM(Send, "ncclSend");
@@ -106,7 +108,7 @@ static void nccl_load() {
     SYM(GroupEnd, "ncclGroupEnd");
     SYM(GetErrorString, "ncclGetErrorString");
 #undef SYM
-    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllReduce &&
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.CommSplit && g_nccl.AllReduce &&
                 g_nccl.AllGather && g_nccl.Send && g_nccl.Recv && g_nccl.GroupStart && g_nccl.GroupEnd;
 }
 
@@ -244,6 +246,7 @@ struct pbcg_handle {
     int dev = 0, nsm = 148;
     cudaStream_t stream = nullptr, side = nullptr;
     int nranks = 1, rank = 0, V = 1;  // real ranks, this rank, virtual ranks
+    bool comm = false;                // NCCL communicators exist (nranks > 1, or forced for testing)
     int64_t n_global = 0;
     bool comm_only = false;
     std::vector<Rank> R;
@@ -499,7 +502,7 @@ static int halo(pbcg_handle *h, int which) {
         }
         return PBCG_OK;
     }
-    if (h->nranks == 1) return PBCG_OK;
+    if (!h->comm) return PBCG_OK;
     Rank &R = h->R[0];
     NCCL_TRY(g_nccl.GroupStart());
     for (int q = 0; q < h->nranks; ++q) {
@@ -521,7 +524,7 @@ static int reduce_finalize(pbcg_handle *h, int ph, int phase, cudaStream_t st, d
     if (h->V > 1) {
         vallreduce_kernel<<<(words + 127) / 128, 128, 0, st>>>(h->vgacc + (size_t)ph * h->V, h->V, words);
         CUDA_TRY(cudaGetLastError());
-    } else if (h->nranks > 1) {
+    } else if (h->comm) {
         NCCL_TRY(g_nccl.AllReduce(h->R[0].gacc[ph], h->R[0].gacc[ph], (size_t)words, ncclInt64, ncclSum, h->comm_red, st));
     }
     for (auto &R : h->R) {
@@ -533,7 +536,7 @@ static int reduce_finalize(pbcg_handle *h, int ph, int phase, cudaStream_t st, d
     return PBCG_OK;
 }
 
-static bool multi(const pbcg_handle *h) { return h->V > 1 || h->nranks > 1; }
+static bool multi(const pbcg_handle *h) { return h->V > 1 || h->comm; }
 
 static int g_spmv_rpt = 0;
 static int spmv_rpt() {  // rows per thread of the SELL SpMV (PBCG_SPMV_RPT = 1 | 2)
@@ -740,13 +743,19 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
     // communicators first: real ranks need the allgathered row ranges + hulls
     std::vector<int64_t> all_ranges;
     std::vector<int32_t> h_rp;
-    if (nranks > 1) {
+    const bool force_comm = d && d->comm_mode == 1 && nranks == 1 && d->virtual_ranks <= 1;
+    if (nranks > 1 || force_comm) {
         if (!nccl_available()) return fail(PBCG_ENCCL, "nranks > 1 but libnccl.so.2 could not be loaded");
-        if (!d->nccl_uid) return fail(PBCG_EINVAL, "nranks > 1 needs nccl_uid");
         ncclUniqueId uid;
-        memcpy(&uid, d->nccl_uid, sizeof(uid));
+        if (d->nccl_uid) memcpy(&uid, d->nccl_uid, sizeof(uid));
+        else if (force_comm) NCCL_TRY(g_nccl.GetUniqueId(&uid));
+        else return fail(PBCG_EINVAL, "nranks > 1 needs nccl_uid");
+        h->comm = true;
+        // two communicators (halo on the main stream, reductions on the side
+        // stream, so they can run concurrently); one unique id bootstraps one
+        // communicator, the second is split from it
         NCCL_TRY(g_nccl.CommInitRank(&h->comm_halo, nranks, uid, d->rank));
-        NCCL_TRY(g_nccl.CommInitRank(&h->comm_red, nranks, uid, d->rank));
+        NCCL_TRY(g_nccl.CommSplit(h->comm_halo, 0, d->rank, &h->comm_red, nullptr));
         // hull of my rows, then allgather (rb, re, cmin, cmax) of every rank
         RC_TRY(validate_csr(A, d));
         if (!A) return fail(PBCG_EINVAL, "nranks > 1 needs a matrix (comm-only handles are single-rank)");
@@ -768,7 +777,7 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
         if (all_ranges[0] != 0 || all_ranges[4 * (nranks - 1) + 1] != A->n_global)
             return fail(PBCG_EINVAL, "row blocks of the ranks do not cover [0, n_global)");
     }
-    RC_TRY(prepare(h, A, d, h_rp, nranks > 1 ? &all_ranges : nullptr));
+    RC_TRY(prepare(h, A, d, h_rp, h->comm ? &all_ranges : nullptr));
     h->nranks = nranks;
     h->rank = d ? d->rank : 0;
     const size_t need = total_size(h);
@@ -1129,7 +1138,7 @@ extern "C" int exdot(pbcg_handle *h, int64_t n, const double *x, const double *y
     RC_TRY(scratch(&S));
     double *out = on_device ? result : S->out;
     int32_t *ofl = on_device ? flags : S->flags;
-    if (!h || (h->V == 1 && h->nranks == 1)) {
+    if (!h || (h->V == 1 && !h->comm)) {
         MultiDotArgs a{};
         a.n = n;
         a.x[0] = x;

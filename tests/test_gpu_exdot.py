@@ -148,3 +148,14 @@ def test_on_device_result_and_plain_dot(pb):
     p = pb.dot_plain(x, y)
     torch.cuda.synchronize()
     assert abs(p.item() - want) <= 1e-12 * float(torch.sum(torch.abs(x * y)))
+
+
+def test_nccl_single_rank_handle(pb):
+    # distributed EXDOT path (per-rank superaccumulator, ncclAllReduce int64,
+    # finalize) with a 1-rank communicator
+    x, y = gen.ill_pair(1 << 16, seed=9, block=1 << 12)
+    A = gen.stencil(2, 16, 10.0)
+    S = pb.Solver(A.row_ptr, A.col, A.val, A.n, force_nccl=True)
+    got, f = gpu_exdot(pb, x, y, handle=S)
+    assert f == 0 and bits(got) == bits(oracle.exdot(x, y)[0])
+    S.close()

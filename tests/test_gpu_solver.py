@@ -97,7 +97,7 @@ def test_setup_rejects_bad_csr(pb):
 
 def run_both(pb, A, tol, max_iter, steps=None, **kw):
     import torch
-    S = solver(pb, A, history_capacity=max_iter + 1, **{k: v for k, v in kw.items() if k == "virtual_ranks"})
+    S = solver(pb, A, history_capacity=max_iter + 1, **{k: v for k, v in kw.items() if k in ("virtual_ranks", "force_nccl")})
     b = gpu_b(pb, S, A)
     O = oracle.PBiCGStab(A, b=None if A.rhs != "given" else A.b, tol=tol, max_iter=max_iter)
     assert O.rc == 0
@@ -219,3 +219,15 @@ def test_host_buffers_end_to_end(pb):
     assert isinstance(xh, np.ndarray)
     assert rd.iterations == rh.iterations and np.array_equal(u64(xd.cpu().numpy()), u64(xh))
     S.close()
+
+
+def test_nccl_dataflow_single_rank(pb):
+    # The multi-GPU code path (K2/K3 publish -> int64 ncclAllReduce on the side
+    # stream -> finalize_kernel; ncclSend/Recv halo) run on one GPU with a
+    # 1-rank NCCL communicator, inside the CUDA graphs: identical bits.
+    A = gen.make_config("c1_2d64")
+    S, O, x, r, H = run_both(pb, A, tol=1e-10, max_iter=500, force_nccl=True)
+    assert_same(O, x, r, H, A)
+    A = gen.random_banded(30_000, seed=17, band=2500)
+    S, O, x, r, H = run_both(pb, A, tol=1e-10, max_iter=400, force_nccl=True)
+    assert_same(O, x, r, H, A)
