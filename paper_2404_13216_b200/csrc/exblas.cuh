@@ -386,9 +386,10 @@ struct Prod {
     double p, e;
 };
 
-template <int NH, int NC>
+template <int NH, int NC, int NHE = NH>
 struct ExAccT {
-    Fpe<NH> P, E;
+    Fpe<NH> P;   // hot levels of the p stream
+    Fpe<NHE> E;  // hot levels of the e stream (e sits 53 bits below p: usually needs fewer)
     Fpe<NC> CP, CE;
     __device__ __forceinline__ void zero() {
         P.zero(); E.zero(); CP.zero(); CE.zero();
@@ -420,7 +421,7 @@ struct ExAccT {
     // all 32 lanes of the warp, converged (callers __syncwarp() first)
     __device__ __forceinline__ void warp_merge(unsigned long long *sacc) {
         drain_fpe<NH>(P, sacc);
-        drain_fpe<NH>(E, sacc);
+        drain_fpe<NHE>(E, sacc);
         drain_fpe<NC>(CP, sacc);
         drain_fpe<NC>(CE, sacc);
     }

@@ -598,18 +598,20 @@ static int multidot(pbcg_handle *h, int ph, int phase, int nd, const double *con
 // one iteration of Algorithm 2 (enqueue only)
 // ----------------------------------------------------------------------------
 // Streaming (TMA-pipelined) kernel geometry -- performance parameters only.
-#ifndef PBCG_S_NC
-#define PBCG_S_NC 3
-#endif
-static constexpr int S_NH = 2, S_NL = PBCG_S_NC, S_NCW = 7;  // hot/cold levels; S_NCW warps per dot group (2*7+1 = 15 warps)
+// FPE levels (performance parameters only, R-16): hot p / hot e / cold, per
+// kernel.  Chosen on C3/C4/C5 (profiles/r01): the p stream of the solver
+// vectors spills more than the e stream, K3's cold levels rarely overflow.
+static constexpr int K2_NH = 3, K2_NHE = 2, K2_NC = 3;
+static constexpr int K3_NH = 3, K3_NHE = 2, K3_NC = 2;
+static constexpr int S_NCW = 7;  // warps per dot group (2*7+1 = 15 warps per CTA)
 static constexpr int X_NCW = 8;
 #ifndef PBCG_X_NH
 #define PBCG_X_NH 2
 #endif
 static constexpr int X_NH = PBCG_X_NH, X_NL = 2;  // standalone EXDOT: hot / cold levels
 static constexpr int K2_PPT = 1, K2_ST = 4, K3_PPT = 1, K3_ST = 4, XD_PPT = 4, XD_ST = 4;
-#define K2S k2_stream<S_NH, S_NL, S_NCW, K2_PPT, K2_ST>
-#define K3S k3_stream<S_NH, S_NL, S_NCW, K3_PPT, K3_ST>
+#define K2S k2_stream<K2_NH, K2_NC, S_NCW, K2_PPT, K2_ST, K2_NHE>
+#define K3S k3_stream<K3_NH, K3_NC, S_NCW, K3_PPT, K3_ST, K3_NHE>
 #define XDS exdot_stream<X_NH, X_NL, X_NCW, XD_PPT, XD_ST>
 static constexpr size_t ring_bytes(int nv, int ncw, int ppt, int stages) {
     return sizeof(double) * (size_t)stages * nv * (2 * ncw * 32 * ppt) + 2 * sizeof(uint64_t) * stages;

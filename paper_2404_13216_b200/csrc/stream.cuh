@@ -91,9 +91,9 @@ __device__ __forceinline__ size_t stream_smem_bytes() {
 // Splitting the dots halves the accumulator registers per thread, which buys
 // twice the warps (the ExBLAS cascades are latency-bound chains of DADDs).
 // ---------------------------------------------------------------------------
-template <int NH, int NL>
+template <int NH, int NL, int NHE>
 struct K2Op {
-    ExAccT<NH, NL> d0, d1;
+    ExAccT<NH, NL, NHE> d0, d1;
     double be, nom, nal;
     bool first;
     __device__ __forceinline__ void sz(double w, double t, double v, double &s, double &z) const {
@@ -125,7 +125,7 @@ struct K2Op {
     }
 };
 
-template <int NH, int NL, int W, int PPT, int STAGES>
+template <int NH, int NL, int W, int PPT, int STAGES, int NHE>
 __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
     constexpr int NV = 8;  // r, rh, w, t | p, s, z, v
     constexpr int NCW = 2 * W;
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
     const bool first = (sc->it == 0);
     const int64_t n = a.n;
     unsigned flags = 0;
-    K2Op<NH, NL> R;
+    K2Op<NH, NL, NHE> R;
     R.first = first;
     R.be = sc->beta;
     R.nom = -sc->omega;
@@ -246,9 +246,9 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
 // K3 (Alg. 2 l.77-79) + phase-B dots.  Group 0: x, r' and (r0,r'), (r',r');
 // group 1: w' and (r0,w').
 // ---------------------------------------------------------------------------
-template <int NH, int NL>
+template <int NH, int NL, int NHE>
 struct K3Op {
-    ExAccT<NH, NL> d0, d1;
+    ExAccT<NH, NL, NHE> d0, d1;
     double al, om, nal, nom;
     // group 0: x, r' and the products of (r0,r'), (r',r')
     __device__ __forceinline__ void row0(unsigned &flags, double rh, double p, double q, double y, double &x, double &r,
@@ -267,7 +267,7 @@ struct K3Op {
     }
 };
 
-template <int NH, int NL, int W, int PPT, int STAGES>
+template <int NH, int NL, int W, int PPT, int STAGES, int NHE>
 __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
     constexpr int NV = 7;  // rh, p, q, y, t, v, x
     constexpr int NCW = 2 * W;
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
     __syncthreads();
     const int64_t n = a.n;
     unsigned flags = 0;
-    K3Op<NH, NL> R;
+    K3Op<NH, NL, NHE> R;
     R.al = sc->alpha;
     R.om = sc->omega;
     R.nal = -R.al;

@@ -15,7 +15,7 @@ for it in (0, 10, 50, 100, 200):
     pb.debug_counters(reset=True)
     ms = S.profile(1)
     c = pb.debug_counters(reset=True)
-    print(f"{name} iter {it}: products {7*A.n} warp-batches ~{A.n//64*5} mixed {c[1]} all-lo {c[2]} deposits {c[3]} ({c[3]/(7*A.n):.3%})  ms K2 {ms[0]:.3f} K3 {ms[2]:.3f}")
+    print(f"{name} iter {it}: products {7*A.n} warp-batches ~{A.n//64*5} cold-p warp-products {c[1]} cold-e {c[2]} deposits {c[3]} ({c[3]/(7*A.n):.3%})  ms K2 {ms[0]:.3f} K3 {ms[2]:.3f}")
 if len(sys.argv) > 2:
     n = 1 << 24
     for kind, (x, y) in (("well", (gen.uniform(n, 1), gen.uniform(n, 2))), ("ill", gen.ill_pair(n, seed=3))):
