@@ -528,6 +528,89 @@ __global__ void __launch_bounds__(256) spmv_sell_kernel(SellMat A, const double 
     }
 }
 
+// Software-pipelined SELL SpMV.  A thread owns positions pos, pos + stride,
+// ... (persistent grid).  Work is a stream of batches of UNR slots: while the
+// x-gathers of batch j are in flight, the val/col loads of batch j+1 (the next
+// batch of this row, or the first batch of the next row, whose descriptor was
+// loaded one row ahead) are already issued.  Each thread therefore waits on
+// one round trip per batch instead of three per row (descriptor -> val/col ->
+// x).  The fold is unchanged: one fma per nonzero, ascending columns, +0.0
+// start, never over padding (R-6).
+template <int MODE, int UNR>
+__global__ void __launch_bounds__(256) spmv_sell_pipe_kernel(SellMat A, const double *__restrict__ x,
+                                                             double *__restrict__ y, const double *__restrict__ b,
+                                                             double *__restrict__ y2, const Scalars *sc) {
+    if (sc && sc->done) return;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // descriptor of a position: slot-0 offset and row length (0 past the end)
+    auto desc = [&](int64_t p, int64_t &base, int &len) {
+        base = 0;
+        len = 0;
+        if (p < A.n) {
+            base = __ldg(&A.slice_off[p >> 5]) + (p & 31);
+            len = __ldg(&A.row_len[p]);
+        }
+    };
+    auto load_vc = [&](int64_t base, int k0, int len, double *v, int *c) {
+#pragma unroll
+        for (int j = 0; j < UNR; ++j)
+            if (k0 + j < len) {
+                v[j] = __ldcs(A.val + base + 32 * (k0 + j));
+                c[j] = __ldcs(A.col + base + 32 * (k0 + j));
+            }
+    };
+    int64_t cbase, nbase;
+    int clen, nlen;
+    desc(pos, cbase, clen);
+    desc(pos + stride, nbase, nlen);
+    double v[UNR], vn[UNR], xv[UNR];
+    int c[UNR], cn[UNR];
+    load_vc(cbase, 0, clen, v, c);
+    while (pos < A.n) {
+        double acc = 0.0;
+        for (int k0 = 0;; k0 += UNR) {
+#pragma unroll
+            for (int j = 0; j < UNR; ++j)
+                if (k0 + j < clen) xv[j] = __ldg(x + c[j]);
+            const bool more = k0 + UNR < clen;
+            // prefetch the next batch: rest of this row, or the next row's first
+            int64_t nnbase = 0;
+            int nnlen = 0;
+            if (more) {
+                load_vc(cbase, k0 + UNR, clen, vn, cn);
+            } else {
+                load_vc(nbase, 0, nlen, vn, cn);
+                desc(pos + 2 * stride, nnbase, nnlen);
+            }
+#pragma unroll
+            for (int j = 0; j < UNR; ++j)
+                if (k0 + j < clen) acc = __fma_rn(v[j], xv[j], acc);
+#pragma unroll
+            for (int j = 0; j < UNR; ++j) {
+                v[j] = vn[j];
+                c[j] = cn[j];
+            }
+            if (!more) {
+                const int64_t row = A.perm ? (int64_t)__ldg(&A.perm[pos]) : pos;
+                if (MODE == SPMV_PLAIN) {
+                    y[row] = acc;
+                } else {
+                    const double r = __dsub_rn(b[row], acc);  // r0 := b - A x0 (l.64)
+                    y[row] = r;
+                    if (y2) y2[row] = r;
+                }
+                pos += stride;
+                cbase = nbase;
+                clen = nlen;
+                nbase = nnbase;
+                nlen = nnlen;
+                break;
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------------
 // setup helpers
 // ------------------------------------------------------------------------

@@ -238,6 +238,7 @@ struct Rank {
     double *z() const { return zpad + own_off; }
     double *w() const { return wpad + own_off; }
     std::vector<int32_t> h_perm;  // SELL position -> local row (empty: identity)
+    int32_t max_len = 0;          // longest row of this rank
     int32_t *perm = nullptr;
     SellMat mat() const { return SellMat{n, slice_off, row_len, sval, scol, h_perm.empty() ? nullptr : perm}; }
 };
@@ -364,6 +365,8 @@ static int plan_ranks(pbcg_handle *h, const pbcg_csr_local *A, const std::vector
             R.sell_nnz = R.h_slice_off[R.nslices];
         };
         slices(nullptr);
+        R.max_len = 0;
+        for (int64_t q = 0; q < R.n; ++q) R.max_len = std::max(R.max_len, rowlen(q));
         const int64_t nnz = (int64_t)h_rp[r0 + R.n] - h_rp[r0];
         R.h_perm.clear();
         if (R.sell_nnz > nnz + nnz / 16) {
@@ -547,10 +550,32 @@ static int spmv_rpt() {  // rows per thread of the SELL SpMV (PBCG_SPMV_RPT = 1 
     return g_spmv_rpt;
 }
 
+// SpMV kernel choice: the software-pipelined persistent kernel for short rows
+// (every row fits one batch of 8 slots: stencils), the one-row-per-thread
+// kernel otherwise (long rows: more warps in flight beat the pipeline).
+// PBCG_SPMV_KERNEL=pipe|plain overrides (A/B runs).
+static int g_spmv_pipe = -2;
+static bool spmv_pipe(const Rank &R) {
+    if (g_spmv_pipe == -2) {
+        const char *e = getenv("PBCG_SPMV_KERNEL");
+        g_spmv_pipe = !e ? -1 : (strcmp(e, "pipe") == 0 ? 1 : 0);
+    }
+    return g_spmv_pipe >= 0 ? g_spmv_pipe == 1 : R.max_len <= 8;
+}
+
 static int launch_spmv(pbcg_handle *h, Rank &R, int mode, const double *xpad, double *y, const double *b, double *y2,
                        bool predicated, cudaStream_t st) {
     if (R.n == 0) return PBCG_OK;
     const Scalars *sc = predicated ? R.sc : nullptr;
+    if (spmv_pipe(R)) {
+        static int grid_pipe = 0;
+        if (!grid_pipe) grid_pipe = grid_for((const void *)spmv_sell_pipe_kernel<SPMV_PLAIN, 8>, 256, h->nsm);
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid_pipe, (R.n + 255) / 256));
+        if (mode == SPMV_PLAIN) spmv_sell_pipe_kernel<SPMV_PLAIN, 8><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
+        else spmv_sell_pipe_kernel<SPMV_RESID, 8><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
+        CUDA_TRY(cudaGetLastError());
+        return PBCG_OK;
+    }
     const int rpt = spmv_rpt();
     const int grid = (int)((R.n + 256 * rpt - 1) / (256 * rpt));
     if (rpt == 2) {
