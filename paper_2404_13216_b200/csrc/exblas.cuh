@@ -161,6 +161,7 @@ inline void sacc_deposit_host(long long *acc, double v) {
 // Carry-normalise (one thread): words 0..L-2 -> [0,2^32), carry into word L-1.
 __host__ __device__ __forceinline__ void sacc_normalize(long long *w) {
     long long carry = 0;
+#pragma unroll 8
     for (int i = 0; i < SACC_L - 1; ++i) {
         long long v = w[i] + carry;
         carry = v >> 32;  // arithmetic shift = floor division
@@ -224,6 +225,84 @@ __host__ __device__ inline double sacc_round(const long long *w, bool *ovf) {
         }
     }
     return neg ? -r : r;
+}
+
+// Warp-parallel twin of sacc_round (all 32 lanes; same result in every lane).
+// Digits are spread over the lanes (digit i in lane i%32, slot i/32); the
+// sign, the lowest / highest nonzero digit and the sticky bit come from
+// ballots, so the cost is a few dozen instructions instead of a serial scan.
+__device__ double sacc_round_warp(const long long *w, bool *ovf) {
+    const int lane = threadIdx.x & 31;
+    constexpr int ND = SACC_L + 1;  // 68 two's complement 32-bit digits
+    const long long top = w[SACC_L - 1];
+    unsigned dg[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int i = lane + 32 * k;
+        dg[k] = i < SACC_L - 1 ? (unsigned)w[i]
+                : i == SACC_L - 1 ? (unsigned)((unsigned long long)top & 0xFFFFFFFFull)
+                : i == SACC_L ? (unsigned)((unsigned long long)top >> 32) : 0u;
+    }
+    auto lowest = [&](const unsigned *m) -> int {
+        for (int k = 0; k < 3; ++k)
+            if (m[k]) return 32 * k + __ffs(m[k]) - 1;
+        return -1;
+    };
+    unsigned msk[3];
+    if (top < 0) {  // magnitude = two's complement negation: ~d + 1 rippling from the lowest nonzero digit
+#pragma unroll
+        for (int k = 0; k < 3; ++k) msk[k] = __ballot_sync(0xFFFFFFFFu, dg[k] != 0u);
+        const int z = lowest(msk);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int i = lane + 32 * k;
+            dg[k] = i >= ND ? 0u : (i < z) ? 0u : (i == z) ? (0u - dg[k]) : ~dg[k];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) msk[k] = __ballot_sync(0xFFFFFFFFu, dg[k] != 0u);
+    int H = -1;
+    for (int k = 2; k >= 0 && H < 0; --k)
+        if (msk[k]) H = 32 * k + 31 - __clz(msk[k]);
+    if (H < 0) return 0.0;
+    auto get = [&](int i) -> unsigned {  // digit i, i uniform across the warp
+        const int kk = i < 0 ? 0 : i >> 5;
+        const unsigned v = kk == 0 ? dg[0] : kk == 1 ? dg[1] : dg[2];
+        const unsigned r = __shfl_sync(0xFFFFFFFFu, v, i < 0 ? 0 : (i & 31));
+        return i < 0 ? 0u : r;
+    };
+    const unsigned hi = get(H), mid = get(H - 1), lo = get(H - 2);
+    bool below = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) below |= __any_sync(0xFFFFFFFFu, dg[k] != 0u && (lane + 32 * k) < H - 2);
+    const int p = 31 - __clz(hi);
+    const int B = 32 * H + p;  // index of the most significant bit (bit 0 = 2^-1074)
+    double r;
+    if (B < 52) {  // subnormal: exact, digits 0 and 1 only
+        const unsigned long long m = ((unsigned long long)get(1) << 32) | get(0);
+        r = bits_to_double(m);
+    } else {
+        const int sft = 31 - p;
+        const unsigned long long top64 = ((unsigned long long)hi << 32) | mid;
+        const unsigned long long T = sft ? ((top64 << sft) | ((unsigned long long)lo >> (32 - sft))) : top64;
+        const unsigned rest = sft ? (unsigned)(lo << sft) : lo;
+        unsigned long long m = T >> 11;  // 53 bits, MSB at bit 52
+        const unsigned rb = (unsigned)(T >> 10) & 1u;
+        const bool sticky = ((T & 0x3FFull) != 0) || rest != 0 || below;
+        int k0 = B - 52;
+        if (rb && (sticky || (m & 1ull))) {
+            m += 1;
+            if (m == (1ull << 53)) { m >>= 1; k0 += 1; }
+        }
+        const long long be = (long long)k0 + 1;
+        if (be >= 2047) {
+            *ovf = true;
+            r = bits_to_double(0x7FF0000000000000ull);
+        } else {
+            r = bits_to_double(((unsigned long long)be << 52) | (m & 0xFFFFFFFFFFFFFull));
+        }
+    }
+    return top < 0 ? -r : r;
 }
 
 template <int N>

@@ -129,10 +129,13 @@ __device__ void last_cta_finish(CtaSacc<ND> &S, long long *gacc, unsigned *ticke
     cta_sacc_collect<ND>(S, gacc, gflags);
     long long *w = (long long *)&S.w[0][0];
     if (finalize) {
-        if (threadIdx.x < ND) {
+        if ((threadIdx.x >> 5) < ND) {  // one warp per dot
             bool ovf = false;
-            S.rounded[threadIdx.x] = sacc_round(w + threadIdx.x * SACC_L, &ovf);
-            if (ovf) atomicOr(&S.flags, FLAG_RANGE);
+            const double rv = sacc_round_warp(w + (threadIdx.x >> 5) * SACC_L, &ovf);
+            if ((threadIdx.x & 31) == 0) {
+                S.rounded[threadIdx.x >> 5] = rv;
+                if (ovf) atomicOr(&S.flags, FLAG_RANGE);
+            }
         }
         __syncthreads();
         // rare error path: a flagged standalone dot is classified as
@@ -431,10 +434,13 @@ __global__ void finalize_kernel(long long *gacc, int phase, Scalars *sc, double 
     unsigned gflags;
     cta_sacc_collect<ND>(S, gacc, gflags);
     long long *w = (long long *)&S.w[0][0];
-    if (threadIdx.x < ND) {
+    if ((threadIdx.x >> 5) < ND) {  // one warp per dot
         bool ovf = false;
-        S.rounded[threadIdx.x] = sacc_round(w + threadIdx.x * SACC_L, &ovf);
-        if (ovf) atomicOr(&S.flags, FLAG_RANGE);
+        const double rv = sacc_round_warp(w + (threadIdx.x >> 5) * SACC_L, &ovf);
+        if ((threadIdx.x & 31) == 0) {
+            S.rounded[threadIdx.x >> 5] = rv;
+            if (ovf) atomicOr(&S.flags, FLAG_RANGE);
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) phase_finalize(phase, sc, S.rounded, gflags | (S.flags & FLAG_RANGE), hist, out, out_flags);

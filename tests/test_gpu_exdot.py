@@ -62,6 +62,16 @@ def test_spec_examples(pb):
 def test_edge_values(pb):
     u = 2.0 ** -52
     check(pb, [(1 + u) * 2.0 ** -480, -(1 + 2 * u) * 2.0 ** -480], [(1 + u) * 2.0 ** -480, 2.0 ** -480])
+    # the same magnitudes with negative sums: the rounding works on the
+    # two's complement superaccumulator (negation, ties, subnormals)
+    check(pb, [-(1 + u) * 2.0 ** -480, (1 + 2 * u) * 2.0 ** -480], [(1 + u) * 2.0 ** -480, 2.0 ** -480])
+    for sgn in (1.0, -1.0):
+        check(pb, [sgn, sgn * 2.0 ** -53], [1.0, 1.0])                      # tie to even
+        check(pb, [sgn * (1.0 + 2.0 ** -52), sgn * 2.0 ** -53], [1.0, 1.0])  # tie to even, rounds away
+        check(pb, [sgn, sgn * 2.0 ** -53, sgn * 2.0 ** -300], [1.0, 1.0, 1.0])  # sticky far below
+        check(pb, [sgn * 2.0 ** 900, -sgn * 2.0 ** 900, sgn * 3.0], [2.0 ** 90, 2.0 ** 90, 2.0 ** -900])
+        check(pb, [sgn * 2.0 ** 400] * 8, [2.0 ** 599] * 8)                 # near overflow, in range
+        check(pb, [sgn * (2.0 - 2.0 ** -52) * 2.0 ** 499] * 2, [2.0 ** 499, 2.0 ** 499])
     # range zone and non-finite flags mirror the oracle (R-9)
     check(pb, [2.0 ** -1074], [1.0])
     check(pb, [2.0 ** -480], [2.0 ** -481])
