@@ -101,10 +101,14 @@ class Clocks:
 
 
 # --------------------------------------------------------------- workloads --
-def algorithmic_bytes(n: int, nnz: int):
-    """SpMV 12 nnz + 4 (n+1) + 16 n; K2 104 n; K3 80 n."""
-    spmv = 12 * nnz + 4 * (n + 1) + 16 * n
-    return {"k2": 104 * n, "spmv": spmv, "k3": 80 * n, "iteration": 2 * spmv + 184 * n}
+def algorithmic_bytes(n: int, nnz: int, spmv_format_bytes=None):
+    """K2 104 n; K3 80 n; SpMV 12 nnz + 4 (n+1) + 16 n for
+    CSR.  With the stored format's own count (pbcg_spmv_format [5]: 8 nnz +
+    4 per explicit column id + slot records + lengths + x once + y) the SpMV
+    figure is the bytes that format must move; `spmv_csr` keeps the CSR one."""
+    csr = 12 * nnz + 4 * (n + 1) + 16 * n
+    spmv = spmv_format_bytes if spmv_format_bytes else csr
+    return {"k2": 104 * n, "spmv": spmv, "spmv_csr": csr, "k3": 80 * n, "iteration": 2 * spmv + 184 * n}
 
 
 def local_rows(A, rank, world):
@@ -175,7 +179,10 @@ def run_gpu(args, rank, world, local_rank, dist):
     out = {"ms": ms, "ok": ok, "iters": res.iterations, "clocks": clk}
     # ---- per-kernel times: a second timed pass over the same K steps with
     # CUDA events around every launch (single rank) ----
-    by = algorithmic_bytes(nloc, Al.nnz)
+    fmt = S.spmv_format()
+    by = algorithmic_bytes(nloc, Al.nnz, fmt["bytes_per_spmv"])
+    out["spmv_format"] = fmt
+    out["by"] = by
     kern = None
     if world == 1:
         S.start(b, tol=0.0, max_iter=W + K + 8)
@@ -381,9 +388,10 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": args.gpus, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_config(args, A),
-            "valid": out["ok"], "gpu_launches": 4 * K if args.gpus == 1 else None}
-    if args.gpus > 1:
-        line["gpu_launches"] = 8 * K  # K2, finalize A, SpMV, K3, finalize B, SpMV per rank per iteration (+NCCL)
+            "valid": out["ok"],
+            # K2, finalize A, SpMV, K3, finalize B, SpMV per iteration (per rank; NCCL kernels not counted)
+            "gpu_launches": 6 * K}
+    line["spmv_format"] = out["spmv_format"]
     line["bytes_per_iteration_per_gpu"] = by["iteration"]
     line["iteration_GBps_per_gpu"] = by["iteration"] / (ms_step * 1e-3) / 1e9
     line["iteration_frac_hbm"] = line["iteration_GBps_per_gpu"] / hbm

@@ -211,6 +211,17 @@ int pbcg_set_chunk(int32_t iters);
  * (device or host, n_local doubles).  Synchronises.  Tests and diagnostics. */
 int pbcg_get_vector(pbcg_handle *h, int32_t which, double *out);
 
+/* Stored SpMV format of this handle (all its ranks), 8 int64:
+ * [0] rows, [1] nonzeros, [2] sliced-ELL entries incl. padding, [3] column ids
+ * read explicitly (the rest follow from a per slice-slot offset: every row of
+ * the 32-row slice finds its k-th nonzero at x index row + d, k < 15),
+ * [4] slot-record words (16 per slice, 0 if unused), [5] algorithmic bytes of
+ * one SpMV = 8 nnz + 4 [3] + 4 [4] + 4 rows (lengths) + 8 slices + 16 rows
+ * (x once, y) (+ 4 rows sigma-permutation), [6] longest row, [7] 1 if rows
+ * are sigma-sorted.  The fold of every row is the CSR fma chain regardless
+ * (R-6).  Host-only, no synchronisation. */
+int pbcg_spmv_format(pbcg_handle *h, int64_t *out8);
+
 /* Spill counters of a -DPBCG_DEBUG_COUNTERS build (16 uint64; zeros in the
  * release build): [1] warp spill votes, [2] overflow-tier entries, [3]
  * superaccumulator deposits.  reset != 0 clears them. */

@@ -93,6 +93,7 @@ def lib(build_if_missing: bool = True) -> ctypes.CDLL:
         L.pbcg_set_chunk.argtypes = [i32]
         L.pbcg_profile_iterations.argtypes = [vp, i32, vp]
         L.pbcg_debug_counters.argtypes = [vp, i32]
+        L.pbcg_spmv_format.argtypes = [vp, vp]
         L.pbcg_get_vector.argtypes = [vp, i32, vp]
         _lib = L
     return _lib
@@ -254,6 +255,14 @@ class Solver:
         ms = np.zeros(6, np.float64)
         _check(lib().pbcg_profile_iterations(self._h, int(k), ctypes.c_void_p(ms.ctypes.data)))
         return ms
+
+    def spmv_format(self) -> dict:
+        """The stored SpMV format (include/pbicgstab.h pbcg_spmv_format)."""
+        out = np.zeros(8, np.int64)
+        _check(lib().pbcg_spmv_format(self._h, ctypes.c_void_p(out.ctypes.data)))
+        keys = ("rows", "nnz", "sell_entries", "explicit_cols", "slot_records", "bytes_per_spmv", "max_row_len",
+                "sigma_sorted")
+        return {k: int(v) for k, v in zip(keys, out)}
 
     VEC = dict(b=0, x=1, r=2, rh=3, p=4, s=5, z=6, q=7, y=8, w=9, t=10, v=11)
 

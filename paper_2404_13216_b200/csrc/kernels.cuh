@@ -467,9 +467,20 @@ struct SellMat {
     const int64_t *slice_off;  // nslices+1, element offsets of each slice
     const int32_t *row_len;    // by position
     const double *val;
-    const int32_t *col;        // indices into the rank's padded x buffer
+    const int32_t *col;        // x-buffer index of the nonzero minus the position (pos-relative)
     const int32_t *perm;       // position -> row (sigma-sorted windows), or null (identity)
+    // Per slice-slot column offsets (index compression of the sliced ELL):
+    // SELL_RS int32 per slice s: rec[16 s + 15] = mask; bit k (k < 15) set
+    // <=> every row of slice s that has a k-th nonzero finds it at x-buffer
+    // index pos + rec[16 s + k]; the column ids of that slice-slot are then
+    // never read.  Slots k >= 15 are always explicit.  Null: every slot
+    // explicit.  The same nonzeros are folded in the same order (R-6).
+    const int32_t *slot_rec;
 };
+
+static constexpr int SELL_RS = 16, SELL_MASK = 15;
+
+static constexpr int32_t SELL_EXPLICIT = INT32_MIN;
 
 enum { SPMV_PLAIN = 0, SPMV_RESID = 1 };
 
@@ -512,7 +523,7 @@ __global__ void __launch_bounds__(256) spmv_sell_kernel(SellMat A, const double 
         for (int u = 0; u < RPT; ++u)
 #pragma unroll
             for (int j = 0; j < UNR; ++j)
-                if (k + j < len[u]) xv[u][j] = __ldg(x + c[u][j]);
+                if (k + j < len[u]) xv[u][j] = __ldg(x + (pos0 + 256 * u + c[u][j]));
 #pragma unroll
         for (int u = 0; u < RPT; ++u)
 #pragma unroll
@@ -578,7 +589,7 @@ __global__ void __launch_bounds__(256) spmv_sell_pipe_kernel(SellMat A, const do
         for (int k0 = 0;; k0 += UNR) {
 #pragma unroll
             for (int j = 0; j < UNR; ++j)
-                if (k0 + j < clen) xv[j] = __ldg(x + c[j]);
+                if (k0 + j < clen) xv[j] = __ldg(x + (pos + c[j]));
             const bool more = k0 + UNR < clen;
             // prefetch the next batch: rest of this row, or the next row's first
             int64_t nnbase = 0;
@@ -659,7 +670,7 @@ __global__ void csr_to_sell_kernel(int64_t n, const int32_t *rp, const int32_t *
             if (!isfinite(v)) atomicOr(bad, 2);
             prev = c;
             sval[base + 32 * k] = v;
-            scol[base + 32 * k] = (int32_t)((int64_t)c - col_shift);
+            scol[base + 32 * k] = (int32_t)((int64_t)c - col_shift - r);  // pos-relative
         }
         const int64_t width = (slice_off[(r >> 5) + 1] - slice_off[r >> 5]) >> 5;
         for (int64_t k = len; k < width; ++k) {  // padding: never folded, kept addressable
@@ -667,6 +678,42 @@ __global__ void csr_to_sell_kernel(int64_t n, const int32_t *rp, const int32_t *
             scol[base + 32 * k] = 0;
         }
     }
+}
+
+// Slot records of the sliced ELL (SellMat::slot_rec): one warp per slice.
+// For slot k < SELL_MASK the lanes whose row has a k-th nonzero compare their
+// pos-relative column; all equal -> record it and set mask bit k.  n_explicit
+// counts the column ids that stay explicit (the format's index bytes).
+__global__ void sell_slot_records_kernel(int64_t n, int64_t nslices, const int64_t *slice_off, const int32_t *row_len,
+                                         const int32_t *scol, int32_t *slot_rec, unsigned long long *n_explicit) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long expl = 0;
+    for (int64_t sl = wid; sl < nslices; sl += nw) {
+        const int64_t pos = sl * 32 + lane;
+        const int len = pos < n ? row_len[pos] : 0;
+        const int64_t so = slice_off[sl];
+        const int64_t width = (slice_off[sl + 1] - so) >> 5;
+        uint32_t mask = 0;
+        int32_t d_lane = 0;  // lane k keeps the record of slot k
+        for (int64_t k = 0; k < width; ++k) {
+            const bool act = k < len;
+            const int d = act ? scol[so + lane + 32 * k] : 0;
+            const int dmin = __reduce_min_sync(0xFFFFFFFFu, act ? d : INT32_MAX);
+            const int dmax = __reduce_max_sync(0xFFFFFFFFu, act ? d : INT32_MIN);
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, act);
+            const bool uni = dmin == dmax && k < SELL_MASK;
+            if (uni) {
+                mask |= 1u << k;
+                if (lane == k) d_lane = dmin;
+            } else {
+                expl += __popc(m);
+            }
+        }
+        if (lane < SELL_RS) slot_rec[sl * SELL_RS + lane] = lane == SELL_MASK ? (int32_t)mask : d_lane;
+    }
+    if (lane == 0 && expl) atomicAdd(n_explicit, expl);
 }
 
 __global__ void nonfinite_scan_kernel(int64_t n, const double *v, int *bad) {

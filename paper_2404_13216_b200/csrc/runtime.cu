@@ -215,6 +215,20 @@ static constexpr int K_BS = 256;
 static constexpr int K_NP = 4, K_NE = 4;             // FPE depth for products / errors (performance only, R-16)
 static constexpr int U_K2 = 2, U_K3 = 2, U_MD4 = 2, U_MD1 = 4;  // row pairs in flight per thread
 
+// packed SELL-P geometry (spmv_sellp_kernel): slices per chunk, slices per
+// consumer warp, ring stages
+#ifndef PBCG_PS_SPS
+#define PBCG_PS_SPS 32
+#endif
+#ifndef PBCG_PS_RPW
+#define PBCG_PS_RPW 2
+#endif
+#ifndef PBCG_PS_MAXSTAGES
+#define PBCG_PS_MAXSTAGES 8
+#endif
+static constexpr int PS_SPS = PBCG_PS_SPS, PS_RPW = PBCG_PS_RPW, PS_MAXSTAGES = PBCG_PS_MAXSTAGES;
+static constexpr int PS_SMEM_MAX = 227 * 1024;
+
 struct Rank {
     int id = 0;
     int64_t rb = 0, re = 0, n = 0;
@@ -240,7 +254,20 @@ struct Rank {
     std::vector<int32_t> h_perm;  // SELL position -> local row (empty: identity)
     int32_t max_len = 0;          // longest row of this rank
     int32_t *perm = nullptr;
-    SellMat mat() const { return SellMat{n, slice_off, row_len, sval, scol, h_perm.empty() ? nullptr : perm}; }
+    int32_t *slot_rec = nullptr;  // SELL_RS slot records per slice (SellMat::slot_rec)
+    bool use_slots = true;
+    int64_t nnz = 0, n_explicit = 0;  // stored nonzeros, column ids that stay explicit
+    int spmv_kind = 0;                // SpMV kernel (set at setup)
+    // packed SELL-P chunks (rows <= 8 nonzeros): blob + byte offsets per chunk
+    int64_t nchunks = 0, blob_cap = 0, blob_bytes = 0;
+    unsigned char *blob = nullptr;
+    int64_t *blob_off = nullptr;
+    uint8_t *nexp = nullptr;
+    int ps_stage = 0, ps_stages = 0;  // ring geometry of spmv_sellp_kernel (bytes per stage, stages)
+    SellMat mat() const {
+        return SellMat{n, slice_off, row_len, sval, scol, h_perm.empty() ? nullptr : perm,
+                       use_slots ? slot_rec : nullptr};
+    }
 };
 
 struct pbcg_handle {
@@ -285,10 +312,18 @@ struct Carver {
 
 static void carve_rank(Carver &C, Rank &R, int hist_cap, bool comm_only) {
     if (!comm_only) {
-        R.slice_off = C.take<int64_t>(R.nslices + 1);
-        R.row_len = C.take<int32_t>(R.n);
+        R.slice_off = C.take<int64_t>(R.nslices + 16);      // + tail read by the TMA SpMV
+        R.row_len = C.take<int32_t>((size_t)R.nslices * 32);  // whole slices, zero past n
         R.sval = C.take<double>(R.sell_nnz);
         R.scol = C.take<int32_t>(R.sell_nnz);
+        R.slot_rec = C.take<int32_t>((size_t)R.nslices * SELL_RS);
+        if (R.max_len <= 8) {  // SELL-P blob: worst case every slot explicit
+            R.nchunks = (R.nslices + PS_SPS - 1) / PS_SPS;
+            R.blob_cap = R.nchunks * (int64_t)(SellPGeo<PS_SPS>::H + 16) + 12 * R.sell_nnz;
+            R.blob = C.take<unsigned char>((size_t)R.blob_cap);
+            R.blob_off = C.take<int64_t>((size_t)R.nchunks + 1);
+            R.nexp = C.take<uint8_t>((size_t)R.nslices);
+        }
         R.perm = C.take<int32_t>(R.h_perm.size());
         const size_t n = (size_t)R.n + 2;
         R.x = C.take<double>(n); R.r = C.take<double>(n); R.rh = C.take<double>(n); R.p = C.take<double>(n);
@@ -368,6 +403,7 @@ static int plan_ranks(pbcg_handle *h, const pbcg_csr_local *A, const std::vector
         R.max_len = 0;
         for (int64_t q = 0; q < R.n; ++q) R.max_len = std::max(R.max_len, rowlen(q));
         const int64_t nnz = (int64_t)h_rp[r0 + R.n] - h_rp[r0];
+        R.nnz = nnz;
         R.h_perm.clear();
         if (R.sell_nnz > nnz + nnz / 16) {
             // sigma-sorting (sliced ELL-C-sigma, C = 32, sigma = SELL_SIGMA): rows
@@ -541,50 +577,54 @@ static int reduce_finalize(pbcg_handle *h, int ph, int phase, cudaStream_t st, d
 
 static bool multi(const pbcg_handle *h) { return h->V > 1 || h->comm; }
 
-static int g_spmv_rpt = 0;
-static int spmv_rpt() {  // rows per thread of the SELL SpMV (PBCG_SPMV_RPT = 1 | 2)
-    if (!g_spmv_rpt) {
-        const char *e = getenv("PBCG_SPMV_RPT");
-        g_spmv_rpt = (e && atoi(e) == 2) ? 2 : 1;
-    }
-    return g_spmv_rpt;
+
+// SpMV kernel choice.  Short rows (every row <= 8 nonzeros: stencils) and
+// at least SELLP_MIN_CHUNKS chunks per SM: the TMA kernel on the packed
+// SELL-P chunks (spmv_sellp_kernel); smaller short-row matrices: the
+// register-pipelined persistent kernel (no ring to fill); long rows: one row
+// per thread (more warps in flight).  PBCG_SPMV_KERNEL=tma|pipe|plain
+// overrides (A/B runs).
+enum { SPMV_K_PLAIN = 0, SPMV_K_PIPE = 1, SPMV_K_TMA = 2 };
+static constexpr int SELLP_MIN_CHUNKS = 16;
+static int spmv_kind_for(const Rank &R, int nsm) {  // at setup
+    if (R.max_len > 8) return SPMV_K_PLAIN;
+    const char *e = getenv("PBCG_SPMV_KERNEL");
+    if (!e) return R.nchunks >= (int64_t)SELLP_MIN_CHUNKS * nsm ? SPMV_K_TMA : SPMV_K_PIPE;
+    return strcmp(e, "pipe") == 0 ? SPMV_K_PIPE : strcmp(e, "tma") == 0 ? SPMV_K_TMA : SPMV_K_PLAIN;
 }
 
-// SpMV kernel choice: the software-pipelined persistent kernel for short rows
-// (every row fits one batch of 8 slots: stencils), the one-row-per-thread
-// kernel otherwise (long rows: more warps in flight beat the pipeline).
-// PBCG_SPMV_KERNEL=pipe|plain overrides (A/B runs).
-static int g_spmv_pipe = -2;
-static bool spmv_pipe(const Rank &R) {
-    if (g_spmv_pipe == -2) {
-        const char *e = getenv("PBCG_SPMV_KERNEL");
-        g_spmv_pipe = !e ? -1 : (strcmp(e, "pipe") == 0 ? 1 : 0);
+template <int MODE>
+static void spmv_dispatch(pbcg_handle *h, const Rank &R, const double *xpad, double *y, const double *b, double *y2,
+                          const Scalars *sc, cudaStream_t st) {
+    if (R.spmv_kind == SPMV_K_TMA) {
+        auto *k = spmv_sellp_kernel<MODE, PS_SPS, PS_RPW>;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute((const void *)k, cudaFuncAttributeMaxDynamicSharedMemorySize, PS_SMEM_MAX);
+            attr = true;
+        }
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->nsm, R.nchunks));
+        const size_t smem = (size_t)R.ps_stages * R.ps_stage + 2 * R.ps_stages * sizeof(uint64_t);
+        k<<<grid, (PS_SPS / PS_RPW + 1) * 32, smem, st>>>(R.n, R.nslices, R.blob, R.blob_off,
+                                                          R.h_perm.empty() ? nullptr : R.perm, xpad, y, b, y2, sc,
+                                                          R.ps_stage, R.ps_stages);
+    } else if (R.spmv_kind == SPMV_K_PIPE) {
+        static int grid_pipe = 0;
+        if (!grid_pipe) grid_pipe = grid_for((const void *)spmv_sell_pipe_kernel<MODE, 8>, 256, h->nsm);
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid_pipe, (R.n + 255) / 256));
+        spmv_sell_pipe_kernel<MODE, 8><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
+    } else {
+        const int grid = (int)((R.n + 255) / 256);
+        spmv_sell_kernel<MODE, 8, 1><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
     }
-    return g_spmv_pipe >= 0 ? g_spmv_pipe == 1 : R.max_len <= 8;
 }
 
 static int launch_spmv(pbcg_handle *h, Rank &R, int mode, const double *xpad, double *y, const double *b, double *y2,
                        bool predicated, cudaStream_t st) {
     if (R.n == 0) return PBCG_OK;
     const Scalars *sc = predicated ? R.sc : nullptr;
-    if (spmv_pipe(R)) {
-        static int grid_pipe = 0;
-        if (!grid_pipe) grid_pipe = grid_for((const void *)spmv_sell_pipe_kernel<SPMV_PLAIN, 8>, 256, h->nsm);
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid_pipe, (R.n + 255) / 256));
-        if (mode == SPMV_PLAIN) spmv_sell_pipe_kernel<SPMV_PLAIN, 8><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
-        else spmv_sell_pipe_kernel<SPMV_RESID, 8><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
-        CUDA_TRY(cudaGetLastError());
-        return PBCG_OK;
-    }
-    const int rpt = spmv_rpt();
-    const int grid = (int)((R.n + 256 * rpt - 1) / (256 * rpt));
-    if (rpt == 2) {
-        if (mode == SPMV_PLAIN) spmv_sell_kernel<SPMV_PLAIN, 8, 2><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
-        else spmv_sell_kernel<SPMV_RESID, 8, 2><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
-    } else {
-        if (mode == SPMV_PLAIN) spmv_sell_kernel<SPMV_PLAIN, 8, 1><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
-        else spmv_sell_kernel<SPMV_RESID, 8, 1><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
-    }
+    if (mode == SPMV_PLAIN) spmv_dispatch<SPMV_PLAIN>(h, R, xpad, y, b, y2, sc, st);
+    else spmv_dispatch<SPMV_RESID>(h, R, xpad, y, b, y2, sc, st);
     CUDA_TRY(cudaGetLastError());
     return PBCG_OK;
 }
@@ -757,6 +797,46 @@ static int enqueue_iteration(pbcg_handle *h) {
 // ----------------------------------------------------------------------------
 // setup / destroy
 // ----------------------------------------------------------------------------
+// Packed SELL-P chunks (spmv_sellp_kernel): explicit-slot counts on the
+// device, chunk byte offsets on the host (prefix sum), then the scatter.
+static int build_sellp(pbcg_handle *h, Rank &R) {
+    using Geo = SellPGeo<PS_SPS>;
+    const int32_t *rec = R.use_slots ? R.slot_rec : nullptr;
+    const int g = (int)std::min<int64_t>((R.nslices + 255) / 256, 65535);
+    sellp_count_kernel<<<g, 256, 0, h->stream>>>(R.nslices, R.slice_off, rec, R.nexp);
+    CUDA_TRY(cudaGetLastError());
+    std::vector<uint8_t> ne(R.nslices);
+    CUDA_TRY(cudaMemcpyAsync(ne.data(), R.nexp, R.nslices, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    std::vector<int64_t> off(R.nchunks + 1, 0);
+    for (int64_t c = 0; c < R.nchunks; ++c) {
+        const int64_t s0 = c * PS_SPS, s1 = std::min<int64_t>(s0 + PS_SPS, R.nslices);
+        int64_t nx = 0;
+        for (int64_t s = s0; s < s1; ++s) nx += 32 * ne[s];
+        const int64_t nv = R.h_slice_off[s1] - R.h_slice_off[s0];
+        off[c + 1] = off[c] + ((Geo::H + 8 * nv + 4 * nx + 15) & ~int64_t(15));
+    }
+    if (off[R.nchunks] > R.blob_cap) return fail(PBCG_ENOMEM, "sellp: packed chunks exceed their bound");
+    R.blob_bytes = off[R.nchunks];
+    int64_t mx = 0;
+    for (int64_t c = 0; c < R.nchunks; ++c) mx = std::max(mx, off[c + 1] - off[c]);
+    R.ps_stage = (int)((mx + 127) & ~int64_t(127));
+    R.ps_stages = (int)std::min<int64_t>(PS_MAXSTAGES, (PS_SMEM_MAX - 256) / R.ps_stage);
+    if (R.ps_stages < 2) {  // chunks too large for a double-buffered ring: register-pipelined kernel
+        R.spmv_kind = SPMV_K_PIPE;
+        return PBCG_OK;
+    }
+    CUDA_TRY(cudaMemcpyAsync(R.blob_off, off.data(), sizeof(int64_t) * off.size(), cudaMemcpyHostToDevice, h->stream));
+    CUDA_TRY(cudaMemsetAsync(R.blob, 0, (size_t)R.blob_bytes, h->stream));
+    SellMat M = R.mat();
+    M.slot_rec = rec;
+    const int gf = (int)std::min<int64_t>((R.nslices + 7) / 8, 65535);
+    sellp_fill_kernel<PS_SPS><<<gf, 256, 0, h->stream>>>(R.n, R.nslices, M, R.nexp, R.blob_off, R.blob);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(h->stream));  // off (host vector) must outlive the copy
+    return PBCG_OK;
+}
+
 extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void *stream, void *workspace,
                                size_t workspace_bytes, pbcg_handle **out) {
     if (!out) return fail(PBCG_EINVAL, "out == NULL");
@@ -831,8 +911,10 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
     if (!h->comm_only) {
         for (size_t v = 0; v < h->R.size(); ++v) {
             Rank &R = h->R[v];
+            CUDA_TRY(cudaMemsetAsync(R.slice_off, 0, sizeof(int64_t) * (R.nslices + 16), h->stream));
             CUDA_TRY(cudaMemcpyAsync(R.slice_off, R.h_slice_off.data(), sizeof(int64_t) * (R.nslices + 1),
                                      cudaMemcpyHostToDevice, h->stream));
+            CUDA_TRY(cudaMemsetAsync(R.row_len, 0, sizeof(int32_t) * R.nslices * 32, h->stream));
             if (!R.h_perm.empty())
                 CUDA_TRY(cudaMemcpyAsync(R.perm, R.h_perm.data(), sizeof(int32_t) * R.h_perm.size(),
                                          cudaMemcpyHostToDevice, h->stream));
@@ -846,14 +928,37 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
                                                                 R.slice_off, R.row_len, R.sval, R.scol,
                                                                 R.h_perm.empty() ? nullptr : R.perm, R.bad);
                 CUDA_TRY(cudaGetLastError());
+                // column offsets per slice-slot (index compression of the SELL)
+                CUDA_TRY(cudaMemsetAsync(R.bad + 2, 0, sizeof(unsigned long long), h->stream));
+                const int gs = (int)std::min<int64_t>((R.nslices + 7) / 8, 65535);
+                sell_slot_records_kernel<<<gs, 256, 0, h->stream>>>(R.n, R.nslices, R.slice_off, R.row_len, R.scol,
+                                                                     R.slot_rec,
+                                                                     (unsigned long long *)(R.bad + 2));
+                CUDA_TRY(cudaGetLastError());
             }
         }
         CUDA_TRY(cudaStreamSynchronize(h->stream));
+        const char *es = getenv("PBCG_SELL_SLOTS");
         for (auto &R : h->R) {
+            R.spmv_kind = spmv_kind_for(R, h->nsm);
+            unsigned long long ne = 0;
+            if (R.n > 0) CUDA_TRY(cudaMemcpy(&ne, R.bad + 2, sizeof(ne), cudaMemcpyDeviceToHost));
+            // the slot records replace column ids in the packed SELL-P chunks
+            // when they spare at least a quarter of them
+            R.use_slots = R.spmv_kind == SPMV_K_TMA && !(es && es[0] == '0') && 4 * (int64_t)ne <= 3 * R.nnz;
+            R.n_explicit = R.use_slots ? (int64_t)ne : R.nnz;
             int bad = 0;
             CUDA_TRY(cudaMemcpy(&bad, R.bad, sizeof(int), cudaMemcpyDeviceToHost));
             if (bad & 1) return fail(PBCG_EINVAL, "csr: column ids not strictly increasing / out of range");
             if (bad & 2) return fail(PBCG_ENONFINITE, "csr: NaN/Inf value");
+            if (R.spmv_kind == SPMV_K_TMA) {
+                if (R.blob && R.n > 0) RC_TRY(build_sellp(h, R));
+                else R.spmv_kind = SPMV_K_PIPE;
+            }
+            if (R.spmv_kind != SPMV_K_TMA) {
+                R.use_slots = false;
+                R.n_explicit = R.nnz;
+            }
         }
     }
     RC_TRY(stream_attrs());
@@ -1296,6 +1401,28 @@ extern "C" int pbcg_get_vector(pbcg_handle *h, int32_t which, double *out) {
 }
 
 // Diagnostic spill counters (non-zero only in a -DPBCG_DEBUG_COUNTERS build).
+extern "C" int pbcg_spmv_format(pbcg_handle *h, int64_t *out8) {
+    if (!h || !out8) return fail(PBCG_EINVAL, "spmv_format: null argument");
+    if (h->comm_only) return fail(PBCG_EINVAL, "spmv_format: handle has no matrix");
+    for (int i = 0; i < 8; ++i) out8[i] = 0;
+    for (const auto &R : h->R) {
+        const int64_t slots = R.use_slots ? R.nslices * SELL_RS : 0;
+        out8[0] += R.n;
+        out8[1] += R.nnz;
+        out8[2] += R.sell_nnz;
+        out8[3] += R.n_explicit;
+        out8[4] += slots;
+        if (R.spmv_kind == SPMV_K_TMA && R.blob)  // the packed chunks read once, x once, y
+            out8[5] += R.blob_bytes + 8 * (R.nchunks + 1) + 16 * R.n + (R.h_perm.empty() ? 0 : 4 * R.n);
+        else
+            out8[5] += 8 * R.nnz + 4 * R.n_explicit + 4 * slots + 4 * R.n + 8 * R.nslices + 16 * R.n +
+                       (R.h_perm.empty() ? 0 : 4 * R.n);
+        out8[6] = std::max<int64_t>(out8[6], R.max_len);
+        out8[7] |= R.h_perm.empty() ? 0 : 1;
+    }
+    return PBCG_OK;
+}
+
 extern "C" int pbcg_debug_counters(uint64_t *out16, int32_t reset) {
     if (!out16) return fail(PBCG_EINVAL, "null");
     CUDA_TRY(cudaMemcpyFromSymbol(out16, g_dbg, sizeof(unsigned long long) * 16));

@@ -460,4 +460,198 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a
                            a.phase == PH_EXDOT ? a.x[0] : nullptr, a.y[0], a.n);
 }
 
+// ---------------------------------------------------------------------------
+// SpMV (Alg. 2 l.75 v = A z, l.80 t = A w) for matrices whose rows hold <= 8
+// nonzeros (the stencil configs), from the packed sliced-ELL format SELL-P:
+// chunk c = SPS consecutive 32-row slices stored as ONE contiguous blob
+//   header: vo[SPS+1] (int32, value offset of each slice in the blob's value
+//           area), xo[SPS+1] (int32, offset of each slice's explicit column
+//           ids), len[SPS*32] (uint8 row lengths), rec[SPS*16] (slot records:
+//           uniform pos-relative column per slot + mask, SellMat::slot_rec)
+//   values: slot-major, 32 per slot, widths of the slices
+//   explicit column ids: pos-relative, 32 per non-uniform slot
+// so the producer lane moves a chunk with one bulk copy (the TMA engine's
+// per-copy cost is what limits small-copy streaming).  All consumer warps read
+// each stage: warp j folds slice j -- x gathered through L1/L2 (x is read
+// from HBM once: banded matrix), the row's ordered fma chain (R-6) -- and
+// stores y.  Column ids of uniform slots are never stored.
+// ---------------------------------------------------------------------------
+template <int SPS>
+struct SellPGeo {
+    static constexpr int HO1 = ((SPS + 1) * 4 + 15) / 16 * 16;       // xo[]
+    static constexpr int HO2 = 2 * HO1;                              // len[] (uint8)
+    static constexpr int HO3 = HO2 + SPS * 32;                       // rec[]
+    static constexpr int H = (HO3 + SPS * SELL_RS * 4 + 127) / 128 * 128;  // values start
+    static constexpr int MAXBLOB = H + SPS * 32 * 8 * (8 + 4);       // width <= 8, all slots explicit
+};
+
+// per slice: number of explicit (non-uniform) slots among its width
+__global__ void sellp_count_kernel(int64_t nslices, const int64_t *slice_off, const int32_t *slot_rec, uint8_t *nexp) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nslices; s += (int64_t)gridDim.x * blockDim.x) {
+        const int W = (int)((slice_off[s + 1] - slice_off[s]) >> 5);
+        const uint32_t m = slot_rec ? (uint32_t)slot_rec[s * SELL_RS + SELL_MASK] : 0u;
+        nexp[s] = (uint8_t)__popc(~m & ((1u << W) - 1u));
+    }
+}
+
+// one warp per slice: scatter its header entries, values and explicit column
+// ids into its chunk's blob (blob zeroed beforehand: lengths past n stay 0)
+template <int SPS>
+__global__ void sellp_fill_kernel(int64_t n, int64_t nslices, SellMat A, const uint8_t *nexp, const int64_t *blob_off,
+                                  unsigned char *blob) {
+    using Geo = SellPGeo<SPS>;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nslices; s += nw) {
+        const int64_t c = s / SPS;
+        const int j = (int)(s % SPS);
+        unsigned char *bb = blob + blob_off[c];
+        const int64_t so = A.slice_off[s], so0 = A.slice_off[c * SPS];
+        const int W = (int)((A.slice_off[s + 1] - so) >> 5);
+        const int vo = (int)(so - so0);
+        int xo = (lane < j) ? nexp[c * SPS + lane] : 0;
+        xo = 32 * __reduce_add_sync(0xFFFFFFFFu, xo);
+        const uint32_t m = A.slot_rec ? (uint32_t)A.slot_rec[s * SELL_RS + SELL_MASK] : 0u;
+        const int64_t nvc = A.slice_off[min((c + 1) * SPS, nslices)] - so0;  // values of the chunk
+        if (lane == 0) {
+            ((int32_t *)bb)[j] = vo;
+            ((int32_t *)(bb + Geo::HO1))[j] = xo;
+            if (j == 0) ((int32_t *)bb)[SPS] = (int32_t)nvc;
+        }
+        const int64_t pos = s * 32 + lane;
+        bb[Geo::HO2 + j * 32 + lane] = (uint8_t)(pos < n ? A.row_len[pos] : 0);
+        if (lane < SELL_RS)
+            ((int32_t *)(bb + Geo::HO3))[j * SELL_RS + lane] = A.slot_rec ? A.slot_rec[s * SELL_RS + lane] : 0;
+        double *bv = (double *)(bb + Geo::H);
+        int32_t *bx = (int32_t *)(bb + Geo::H + 8 * nvc);
+        int q = 0;
+        for (int k = 0; k < W; ++k) {
+            bv[vo + 32 * k + lane] = A.val[so + 32 * k + lane];
+            if (!((m >> k) & 1u)) bx[xo + 32 * (q++) + lane] = A.col[so + 32 * k + lane];
+        }
+    }
+}
+
+// STAGE (bytes, multiple of 128) = the largest chunk blob of this matrix,
+// STAGES = as many as fit in shared memory (set at setup).
+template <int MODE, int SPS, int RPW>
+__global__ void __launch_bounds__((SPS / RPW + 1) * 32, 1)
+    spmv_sellp_kernel(int64_t n, int64_t nslices, const unsigned char *__restrict__ blob,
+                      const int64_t *__restrict__ blob_off, const int32_t *__restrict__ perm,
+                      const double *__restrict__ x, double *__restrict__ y, const double *__restrict__ b,
+                      double *__restrict__ y2, const Scalars *sc, int STAGE, int STAGES) {
+    using Geo = SellPGeo<SPS>;
+    constexpr int NCW = SPS / RPW;  // consumer warps
+    static_assert(SPS % RPW == 0, "SPS must be a multiple of RPW");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t *full = (uint64_t *)(smem_raw + (size_t)STAGES * STAGE);
+    uint64_t *empty = full + STAGES;
+    if (sc && sc->done) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int64_t nchunks = (nslices + SPS - 1) / SPS;
+    if (warp == NCW) {  // producer warp: blob extents of 32 chunks per batch, one bulk copy per chunk
+        auto extents = [&](int64_t k, int64_t &c, int64_t &o0, int64_t &o1) {
+            c = blockIdx.x + k * gridDim.x;
+            o0 = o1 = 0;
+            if (c < nchunks) {
+                o0 = __ldg(&blob_off[c]);
+                o1 = __ldg(&blob_off[c + 1]);
+            }
+        };
+        int64_t cc, c0, c1, nc, n0, n1;
+        extents(lane, cc, c0, c1);
+        int st = 0;
+        uint32_t ph = 0;
+        for (int64_t kb = 0;; kb += 32) {
+            if (__shfl_sync(0xFFFFFFFFu, cc, 0) >= nchunks) break;
+            extents(kb + 32 + lane, nc, n0, n1);  // next batch, in flight during this one
+            for (int l = 0; l < 32; ++l) {
+                const int64_t c = __shfl_sync(0xFFFFFFFFu, cc, l);
+                if (c >= nchunks) break;
+                const int64_t o0 = __shfl_sync(0xFFFFFFFFu, c0, l), o1 = __shfl_sync(0xFFFFFFFFu, c1, l);
+                if (lane == 0) {
+                    mbar_wait(&empty[st], ph ^ 1u);
+                    mbar_expect_tx(&full[st], (uint32_t)(o1 - o0));
+                    bulk_g2s(smem_raw + (size_t)st * STAGE, blob + o0, (uint32_t)(o1 - o0), &full[st]);
+                }
+                if (++st == STAGES) {
+                    st = 0;
+                    ph ^= 1u;
+                }
+                __syncwarp();
+            }
+            cc = nc;
+            c0 = n0;
+            c1 = n1;
+        }
+        return;
+    }
+    int st = 0;
+    uint32_t ph = 0;
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        mbar_wait(&full[st], ph);
+        const unsigned char *sb = smem_raw + (size_t)st * STAGE;
+        const int32_t *vo = (const int32_t *)sb;
+        const int32_t *xo = (const int32_t *)(sb + Geo::HO1);
+        const int32_t *rec = (const int32_t *)(sb + Geo::HO3);
+        const double *bv = (const double *)(sb + Geo::H);
+        const int32_t *bx = (const int32_t *)(bv + vo[SPS]);  // explicit column ids after the values
+        int len[RPW];
+        double xv[RPW][8];
+#pragma unroll
+        for (int u = 0; u < RPW; ++u) {
+            const int j = warp * RPW + u;
+            const int64_t s = c * SPS + j;
+            len[u] = s < nslices ? sb[Geo::HO2 + j * 32 + lane] : 0;
+            const int64_t pos = s * 32 + lane;
+            const uint32_t m = (uint32_t)rec[j * SELL_RS + SELL_MASK];
+            const int32_t *xs = bx + xo[j] + lane;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                // uniform slot: the record; else the next explicit column id
+                if (k < len[u]) {
+                    const bool uni = (m >> k) & 1u;
+                    const int q = __popc(~m & ((1u << k) - 1u));
+                    const int rel = uni ? rec[j * SELL_RS + k] : xs[32 * q];
+                    xv[u][k] = __ldg(x + (pos + rel));
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < RPW; ++u) {
+            const int j = warp * RPW + u;
+            const int64_t pos = (c * SPS + j) * 32 + lane;
+            const double *vs = bv + vo[j] + lane;
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k < len[u]) acc = __fma_rn(vs[32 * k], xv[u][k], acc);  // ordered chain, +0.0 start (R-6)
+            if (pos < n) {
+                const int64_t row = perm ? (int64_t)__ldg(&perm[pos]) : pos;
+                if (MODE == SPMV_PLAIN) {
+                    y[row] = acc;
+                } else {
+                    const double r = __dsub_rn(b[row], acc);  // r0 := b - A x0 (l.64)
+                    y[row] = r;
+                    if (y2) y2[row] = r;
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        if (++st == STAGES) {
+            st = 0;
+            ph ^= 1u;
+        }
+    }
+}
+
 }  // namespace pbcg

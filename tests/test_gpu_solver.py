@@ -231,3 +231,74 @@ def test_nccl_dataflow_single_rank(pb):
     A = gen.random_banded(30_000, seed=17, band=2500)
     S, O, x, r, H = run_both(pb, A, tol=1e-10, max_iter=400, force_nccl=True)
     assert_same(O, x, r, H, A)
+
+
+def banded_with_holes(n, half, seed, holes_per_slice=0.3):
+    """Band matrix |i-j| <= half with off-diagonal entries dropped at random
+    (about `holes_per_slice` per 32 rows): slices mix uniform and explicit
+    slot offsets."""
+    rng = np.random.default_rng(seed)
+    drop = holes_per_slice / (32 * (2 * half + 1))
+    rows, cols = [], []
+    for k in range(-half, half + 1):
+        i = np.arange(max(0, -k), min(n, n - k))
+        keep = (k == 0) | (rng.random(i.size) >= drop)
+        rows.append(i[keep])
+        cols.append(i[keep] + k)
+    r = np.concatenate(rows)
+    c = np.concatenate(cols)
+    o = np.lexsort((c, r))
+    r, c = r[o], c[o]
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, r + 1, 1)
+    rp = np.cumsum(rp).astype(np.int32)
+    val = gen.loguniform(r.size, seed + 1, -3, 3)
+    return gen.CSR(n, rp, c.astype(np.int32), val)
+
+
+@pytest.mark.parametrize("kind", ["stencil3d", "band7", "band21"])
+def test_spmv_slot_offsets(pb, kind, monkeypatch):
+    # index compression of the sliced ELL (pbcg_spmv_format): per slice-slot
+    # column offsets replace most column ids; identical bits with and without
+    # them, for every SpMV kernel (TMA ring, register pipeline, row per thread)
+    import torch
+    A = {"stencil3d": lambda: gen.stencil(3, 96, 100.0),
+         "band7": lambda: banded_with_holes(70_001, 3, 5),
+         "band21": lambda: banded_with_holes(70_001, 10, 6)}[kind]()
+    x = gen.loguniform(A.n, 3, -20, 20)
+    xt = torch.from_numpy(x).cuda()
+    want = u64(oracle.spmv(A, x))
+    fmt = {}
+    for kern in ("tma", "pipe", "plain"):
+        monkeypatch.setenv("PBCG_SPMV_KERNEL", kern)
+        for slots in ("1", "0"):
+            monkeypatch.setenv("PBCG_SELL_SLOTS", slots)
+            S = solver(pb, A)
+            fmt[kern, slots] = f = S.spmv_format()
+            assert f["rows"] == A.n and f["nnz"] == A.row_ptr[-1]
+            assert np.array_equal(u64(S.spmv(xt).cpu().numpy()), want), (kern, slots)
+            S.close()
+    short_rows = int(np.diff(A.row_ptr).max()) <= 8
+    for key, f in fmt.items():
+        if key == ("tma", "1") and short_rows:
+            # packed SELL-P chunks with slot records (the TMA kernel)
+            assert 0 < f["explicit_cols"] < f["nnz"] // 2, f
+            assert f["slot_records"] == 16 * ((A.n + 31) // 32)
+            assert f["bytes_per_spmv"] < fmt["tma", "0"]["bytes_per_spmv"]
+        else:  # every column id stored (plain / pipe kernels, long rows, slots off)
+            assert f["explicit_cols"] == f["nnz"] and f["slot_records"] == 0, (key, f)
+    # partitions: the records are per rank (offsets relative to each rank's buffer)
+    monkeypatch.delenv("PBCG_SELL_SLOTS")
+    monkeypatch.delenv("PBCG_SPMV_KERNEL")
+    S = solver(pb, A, virtual_ranks=3)
+    assert np.array_equal(u64(S.spmv(xt).cpu().numpy()), want)
+    S.close()
+
+
+def test_spmv_format_random_keeps_explicit(pb):
+    # random banded rows (C4-like): no slot shares an offset, the plain kernels run
+    A = gen.random_banded(40_000, seed=11, band=3000)
+    S = solver(pb, A)
+    f = S.spmv_format()
+    assert f["explicit_cols"] == f["nnz"] and f["slot_records"] == 0 and f["sigma_sorted"] == 1
+    S.close()
