@@ -674,7 +674,20 @@ static constexpr int X_NCW = 8;
 #define PBCG_X_NH 2
 #endif
 static constexpr int X_NH = PBCG_X_NH, X_NL = 2;  // standalone EXDOT: hot / cold levels
-static constexpr int K2_PPT = 1, K2_ST = 4, K3_PPT = 1, K3_ST = 4, XD_PPT = 4, XD_ST = 4;
+#ifndef PBCG_K2_PPT
+#define PBCG_K2_PPT 1
+#endif
+#ifndef PBCG_K2_ST
+#define PBCG_K2_ST 5
+#endif
+#ifndef PBCG_K3_PPT
+#define PBCG_K3_PPT 1
+#endif
+#ifndef PBCG_K3_ST
+#define PBCG_K3_ST 5
+#endif
+static constexpr int K2_PPT = PBCG_K2_PPT, K2_ST = PBCG_K2_ST, K3_PPT = PBCG_K3_PPT, K3_ST = PBCG_K3_ST, XD_PPT = 4,
+                     XD_ST = 4;
 #define K2S k2_stream<K2_NH, K2_NC, S_NCW, K2_PPT, K2_ST, K2_NHE>
 #define K3S k3_stream<K3_NH, K3_NC, S_NCW, K3_PPT, K3_ST, K3_NHE>
 #define XDS exdot_stream<X_NH, X_NL, X_NCW, XD_PPT, XD_ST>
