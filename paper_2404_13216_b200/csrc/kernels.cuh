@@ -733,11 +733,25 @@ __global__ void __launch_bounds__(BS) plain_dot_kernel(int64_t n, const double *
     double s = 0.0;
     const int64_t npair = n >> 1;
     const int64_t stride = (int64_t)gridDim.x * BS;
-    for (int64_t k = (int64_t)blockIdx.x * BS + threadIdx.x; k < npair; k += stride) {
+    int64_t k = (int64_t)blockIdx.x * BS + threadIdx.x;
+    // 4 independent pairs in flight per thread, then the remainder
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+    for (; k + 3 * stride < npair; k += 4 * stride) {
+        double2 a[4], b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a[u] = __ldcs((const double2 *)x + k + u * stride);
+            b[u] = __ldcs((const double2 *)y + k + u * stride);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s4[u] = __fma_rn(a[u].y, b[u].y, __fma_rn(a[u].x, b[u].x, s4[u]));
+    }
+    for (; k < npair; k += stride) {
         const double2 a = ((const double2 *)x)[k], b = ((const double2 *)y)[k];
         s = __fma_rn(a.x, b.x, s);
         s = __fma_rn(a.y, b.y, s);
     }
+    s = __dadd_rn(__dadd_rn(s, s4[0]), __dadd_rn(__dadd_rn(s4[1], s4[2]), s4[3]));
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) s = __fma_rn(x[n - 1], y[n - 1], s);
     for (int o = 16; o; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xFFFFFFFFu, s, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;

@@ -669,7 +669,10 @@ static int multidot(pbcg_handle *h, int ph, int phase, int nd, const double *con
 static constexpr int K2_NH = 3, K2_NHE = 2, K2_NC = 3;
 static constexpr int K3_NH = 3, K3_NHE = 2, K3_NC = 2;
 static constexpr int S_NCW = 7;  // warps per dot group (2*7+1 = 15 warps per CTA)
-static constexpr int X_NCW = 8;
+#ifndef PBCG_X_NCW
+#define PBCG_X_NCW 12
+#endif
+static constexpr int X_NCW = PBCG_X_NCW;
 #ifndef PBCG_X_NH
 #define PBCG_X_NH 2
 #endif
@@ -686,8 +689,14 @@ static constexpr int X_NH = PBCG_X_NH, X_NL = 2;  // standalone EXDOT: hot / col
 #ifndef PBCG_K3_ST
 #define PBCG_K3_ST 5
 #endif
-static constexpr int K2_PPT = PBCG_K2_PPT, K2_ST = PBCG_K2_ST, K3_PPT = PBCG_K3_PPT, K3_ST = PBCG_K3_ST, XD_PPT = 4,
-                     XD_ST = 4;
+#ifndef PBCG_XD_PPT
+#define PBCG_XD_PPT 6
+#endif
+#ifndef PBCG_XD_ST
+#define PBCG_XD_ST 2
+#endif
+static constexpr int K2_PPT = PBCG_K2_PPT, K2_ST = PBCG_K2_ST, K3_PPT = PBCG_K3_PPT, K3_ST = PBCG_K3_ST,
+                     XD_PPT = PBCG_XD_PPT, XD_ST = PBCG_XD_ST;
 #define K2S k2_stream<K2_NH, K2_NC, S_NCW, K2_PPT, K2_ST, K2_NHE>
 #define K3S k3_stream<K3_NH, K3_NC, S_NCW, K3_PPT, K3_ST, K3_NHE>
 #define XDS exdot_stream<X_NH, X_NL, X_NCW, XD_PPT, XD_ST>
