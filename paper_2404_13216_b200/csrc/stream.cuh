@@ -532,6 +532,49 @@ __global__ void sellp_fill_kernel(int64_t n, int64_t nslices, SellMat A, const u
     }
 }
 
+// Producer warp of the SELL-P kernels: the blob extents of 32 chunks per
+// batch are loaded one per lane (the next batch in flight during this one),
+// lane 0 moves each chunk of this CTA with ONE bulk copy into the ring.
+__device__ __forceinline__ void sellp_produce(int64_t nchunks, const unsigned char *blob, const int64_t *blob_off,
+                                              unsigned char *smem, int STAGE, int STAGES, uint64_t *full,
+                                              uint64_t *empty) {
+    const int lane = threadIdx.x & 31;
+    auto extents = [&](int64_t k, int64_t &c, int64_t &o0, int64_t &o1) {
+        c = blockIdx.x + k * gridDim.x;
+        o0 = o1 = 0;
+        if (c < nchunks) {
+            o0 = __ldg(&blob_off[c]);
+            o1 = __ldg(&blob_off[c + 1]);
+        }
+    };
+    int64_t cc, c0, c1, nc, n0, n1;
+    extents(lane, cc, c0, c1);
+    int st = 0;
+    uint32_t ph = 0;
+    for (int64_t kb = 0;; kb += 32) {
+        if (__shfl_sync(0xFFFFFFFFu, cc, 0) >= nchunks) break;
+        extents(kb + 32 + lane, nc, n0, n1);
+        for (int l = 0; l < 32; ++l) {
+            const int64_t c = __shfl_sync(0xFFFFFFFFu, cc, l);
+            if (c >= nchunks) break;
+            const int64_t o0 = __shfl_sync(0xFFFFFFFFu, c0, l), o1 = __shfl_sync(0xFFFFFFFFu, c1, l);
+            if (lane == 0) {
+                mbar_wait(&empty[st], ph ^ 1u);
+                mbar_expect_tx(&full[st], (uint32_t)(o1 - o0));
+                bulk_g2s(smem + (size_t)st * STAGE, blob + o0, (uint32_t)(o1 - o0), &full[st]);
+            }
+            if (++st == STAGES) {
+                st = 0;
+                ph ^= 1u;
+            }
+            __syncwarp();
+        }
+        cc = nc;
+        c0 = n0;
+        c1 = n1;
+    }
+}
+
 // STAGE (bytes, multiple of 128) = the largest chunk blob of this matrix,
 // STAGES = as many as fit in shared memory (set at setup).
 template <int MODE, int SPS, int RPW>
@@ -557,41 +600,8 @@ __global__ void __launch_bounds__((SPS / RPW + 1) * 32, 1)
     }
     __syncthreads();
     const int64_t nchunks = (nslices + SPS - 1) / SPS;
-    if (warp == NCW) {  // producer warp: blob extents of 32 chunks per batch, one bulk copy per chunk
-        auto extents = [&](int64_t k, int64_t &c, int64_t &o0, int64_t &o1) {
-            c = blockIdx.x + k * gridDim.x;
-            o0 = o1 = 0;
-            if (c < nchunks) {
-                o0 = __ldg(&blob_off[c]);
-                o1 = __ldg(&blob_off[c + 1]);
-            }
-        };
-        int64_t cc, c0, c1, nc, n0, n1;
-        extents(lane, cc, c0, c1);
-        int st = 0;
-        uint32_t ph = 0;
-        for (int64_t kb = 0;; kb += 32) {
-            if (__shfl_sync(0xFFFFFFFFu, cc, 0) >= nchunks) break;
-            extents(kb + 32 + lane, nc, n0, n1);  // next batch, in flight during this one
-            for (int l = 0; l < 32; ++l) {
-                const int64_t c = __shfl_sync(0xFFFFFFFFu, cc, l);
-                if (c >= nchunks) break;
-                const int64_t o0 = __shfl_sync(0xFFFFFFFFu, c0, l), o1 = __shfl_sync(0xFFFFFFFFu, c1, l);
-                if (lane == 0) {
-                    mbar_wait(&empty[st], ph ^ 1u);
-                    mbar_expect_tx(&full[st], (uint32_t)(o1 - o0));
-                    bulk_g2s(smem_raw + (size_t)st * STAGE, blob + o0, (uint32_t)(o1 - o0), &full[st]);
-                }
-                if (++st == STAGES) {
-                    st = 0;
-                    ph ^= 1u;
-                }
-                __syncwarp();
-            }
-            cc = nc;
-            c0 = n0;
-            c1 = n1;
-        }
+    if (warp == NCW) {  // producer warp
+        sellp_produce(nchunks, blob, blob_off, smem_raw, STAGE, STAGES, full, empty);
         return;
     }
     int st = 0;
