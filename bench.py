@@ -177,6 +177,27 @@ def run_gpu(args, rank, world, local_rank, dist):
         ok = bool(okt.item())
     clk = clocks.summary(tc0 - 0.05, tc1 + 0.05)
     out = {"ms": ms, "ok": ok, "iters": res.iterations, "clocks": clk}
+    # ---- the same K steps with plain fp64 dots (the
+    # paper's non-reproducible arm; its cost ratio is the ExBLAS overhead) ----
+    if not args.no_extras:
+        S.start(b, tol=0.0, max_iter=W + K + 8, dot_mode="plain")
+        S.iterate(W)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(S.stream)
+        S.iterate(K)
+        p1.record(S.stream)
+        torch.cuda.synchronize()
+        pms = p0.elapsed_time(p1)
+        pres = S.finish(None)
+        if dist:
+            t = torch.tensor([pms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            pms = float(t.item())
+        out["plain"] = {"value": K / (pms * 1e-3), "unit": "iter/s", "ms_per_step": pms / K,
+                        "valid": pres.iterations == W + K}
     # ---- per-kernel times: a second timed pass over the same K steps with
     # CUDA events around every launch (single rank) ----
     fmt = S.spmv_format()
@@ -392,6 +413,12 @@ def main():
             # K2, finalize A, SpMV, K3, finalize B, SpMV per iteration (per rank; NCCL kernels not counted)
             "gpu_launches": 6 * K}
     line["spmv_format"] = out["spmv_format"]
+    if "plain" in out:
+        pl = out["plain"]
+        pl["exact_over_plain"] = value / pl["value"]
+        pl["note"] = ("same workload and K with dot_mode=plain (fp64 dots, per-thread fma chains + fixed trees; "
+                      "not reproducible across partitions); exact_over_plain = the ExBLAS cost on this GPU")
+        line["plain_dots"] = pl
     line["bytes_per_iteration_per_gpu"] = by["iteration"]
     line["iteration_GBps_per_gpu"] = by["iteration"] / (ms_step * 1e-3) / 1e9
     line["iteration_frac_hbm"] = line["iteration_GBps_per_gpu"] / hbm

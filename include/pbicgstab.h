@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define PBCG_ABI_VERSION 1
+#define PBCG_ABI_VERSION 2
 
 /* return codes of every entry point (never an abort across the ABI) */
 enum pbcg_rc {
@@ -99,7 +99,15 @@ typedef struct {
     double breakdown_eps;     /* relative breakdown threshold, default 1e-30; <= 0 -> 1e-30 */
     int32_t poll_every;       /* iterations per CUDA-graph chunk / host poll; <= 0 -> 16 */
     int32_t use_graphs;       /* 1: replay captured CUDA graphs of poll_every iterations; 0: direct launches */
+    int32_t dot_mode;         /* PBCG_DOT_EXACT (0, default): ExBLAS exactly rounded dots, reproducible;
+                                 PBCG_DOT_PLAIN (1): plain fp64 per-iteration dots (per-thread fma chains,
+                                 fixed warp tree, CTA and grid sums in order; across NCCL ranks an fp64
+                                 allreduce) -- the paper's non-reproducible comparison arm (SURVEY §8(f)
+                                 NEXT-1); bits depend on the launch geometry and the partition.
+                                 Init / true-residual dots stay exact in both modes. */
 } pbcg_opts;
+
+enum pbcg_dot_mode { PBCG_DOT_EXACT = 0, PBCG_DOT_PLAIN = 1 };
 
 /* Solve result.  history row layout (12 doubles per row, row 0 = init, row
  * i+1 = iteration i), identical to the oracle's:

@@ -47,9 +47,13 @@ class _Dist(ctypes.Structure):
                 ("virtual_ranks", ctypes.c_int32), ("history_capacity", ctypes.c_int32), ("comm_mode", ctypes.c_int32)]
 
 
+# pbcg_opts.dot_mode: "exact" = ExBLAS dots (reproducible), "plain" = fp64 dots (NEXT-1 comparison arm)
+DOT_MODES = {"exact": 0, "plain": 1}
+
+
 class _Opts(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("max_iter", ctypes.c_int32), ("breakdown_eps", ctypes.c_double),
-                ("poll_every", ctypes.c_int32), ("use_graphs", ctypes.c_int32)]
+                ("poll_every", ctypes.c_int32), ("use_graphs", ctypes.c_int32), ("dot_mode", ctypes.c_int32)]
 
 
 class _Result(ctypes.Structure):
@@ -177,8 +181,8 @@ class Solver:
         del rp, ci, va
 
     # -- helpers ------------------------------------------------------------
-    def _opts(self, tol, max_iter, eps, poll_every, use_graphs):
-        return _Opts(float(tol), int(max_iter), float(eps), int(poll_every), int(use_graphs))
+    def _opts(self, tol, max_iter, eps, poll_every, use_graphs, dot_mode="exact"):
+        return _Opts(float(tol), int(max_iter), float(eps), int(poll_every), int(use_graphs), DOT_MODES[dot_mode])
 
     def _vec(self, v, allow_host: bool):
         torch = self.torch
@@ -202,7 +206,8 @@ class Solver:
         self.torch.cuda.current_stream().wait_stream(self.stream)
 
     # -- API ------------------------------------------------------------------
-    def solve(self, b, x0=None, tol=1e-10, max_iter=10000, eps=1e-30, poll_every=16, use_graphs=True):
+    def solve(self, b, x0=None, tol=1e-10, max_iter=10000, eps=1e-30, poll_every=16, use_graphs=True,
+              dot_mode="exact"):
         """Solve; b/x0 may be CUDA tensors or host arrays/tensors (host buffers
         go through the library's staging path).  Returns (x, Result) with x on
         the same side as b."""
@@ -217,7 +222,7 @@ class Solver:
             x = x.copy() if isinstance(x, np.ndarray) else x.clone()
         xp = x.ctypes.data if isinstance(x, np.ndarray) else x.data_ptr()
         res = _Result()
-        opts = self._opts(tol, max_iter, eps, poll_every, use_graphs)
+        opts = self._opts(tol, max_iter, eps, poll_every, use_graphs, dot_mode)
         _check(lib().pbicgstab_solve(self._h, ctypes.c_void_p(bp), ctypes.c_void_p(xp), ctypes.byref(opts), ctypes.byref(res)))
         self._sync_out()
         return x, self._result(res)
@@ -226,14 +231,15 @@ class Solver:
     def n_local_vec(self) -> int:
         return self.n_global if self._dist.virtual_ranks > 1 else self.n_local
 
-    def start(self, b, x0=None, tol=1e-10, max_iter=10000, eps=1e-30, poll_every=16, use_graphs=True):
+    def start(self, b, x0=None, tol=1e-10, max_iter=10000, eps=1e-30, poll_every=16, use_graphs=True,
+              dot_mode="exact"):
         torch = self.torch
         self._sync_in()
         self._b, bp = self._vec(b, allow_host=True)
         if x0 is None:
             x0 = torch.zeros(self.n_local_vec, dtype=torch.float64, device="cuda")
         self._x0, xp = self._vec(x0, allow_host=True)
-        opts = self._opts(tol, max_iter, eps, poll_every, use_graphs)
+        opts = self._opts(tol, max_iter, eps, poll_every, use_graphs, dot_mode)
         _check(lib().pbicgstab_start(self._h, ctypes.c_void_p(bp), ctypes.c_void_p(xp), ctypes.byref(opts)))
 
     def iterate(self, k: int):

@@ -563,6 +563,41 @@ __device__ __forceinline__ void cascade_one(A &d, const Prod &q, unsigned long l
     }
 }
 
+// ---------------------------------------------------------------------------
+// Plain fp64 accumulation (dot_mode = PBCG_DOT_PLAIN: the
+// paper's non-reproducible comparison arm).  Same interface as ExAccT: each
+// thread keeps one fma chain per dot, warps reduce by a fixed shuffle tree,
+// the CTA sums its warps in order (plain_publish) and the CTA partials are
+// summed in grid order by plain_finalize_kernel -- deterministic for one
+// launch geometry, but the grouping (hence the bits) follows the partition.
+// ---------------------------------------------------------------------------
+struct PlainAcc {
+    double s;
+    int slot;  // this warp's slot in the CTA's per-dot warp sums (-1: unused accumulator)
+    __device__ __forceinline__ void zero() { s = 0.0; }
+    __device__ __forceinline__ Prod prep(double x, double y, bool, unsigned &) const { return Prod{x, y}; }
+    __device__ __forceinline__ void add(const Prod &q) { s = __fma_rn(q.p, q.e, s); }
+    // all 32 lanes, converged: lane 0 stores the warp's sum as a double
+    __device__ __forceinline__ void warp_merge(unsigned long long *slots) {
+        double v = s;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+        if ((threadIdx.x & 31) == 0 && slot >= 0) ((double *)slots)[slot] = v;
+    }
+};
+
+template <int K, bool ALT>
+__device__ __forceinline__ void cascade_batch(PlainAcc &d0, PlainAcc &d1, const Prod (&P)[K], unsigned long long *,
+                                              unsigned long long *) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        if (ALT && (k & 1)) d1.add(P[k]);
+        else d0.add(P[k]);
+    }
+}
+
+__device__ __forceinline__ void cascade_one(PlainAcc &d, const Prod &q, unsigned long long *) { d.add(q); }
+
 // Shared-memory state of a CTA computing ND dots.
 template <int ND>
 struct CtaSacc {
@@ -602,6 +637,19 @@ __device__ bool cta_sacc_publish(CtaSacc<ND> &S, unsigned flags, long long *gacc
     __syncthreads();
     if (S.last) __threadfence();
     return S.last != 0;
+}
+
+// Plain mode: sum the W warp sums of each dot in order, store the CTA's
+// partials part[blockIdx.x * ND + k].
+template <int ND, int W>
+__device__ void plain_publish(CtaSacc<ND> &S, double *part) {
+    __syncthreads();
+    if (threadIdx.x < ND) {
+        const double *ws = (const double *)S.w[threadIdx.x];
+        double t = 0.0;
+        for (int i = 0; i < W; ++i) t = __dadd_rn(t, ws[i]);
+        part[(size_t)blockIdx.x * ND + threadIdx.x] = t;
+    }
 }
 
 // In the last CTA: pull gacc into shared memory and normalise it.

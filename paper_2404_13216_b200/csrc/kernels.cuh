@@ -170,6 +170,7 @@ struct K2Args {
     unsigned *ticket;
     double *hist;
     int finalize;
+    double *part;  // plain dot mode: CTA partials [grid][ND] (exact mode: unused)
 };
 
 template <int NP, int NE>
@@ -269,6 +270,7 @@ struct K3Args {
     unsigned *ticket;
     double *hist;
     int finalize;
+    double *part;  // plain dot mode: CTA partials [grid][ND] (exact mode: unused)
 };
 
 template <int NP, int NE>
@@ -626,6 +628,29 @@ __global__ void __launch_bounds__(256) spmv_sell_pipe_kernel(SellMat A, const do
             }
         }
     }
+}
+
+// Plain dot mode: d[k] = sum over ranks v (in order) and CTAs c (in order) of
+// part[v][c*ND + k], then the phase's scalar step (the same phase_finalize as
+// the exact mode).  pd (if not null) receives d[] (NCCL ranks: the local sums,
+// allreduced before plain_phase_kernel).
+template <int ND>
+__global__ void plain_finalize_kernel(const double *const *parts, int V, int grid, int phase, Scalars *sc,
+                                      double *hist, double *pd, int run_phase) {
+    __shared__ double d[ND];
+    if (threadIdx.x < ND) {
+        double t = 0.0;
+        for (int v = 0; v < V; ++v)
+            for (int c = 0; c < grid; ++c) t = __dadd_rn(t, parts[v][(size_t)c * ND + threadIdx.x]);
+        d[threadIdx.x] = t;
+        if (pd) pd[threadIdx.x] = t;
+    }
+    __syncthreads();
+    if (run_phase && threadIdx.x == 0) phase_finalize(phase, sc, d, 0u, hist, nullptr, nullptr);
+}
+
+__global__ void plain_phase_kernel(int phase, Scalars *sc, const double *pd, double *hist) {
+    if (threadIdx.x == 0) phase_finalize(phase, sc, pd, 0u, hist, nullptr, nullptr);
 }
 
 // ------------------------------------------------------------------------

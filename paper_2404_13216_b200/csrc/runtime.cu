@@ -212,6 +212,7 @@ extern "C" int pbcg_sacc_words(void) { return SACC_L; }
 static constexpr int GW4 = 4 * SACC_L + SACC_FLAGW;  // words of a 4-dot reduction buffer
 static constexpr int NPH = 5;                        // reduction buffers: init, A, B, true, exdot
 static constexpr int K_BS = 256;
+static constexpr int PLAIN_GRID = 1024;  // >= any K2/K3 stream grid (one CTA per SM)
 static constexpr int K_NP = 4, K_NE = 4;             // FPE depth for products / errors (performance only, R-16)
 static constexpr int U_K2 = 2, U_K3 = 2, U_MD4 = 2, U_MD1 = 4;  // row pairs in flight per thread
 
@@ -258,6 +259,8 @@ struct Rank {
     bool use_slots = true;
     int64_t nnz = 0, n_explicit = 0;  // stored nonzeros, column ids that stay explicit
     int spmv_kind = 0;                // SpMV kernel (set at setup)
+    double *part[NPH] = {};           // plain dot mode: CTA partials [PLAIN_GRID][4] per phase
+    double *pdsum = nullptr;          // plain dot mode, NCCL ranks: local sums [NPH][4] (allreduced)
     // packed SELL-P chunks (rows <= 8 nonzeros): blob + byte offsets per chunk
     int64_t nchunks = 0, blob_cap = 0, blob_bytes = 0;
     unsigned char *blob = nullptr;
@@ -280,6 +283,9 @@ struct pbcg_handle {
     std::vector<Rank> R;
     ncclComm_t comm_halo = nullptr, comm_red = nullptr;
     long long **vgacc = nullptr;  // device array [NPH][V] of gacc pointers (virtual ranks)
+    double **vpart = nullptr;     // device array [NPH][V] of plain-mode partial arrays
+    int dot_mode = PBCG_DOT_EXACT;  // of the running solve (pbcg_opts.dot_mode)
+    int g_mode = -1;                // dot mode the captured graph was built with
     int hist_cap = 10001;
     Scalars *h_sc = nullptr;      // pinned mirror of rank 0's scalars
     int grid_k2 = 0, grid_k3 = 0, grid_md = 0;
@@ -334,6 +340,8 @@ static void carve_rank(Carver &C, Rank &R, int hist_cap, bool comm_only) {
         R.hist = C.take<double>((size_t)hist_cap * H_COLS);
     }
     for (int k = 0; k < NPH; ++k) R.gacc[k] = C.take<long long>(GW4);
+    for (int k = 0; k < NPH; ++k) R.part[k] = C.take<double>((size_t)PLAIN_GRID * 4);
+    R.pdsum = C.take<double>((size_t)NPH * 4);
     R.tickets = C.take<unsigned>(16);
     R.sc = C.take<Scalars>(1);
     R.bad = C.take<int>(4);
@@ -341,6 +349,7 @@ static void carve_rank(Carver &C, Rank &R, int hist_cap, bool comm_only) {
 
 static size_t carve_handle_extra(Carver &C, pbcg_handle *h) {
     h->vgacc = C.take<long long *>((size_t)NPH * h->V);
+    h->vpart = C.take<double *>((size_t)NPH * h->V);
     h->xd_out = C.take<double>(4);
     h->xd_flags = C.take<int32_t>(4);
     return C.off;
@@ -559,6 +568,24 @@ static int halo(pbcg_handle *h, int which) {
 // sum the phase-`ph` superaccumulators over ranks, then round + finalise
 template <int ND>
 static int reduce_finalize(pbcg_handle *h, int ph, int phase, cudaStream_t st, double *out, int32_t *oflags) {
+    if (h->dot_mode == PBCG_DOT_PLAIN && (phase == PH_A || phase == PH_B)) {
+        // plain dots: every rank sums all partials in the same order (virtual
+        // ranks), or its own and then an fp64 allreduce (NCCL: order chosen by NCCL)
+        for (auto &R : h->R) {
+            if (h->comm) {
+                plain_finalize_kernel<ND><<<1, 32, 0, st>>>(h->vpart + (size_t)ph * h->V, 1, h->nsm, phase, R.sc,
+                                                           R.hist, R.pdsum + 4 * ph, 0);
+                CUDA_TRY(cudaGetLastError());
+                NCCL_TRY(g_nccl.AllReduce(R.pdsum + 4 * ph, R.pdsum + 4 * ph, ND, ncclFloat64, ncclSum, h->comm_red, st));
+                plain_phase_kernel<<<1, 32, 0, st>>>(phase, R.sc, R.pdsum + 4 * ph, R.hist);
+            } else {
+                plain_finalize_kernel<ND><<<1, 32, 0, st>>>(h->vpart + (size_t)ph * h->V, h->V, h->nsm, phase, R.sc,
+                                                           R.hist, nullptr, 1);
+            }
+            CUDA_TRY(cudaGetLastError());
+        }
+        return PBCG_OK;
+    }
     const int words = ND * SACC_L + SACC_FLAGW;
     if (h->V > 1) {
         vallreduce_kernel<<<(words + 127) / 128, 128, 0, st>>>(h->vgacc + (size_t)ph * h->V, h->V, words);
@@ -699,6 +726,8 @@ static constexpr int K2_PPT = PBCG_K2_PPT, K2_ST = PBCG_K2_ST, K3_PPT = PBCG_K3_
                      XD_PPT = PBCG_XD_PPT, XD_ST = PBCG_XD_ST;
 #define K2S k2_stream<K2_NH, K2_NC, S_NCW, K2_PPT, K2_ST, K2_NHE>
 #define K3S k3_stream<K3_NH, K3_NC, S_NCW, K3_PPT, K3_ST, K3_NHE>
+#define K2SP k2_stream<K2_NH, K2_NC, S_NCW, K2_PPT, K2_ST, K2_NHE, false>
+#define K3SP k3_stream<K3_NH, K3_NC, S_NCW, K3_PPT, K3_ST, K3_NHE, false>
 #define XDS exdot_stream<X_NH, X_NL, X_NCW, XD_PPT, XD_ST>
 static constexpr size_t ring_bytes(int nv, int ncw, int ppt, int stages) {
     return sizeof(double) * (size_t)stages * nv * (2 * ncw * 32 * ppt) + 2 * sizeof(uint64_t) * stages;
@@ -723,6 +752,8 @@ static int stream_attrs() {
     if (done) return PBCG_OK;
     CUDA_TRY(cudaFuncSetAttribute((const void *)K2S, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)K3S, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM));
+    CUDA_TRY(cudaFuncSetAttribute((const void *)K2SP, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM));
+    CUDA_TRY(cudaFuncSetAttribute((const void *)K3SP, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)XDS, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XD_SMEM));
     done = 1;
     return PBCG_OK;
@@ -735,8 +766,10 @@ static int stream_grid(pbcg_handle *h, int64_t n, int rows_per_tile) {
 
 static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     // fin = 1: the last CTA rounds and runs the scalar step; fin = 0: publish only (finalize_kernel follows)
-    K2Args a{R.n, R.r, R.rh, R.w(), R.t, R.v, R.p, R.s, R.z(), R.q, R.y, R.sc, R.gacc[1], fin ? R.tickets + 1 : nullptr, R.hist, fin};
-    if (use_ldg_kernels()) {
+    K2Args a{R.n, R.r, R.rh, R.w(), R.t, R.v, R.p, R.s, R.z(), R.q, R.y, R.sc, R.gacc[1], fin ? R.tickets + 1 : nullptr, R.hist, fin, R.part[1]};
+    if (h->dot_mode == PBCG_DOT_PLAIN) {
+        K2SP<<<stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T), KSTREAM_THREADS, K2_SMEM, st>>>(a);
+    } else if (use_ldg_kernels()) {
         const int grid = std::max(1, std::min<int>(h->grid_k2, (int)((R.n / 2 + K_BS - 1) / K_BS)));
         k2_kernel<K_NP, K_NE, K_BS, U_K2><<<grid, K_BS, 0, st>>>(a);
     } else {
@@ -747,8 +780,10 @@ static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
 }
 
 static int launch_k3(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
-    K3Args a{R.n, R.rh, R.p, R.q, R.y, R.t, R.v, R.x, R.r, R.w(), R.sc, R.gacc[2], fin ? R.tickets + 2 : nullptr, R.hist, fin};
-    if (use_ldg_kernels()) {
+    K3Args a{R.n, R.rh, R.p, R.q, R.y, R.t, R.v, R.x, R.r, R.w(), R.sc, R.gacc[2], fin ? R.tickets + 2 : nullptr, R.hist, fin, R.part[2]};
+    if (h->dot_mode == PBCG_DOT_PLAIN) {
+        K3SP<<<stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T), KSTREAM_THREADS, K3_SMEM, st>>>(a);
+    } else if (use_ldg_kernels()) {
         const int grid = std::max(1, std::min<int>(h->grid_k3, (int)((R.n / 2 + K_BS - 1) / K_BS)));
         k3_kernel<K_NP, K_NE, K_BS, U_K3><<<grid, K_BS, 0, st>>>(a);
     } else {
@@ -769,7 +804,8 @@ static int enqueue_iteration(pbcg_handle *h) {
         RC_TRY(launch_k2(h, R, 0, st));
         CUDA_TRY(cudaEventRecord(h->ev[4], st));
         CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev[4], 0));
-        finalize_kernel<4><<<1, 128, 0, h->side>>>(R.gacc[1], PH_A, R.sc, R.hist, nullptr, nullptr);
+        if (h->dot_mode == PBCG_DOT_PLAIN) RC_TRY(reduce_finalize<4>(h, 1, PH_A, h->side, nullptr, nullptr));
+        else finalize_kernel<4><<<1, 128, 0, h->side>>>(R.gacc[1], PH_A, R.sc, R.hist, nullptr, nullptr);
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaEventRecord(h->ev[5], h->side));
         RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.zpad, R.v, nullptr, nullptr, true, st));
@@ -777,7 +813,8 @@ static int enqueue_iteration(pbcg_handle *h) {
         RC_TRY(launch_k3(h, R, 0, st));
         CUDA_TRY(cudaEventRecord(h->ev[6], st));
         CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev[6], 0));
-        finalize_kernel<3><<<1, 128, 0, h->side>>>(R.gacc[2], PH_B, R.sc, R.hist, nullptr, nullptr);
+        if (h->dot_mode == PBCG_DOT_PLAIN) RC_TRY(reduce_finalize<3>(h, 2, PH_B, h->side, nullptr, nullptr));
+        else finalize_kernel<3><<<1, 128, 0, h->side>>>(R.gacc[2], PH_B, R.sc, R.hist, nullptr, nullptr);
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaEventRecord(h->ev[7], h->side));
         RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, true, st));
@@ -919,6 +956,7 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
     // zero reduction state
     for (auto &R : h->R) {
         for (int k = 0; k < NPH; ++k) CUDA_TRY(cudaMemsetAsync(R.gacc[k], 0, sizeof(long long) * GW4, h->stream));
+        for (int k = 0; k < NPH; ++k) CUDA_TRY(cudaMemsetAsync(R.part[k], 0, sizeof(double) * PLAIN_GRID * 4, h->stream));
         CUDA_TRY(cudaMemsetAsync(R.tickets, 0, sizeof(unsigned) * 16, h->stream));
         CUDA_TRY(cudaMemsetAsync(R.sc, 0, sizeof(Scalars), h->stream));
         CUDA_TRY(cudaMemsetAsync(R.bad, 0, sizeof(int) * 4, h->stream));
@@ -928,6 +966,10 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
         for (int ph = 0; ph < NPH; ++ph)
             for (int v = 0; v < h->V; ++v) vg[(size_t)ph * h->V + v] = h->R[v].gacc[ph];
         CUDA_TRY(cudaMemcpyAsync(h->vgacc, vg.data(), sizeof(long long *) * vg.size(), cudaMemcpyHostToDevice, h->stream));
+        std::vector<double *> vp((size_t)NPH * h->V);
+        for (int ph = 0; ph < NPH; ++ph)
+            for (int v = 0; v < h->V; ++v) vp[(size_t)ph * h->V + v] = h->R[v].part[ph];
+        CUDA_TRY(cudaMemcpyAsync(h->vpart, vp.data(), sizeof(double *) * vp.size(), cudaMemcpyHostToDevice, h->stream));
         CUDA_TRY(cudaStreamSynchronize(h->stream));
     }
     if (!h->comm_only) {
@@ -1044,6 +1086,7 @@ static void opts_defaults(const pbcg_opts *o, pbcg_opts &e) {
     e.breakdown_eps = 1e-30;
     e.poll_every = 16;
     e.use_graphs = 1;
+    e.dot_mode = PBCG_DOT_EXACT;
     if (o) {
         e = *o;
         if (!(e.breakdown_eps > 0.0)) e.breakdown_eps = 1e-30;
@@ -1063,7 +1106,9 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
     pbcg_opts op;
     opts_defaults(o, op);
     if (!(op.tol >= 0.0) || op.max_iter < 0) return fail(PBCG_EINVAL, "start: bad tol / max_iter");
+    if (op.dot_mode != PBCG_DOT_EXACT && op.dot_mode != PBCG_DOT_PLAIN) return fail(PBCG_EINVAL, "start: bad dot_mode");
     h->max_iter = op.max_iter;
+    h->dot_mode = op.dot_mode;
     Scalars s0{};
     s0.tol = op.tol;
     s0.eps = op.breakdown_eps;
@@ -1122,7 +1167,7 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
 }
 
 static int capture_chunk(pbcg_handle *h, int iters) {
-    if (h->gexec && h->g_iters == iters) return PBCG_OK;
+    if (h->gexec && h->g_iters == iters && h->g_mode == h->dot_mode) return PBCG_OK;
     if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
     cudaGraph_t g;
     CUDA_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
@@ -1134,6 +1179,7 @@ static int capture_chunk(pbcg_handle *h, int iters) {
     CUDA_TRY(cudaGraphInstantiate(&h->gexec, g, 0));
     cudaGraphDestroy(g);
     h->g_iters = iters;
+    h->g_mode = h->dot_mode;
     return PBCG_OK;
 }
 

@@ -12,6 +12,7 @@
 // of their sum, without spending registers on loads in flight.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -91,9 +92,9 @@ __device__ __forceinline__ size_t stream_smem_bytes() {
 // Splitting the dots halves the accumulator registers per thread, which buys
 // twice the warps (the ExBLAS cascades are latency-bound chains of DADDs).
 // ---------------------------------------------------------------------------
-template <int NH, int NL, int NHE>
+template <class Acc>
 struct K2Op {
-    ExAccT<NH, NL, NHE> d0, d1;
+    Acc d0, d1;
     double be, nom, nal;
     bool first;
     __device__ __forceinline__ void sz(double w, double t, double v, double &s, double &z) const {
@@ -125,8 +126,10 @@ struct K2Op {
     }
 };
 
-template <int NH, int NL, int W, int PPT, int STAGES, int NHE>
+// EXACT = false: plain fp64 dots (PlainAcc, dot_mode PBCG_DOT_PLAIN)
+template <int NH, int NL, int W, int PPT, int STAGES, int NHE, bool EXACT = true>
 __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
+    using Acc = typename std::conditional<EXACT, ExAccT<NH, NL, NHE>, PlainAcc>::type;
     constexpr int NV = 8;  // r, rh, w, t | p, s, z, v
     constexpr int NCW = 2 * W;
     constexpr int T = TileGeo<W, PPT>::T;
@@ -148,7 +151,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
     const bool first = (sc->it == 0);
     const int64_t n = a.n;
     unsigned flags = 0;
-    K2Op<NH, NL, NHE> R;
+    K2Op<Acc> R;
     R.first = first;
     R.be = sc->beta;
     R.nom = -sc->omega;
@@ -156,6 +159,10 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
     R.d0.zero();
     R.d1.zero();
     const int g = warp / W, wg = warp % W;
+    if constexpr (!EXACT) {  // per-warp slot of the plain sums (producer warp: none)
+        R.d0.slot = warp < NCW ? wg : -1;
+        R.d1.slot = warp < NCW ? wg : -1;
+    }
     unsigned long long *s0 = S.w[2 * g], *s1 = S.w[2 * g + 1];
     if (warp == NCW) {
         if (lane == 0) {
@@ -235,10 +242,14 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
     R.d0.warp_merge(s0);
     R.d1.warp_merge(s1);
     PBCG_TS(2);
-    if (cta_sacc_publish<4>(S, flags, a.gacc, a.ticket)) {
-        PBCG_TS(3);
-        last_cta_finish<4>(S, a.gacc, a.ticket, PH_A, a.finalize, sc, a.hist, nullptr, nullptr);
-        PBCG_TS(4);
+    if constexpr (EXACT) {
+        if (cta_sacc_publish<4>(S, flags, a.gacc, a.ticket)) {
+            PBCG_TS(3);
+            last_cta_finish<4>(S, a.gacc, a.ticket, PH_A, a.finalize, sc, a.hist, nullptr, nullptr);
+            PBCG_TS(4);
+        }
+    } else {
+        plain_publish<4, W>(S, a.part);
     }
 }
 
@@ -246,9 +257,9 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
 // K3 (Alg. 2 l.77-79) + phase-B dots.  Group 0: x, r' and (r0,r'), (r',r');
 // group 1: w' and (r0,w').
 // ---------------------------------------------------------------------------
-template <int NH, int NL, int NHE>
+template <class Acc>
 struct K3Op {
-    ExAccT<NH, NL, NHE> d0, d1;
+    Acc d0, d1;
     double al, om, nal, nom;
     // group 0: x, r' and the products of (r0,r'), (r',r')
     __device__ __forceinline__ void row0(unsigned &flags, double rh, double p, double q, double y, double &x, double &r,
@@ -267,8 +278,9 @@ struct K3Op {
     }
 };
 
-template <int NH, int NL, int W, int PPT, int STAGES, int NHE>
+template <int NH, int NL, int W, int PPT, int STAGES, int NHE, bool EXACT = true>
 __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
+    using Acc = typename std::conditional<EXACT, ExAccT<NH, NL, NHE>, PlainAcc>::type;
     constexpr int NV = 7;  // rh, p, q, y, t, v, x
     constexpr int NCW = 2 * W;
     constexpr int T = TileGeo<W, PPT>::T;
@@ -288,7 +300,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
     __syncthreads();
     const int64_t n = a.n;
     unsigned flags = 0;
-    K3Op<NH, NL, NHE> R;
+    K3Op<Acc> R;
     R.al = sc->alpha;
     R.om = sc->omega;
     R.nal = -R.al;
@@ -296,6 +308,10 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
     R.d0.zero();
     R.d1.zero();
     const int g = warp / W, wg = warp % W;
+    if constexpr (!EXACT) {  // per-warp slot of the plain sums; group 1 has one dot, the producer none
+        R.d0.slot = warp < NCW ? wg : -1;
+        R.d1.slot = (warp < NCW && g == 0) ? wg : -1;
+    }
     // dot slots: (r0,r') -> 0, (r0,w') -> 1, (r',r') -> 2
     unsigned long long *s0 = S.w[g == 0 ? 0 : 1], *s1 = S.w[2];
     if (warp == NCW) {
@@ -371,8 +387,12 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
     __syncwarp();
     R.d0.warp_merge(s0);
     R.d1.warp_merge(s1);
-    if (cta_sacc_publish<3>(S, flags, a.gacc, a.ticket))
-        last_cta_finish<3>(S, a.gacc, a.ticket, PH_B, a.finalize, sc, a.hist, nullptr, nullptr);
+    if constexpr (EXACT) {
+        if (cta_sacc_publish<3>(S, flags, a.gacc, a.ticket))
+            last_cta_finish<3>(S, a.gacc, a.ticket, PH_B, a.finalize, sc, a.hist, nullptr, nullptr);
+    } else {
+        plain_publish<3, W>(S, a.part);
+    }
 }
 
 // ---------------------------------------------------------------------------

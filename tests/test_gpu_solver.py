@@ -302,3 +302,48 @@ def test_spmv_format_random_keeps_explicit(pb):
     f = S.spmv_format()
     assert f["explicit_cols"] == f["nnz"] and f["slot_records"] == 0 and f["sigma_sorted"] == 1
     S.close()
+
+
+# ------------------------------------------------------ plain fp64 dots ---
+# the paper's non-reproducible comparison arm.
+
+def test_plain_dots_mode(pb):
+    A = gen.make_config("c1_2d64")
+    S = solver(pb, A, history_capacity=600)
+    b = gpu_b(pb, S, A)
+    xe, re = S.solve(b, tol=1e-10, max_iter=500)
+    He = S.history()
+    xp, rp = S.solve(b, tol=1e-10, max_iter=500, dot_mode="plain")
+    Hp = S.history()
+    assert re.status == rp.status == pb.CONVERGED
+    assert abs(rp.iterations - re.iterations) <= max(3, re.iterations // 10), (rp.iterations, re.iterations)
+    assert rp.relres_true <= 1e-9
+    # the same handle and launch geometry: deterministic
+    xp2, rp2 = S.solve(b, tol=1e-10, max_iter=500, dot_mode="plain")
+    assert np.array_equal(u64(S.history()), u64(Hp)) and np.array_equal(u64(xp2.cpu().numpy()), u64(xp.cpu().numpy()))
+    # back to exact dots: the oracle's bits again
+    xe2, re2 = S.solve(b, tol=1e-10, max_iter=500)
+    assert np.array_equal(u64(S.history()), u64(He)) and np.array_equal(u64(xe2.cpu().numpy()), u64(xe.cpu().numpy()))
+    O = oracle.PBiCGStab(A, tol=1e-10, max_iter=500)
+    O.run()
+    assert np.array_equal(u64(He), u64(O.history()))
+    S.close()
+
+
+def test_plain_dots_partition_witness(pb):
+    # exact dots: identical bits for 1/2/4 ranks; plain dots: the grouping of
+    # the fp64 sums follows the partition, so the trajectory does not
+    import torch
+    A = gen.stencil(3, 40, 100.0)
+    hist = {}
+    for mode in ("exact", "plain"):
+        for V in (1, 2, 4):
+            S = solver(pb, A, virtual_ranks=V, history_capacity=64)
+            b = gpu_b(pb, S, A)
+            S.start(b, tol=0.0, max_iter=40, dot_mode=mode)
+            S.iterate(40)
+            S.finish(None)
+            hist[mode, V] = u64(S.history())
+            S.close()
+    assert all(np.array_equal(hist["exact", V], hist["exact", 1]) for V in (2, 4))
+    assert any(not np.array_equal(hist["plain", V], hist["plain", 1]) for V in (2, 4))
