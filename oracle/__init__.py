@@ -95,6 +95,8 @@ def _L():
         lib.orc_true_relres.argtypes = [i64, vp, vp, vp, vp, vp, vp]
         lib.orc_bicgstab.restype = i32
         lib.orc_bicgstab.argtypes = [i64, vp, vp, vp, vp, vp, dbl, i32, vp, vp]
+        lib.orc_bicgstab_dots.restype = i32
+        lib.orc_bicgstab_dots.argtypes = [i64, vp, vp, vp, vp, vp, dbl, i32, i32, vp, vp]
         _lib = lib
     return _lib
 
@@ -244,8 +246,10 @@ def true_relres(A, b, x) -> tuple[float, int]:
     return r, f.value
 
 
-def bicgstab(A, b, x0=None, tol=1e-10, max_iter=10000):
-    """Plain-double Algorithm 1.  Returns (status, iterations, x, history)."""
+def bicgstab(A, b, x0=None, tol=1e-10, max_iter=10000, exact_dots=False):
+    """Algorithm 1.  exact_dots=False: sequential plain
+    double dots (the textbook routine); True: EXDOT (the arithmetic of the
+    GPU's Alg. 1 arm).  Returns (status, iterations, x, relres history)."""
     b = _f64(b)
     x = np.zeros(A.n) if x0 is None else _f64(x0).copy()
     rp = np.ascontiguousarray(A.row_ptr, np.int32)
@@ -253,6 +257,6 @@ def bicgstab(A, b, x0=None, tol=1e-10, max_iter=10000):
     val = _f64(A.val)
     it = ctypes.c_int(0)
     hist = np.zeros(max_iter + 1)
-    st = _L().orc_bicgstab(A.n, _p(rp), _p(col), _p(val), _p(b), _p(x), float(tol), int(max_iter),
-                           ctypes.byref(it), _p(hist))
+    st = _L().orc_bicgstab_dots(A.n, _p(rp), _p(col), _p(val), _p(b), _p(x), float(tol), int(max_iter),
+                                int(bool(exact_dots)), ctypes.byref(it), _p(hist))
     return st, it.value, x, hist[: it.value + 1]

@@ -478,26 +478,44 @@ void orc_pbcg_free(orc_pbcg *S) {
  * Stopping rule: ||r_{i+1}||/||b|| <= tol (same rule as above); plus the
  * usual early exit when ||q_i||/||b|| <= tol (x := x + alpha p).
  * ------------------------------------------------------------------------ */
-int orc_bicgstab(int64_t n, const int32_t *rp, const int32_t *col, const double *val, const double *b,
-                 double *x, double tol, int max_iter, int *iters, double *hist) {
+/* Algorithm 1 with the dot of the caller's choice:
+ * exact = 0: sequential plain double (orc_dot_seq), the textbook routine the
+ * north_star cross-check uses; exact = 1: EXDOT by its definition (orc_exdot)
+ * -- the arithmetic the GPU's Alg. 1 arm reproduces bit for bit (SURVEY
+ * §8(f) NEXT-1; R-20).  Everything else is the same code: -ffp-
+ * contract=off, left-to-right evaluation as written below.  With exact dots
+ * a product outside the exact zone (R-9) ends the solve with ORC_RANGE. */
+static double a1_dot(int exact, int64_t n, const double *x, const double *y, int *flags) {
+    if (!exact) return orc_dot_seq(n, x, y);
+    int f = 0;
+    const double v = orc_exdot(n, x, y, &f);
+    *flags |= f;
+    return v;
+}
+
+int orc_bicgstab_dots(int64_t n, const int32_t *rp, const int32_t *col, const double *val, const double *b,
+                      double *x, double tol, int max_iter, int exact, int *iters, double *hist) {
     double *r = vnew(n), *rh = vnew(n), *p = vnew(n), *s = vnew(n), *q = vnew(n), *y = vnew(n);
-    int status = ORC_MAXITER, it = 0;
+    int status = ORC_MAXITER, it = 0, fl = 0;
     orc_spmv(n, rp, col, val, x, s);
     for (int64_t k = 0; k < n; ++k) r[k] = b[k] - s[k];
     memcpy(rh, r, sizeof(double) * (size_t)n);
     memcpy(p, r, sizeof(double) * (size_t)n);
-    double nb = sqrt(orc_dot_seq(n, b, b));
-    double rho = orc_dot_seq(n, rh, r);
-    double rel = sqrt(orc_dot_seq(n, r, r)) / nb;
+    double nb = sqrt(a1_dot(exact, n, b, b, &fl));
+    double rho = a1_dot(exact, n, rh, r, &fl);
+    double rel = sqrt(a1_dot(exact, n, r, r, &fl)) / nb;
     if (hist) hist[0] = rel;
+    if (fl) { status = ORC_RANGE; goto done; }
     if (rel <= tol) { status = ORC_CONVERGED; goto done; }
     for (int i = 0; i < max_iter; ++i) {
         orc_spmv(n, rp, col, val, p, s);                 /* s := A p */
-        double den = orc_dot_seq(n, rh, s);
+        double den = a1_dot(exact, n, rh, s, &fl);
+        if (fl) { status = ORC_RANGE; break; }
         if (den == 0.0) { status = ORC_BREAKDOWN_ALPHA; break; }
         double a = rho / den;                            /* a := (r0,r)/(r0,s) */
         for (int64_t k = 0; k < n; ++k) q[k] = r[k] - a * s[k];
-        double qn = sqrt(orc_dot_seq(n, q, q)) / nb;
+        double qn = sqrt(a1_dot(exact, n, q, q, &fl)) / nb;
+        if (fl) { status = ORC_RANGE; break; }
         if (qn <= tol) {
             for (int64_t k = 0; k < n; ++k) x[k] = x[k] + a * p[k];
             it = i + 1;
@@ -506,17 +524,20 @@ int orc_bicgstab(int64_t n, const int32_t *rp, const int32_t *col, const double 
             break;
         }
         orc_spmv(n, rp, col, val, q, y);                 /* y := A q */
-        double yy = orc_dot_seq(n, y, y);
+        double yy = a1_dot(exact, n, y, y, &fl);
+        double qy = a1_dot(exact, n, q, y, &fl);
+        if (fl) { status = ORC_RANGE; break; }
         if (yy == 0.0) { status = ORC_BREAKDOWN_OMEGA; break; }
-        double om = orc_dot_seq(n, q, y) / yy;           /* w := (q,y)/(y,y) */
+        double om = qy / yy;                             /* w := (q,y)/(y,y) */
         for (int64_t k = 0; k < n; ++k) {
             x[k] = x[k] + a * p[k] + om * q[k];
             r[k] = q[k] - om * y[k];
         }
-        double rhon = orc_dot_seq(n, rh, r);
+        double rhon = a1_dot(exact, n, rh, r, &fl);
         it = i + 1;
-        rel = sqrt(orc_dot_seq(n, r, r)) / nb;
+        rel = sqrt(a1_dot(exact, n, r, r, &fl)) / nb;
         if (hist) hist[it] = rel;
+        if (fl) { status = ORC_RANGE; break; }
         if (rel <= tol) { status = ORC_CONVERGED; break; }
         if (om == 0.0 || rho == 0.0 || rhon == 0.0) { status = ORC_BREAKDOWN_RHO; break; }
         double be = (a / om) * (rhon / rho);             /* beta := (a/w)(r0,r')/(r0,r) */
@@ -528,3 +549,9 @@ done:
     free(r); free(rh); free(p); free(s); free(q); free(y);
     return status;
 }
+
+int orc_bicgstab(int64_t n, const int32_t *rp, const int32_t *col, const double *val, const double *b,
+                 double *x, double tol, int max_iter, int *iters, double *hist) {
+    return orc_bicgstab_dots(n, rp, col, val, b, x, tol, max_iter, 0, iters, hist);
+}
+

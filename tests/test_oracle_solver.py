@@ -259,3 +259,51 @@ def test_deterministic():
     S1.run(), S2.run()
     assert np.array_equal(S1.history().view(np.uint64), S2.history().view(np.uint64))
     assert np.array_equal(S1.vec("x").view(np.uint64), S2.vec("x").view(np.uint64))
+
+
+# ---- Algorithm 1 with exact dots (the GPU's Alg. 1 arm) ----
+
+def test_alg1_exact_dots_vs_direct_solve():
+    # same pin as Alg. 2: random well-conditioned systems against a dense
+    # direct solve, and the true residual within 10 tol
+    rng = np.random.default_rng(77)
+    for k in range(40):
+        n = int(rng.integers(4, 65))
+        A = gen.dense_as_sparse(n, seed=300 + k, density=0.5)
+        M = np.zeros((n, n))
+        for i in range(n):
+            M[i, A.col[A.row_ptr[i]:A.row_ptr[i + 1]]] = A.val[A.row_ptr[i]:A.row_ptr[i + 1]]
+        b = rng.uniform(-1, 1, n)
+        st, it, x, h = oracle.bicgstab(A, b, tol=1e-10, max_iter=1000, exact_dots=True)
+        assert st == oracle.CONVERGED, (k, st)
+        xs = np.linalg.solve(M, b)
+        assert np.linalg.norm(x - xs) <= 1e-6 * np.linalg.norm(xs)
+        assert oracle.true_relres(A, b, x)[0] <= 10 * 1e-10
+        assert h[-1] <= 1e-10
+
+
+def test_alg1_exact_vs_plain_dots_track():
+    # the two dot choices differ by rounding only: on a well-conditioned
+    # stencil the residual histories agree to many digits for the first
+    # iterations and both reach the tolerance
+    A = gen.stencil(2, 24, 10.0)
+    b = oracle.spmv(A, np.ones(A.n))
+    st0, it0, x0, h0 = oracle.bicgstab(A, b, tol=1e-10, max_iter=1000)
+    st1, it1, x1, h1 = oracle.bicgstab(A, b, tol=1e-10, max_iter=1000, exact_dots=True)
+    assert st0 == st1 == oracle.CONVERGED
+    assert abs(it0 - it1) <= 3
+    k = min(8, it0, it1)
+    assert np.allclose(h0[:k], h1[:k], rtol=1e-9, atol=0)
+    assert np.abs(x1 - 1.0).max() < 1e-6
+
+
+def test_alg1_exact_dots_equals_alg2_solution():
+    # Alg. 1 and Alg. 2 are the same method in exact arithmetic
+    # (test_reading_alg2_equals_alg1_exactly); in fp both land on A^-1 b
+    A = gen.make_config("c1_2d64")
+    S = oracle.PBiCGStab(A, tol=1e-10, max_iter=500)
+    S.run()
+    st, it, x, h = oracle.bicgstab(A, S.vec("b"), tol=1e-10, max_iter=500, exact_dots=True)
+    assert st == oracle.CONVERGED
+    assert np.abs(x - S.vec("x")).max() < 1e-6
+    assert abs(oracle.true_relres(A, S.vec("b"), x)[0] - S.true_relres()) <= 1e-10
