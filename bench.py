@@ -198,6 +198,26 @@ def run_gpu(args, rank, world, local_rank, dist):
             pms = float(t.item())
         out["plain"] = {"value": K / (pms * 1e-3), "unit": "iter/s", "ms_per_step": pms / K,
                         "valid": pres.iterations == W + K}
+        # Algorithm 1 (classic BiCGStab, exact dots) on the same workload: the
+        # paper's other comparison column
+        S.start(b, tol=0.0, max_iter=W + K + 8, method="bicgstab")
+        S.iterate(W)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record(S.stream)
+        S.iterate(K)
+        q1.record(S.stream)
+        torch.cuda.synchronize()
+        ams = q0.elapsed_time(q1)
+        ares = S.finish(None)
+        if dist:
+            t = torch.tensor([ams], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ams = float(t.item())
+        out["alg1"] = {"value": K / (ams * 1e-3), "unit": "iter/s", "ms_per_step": ams / K,
+                       "valid": ares.iterations == W + K}
     # ---- per-kernel times: a second timed pass over the same K steps with
     # CUDA events around every launch (single rank) ----
     fmt = S.spmv_format()
@@ -419,6 +439,12 @@ def main():
         pl["note"] = ("same workload and K with dot_mode=plain (fp64 dots, per-thread fma chains + fixed trees; "
                       "not reproducible across partitions); exact_over_plain = the ExBLAS cost on this GPU")
         line["plain_dots"] = pl
+    if "alg1" in out:
+        a1 = out["alg1"]
+        a1["pbicgstab_over_bicgstab"] = value / a1["value"]
+        a1["note"] = ("same workload and K with method=bicgstab (Algorithm 1, exact dots, 4 reduction phases per "
+                      "iteration, no overlap); pbicgstab_over_bicgstab = iter/s ratio of Alg. 2 to Alg. 1")
+        line["bicgstab_alg1"] = a1
     line["bytes_per_iteration_per_gpu"] = by["iteration"]
     line["iteration_GBps_per_gpu"] = by["iteration"] / (ms_step * 1e-3) / 1e9
     line["iteration_frac_hbm"] = line["iteration_GBps_per_gpu"] / hbm

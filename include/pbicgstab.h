@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define PBCG_ABI_VERSION 2
+#define PBCG_ABI_VERSION 3
 
 /* return codes of every entry point (never an abort across the ABI) */
 enum pbcg_rc {
@@ -105,9 +105,15 @@ typedef struct {
                                  allreduce) -- the paper's non-reproducible comparison arm (SURVEY §8(f)
                                  NEXT-1); bits depend on the launch geometry and the partition.
                                  Init / true-residual dots stay exact in both modes. */
+    int32_t method;           /* PBCG_METHOD_PBICGSTAB (0, default): Algorithm 2;
+                                 PBCG_METHOD_BICGSTAB (1): Algorithm 1, classic BiCGStab (l.39-54) with
+                                 exact dots, four reduction phases per iteration, the arithmetic of the
+                                 oracle's orc_bicgstab_dots (R-20); requires PBCG_DOT_EXACT.
+                                 history rows: 4 omega, 5 rho, 7 rr, 8 relres, 9 beta, 10 alpha. */
 } pbcg_opts;
 
 enum pbcg_dot_mode { PBCG_DOT_EXACT = 0, PBCG_DOT_PLAIN = 1 };
+enum pbcg_method { PBCG_METHOD_PBICGSTAB = 0, PBCG_METHOD_BICGSTAB = 1 };
 
 /* Solve result.  history row layout (12 doubles per row, row 0 = init, row
  * i+1 = iteration i), identical to the oracle's:

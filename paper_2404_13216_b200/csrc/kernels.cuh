@@ -22,7 +22,9 @@ namespace pbcg {
 enum { H_THETA = 0, H_ETA, H_SIGMA, H_ZETA, H_OMEGA, H_RHO, H_DELTA, H_RR, H_RELRES, H_BETA, H_ALPHA, H_COLS = 12 };
 enum { ST_CONVERGED = 0, ST_MAXITER = 1, ST_BD_INIT = 2, ST_BD_RHO = 3, ST_BD_OMEGA = 4, ST_BD_ALPHA = 5,
        ST_RANGE = 6, ST_RUNNING = -1 };
-enum Phase { PH_INIT = 0, PH_A = 1, PH_B = 2, PH_TRUE = 3, PH_EXDOT = 4 };
+enum Phase { PH_INIT = 0, PH_A = 1, PH_B = 2, PH_TRUE = 3, PH_EXDOT = 4,
+             // Algorithm 1 (classic BiCGStab, reading R-20)
+             PH1_INIT = 5, PH1_DEN = 6, PH1_QQ = 7, PH1_OM = 8, PH1_R = 9 };
 
 // device-resident solver scalars (one copy per rank; identical on all ranks)
 struct Scalars {
@@ -31,7 +33,8 @@ struct Scalars {
     double relres, relres_true;
     int32_t it, done, status, max_iter;
     int32_t hist_cap, err;
-    int32_t pad0, pad1;
+    int32_t qconv;  // Alg. 1: converged at the q check, x += alpha p still to apply
+    int32_t pad1;
 };
 
 // ------------------------------------------------------------------------
@@ -41,8 +44,80 @@ __device__ __forceinline__ void hist_put(double *hist, const Scalars *sc, int ro
     if (hist && row < sc->hist_cap) hist[(int64_t)row * H_COLS + col] = v;
 }
 
+// Algorithm 1 with exact dots: the scalar steps of the oracle's
+// orc_bicgstab_dots (exact = 1) in the same order (reading R-20).
+__device__ void phase1_finalize(int phase, Scalars *sc, const double *d, unsigned flags, double *hist) {
+    if (phase == PH1_INIT) {  // nb, rho0 = (r^,r0), relres0
+        const double bb = d[0], rho = d[1], rr = d[2];
+        sc->it = 0;
+        sc->nb = __dsqrt_rn(bb);
+        if (sc->nb == 0.0) { sc->err = 1; sc->done = 1; sc->status = ST_MAXITER; return; }  // EINVAL
+        const double rel = __ddiv_rn(__dsqrt_rn(rr), sc->nb);
+        sc->rho = rho;
+        sc->relres = rel;
+        hist_put(hist, sc, 0, H_RHO, rho);
+        hist_put(hist, sc, 0, H_RELRES, rel);
+        if (flags) { sc->status = ST_RANGE; sc->done = 1; return; }
+        if (rel <= sc->tol) { sc->status = ST_CONVERGED; sc->done = 1; return; }
+        if (sc->max_iter == 0) { sc->status = ST_MAXITER; sc->done = 1; return; }
+        sc->status = ST_RUNNING;
+        return;
+    }
+    if (sc->done) return;
+    const int i = sc->it;
+    if (phase == PH1_DEN) {  // a := (r0,r)/(r0,s)
+        if (flags) { sc->status = ST_RANGE; sc->done = 1; return; }
+        if (d[0] == 0.0) { sc->status = ST_BD_ALPHA; sc->done = 1; return; }
+        sc->alpha = __ddiv_rn(sc->rho, d[0]);
+        hist_put(hist, sc, i + 1, H_ALPHA, sc->alpha);
+        return;
+    }
+    if (phase == PH1_QQ) {  // early exit on ||q||/||b|| <= tol: x := x + a p, done
+        const double qn = __ddiv_rn(__dsqrt_rn(d[0]), sc->nb);
+        if (flags) { sc->status = ST_RANGE; sc->done = 1; return; }
+        if (qn <= sc->tol) {
+            sc->it = i + 1;
+            sc->relres = qn;
+            hist_put(hist, sc, i + 1, H_RELRES, qn);
+            sc->status = ST_CONVERGED;
+            sc->qconv = 1;
+            sc->done = 1;
+        }
+        return;
+    }
+    if (phase == PH1_OM) {  // w := (q,y)/(y,y)
+        const double qy = d[0], yy = d[1];
+        if (flags) { sc->status = ST_RANGE; sc->done = 1; return; }
+        if (yy == 0.0) { sc->status = ST_BD_OMEGA; sc->done = 1; return; }
+        sc->omega = __ddiv_rn(qy, yy);
+        hist_put(hist, sc, i + 1, H_OMEGA, sc->omega);
+        return;
+    }
+    // PH1_R: rho' = (r0,r'), relres; stopping; beta := (a/w)(rho'/rho)
+    const double rhon = d[0], rr = d[1];
+    const double rel = __ddiv_rn(__dsqrt_rn(rr), sc->nb);
+    sc->it = i + 1;
+    sc->relres = rel;
+    hist_put(hist, sc, i + 1, H_RHO, rhon);
+    hist_put(hist, sc, i + 1, H_RR, rr);
+    hist_put(hist, sc, i + 1, H_RELRES, rel);
+    if (flags) { sc->status = ST_RANGE; sc->done = 1; return; }
+    if (rel <= sc->tol) { sc->status = ST_CONVERGED; sc->done = 1; return; }
+    const double om = sc->omega;
+    if (om == 0.0 || sc->rho == 0.0 || rhon == 0.0) { sc->status = ST_BD_RHO; sc->done = 1; return; }
+    const double be = __dmul_rn(__ddiv_rn(sc->alpha, om), __ddiv_rn(rhon, sc->rho));
+    hist_put(hist, sc, i + 1, H_BETA, be);
+    sc->beta = be;
+    sc->rho = rhon;
+    if (sc->it >= sc->max_iter) { sc->status = ST_MAXITER; sc->done = 1; }
+}
+
 __device__ void phase_finalize(int phase, Scalars *sc, const double *d, unsigned flags, double *hist,
                                double *out, int32_t *out_flags) {
+    if (phase >= PH1_INIT) {
+        phase1_finalize(phase, sc, d, flags, hist);
+        return;
+    }
     if (phase == PH_EXDOT) {
         if (out) *out = d[0];
         if (out_flags) *out_flags = (int32_t)flags;
@@ -628,6 +703,44 @@ __global__ void __launch_bounds__(256) spmv_sell_pipe_kernel(SellMat A, const do
             }
         }
     }
+}
+
+// ------------------------------------------------------------------------
+// Algorithm 1 vector updates, the oracle's arithmetic
+// (orc_bicgstab_dots): separate RN multiply / add, left to right, no fma.
+// ------------------------------------------------------------------------
+__global__ void a1_q_kernel(int64_t n, const double *r, const double *s, double *q, const Scalars *sc) {
+    if (sc->done) return;
+    const double a = sc->alpha;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        q[k] = __dsub_rn(r[k], __dmul_rn(a, s[k]));  // q := r - a s
+}
+
+__global__ void a1_xconv_kernel(int64_t n, double *x, const double *p, const Scalars *sc) {
+    if (!sc->qconv) return;
+    const double a = sc->alpha;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        x[k] = __dadd_rn(x[k], __dmul_rn(a, p[k]));  // x := x + a p (converged at the q check)
+}
+
+__global__ void a1_qclear_kernel(Scalars *sc) { sc->qconv = 0; }
+
+__global__ void a1_xr_kernel(int64_t n, double *x, const double *p, const double *q, const double *y, double *r,
+                             const Scalars *sc) {
+    if (sc->done) return;
+    const double a = sc->alpha, om = sc->omega;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const double qk = q[k];
+        x[k] = __dadd_rn(__dadd_rn(x[k], __dmul_rn(a, p[k])), __dmul_rn(om, qk));  // x := x + a p + w q
+        r[k] = __dsub_rn(qk, __dmul_rn(om, y[k]));                                 // r := q - w y
+    }
+}
+
+__global__ void a1_p_kernel(int64_t n, const double *r, double *p, const double *s, const Scalars *sc) {
+    if (sc->done) return;
+    const double be = sc->beta, om = sc->omega;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        p[k] = __dadd_rn(r[k], __dmul_rn(be, __dsub_rn(p[k], __dmul_rn(om, s[k]))));  // p := r + b (p - w s)
 }
 
 // Plain dot mode: d[k] = sum over ranks v (in order) and CTAs c (in order) of

@@ -285,7 +285,8 @@ struct pbcg_handle {
     long long **vgacc = nullptr;  // device array [NPH][V] of gacc pointers (virtual ranks)
     double **vpart = nullptr;     // device array [NPH][V] of plain-mode partial arrays
     int dot_mode = PBCG_DOT_EXACT;  // of the running solve (pbcg_opts.dot_mode)
-    int g_mode = -1;                // dot mode the captured graph was built with
+    int method = PBCG_METHOD_PBICGSTAB;  // of the running solve (pbcg_opts.method)
+    int g_mode = -1;                // dot mode + 2 method the captured graph was built with
     int hist_cap = 10001;
     Scalars *h_sc = nullptr;      // pinned mirror of rank 0's scalars
     int grid_k2 = 0, grid_k3 = 0, grid_md = 0;
@@ -657,6 +658,8 @@ static int launch_spmv(pbcg_handle *h, Rank &R, int mode, const double *xpad, do
 }
 
 // up-to-4 fused EXDOTs over every rank's rows (phase PH_INIT / PH_TRUE)
+static int launch_xd1(pbcg_handle *h, const MultiDotArgs &a);
+
 static int multidot(pbcg_handle *h, int ph, int phase, int nd, const double *const *xs_per_rank[4],
                     const double *const *ys_per_rank[4]) {
     const bool fin = !multi(h);
@@ -675,12 +678,16 @@ static int multidot(pbcg_handle *h, int ph, int phase, int nd, const double *con
         a.phase = phase;
         a.finalize = fin;
         const int grid = std::max(1, std::min<int>(h->grid_md, (int)((R.n / 2 + K_BS - 1) / K_BS)));
-        if (nd == 4) multidot_kernel<4, K_NP, K_NE, K_BS, U_MD4><<<grid, K_BS, 0, h->stream>>>(a);
+        if (nd == 1 && R.n > 0 && ((((uintptr_t)a.x[0]) | ((uintptr_t)a.y[0])) & 15) == 0) {
+            RC_TRY(launch_xd1(h, a));  // one dot over aligned vectors: the TMA-streamed EXDOT kernel
+        } else if (nd == 4) multidot_kernel<4, K_NP, K_NE, K_BS, U_MD4><<<grid, K_BS, 0, h->stream>>>(a);
+        else if (nd == 2) multidot_kernel<2, K_NP, K_NE, K_BS, U_MD4><<<grid, K_BS, 0, h->stream>>>(a);
         else multidot_kernel<1, K_NP, K_NE, K_BS, U_MD1><<<grid, K_BS, 0, h->stream>>>(a);
         CUDA_TRY(cudaGetLastError());
     }
     if (!fin) {
         if (nd == 4) RC_TRY(reduce_finalize<4>(h, ph, phase, h->stream, nullptr, nullptr));
+        else if (nd == 2) RC_TRY(reduce_finalize<2>(h, ph, phase, h->stream, nullptr, nullptr));
         else RC_TRY(reduce_finalize<1>(h, ph, phase, h->stream, nullptr, nullptr));
     }
     return PBCG_OK;
@@ -764,6 +771,13 @@ static int stream_grid(pbcg_handle *h, int64_t n, int rows_per_tile) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(h ? h->nsm : 148, tiles));
 }
 
+static int launch_xd1(pbcg_handle *h, const MultiDotArgs &a) {
+    RC_TRY(stream_attrs());
+    XDS<<<stream_grid(h, a.n, TileGeo<X_NCW, XD_PPT>::T), STREAM_THREADS, XD_SMEM, h->stream>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    return PBCG_OK;
+}
+
 static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     // fin = 1: the last CTA rounds and runs the scalar step; fin = 0: publish only (finalize_kernel follows)
     K2Args a{R.n, R.r, R.rh, R.w(), R.t, R.v, R.p, R.s, R.z(), R.q, R.y, R.sc, R.gacc[1], fin ? R.tickets + 1 : nullptr, R.hist, fin, R.part[1]};
@@ -793,7 +807,10 @@ static int launch_k3(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     return PBCG_OK;
 }
 
+static int enqueue_alg1(pbcg_handle *h);
+
 static int enqueue_iteration(pbcg_handle *h) {
+    if (h->method == PBCG_METHOD_BICGSTAB) return enqueue_alg1(h);
     cudaStream_t st = h->stream;
     if (!multi(h)) {
         // single rank: the rounding + scalar step of each phase (finalize_kernel,
@@ -1087,6 +1104,7 @@ static void opts_defaults(const pbcg_opts *o, pbcg_opts &e) {
     e.poll_every = 16;
     e.use_graphs = 1;
     e.dot_mode = PBCG_DOT_EXACT;
+    e.method = PBCG_METHOD_PBICGSTAB;
     if (o) {
         e = *o;
         if (!(e.breakdown_eps > 0.0)) e.breakdown_eps = 1e-30;
@@ -1098,6 +1116,8 @@ static void opts_defaults(const pbcg_opts *o, pbcg_opts &e) {
 // start / iterate / finish / solve
 // ----------------------------------------------------------------------------
 static int capture_chunk(pbcg_handle *h, int iters);
+static int start_alg1(pbcg_handle *h);
+static int start_alg2_rest(pbcg_handle *h);
 static int g_default_chunk = 16;
 
 extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0, const pbcg_opts *o) {
@@ -1107,8 +1127,13 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
     opts_defaults(o, op);
     if (!(op.tol >= 0.0) || op.max_iter < 0) return fail(PBCG_EINVAL, "start: bad tol / max_iter");
     if (op.dot_mode != PBCG_DOT_EXACT && op.dot_mode != PBCG_DOT_PLAIN) return fail(PBCG_EINVAL, "start: bad dot_mode");
+    if (op.method != PBCG_METHOD_PBICGSTAB && op.method != PBCG_METHOD_BICGSTAB)
+        return fail(PBCG_EINVAL, "start: bad method");
+    if (op.method == PBCG_METHOD_BICGSTAB && op.dot_mode != PBCG_DOT_EXACT)
+        return fail(PBCG_EINVAL, "start: Algorithm 1 runs with exact dots only");
     h->max_iter = op.max_iter;
     h->dot_mode = op.dot_mode;
+    h->method = op.method;
     Scalars s0{};
     s0.tol = op.tol;
     s0.eps = op.breakdown_eps;
@@ -1133,22 +1158,8 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
     RC_TRY(copy_own_to_pad(h, &Rank::x, 2));
     RC_TRY(halo(h, 2));
     for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_RESID, R.xpad, R.r, R.b, R.rh, false, h->stream));
-    RC_TRY(copy_own_to_pad(h, &Rank::r, 2));
-    RC_TRY(halo(h, 2));
-    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.xpad, R.w(), nullptr, nullptr, false, h->stream));
-    RC_TRY(halo(h, 1));
-    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, false, h->stream));
-    // I2-I4: ||b||, rho0 = (r^,r0), delta0 = (r^,w0), (r0,r0); alpha0
-    std::vector<const double *> xb, yb, xr, yr, xw, yw, xn, yn;
-    for (auto &R : h->R) {
-        xb.push_back(R.b); yb.push_back(R.b);
-        xr.push_back(R.rh); yr.push_back(R.r);
-        xw.push_back(R.rh); yw.push_back(R.w());
-        xn.push_back(R.r); yn.push_back(R.r);
-    }
-    const double *const *xs[4] = {xb.data(), xr.data(), xw.data(), xn.data()};
-    const double *const *ys[4] = {yb.data(), yr.data(), yw.data(), yn.data()};
-    RC_TRY(multidot(h, 0, PH_INIT, 4, xs, ys));
+    if (h->method == PBCG_METHOD_BICGSTAB) RC_TRY(start_alg1(h));
+    else RC_TRY(start_alg2_rest(h));
     CUDA_TRY(cudaMemcpyAsync(h->h_sc, h->R[0].sc, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
     int bad = 0;
@@ -1166,8 +1177,97 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
     return PBCG_OK;
 }
 
+// I1 (rest) - I4 of Algorithm 2
+static int start_alg2_rest(pbcg_handle *h) {
+    RC_TRY(copy_own_to_pad(h, &Rank::r, 2));
+    RC_TRY(halo(h, 2));
+    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.xpad, R.w(), nullptr, nullptr, false, h->stream));
+    RC_TRY(halo(h, 1));
+    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, false, h->stream));
+    // I2-I4: ||b||, rho0 = (r^,r0), delta0 = (r^,w0), (r0,r0); alpha0
+    std::vector<const double *> xb, yb, xr, yr, xw, yw, xn, yn;
+    for (auto &R : h->R) {
+        xb.push_back(R.b); yb.push_back(R.b);
+        xr.push_back(R.rh); yr.push_back(R.r);
+        xw.push_back(R.rh); yw.push_back(R.w());
+        xn.push_back(R.r); yn.push_back(R.r);
+    }
+    const double *const *xs[4] = {xb.data(), xr.data(), xw.data(), xn.data()};
+    const double *const *ys[4] = {yb.data(), yr.data(), yw.data(), yn.data()};
+    return multidot(h, 0, PH_INIT, 4, xs, ys);
+}
+
+// Algorithm 1 init: r^ := r0 (written with r0), p0 := r0;
+// ||b||, rho0 = (r^,r0), (r0,r0)
+static int start_alg1(pbcg_handle *h) {
+    for (auto &R : h->R)
+        CUDA_TRY(cudaMemcpyAsync(R.z(), R.r, sizeof(double) * R.n, cudaMemcpyDeviceToDevice, h->stream));
+    std::vector<const double *> xb, xr, yr, xn;
+    for (auto &R : h->R) {
+        xb.push_back(R.b);
+        xr.push_back(R.rh);
+        yr.push_back(R.r);
+        xn.push_back(R.r);
+    }
+    const double *const *xs[4] = {xb.data(), xr.data(), xn.data(), xn.data()};
+    const double *const *ys[4] = {xb.data(), yr.data(), xn.data(), xn.data()};
+    return multidot(h, 0, PH1_INIT, 4, xs, ys);
+}
+
+// One iteration of Algorithm 1 with exact dots, vectors
+// p -> z buffer (padded, SpMV input), s -> s, q -> w buffer (padded), y -> y.
+// Four reduction phases, each a multidot whose last CTA (single rank) or
+// finalize (ranks) runs phase1_finalize; every kernel is predicated on done.
+static int enqueue_alg1(pbcg_handle *h) {
+    cudaStream_t st = h->stream;
+    auto grid1 = [&](const Rank &R) { return (int)std::max<int64_t>(1, std::min<int64_t>((R.n + 255) / 256, 4 * h->nsm)); };
+    auto ptrs = [&](double *Rank::*m) {
+        std::vector<const double *> v;
+        for (auto &R : h->R) v.push_back(R.*m);
+        return v;
+    };
+    std::vector<const double *> vz, vw;
+    for (auto &R : h->R) { vz.push_back(R.z()); vw.push_back(R.w()); }
+    const auto vrh = ptrs(&Rank::rh), vs = ptrs(&Rank::s), vy = ptrs(&Rank::y), vr = ptrs(&Rank::r);
+    RC_TRY(halo(h, 0));  // s := A p
+    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.zpad, R.s, nullptr, nullptr, true, st));
+    {
+        const double *const *xs[4] = {vrh.data(), nullptr, nullptr, nullptr};
+        const double *const *ys[4] = {vs.data(), nullptr, nullptr, nullptr};
+        RC_TRY(multidot(h, 1, PH1_DEN, 1, xs, ys));  // a := rho/(r^,s)
+    }
+    for (auto &R : h->R) a1_q_kernel<<<grid1(R), 256, 0, st>>>(R.n, R.r, R.s, R.w(), R.sc);
+    CUDA_TRY(cudaGetLastError());
+    {
+        const double *const *xs[4] = {vw.data(), nullptr, nullptr, nullptr};
+        RC_TRY(multidot(h, 2, PH1_QQ, 1, xs, xs));  // ||q||/||b|| <= tol?
+    }
+    for (auto &R : h->R) {
+        a1_xconv_kernel<<<grid1(R), 256, 0, st>>>(R.n, R.x, R.z(), R.sc);
+        a1_qclear_kernel<<<1, 1, 0, st>>>(R.sc);
+    }
+    CUDA_TRY(cudaGetLastError());
+    RC_TRY(halo(h, 1));  // y := A q
+    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.y, nullptr, nullptr, true, st));
+    {
+        const double *const *xs[4] = {vw.data(), vy.data(), nullptr, nullptr};
+        const double *const *ys[4] = {vy.data(), vy.data(), nullptr, nullptr};
+        RC_TRY(multidot(h, 1, PH1_OM, 2, xs, ys));  // w := (q,y)/(y,y)
+    }
+    for (auto &R : h->R) a1_xr_kernel<<<grid1(R), 256, 0, st>>>(R.n, R.x, R.z(), R.w(), R.y, R.r, R.sc);
+    CUDA_TRY(cudaGetLastError());
+    {
+        const double *const *xs[4] = {vrh.data(), vr.data(), nullptr, nullptr};
+        const double *const *ys[4] = {vr.data(), vr.data(), nullptr, nullptr};
+        RC_TRY(multidot(h, 2, PH1_R, 2, xs, ys));  // rho', relres, beta
+    }
+    for (auto &R : h->R) a1_p_kernel<<<grid1(R), 256, 0, st>>>(R.n, R.r, R.z(), R.s, R.sc);
+    CUDA_TRY(cudaGetLastError());
+    return PBCG_OK;
+}
+
 static int capture_chunk(pbcg_handle *h, int iters) {
-    if (h->gexec && h->g_iters == iters && h->g_mode == h->dot_mode) return PBCG_OK;
+    if (h->gexec && h->g_iters == iters && h->g_mode == h->dot_mode + 2 * h->method) return PBCG_OK;
     if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
     cudaGraph_t g;
     CUDA_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
@@ -1179,7 +1279,7 @@ static int capture_chunk(pbcg_handle *h, int iters) {
     CUDA_TRY(cudaGraphInstantiate(&h->gexec, g, 0));
     cudaGraphDestroy(g);
     h->g_iters = iters;
-    h->g_mode = h->dot_mode;
+    h->g_mode = h->dot_mode + 2 * h->method;
     return PBCG_OK;
 }
 

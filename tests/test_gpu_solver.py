@@ -347,3 +347,54 @@ def test_plain_dots_partition_witness(pb):
             S.close()
     assert all(np.array_equal(hist["exact", V], hist["exact", 1]) for V in (2, 4))
     assert any(not np.array_equal(hist["plain", V], hist["plain", 1]) for V in (2, 4))
+
+
+# ------------------------------------------ Algorithm 1 with exact dots ---
+# SURVEY §8(f) NEXT-1 second half: classic BiCGStab on the GPU, bit-exact
+# against the oracle's orc_bicgstab_dots(exact = 1) (R-20).
+
+def alg1_both(pb, A, tol, max_iter, **kw):
+    S = solver(pb, A, history_capacity=max_iter + 2, **kw)
+    b = gpu_b(pb, S, A)
+    bh = b.cpu().numpy()
+    st, it, xo, ho = oracle.bicgstab(A, bh, tol=tol, max_iter=max_iter, exact_dots=True)
+    x, r = S.solve(b, tol=tol, max_iter=max_iter, method="bicgstab")
+    H = S.history()
+    S.close()
+    return st, it, xo, ho, x.cpu().numpy(), r, H
+
+
+@pytest.mark.parametrize("name", ["c1", "small3d", "rand", "dense"])
+def test_alg1_matches_oracle(pb, name):
+    A = {"c1": lambda: gen.make_config("c1_2d64"),
+         "small3d": lambda: gen.stencil(3, 20, 100.0),
+         "rand": lambda: gen.random_banded(20_000, seed=9, band=1500),
+         "dense": lambda: gen.dense_as_sparse(57, seed=5, density=0.5)}[name]()
+    st, it, xo, ho, x, r, H = alg1_both(pb, A, 1e-10, 3000)
+    assert r.status == st and r.iterations == it, (r.status, st, r.iterations, it)
+    assert np.array_equal(u64(H[:, oracle.H_RELRES]), u64(ho))
+    assert np.array_equal(u64(x), u64(xo))
+    if st == oracle.CONVERGED:
+        assert r.relres_true <= 10 * 1e-10
+
+
+def test_alg1_virtual_ranks_identical(pb):
+    A = gen.stencil(3, 20, 100.0)
+    ref = alg1_both(pb, A, 1e-10, 3000)
+    for V in (2, 3):
+        st, it, xo, ho, x, r, H = alg1_both(pb, A, 1e-10, 3000, virtual_ranks=V)
+        assert np.array_equal(u64(x), u64(ref[4])) and np.array_equal(u64(H), u64(ref[6])), V
+
+
+def test_alg1_q_convergence_and_errors(pb):
+    # 1x1 diag(2): converges at the q check of the first iteration (x := x + a p)
+    import torch
+    A = gen.from_dense(np.array([[2.0]]))
+    S = solver(pb, A)
+    x, r = S.solve(torch.tensor([2.0], dtype=torch.float64, device="cuda"), method="bicgstab")
+    assert r.status == pb.CONVERGED and r.iterations == 1 and x.item() == 1.0
+    with pytest.raises(pb.PbcgError):
+        S.solve(torch.tensor([2.0], dtype=torch.float64, device="cuda"), method="bicgstab", dot_mode="plain")
+    S.close()
+    st, it, xo, ho = oracle.bicgstab(A, np.array([2.0]), exact_dots=True)
+    assert st == oracle.CONVERGED and it == 1 and xo[0] == 1.0
