@@ -700,8 +700,14 @@ static int multidot(pbcg_handle *h, int ph, int phase, int nd, const double *con
 // FPE levels (performance parameters only, R-16): hot p / hot e / cold, per
 // kernel.  Chosen on C3/C4/C5 (profiles/r01): the p stream of the solver
 // vectors spills more than the e stream, K3's cold levels rarely overflow.
-static constexpr int K2_NH = 3, K2_NHE = 2, K2_NC = 3;
-static constexpr int K3_NH = 3, K3_NHE = 2, K3_NC = 2;
+#ifndef PBCG_K2_FPE
+#define PBCG_K2_FPE 3, K2_NHE = 2, K2_NC = 3
+#endif
+#ifndef PBCG_K3_FPE
+#define PBCG_K3_FPE 3, K3_NHE = 2, K3_NC = 2
+#endif
+static constexpr int K2_NH = PBCG_K2_FPE;
+static constexpr int K3_NH = PBCG_K3_FPE;
 static constexpr int S_NCW = 7;  // warps per dot group (2*7+1 = 15 warps per CTA)
 #ifndef PBCG_X_NCW
 #define PBCG_X_NCW 12
@@ -733,6 +739,11 @@ static constexpr int K2_PPT = PBCG_K2_PPT, K2_ST = PBCG_K2_ST, K3_PPT = PBCG_K3_
                      XD_PPT = PBCG_XD_PPT, XD_ST = PBCG_XD_ST;
 #define K2S k2_stream<K2_NH, K2_NC, S_NCW, K2_PPT, K2_ST, K2_NHE>
 #define K3S k3_stream<K3_NH, K3_NC, S_NCW, K3_PPT, K3_ST, K3_NHE>
+// lean variants (one cold level less): less end-of-kernel drain, which is
+// what counts below LEAN_ROWS rows per rank (C1/C3/C4 measured faster, C5 slower)
+#define K2SL k2_stream<K2_NH, K2_NC - 1, S_NCW, K2_PPT, K2_ST, K2_NHE>
+#define K3SL k3_stream<K3_NH, K3_NC - 1, S_NCW, K3_PPT, K3_ST, K3_NHE>
+static constexpr int64_t LEAN_ROWS = 8 << 20;
 #define K2SP k2_stream<K2_NH, K2_NC, S_NCW, K2_PPT, K2_ST, K2_NHE, false>
 #define K3SP k3_stream<K3_NH, K3_NC, S_NCW, K3_PPT, K3_ST, K3_NHE, false>
 #define XDS exdot_stream<X_NH, X_NL, X_NCW, XD_PPT, XD_ST>
@@ -760,6 +771,8 @@ static int stream_attrs() {
     CUDA_TRY(cudaFuncSetAttribute((const void *)K2S, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)K3S, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)K2SP, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM));
+    CUDA_TRY(cudaFuncSetAttribute((const void *)K2SL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM));
+    CUDA_TRY(cudaFuncSetAttribute((const void *)K3SL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)K3SP, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)XDS, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XD_SMEM));
     done = 1;
@@ -786,6 +799,8 @@ static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     } else if (use_ldg_kernels()) {
         const int grid = std::max(1, std::min<int>(h->grid_k2, (int)((R.n / 2 + K_BS - 1) / K_BS)));
         k2_kernel<K_NP, K_NE, K_BS, U_K2><<<grid, K_BS, 0, st>>>(a);
+    } else if (R.n < LEAN_ROWS) {
+        K2SL<<<stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T), KSTREAM_THREADS, K2_SMEM, st>>>(a);
     } else {
         K2S<<<stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T), KSTREAM_THREADS, K2_SMEM, st>>>(a);
     }
@@ -800,6 +815,8 @@ static int launch_k3(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     } else if (use_ldg_kernels()) {
         const int grid = std::max(1, std::min<int>(h->grid_k3, (int)((R.n / 2 + K_BS - 1) / K_BS)));
         k3_kernel<K_NP, K_NE, K_BS, U_K3><<<grid, K_BS, 0, st>>>(a);
+    } else if (R.n < LEAN_ROWS) {
+        K3SL<<<stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T), KSTREAM_THREADS, K3_SMEM, st>>>(a);
     } else {
         K3S<<<stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T), KSTREAM_THREADS, K3_SMEM, st>>>(a);
     }

@@ -243,8 +243,9 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
     R.d1.warp_merge(s1);
     PBCG_TS(2);
     if constexpr (EXACT) {
-        if (cta_sacc_publish<4>(S, flags, a.gacc, a.ticket)) {
-            PBCG_TS(3);
+        const bool last = cta_sacc_publish<4>(S, flags, a.gacc, a.ticket);
+        PBCG_TS(3);
+        if (last) {
             last_cta_finish<4>(S, a.gacc, a.ticket, PH_A, a.finalize, sc, a.hist, nullptr, nullptr);
             PBCG_TS(4);
         }

@@ -13,4 +13,4 @@ for rep in range(3):
     ms = S.profile(1)
     c = pb.debug_counters(reset=True).astype(np.int64)
     t = c[8:13]
-    print(f"K2 {ms[0]*1e3:.1f} us; start->tiles {(t[1]-t[0])/1e3:.1f} ->merged {(t[2]-t[1])/1e3:.1f} ->last-CTA {(t[3]-t[2])/1e3:.1f} ->tail done {(t[4]-t[3])/1e3:.1f} us")
+    print(f"K2 {ms[0]*1e3:.1f} us; start->tiles {(t[1]-t[0])/1e3:.1f} ->merged {(t[2]-t[1])/1e3:.1f} ->published {(t[3]-t[2])/1e3:.1f} us (end of kernel = max over CTAs)")
