@@ -412,15 +412,14 @@ __device__ __forceinline__ void deposit_residuals(const double *res, int n, unsi
         if (is_nonzero(res[i])) sacc_deposit(sacc, res[i]);
 }
 
-// int64 sum over the warp with 4 REDUX.SUM on 16-bit limbs (exact mod 2^64;
-// each limb sum is < 32 * 2^16).  Result valid in every lane.
+// Exact warp sum of digit chunks with two REDUX.SUM.  Result valid in every lane.
 __device__ __forceinline__ long long warp_sum_i64(long long v) {
-    const unsigned long long u = (unsigned long long)v;
-    const unsigned long long l0 = __reduce_add_sync(0xFFFFFFFFu, (unsigned)(u & 0xFFFFu));
-    const unsigned long long l1 = __reduce_add_sync(0xFFFFFFFFu, (unsigned)((u >> 16) & 0xFFFFu));
-    const unsigned long long l2 = __reduce_add_sync(0xFFFFFFFFu, (unsigned)((u >> 32) & 0xFFFFu));
-    const unsigned long long l3 = __reduce_add_sync(0xFFFFFFFFu, (unsigned)(u >> 48));
-    return (long long)(l0 + (l1 << 16) + (l2 << 32) + (l3 << 48));
+    // |v| < 2^32 (a digit chunk of sacc_split, possibly negated): a 16-bit
+    // unsigned low limb and a signed high limb; 32 lanes sum each limb
+    // without overflow (2^21), so two REDUX give the exact sum.
+    const unsigned lo = __reduce_add_sync(0xFFFFFFFFu, (unsigned)((unsigned long long)v & 0xFFFFu));
+    const int hi = __reduce_add_sync(0xFFFFFFFFu, (int)(v >> 16));
+    return (long long)hi * 65536 + (long long)lo;
 }
 
 // Deposit one double per lane (zeros allowed) into a shared superaccumulator.
