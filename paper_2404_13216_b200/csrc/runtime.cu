@@ -219,10 +219,10 @@ static constexpr int U_K2 = 2, U_K3 = 2, U_MD4 = 2, U_MD1 = 4;  // row pairs in 
 // packed SELL-P geometry (spmv_sellp_kernel): slices per chunk, slices per
 // consumer warp, ring stages
 #ifndef PBCG_PS_SPS
-#define PBCG_PS_SPS 32
+#define PBCG_PS_SPS 30
 #endif
 #ifndef PBCG_PS_RPW
-#define PBCG_PS_RPW 2
+#define PBCG_PS_RPW 1
 #endif
 #ifndef PBCG_PS_MAXSTAGES
 #define PBCG_PS_MAXSTAGES 8
@@ -607,17 +607,17 @@ static bool multi(const pbcg_handle *h) { return h->V > 1 || h->comm; }
 
 
 // SpMV kernel choice.  Short rows (every row <= 8 nonzeros: stencils) and
-// at least SELLP_MIN_CHUNKS chunks per SM: the TMA kernel on the packed
+// at least SELLP_MIN_SLICES_PER_SM slices per SM: the TMA kernel on the packed
 // SELL-P chunks (spmv_sellp_kernel); smaller short-row matrices: the
 // register-pipelined persistent kernel (no ring to fill); long rows: one row
 // per thread (more warps in flight).  PBCG_SPMV_KERNEL=tma|pipe|plain
 // overrides (A/B runs).
 enum { SPMV_K_PLAIN = 0, SPMV_K_PIPE = 1, SPMV_K_TMA = 2 };
-static constexpr int SELLP_MIN_CHUNKS = 16;
+static constexpr int64_t SELLP_MIN_SLICES_PER_SM = 512;  // C3 (443 per SM): the pipe kernel measured faster
 static int spmv_kind_for(const Rank &R, int nsm) {  // at setup
     if (R.max_len > 8) return SPMV_K_PLAIN;
     const char *e = getenv("PBCG_SPMV_KERNEL");
-    if (!e) return R.nchunks >= (int64_t)SELLP_MIN_CHUNKS * nsm ? SPMV_K_TMA : SPMV_K_PIPE;
+    if (!e) return R.nslices >= SELLP_MIN_SLICES_PER_SM * nsm ? SPMV_K_TMA : SPMV_K_PIPE;
     return strcmp(e, "pipe") == 0 ? SPMV_K_PIPE : strcmp(e, "tma") == 0 ? SPMV_K_TMA : SPMV_K_PLAIN;
 }
 

@@ -625,18 +625,13 @@ __global__ void __launch_bounds__((SPS / RPW + 1) * 32, 1)
         sellp_produce(nchunks, blob, blob_off, smem_raw, STAGE, STAGES, full, empty);
         return;
     }
-    int st = 0;
-    uint32_t ph = 0;
-    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        mbar_wait(&full[st], ph);
+    // gathers of a chunk's RPW slices of this warp (stage st)
+    auto issue = [&](int64_t c, int st, int (&len)[RPW], double (&xv)[RPW][8]) {
         const unsigned char *sb = smem_raw + (size_t)st * STAGE;
         const int32_t *vo = (const int32_t *)sb;
         const int32_t *xo = (const int32_t *)(sb + Geo::HO1);
         const int32_t *rec = (const int32_t *)(sb + Geo::HO3);
-        const double *bv = (const double *)(sb + Geo::H);
-        const int32_t *bx = (const int32_t *)(bv + vo[SPS]);  // explicit column ids after the values
-        int len[RPW];
-        double xv[RPW][8];
+        const int32_t *bx = (const int32_t *)((const double *)(sb + Geo::H) + vo[SPS]);  // explicit ids after values
 #pragma unroll
         for (int u = 0; u < RPW; ++u) {
             const int j = warp * RPW + u;
@@ -656,6 +651,12 @@ __global__ void __launch_bounds__((SPS / RPW + 1) * 32, 1)
                 }
             }
         }
+    };
+    // the folds and stores of those slices, then the stage goes back
+    auto fold = [&](int64_t c, int st, const int (&len)[RPW], const double (&xv)[RPW][8]) {
+        const unsigned char *sb = smem_raw + (size_t)st * STAGE;
+        const int32_t *vo = (const int32_t *)sb;
+        const double *bv = (const double *)(sb + Geo::H);
 #pragma unroll
         for (int u = 0; u < RPW; ++u) {
             const int j = warp * RPW + u;
@@ -678,6 +679,15 @@ __global__ void __launch_bounds__((SPS / RPW + 1) * 32, 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
+    };
+    int st = 0;
+    uint32_t ph = 0;
+    int len[RPW];
+    double xv[RPW][8];
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        mbar_wait(&full[st], ph);
+        issue(c, st, len, xv);
+        fold(c, st, len, xv);
         if (++st == STAGES) {
             st = 0;
             ph ^= 1u;
