@@ -1534,6 +1534,7 @@ extern "C" int pbcg_abi_version(void) { return PBCG_ABI_VERSION; }
 extern "C" int pbcg_profile_iterations(pbcg_handle *h, int32_t k, double *ms) {
     if (!h || !h->started || k < 1 || !ms) return fail(PBCG_EINVAL, "profile: bad arguments");
     if (multi(h)) return fail(PBCG_EINVAL, "profile: single-rank handles only");
+    if (h->method != PBCG_METHOD_PBICGSTAB) return fail(PBCG_EINVAL, "profile: Algorithm 2 only");
     constexpr int NK = 6;  // K2, finalize A, SpMV z, K3, finalize B, SpMV w (serialised here)
     std::vector<cudaEvent_t> ev((size_t)(NK + 1) * k);
     for (auto &e : ev) CUDA_TRY(cudaEventCreate(&e));
@@ -1545,13 +1546,15 @@ extern "C" int pbcg_profile_iterations(pbcg_handle *h, int32_t k, double *ms) {
         cudaEventRecord(e[0], st);
         rc = launch_k2(h, R, 0, st);
         cudaEventRecord(e[1], st);
-        finalize_kernel<4><<<1, 128, 0, st>>>(R.gacc[1], PH_A, R.sc, R.hist, nullptr, nullptr);
+        if (h->dot_mode == PBCG_DOT_PLAIN) rc = reduce_finalize<4>(h, 1, PH_A, st, nullptr, nullptr);
+        else finalize_kernel<4><<<1, 128, 0, st>>>(R.gacc[1], PH_A, R.sc, R.hist, nullptr, nullptr);
         cudaEventRecord(e[2], st);
         if (rc == PBCG_OK) rc = launch_spmv(h, R, SPMV_PLAIN, R.zpad, R.v, nullptr, nullptr, true, st);
         cudaEventRecord(e[3], st);
         if (rc == PBCG_OK) rc = launch_k3(h, R, 0, st);
         cudaEventRecord(e[4], st);
-        finalize_kernel<3><<<1, 128, 0, st>>>(R.gacc[2], PH_B, R.sc, R.hist, nullptr, nullptr);
+        if (rc == PBCG_OK && h->dot_mode == PBCG_DOT_PLAIN) rc = reduce_finalize<3>(h, 2, PH_B, st, nullptr, nullptr);
+        else if (h->dot_mode != PBCG_DOT_PLAIN) finalize_kernel<3><<<1, 128, 0, st>>>(R.gacc[2], PH_B, R.sc, R.hist, nullptr, nullptr);
         cudaEventRecord(e[5], st);
         if (rc == PBCG_OK) rc = launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, true, st);
         cudaEventRecord(e[6], st);
