@@ -181,12 +181,17 @@ int pbicgstab_spmv(pbcg_handle *h, const double *x_local, double *y_local);
  * superaccumulators are allreduced (int64 sum) before the single rounding.
  * result_on_device = 1: `result` (1 double) and `flags` (1 int32, may be
  * NULL) are device pointers, the call is stream-ordered on `stream` and
- * returns PBCG_OK; = 0: host pointers, the call synchronises and returns
- * PBCG_ERANGE / PBCG_ENONFINITE when flagged (result still written).
- * flags: bit 1 (2) = some input is NaN/Inf; otherwise bit 0 (1) = some
- * nonzero product has |fl(x*y)| < 2^-960 or >= 2^1000 (R-9) or the
- * rounded sum overflowed.  When bit 1 is set, bit 0 is unspecified.
- * n_local = 0 gives +0.0. */
+ * returns PBCG_OK; = 0: host pointers, the call synchronises.
+ * flags: bit 1 (2) = some input is NaN/Inf (PBCG_ENONFINITE); otherwise
+ * bit 0 (1) = some nonzero product has |fl(x*y)| < 2^-960 or >= 2^1000
+ * (R-9), i.e. lies outside the fast pass's exact zone.  Single GPU
+ * (h NULL, or one rank without NCCL): such a dot is recomputed by the
+ * full-range pass (exact 106-bit products, accumulator down to 2^-2148;
+ * SURVEY §8(f) NEXT-4), so the result is still the exactly rounded sum and
+ * the call returns PBCG_OK unless that sum overflows binary64 (+-inf,
+ * PBCG_ERANGE).  Distributed handles: PBCG_ERANGE, result unspecified.
+ * When bit 1 is set, bit 0 is unspecified.  n_local = 0 gives +0.0
+ * (SPEC.md l.69). */
 int exdot(pbcg_handle *h, int64_t n_local, const double *x, const double *y, double *result, int32_t *flags,
           int result_on_device, void *stream);
 

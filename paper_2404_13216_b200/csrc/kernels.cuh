@@ -194,6 +194,92 @@ __device__ void phase_finalize(int phase, Scalars *sc, const double *d, unsigned
     if (sc->it >= sc->max_iter) { sc->status = ST_MAXITER; sc->done = 1; }
 }
 
+// ------------------------------------------------------------------------
+// Full-range EXDOT (closes reading R-9 for exdot).  The
+// fast kernels are exact for every product whose TwoProd is exact; a product
+// outside that zone raises FLAG_RANGE.  The last CTA of a flagged standalone
+// dot then recomputes it from the definition: each product formed exactly as
+// the 106-bit integer mx*my times 2^(ex+ey), ex+ey >= -2148, added into an
+// extended superaccumulator of XS_L 32-bit digits with LSB weight 2^-2148
+// (the binary64 product range), and rounded once (RN-even, subnormals,
+// overflow to +-inf).  One CTA: a rare, slow fallback.
+// ------------------------------------------------------------------------
+constexpr int XS_L = 136;  // 4352 bits: 2^-2148 .. 2^2204 (products < 2^2048, sums of < 2^40 of them)
+
+__device__ __forceinline__ void dbl_parts(double v, unsigned long long &m, int &e) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const int E = (int)((b >> 52) & 0x7FF);
+    m = b & 0xFFFFFFFFFFFFFull;
+    if (E) { m |= 1ull << 52; e = E - 1075; } else { e = -1074; }
+}
+
+// all threads of the CTA; returns the exactly rounded sum in every thread
+__device__ double full_range_dot_cta(int64_t n, const double *x, const double *y) {
+    __shared__ unsigned long long S[XS_L];
+    __shared__ double res;
+    for (int i = threadIdx.x; i < XS_L; i += blockDim.x) S[i] = 0ull;
+    __syncthreads();
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+        const double a = x[k], b = y[k];
+        if (a == 0.0 || b == 0.0) continue;
+        unsigned long long ma, mb;
+        int ea, eb;
+        dbl_parts(a, ma, ea);
+        dbl_parts(b, mb, eb);
+        const unsigned long long lo = ma * mb, hi = __umul64hi(ma, mb);  // the 106-bit product
+        const int off = ea + eb + 2148;                                    // >= 0
+        const int w = off >> 5, sh = off & 31;
+        const unsigned long long l2 = lo << sh;
+        const unsigned long long h2 = (hi << sh) | (sh ? (lo >> (64 - sh)) : 0ull);
+        const unsigned long long top = sh ? (hi >> (64 - sh)) : 0ull;
+        const long long d[5] = {(long long)(l2 & 0xFFFFFFFFull), (long long)(l2 >> 32), (long long)(h2 & 0xFFFFFFFFull),
+                                (long long)(h2 >> 32), (long long)top};
+        const bool neg = (a < 0.0) != (b < 0.0);
+#pragma unroll
+        for (int j = 0; j < 5; ++j)
+            if (d[j]) sacc_add_shared(&S[w + j], neg ? -d[j] : d[j]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long *wd = (long long *)S;
+        long long carry = 0;
+        for (int i = 0; i < XS_L - 1; ++i) {  // normalise
+            const long long v = wd[i] + carry;
+            carry = v >> 32;
+            wd[i] = v & 0xFFFFFFFFll;
+        }
+        wd[XS_L - 1] += carry;
+        const bool neg = wd[XS_L - 1] < 0;
+        if (neg) {  // magnitude (two's complement negation over the digits)
+            unsigned long long c = 1;
+            for (int i = 0; i < XS_L; ++i) {
+                const unsigned long long v = (unsigned long long)(~(unsigned)wd[i]) + c;
+                wd[i] = (long long)(v & 0xFFFFFFFFull);
+                c = v >> 32;
+            }
+        }
+        int t = -1;  // highest set bit
+        for (int i = XS_L - 1; i >= 0 && t < 0; --i)
+            if (wd[i]) t = 32 * i + 31 - __clz((unsigned)wd[i]);
+        double r = 0.0;
+        if (t >= 0) {
+            auto bit = [&](int k) -> unsigned { return k < 0 ? 0u : (unsigned)(wd[k >> 5] >> (k & 31)) & 1u; };
+            const int q = max(t - 52, 1074);  // the result's LSB: 53 bits, or the subnormal quantum 2^-1074
+            unsigned long long M = 0;
+            for (int k = t; k >= q; --k) M = (M << 1) | bit(k);
+            const unsigned half = bit(q - 1);
+            bool sticky = false;
+            for (int k = q - 2; k >= 0 && !sticky; --k) sticky = bit(k) != 0u;
+            if (half && (sticky || (M & 1ull))) ++M;
+            r = scalbn((double)M, q - 2148);  // exact, or +inf on overflow
+            if (neg) r = -r;
+        }
+        res = r;
+    }
+    __syncthreads();
+    return res;
+}
+
 // Last CTA of a dot kernel: collect + normalise gacc; then either round and
 // finalise (single rank) or leave normalised words for the allreduce.
 template <int ND>
@@ -219,6 +305,12 @@ __device__ void last_cta_finish(CtaSacc<ND> &S, long long *gacc, unsigned *ticke
             for (int64_t i = threadIdx.x; i < cn; i += blockDim.x)
                 if (!isfinite(cx[i]) || !isfinite(cy[i])) atomicOr(&S.flags, FLAG_NONFINITE);
             __syncthreads();
+            // finite inputs, a product outside the fast zone: the full-range pass (NEXT-4)
+            if (!(S.flags & FLAG_NONFINITE)) {
+                const double r = full_range_dot_cta(cn, cx, cy);
+                if (threadIdx.x == 0) S.rounded[0] = r;
+                __syncthreads();
+            }
         }
         if (threadIdx.x == 0) {
             unsigned f = gflags | (S.flags & (FLAG_RANGE | FLAG_NONFINITE));

@@ -1454,7 +1454,7 @@ extern "C" int exdot(pbcg_handle *h, int64_t n, const double *x, const double *y
     Scratch *S = nullptr;
     RC_TRY(scratch(&S));
     double *out = on_device ? result : S->out;
-    int32_t *ofl = on_device ? flags : S->flags;
+    int32_t *ofl = (on_device && flags) ? flags : S->flags;
     if (!h || (h->V == 1 && !h->comm)) {
         MultiDotArgs a{};
         a.n = n;
@@ -1501,7 +1501,10 @@ extern "C" int exdot(pbcg_handle *h, int64_t n, const double *x, const double *y
     CUDA_TRY(cudaStreamSynchronize(st));
     if (flags) *flags = fl;
     if (fl & FLAG_NONFINITE) return fail(PBCG_ENONFINITE, "exdot: NaN/Inf input");
-    if (fl & FLAG_RANGE) return fail(PBCG_ERANGE, "exdot: product outside the exact zone (R-9) or overflow");
+    const bool full = !h || (h->V == 1 && !h->comm);  // the full-range pass ran: the value is exact
+    if ((fl & FLAG_RANGE) && (!full || !std::isfinite(*result)))
+        return fail(PBCG_ERANGE, full ? "exdot: the exact sum overflows binary64"
+                                      : "exdot: product outside the exact zone (R-9), distributed handle");
     return PBCG_OK;
 }
 

@@ -36,12 +36,14 @@ def check(pb, x, y, handle=None):
     want, wf = oracle.exdot(x, y)
     got, gf = gpu_exdot(pb, x, y, handle)
     # flag contract (include/pbicgstab.h): NONFINITE iff an input is NaN/Inf;
-    # otherwise RANGE iff a nonzero product leaves the exact zone (R-9)
+    # otherwise RANGE iff a nonzero product leaves the fast pass's exact zone (R-9)
     assert bool(wf & oracle.F_NONFINITE) == bool(gf & pb.FLAG_NONFINITE), (wf, gf)
     if not wf & oracle.F_NONFINITE:
         assert bool(wf & oracle.F_RANGE) == bool(gf & pb.FLAG_RANGE), (wf, gf)
-    if wf == 0:
-        assert bits(got) == bits(want), (len(x), got, want)
+        # single GPU: RANGE dots go through the full-range pass (NEXT-4) and
+        # are exact too; the oracle's value is exact over the whole range
+        if wf == 0 or handle is None:
+            assert bits(got) == bits(want), (len(x), got, want, wf)
     return got
 
 
@@ -169,3 +171,40 @@ def test_nccl_single_rank_handle(pb):
     got, f = gpu_exdot(pb, x, y, handle=S)
     assert f == 0 and bits(got) == bits(oracle.exdot(x, y)[0])
     S.close()
+
+
+# ---- full-range EXDOT: products outside the fast zone ----
+
+def test_full_range_underflow_zone(pb):
+    # products below 2^-960: TwoProd is inexact there, the full-range pass is not
+    t = 2.0 ** -540
+    check(pb, [t, t], [t, -t * (1 + 2.0 ** -52)])              # cancels to a tiny exact difference
+    check(pb, [2.0 ** -1074, 2.0 ** -1074], [0.5, 0.5])        # survey example: exact 2^-1074
+    check(pb, [2.0 ** -1074] * 3, [0.5, 0.5, 0.5])             # 1.5 * 2^-1074: tie -> even
+    check(pb, [2.0 ** -600] * 64, [2.0 ** -480] * 64)          # sum lands in the subnormals
+    check(pb, [1.0, 2.0 ** -600], [1.0, 2.0 ** -600])          # far below: rounds away (sticky)
+    check(pb, [2.0 ** -1022, -2.0 ** -1022], [2.0 ** -52, 2.0 ** -53])
+
+
+def test_full_range_overflow_zone(pb):
+    big = 2.0 ** 520
+    check(pb, [big, -big, 3.0], [big, big, 1.0])               # huge products cancel exactly
+    check(pb, [2.0 ** 1000, 2.0 ** 1000], [2.0 ** 23, -2.0 ** 23 + 1])
+    v, f = gpu_exdot(pb, [2.0 ** 1000] * 4, [2.0 ** 23] * 4)  # exact sum 2^1025: overflows to +inf
+    assert v == math.inf and f & pb.FLAG_RANGE
+    assert oracle.exdot([2.0 ** 1000] * 4, [2.0 ** 23] * 4)[0] == math.inf
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_full_range_random(pb, seed):
+    # exponents over the whole binary64 range: products from 2^-2140 to 2^1000
+    rng = np.random.default_rng(seed)
+    n = 3000 + 1000 * seed
+    ex = rng.integers(-1070, 500, n)
+    ey = rng.integers(-1070, 500, n)
+    x = np.ldexp(rng.uniform(1, 2, n) * rng.choice([-1.0, 1.0], n), ex)
+    y = np.ldexp(rng.uniform(1, 2, n) * rng.choice([-1.0, 1.0], n), ey)
+    if seed % 2:  # keep only the small ones: the result is decided far below 2^-960
+        keep = (ex + ey) < -1000
+        x, y = x[keep], y[keep]
+    check(pb, x, y)
