@@ -95,6 +95,12 @@ def _L():
         lib.orc_true_relres.argtypes = [i64, vp, vp, vp, vp, vp, vp]
         lib.orc_bicgstab.restype = i32
         lib.orc_bicgstab.argtypes = [i64, vp, vp, vp, vp, vp, dbl, i32, vp, vp]
+        lib.orc_pbcg_replace.restype = i32
+        lib.orc_pbcg_replace.argtypes = [vp]
+        lib.orc_pbcg_set_rr.restype = None
+        lib.orc_pbcg_set_rr.argtypes = [vp, i32]
+        lib.orc_pbcg_replacements.restype = i32
+        lib.orc_pbcg_replacements.argtypes = [vp]
         lib.orc_bicgstab_dots.restype = i32
         lib.orc_bicgstab_dots.argtypes = [i64, vp, vp, vp, vp, vp, dbl, i32, i32, vp, vp]
         _lib = lib
@@ -176,7 +182,7 @@ class PBiCGStab:
     """Algorithm 2 state machine.  ``b=None`` means b := A*ones (each side
     computes it with its own SpMV); ``x0=None`` means x0 := 0."""
 
-    def __init__(self, A, b=None, x0=None, tol=1e-10, eps=1e-30, max_iter=10000, history=True):
+    def __init__(self, A, b=None, x0=None, tol=1e-10, eps=1e-30, max_iter=10000, history=True, rr_period=0):
         L = _L()
         self.A = A
         self._rp = np.ascontiguousarray(A.row_ptr, np.int32)
@@ -192,6 +198,16 @@ class PBiCGStab:
                                   None if self._x0 is None else _p(self._x0),
                                   float(tol), float(eps), int(max_iter),
                                   None if self.hist is None else _p(self.hist))
+        if rr_period:  # residual replacement every rr_period iterations (NEXT-2, R-21)
+            L.orc_pbcg_set_rr(self._S, int(rr_period))
+
+    def replace(self) -> None:
+        """One residual replacement now: r := b - A x; w := A r; s := A p; z := A s; t := A w."""
+        _L().orc_pbcg_replace(self._S)
+
+    @property
+    def replacements(self) -> int:
+        return _L().orc_pbcg_replacements(self._S)
 
     def step(self) -> int:
         return _L().orc_pbcg_step(self._S)

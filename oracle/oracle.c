@@ -264,6 +264,7 @@ typedef struct {
     int it, status, max_iter;
     double *hist; /* (max_iter+1)*H_COLS, caller-owned, may be NULL */
     double loop_seconds;
+    int rr_period, replacements; /* residual replacement every rr_period iterations (0: never) */
 } orc_pbcg;
 
 int orc_pbcg_size(void) { return (int)sizeof(orc_pbcg); }
@@ -337,6 +338,29 @@ int orc_pbcg_init(orc_pbcg *S, int64_t n, const int32_t *rp, const int32_t *col,
 }
 
 /* One pass of the loop body of Algorithm 2. */
+/* Residual replacement (§2 l.93: "resets the residuals r_i, along
+ * with the auxiliary variables w_i, s_i, and z_i, to their original values
+ * every k iterations"; SPEC.md l.246-249 adds t := A w for consistency).  At
+ * the end of iteration i: r := b - A x (one rounding per entry, as r0),
+ * w := A r, s := A p_i, z := A s, t := A w; scalars untouched.  v is left as
+ * it is (R-21). */
+int orc_pbcg_replace(orc_pbcg *S) {
+    const int64_t n = S->n;
+    double *ax = vnew(n);
+    orc_spmv(n, S->rp, S->col, S->val, S->x, ax);
+    for (int64_t k = 0; k < n; ++k) S->r[k] = S->b[k] - ax[k];
+    free(ax);
+    orc_spmv(n, S->rp, S->col, S->val, S->r, S->w);
+    orc_spmv(n, S->rp, S->col, S->val, S->p, S->s);
+    orc_spmv(n, S->rp, S->col, S->val, S->s, S->z);
+    orc_spmv(n, S->rp, S->col, S->val, S->w, S->t);
+    S->replacements += 1;
+    return ORC_OK;
+}
+
+void orc_pbcg_set_rr(orc_pbcg *S, int period) { S->rr_period = period > 0 ? period : 0; }
+int orc_pbcg_replacements(const orc_pbcg *S) { return S->replacements; }
+
 int orc_pbcg_step(orc_pbcg *S) {
     if (S->status != ORC_RUNNING) return S->status;
     struct timespec t0, t1;
@@ -421,6 +445,9 @@ int orc_pbcg_step(orc_pbcg *S) {
     S->sigma = sigma;
     S->zeta = zeta;
     if (S->it >= S->max_iter) S->status = ORC_MAXITER;
+    /* residual replacement (R-21) after every
+     * rr_period-th completed iteration that leaves the solve running */
+    if (S->status == ORC_RUNNING && S->rr_period > 0 && S->it % S->rr_period == 0) orc_pbcg_replace(S);
 out:
     clock_gettime(CLOCK_MONOTONIC, &t1);
     S->loop_seconds += (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);

@@ -307,3 +307,54 @@ def test_alg1_exact_dots_equals_alg2_solution():
     assert st == oracle.CONVERGED
     assert np.abs(x - S.vec("x")).max() < 1e-6
     assert abs(oracle.true_relres(A, S.vec("b"), x)[0] - S.true_relres()) <= 1e-10
+
+
+# ---- residual replacement ----
+
+def test_replacement_definitional_identities():
+    # right after a replacement: r = b - A x, w = A r, s = A p, z = A s, t = A w, bitwise
+    A = gen.stencil(2, 16, 10.0)
+    S = oracle.PBiCGStab(A, tol=0.0, max_iter=50)
+    S.run(7)
+    S.replace()
+    u = lambda a: np.ascontiguousarray(a).view(np.uint64)
+    b, x = S.vec("b"), S.vec("x")
+    assert np.array_equal(u(S.vec("r")), u(b - oracle.spmv(A, x)))
+    assert np.array_equal(u(S.vec("w")), u(oracle.spmv(A, S.vec("r"))))
+    assert np.array_equal(u(S.vec("s")), u(oracle.spmv(A, S.vec("p"))))
+    assert np.array_equal(u(S.vec("z")), u(oracle.spmv(A, S.vec("s"))))
+    assert np.array_equal(u(S.vec("t")), u(oracle.spmv(A, S.vec("w"))))
+    assert S.replacements == 1
+
+
+def test_replacement_period_semantics():
+    A = gen.stencil(2, 20, 10.0)
+    u = lambda a: np.ascontiguousarray(a).view(np.uint64)
+    ref = oracle.PBiCGStab(A, tol=0.0, max_iter=40)
+    ref.run()
+    # a period beyond the run changes nothing
+    S = oracle.PBiCGStab(A, tol=0.0, max_iter=40, rr_period=41)
+    S.run()
+    assert S.replacements == 0 and np.array_equal(u(S.history()), u(ref.history()))
+    # period k: the first k iterations agree, replacements = floor(40 / k)
+    S = oracle.PBiCGStab(A, tol=0.0, max_iter=40, rr_period=10)
+    S.run()
+    assert S.replacements == 3  # after iterations 10, 20, 30 (not after the last)
+    assert np.array_equal(u(S.history()[:11]), u(ref.history()[:11]))
+
+
+def test_replacement_converges_like_direct_solve():
+    rng = np.random.default_rng(11)
+    for k in range(20):
+        n = int(rng.integers(8, 60))
+        A = gen.dense_as_sparse(n, seed=500 + k, density=0.5)
+        M = np.zeros((n, n))
+        for i in range(n):
+            M[i, A.col[A.row_ptr[i]:A.row_ptr[i + 1]]] = A.val[A.row_ptr[i]:A.row_ptr[i + 1]]
+        b = rng.uniform(-1, 1, n)
+        S = oracle.PBiCGStab(A, b=b, tol=1e-10, max_iter=1000, rr_period=5)
+        S.run()
+        assert S.status == oracle.CONVERGED, (k, S.status)
+        xs = np.linalg.solve(M, b)
+        assert np.linalg.norm(S.vec("x") - xs) <= 1e-6 * np.linalg.norm(xs)
+        assert S.true_relres() <= 10 * 1e-10
