@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define PBCG_ABI_VERSION 3
+#define PBCG_ABI_VERSION 4
 
 /* return codes of every entry point (never an abort across the ABI) */
 enum pbcg_rc {
@@ -110,6 +110,10 @@ typedef struct {
                                  exact dots, four reduction phases per iteration, the arithmetic of the
                                  oracle's orc_bicgstab_dots (R-20); requires PBCG_DOT_EXACT.
                                  history rows: 4 omega, 5 rho, 7 rr, 8 relres, 9 beta, 10 alpha. */
+    int32_t rr_period;        /* Algorithm 2 with residual replacement (p-BiCGStabRR; SURVEY
+                                 §8(f) NEXT-2): after every rr_period-th iteration that leaves the solve
+                                 running, r := b - A x, w := A r, s := A p, z := A s, t := A w (DESIGN.md
+                                 R-21).  0 (default) = never. */
 } pbcg_opts;
 
 enum pbcg_dot_mode { PBCG_DOT_EXACT = 0, PBCG_DOT_PLAIN = 1 };

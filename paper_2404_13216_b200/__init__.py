@@ -56,7 +56,7 @@ METHODS = {"pbicgstab": 0, "bicgstab": 1}
 class _Opts(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("max_iter", ctypes.c_int32), ("breakdown_eps", ctypes.c_double),
                 ("poll_every", ctypes.c_int32), ("use_graphs", ctypes.c_int32), ("dot_mode", ctypes.c_int32),
-                ("method", ctypes.c_int32)]
+                ("method", ctypes.c_int32), ("rr_period", ctypes.c_int32)]
 
 
 class _Result(ctypes.Structure):
@@ -184,9 +184,9 @@ class Solver:
         del rp, ci, va
 
     # -- helpers ------------------------------------------------------------
-    def _opts(self, tol, max_iter, eps, poll_every, use_graphs, dot_mode="exact", method="pbicgstab"):
+    def _opts(self, tol, max_iter, eps, poll_every, use_graphs, dot_mode="exact", method="pbicgstab", rr_period=0):
         return _Opts(float(tol), int(max_iter), float(eps), int(poll_every), int(use_graphs), DOT_MODES[dot_mode],
-                     METHODS[method])
+                     METHODS[method], int(rr_period))
 
     def _vec(self, v, allow_host: bool):
         torch = self.torch
@@ -211,7 +211,7 @@ class Solver:
 
     # -- API ------------------------------------------------------------------
     def solve(self, b, x0=None, tol=1e-10, max_iter=10000, eps=1e-30, poll_every=16, use_graphs=True,
-              dot_mode="exact", method="pbicgstab"):
+              dot_mode="exact", method="pbicgstab", rr_period=0):
         """Solve; b/x0 may be CUDA tensors or host arrays/tensors (host buffers
         go through the library's staging path).  Returns (x, Result) with x on
         the same side as b."""
@@ -226,7 +226,7 @@ class Solver:
             x = x.copy() if isinstance(x, np.ndarray) else x.clone()
         xp = x.ctypes.data if isinstance(x, np.ndarray) else x.data_ptr()
         res = _Result()
-        opts = self._opts(tol, max_iter, eps, poll_every, use_graphs, dot_mode, method)
+        opts = self._opts(tol, max_iter, eps, poll_every, use_graphs, dot_mode, method, rr_period)
         _check(lib().pbicgstab_solve(self._h, ctypes.c_void_p(bp), ctypes.c_void_p(xp), ctypes.byref(opts), ctypes.byref(res)))
         self._sync_out()
         return x, self._result(res)
@@ -236,14 +236,14 @@ class Solver:
         return self.n_global if self._dist.virtual_ranks > 1 else self.n_local
 
     def start(self, b, x0=None, tol=1e-10, max_iter=10000, eps=1e-30, poll_every=16, use_graphs=True,
-              dot_mode="exact", method="pbicgstab"):
+              dot_mode="exact", method="pbicgstab", rr_period=0):
         torch = self.torch
         self._sync_in()
         self._b, bp = self._vec(b, allow_host=True)
         if x0 is None:
             x0 = torch.zeros(self.n_local_vec, dtype=torch.float64, device="cuda")
         self._x0, xp = self._vec(x0, allow_host=True)
-        opts = self._opts(tol, max_iter, eps, poll_every, use_graphs, dot_mode, method)
+        opts = self._opts(tol, max_iter, eps, poll_every, use_graphs, dot_mode, method, rr_period)
         _check(lib().pbicgstab_start(self._h, ctypes.c_void_p(bp), ctypes.c_void_p(xp), ctypes.byref(opts)))
 
     def iterate(self, k: int):

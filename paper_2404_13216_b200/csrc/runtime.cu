@@ -286,6 +286,8 @@ struct pbcg_handle {
     double **vpart = nullptr;     // device array [NPH][V] of plain-mode partial arrays
     int dot_mode = PBCG_DOT_EXACT;  // of the running solve (pbcg_opts.dot_mode)
     int method = PBCG_METHOD_PBICGSTAB;  // of the running solve (pbcg_opts.method)
+    int rr_period = 0;                   // residual replacement period of the running solve (0: never)
+    int64_t it_enq = 0;                  // iterations enqueued since start (host-side count)
     int g_mode = -1;                // dot mode + 2 method the captured graph was built with
     int hist_cap = 10001;
     Scalars *h_sc = nullptr;      // pinned mirror of rank 0's scalars
@@ -1122,6 +1124,7 @@ static void opts_defaults(const pbcg_opts *o, pbcg_opts &e) {
     e.use_graphs = 1;
     e.dot_mode = PBCG_DOT_EXACT;
     e.method = PBCG_METHOD_PBICGSTAB;
+    e.rr_period = 0;
     if (o) {
         e = *o;
         if (!(e.breakdown_eps > 0.0)) e.breakdown_eps = 1e-30;
@@ -1148,9 +1151,14 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
         return fail(PBCG_EINVAL, "start: bad method");
     if (op.method == PBCG_METHOD_BICGSTAB && op.dot_mode != PBCG_DOT_EXACT)
         return fail(PBCG_EINVAL, "start: Algorithm 1 runs with exact dots only");
+    if (op.rr_period < 0) return fail(PBCG_EINVAL, "start: rr_period < 0");
+    if (op.rr_period > 0 && op.method != PBCG_METHOD_PBICGSTAB)
+        return fail(PBCG_EINVAL, "start: residual replacement is defined for Algorithm 2");
     h->max_iter = op.max_iter;
     h->dot_mode = op.dot_mode;
     h->method = op.method;
+    h->rr_period = op.rr_period;
+    h->it_enq = 0;
     Scalars s0{};
     s0.tol = op.tol;
     s0.eps = op.breakdown_eps;
@@ -1300,17 +1308,48 @@ static int capture_chunk(pbcg_handle *h, int iters) {
     return PBCG_OK;
 }
 
+// Residual replacement (NEXT-2, R-21): r := b - A x; w := A r; s := A p;
+// z := A s; t := A w.  The SpMVs are predicated on the device done flag, so a
+// solve that has stopped is left as it is.
+static int enqueue_replacement(pbcg_handle *h) {
+    cudaStream_t st = h->stream;
+    RC_TRY(copy_own_to_pad(h, &Rank::x, 2));
+    RC_TRY(halo(h, 2));
+    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_RESID, R.xpad, R.r, R.b, nullptr, true, st));
+    RC_TRY(copy_own_to_pad(h, &Rank::r, 2));
+    RC_TRY(halo(h, 2));
+    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.xpad, R.w(), nullptr, nullptr, true, st));
+    RC_TRY(copy_own_to_pad(h, &Rank::p, 2));
+    RC_TRY(halo(h, 2));
+    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.xpad, R.s, nullptr, nullptr, true, st));
+    RC_TRY(copy_own_to_pad(h, &Rank::s, 2));
+    RC_TRY(halo(h, 2));
+    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.xpad, R.z(), nullptr, nullptr, true, st));
+    RC_TRY(halo(h, 1));
+    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, true, st));
+    return PBCG_OK;
+}
+
 static int iterate_impl(pbcg_handle *h, int32_t k, int chunk, bool graphs) {
     if (graphs && h->stream == nullptr) graphs = false;  // cannot capture the legacy stream
     while (k > 0) {
-        if (graphs && k >= chunk) {
-            RC_TRY(capture_chunk(h, chunk));
-            CUDA_TRY(cudaGraphLaunch(h->gexec, h->stream));
-            k -= chunk;
-        } else {
-            RC_TRY(enqueue_iteration(h));
-            k -= 1;
+        // iterations until the next replacement boundary (all of k without replacement)
+        int32_t run = k;
+        if (h->rr_period > 0) run = std::min<int64_t>(k, h->rr_period - h->it_enq % h->rr_period);
+        k -= run;
+        while (run > 0) {
+            if (graphs && run >= chunk) {
+                RC_TRY(capture_chunk(h, chunk));
+                CUDA_TRY(cudaGraphLaunch(h->gexec, h->stream));
+                run -= chunk;
+                h->it_enq += chunk;
+            } else {
+                RC_TRY(enqueue_iteration(h));
+                run -= 1;
+                h->it_enq += 1;
+            }
         }
+        if (h->rr_period > 0 && h->it_enq % h->rr_period == 0) RC_TRY(enqueue_replacement(h));
     }
     return PBCG_OK;
 }

@@ -398,3 +398,31 @@ def test_alg1_q_convergence_and_errors(pb):
     S.close()
     st, it, xo, ho = oracle.bicgstab(A, np.array([2.0]), exact_dots=True)
     assert st == oracle.CONVERGED and it == 1 and xo[0] == 1.0
+
+
+# ---------------------------------- residual replacement (NEXT-2, R-21) ---
+
+@pytest.mark.parametrize("name,rr", [("c1", 10), ("small3d", 25), ("rand", 7)])
+def test_residual_replacement_matches_oracle(pb, name, rr):
+    A = {"c1": lambda: gen.make_config("c1_2d64"),
+         "small3d": lambda: gen.stencil(3, 20, 100.0),
+         "rand": lambda: gen.random_banded(20_000, seed=9, band=1500)}[name]()
+    S = solver(pb, A, history_capacity=3001)
+    b = gpu_b(pb, S, A)
+    O = oracle.PBiCGStab(A, b=A.b if A.rhs == "given" else None, tol=1e-10, max_iter=3000, rr_period=rr)
+    O.run()
+    for poll, graphs in ((16, True), (7, True), (1, False)):
+        x, r = S.solve(b, tol=1e-10, max_iter=3000, rr_period=rr, poll_every=poll, use_graphs=graphs)
+        assert_same(O, x.cpu().numpy(), r, S.history(), A)
+    assert O.replacements > 0
+    S.close()
+
+
+def test_residual_replacement_virtual_ranks(pb):
+    A = gen.stencil(3, 20, 100.0)
+    O = oracle.PBiCGStab(A, tol=1e-10, max_iter=3000, rr_period=13)
+    O.run()
+    S = solver(pb, A, history_capacity=3001, virtual_ranks=3)
+    x, r = S.solve(gpu_b(pb, S, A), tol=1e-10, max_iter=3000, rr_period=13)
+    assert_same(O, x.cpu().numpy(), r, S.history(), A)
+    S.close()
