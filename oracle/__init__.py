@@ -276,3 +276,24 @@ def bicgstab(A, b, x0=None, tol=1e-10, max_iter=10000, exact_dots=False):
     st = _L().orc_bicgstab_dots(A.n, _p(rp), _p(col), _p(val), _p(b), _p(x), float(tol), int(max_iter),
                                 int(bool(exact_dots)), ctypes.byref(it), _p(hist))
     return st, it.value, x, hist[: it.value + 1]
+
+
+def jacobi_right(A):
+    """Right Jacobi preconditioning as a column scaling (SURVEY §8(f) NEXT-3,
+    DESIGN.md R-22): A' = A D^-1 with D = diag(A), one RN division per stored
+    entry.  Solve A' y = b with Algorithm 2 (y0 = D x0), then x = D^-1 y (one
+    RN division per entry).  Returns (A', d); A' has the attributes
+    PBiCGStab and spmv use (n, row_ptr, col, val, rhs, b)."""
+    import types
+    rp = np.asarray(A.row_ptr, np.int64)
+    col = np.asarray(A.col, np.int64)
+    val = _f64(A.val)
+    rows = np.repeat(np.arange(A.n), np.diff(rp))
+    d = np.zeros(A.n)
+    on = col == rows
+    d[rows[on]] = val[on]
+    if np.any(d == 0.0):
+        raise ValueError("jacobi: zero or missing diagonal entry")
+    As = types.SimpleNamespace(n=A.n, row_ptr=A.row_ptr, col=A.col, val=val / d[col],
+                               rhs=getattr(A, "rhs", "given"), b=getattr(A, "b", None))
+    return As, d

@@ -358,3 +358,55 @@ def test_replacement_converges_like_direct_solve():
         xs = np.linalg.solve(M, b)
         assert np.linalg.norm(S.vec("x") - xs) <= 1e-6 * np.linalg.norm(xs)
         assert S.true_relres() <= 10 * 1e-10
+
+
+# ---- right Jacobi preconditioning (R-22) ----
+
+def test_jacobi_right_scaling_identities():
+    A = gen.random_banded(3000, seed=4, band=200)
+    As, d = oracle.jacobi_right(A)
+    # A' D = A column by column: the scaled diagonal is exactly 1
+    rows = np.repeat(np.arange(A.n), np.diff(A.row_ptr))
+    on = A.col == rows
+    assert np.all(As.val[on] == 1.0)
+    # one RN division per entry: |A'_ij d_j - A_ij| <= ulp/2 * |A_ij|
+    back = As.val * d[A.col]
+    assert np.all(np.abs(back - A.val) <= np.abs(A.val) * 2.0 ** -52)
+
+
+def test_jacobi_preconditioned_solves():
+    # converges to the direct solution of the ORIGINAL system (x = D^-1 y)
+    rng = np.random.default_rng(21)
+    for k in range(15):
+        n = int(rng.integers(8, 60))
+        A = gen.dense_as_sparse(n, seed=700 + k, density=0.5)
+        M = np.zeros((n, n))
+        for i in range(n):
+            M[i, A.col[A.row_ptr[i]:A.row_ptr[i + 1]]] = A.val[A.row_ptr[i]:A.row_ptr[i + 1]]
+        b = rng.uniform(-1, 1, n)
+        As, d = oracle.jacobi_right(A)
+        S = oracle.PBiCGStab(As, b=b, tol=1e-10, max_iter=1000)
+        S.run()
+        assert S.status == oracle.CONVERGED, (k, S.status)
+        x = S.vec("x") / d
+        xs = np.linalg.solve(M, b)
+        assert np.linalg.norm(x - xs) <= 1e-6 * np.linalg.norm(xs)
+
+
+def test_jacobi_helps_a_badly_scaled_system():
+    # rows scaled over 8 orders of magnitude: Jacobi restores the stencil's
+    # convergence; the unpreconditioned solve needs more iterations
+    A = gen.stencil(2, 24, 10.0)
+    rng = np.random.default_rng(3)
+    rs = 10.0 ** rng.uniform(-4, 4, A.n)
+    rows = np.repeat(np.arange(A.n), np.diff(A.row_ptr))
+    B = gen.CSR(A.n, A.row_ptr, A.col, A.val * rs[rows])
+    b = oracle.spmv(B, np.ones(B.n))
+    S0 = oracle.PBiCGStab(B, b=b, tol=1e-10, max_iter=3000)
+    S0.run()
+    Bs, d = oracle.jacobi_right(B)
+    S1 = oracle.PBiCGStab(Bs, b=b, tol=1e-10, max_iter=3000)
+    S1.run()
+    assert S1.status == oracle.CONVERGED
+    assert S0.status != oracle.CONVERGED or S1.iterations < S0.iterations
+    assert np.abs(S1.vec("x") / d - 1.0).max() < 1e-5
