@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define PBCG_ABI_VERSION 4
+#define PBCG_ABI_VERSION 5
 
 /* return codes of every entry point (never an abort across the ABI) */
 enum pbcg_rc {
@@ -90,7 +90,15 @@ typedef struct {
     int32_t comm_mode;        /* 0 = auto; 1 = use the NCCL dataflow even with nranks == 1 (a 1-rank
                                  communicator: halo no-ops, allreduce = identity) -- test vehicle for the
                                  multi-GPU code path on one GPU */
+    int32_t precond;          /* PBCG_PRECOND_NONE (0) or PBCG_PRECOND_JACOBI (1): right Jacobi
+                                 preconditioning (R-22) folded into the
+                                 matrix at setup: A' = A D^-1 (one RN division per stored entry, D =
+                                 diag(A), zero or missing diagonal -> PBCG_EINVAL); solves A' y = b with
+                                 y0 = D x0 and returns x = D^-1 y.  Residuals (and history) are those of
+                                 A' y = b, i.e. of A x = b in exact arithmetic. */
 } pbcg_dist;
+
+enum pbcg_precond { PBCG_PRECOND_NONE = 0, PBCG_PRECOND_JACOBI = 1 };
 
 /* Solver options (SPEC.md l.214-217 SolverConfig subset). */
 typedef struct {

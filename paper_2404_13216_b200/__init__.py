@@ -44,7 +44,8 @@ class _Csr(ctypes.Structure):
 
 class _Dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("nccl_uid", ctypes.c_void_p),
-                ("virtual_ranks", ctypes.c_int32), ("history_capacity", ctypes.c_int32), ("comm_mode", ctypes.c_int32)]
+                ("virtual_ranks", ctypes.c_int32), ("history_capacity", ctypes.c_int32), ("comm_mode", ctypes.c_int32),
+                ("precond", ctypes.c_int32)]
 
 
 # pbcg_opts.dot_mode: "exact" = ExBLAS dots (reproducible), "plain" = fp64 dots (NEXT-1 comparison arm)
@@ -154,7 +155,7 @@ class Solver:
 
     def __init__(self, row_ptr, col, val, n_global: int, row_begin: int = 0, row_end: int | None = None,
                  rank: int = 0, nranks: int = 1, nccl_uid: bytes | None = None, virtual_ranks: int = 1,
-                 history_capacity: int = 0, stream=None, force_nccl: bool = False):
+                 history_capacity: int = 0, stream=None, force_nccl: bool = False, precond: str = "none"):
         torch = _torch()
         L = lib()
         self.torch = torch
@@ -170,7 +171,8 @@ class Solver:
         if nccl_uid is not None:
             self._uid = ctypes.create_string_buffer(bytes(nccl_uid), 128)
         self._dist = _Dist(rank, nranks, ctypes.cast(self._uid, ctypes.c_void_p) if self._uid is not None else None,
-                           virtual_ranks, history_capacity, 1 if force_nccl else 0)
+                           virtual_ranks, history_capacity, 1 if force_nccl else 0,
+                           {"none": 0, "jacobi": 1}[precond])
         nbytes = ctypes.c_size_t(0)
         torch.cuda.synchronize()
         _check(L.pbicgstab_workspace_size(ctypes.byref(self._csr), ctypes.byref(self._dist), ctypes.byref(nbytes)))

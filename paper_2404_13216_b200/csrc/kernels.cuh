@@ -946,6 +946,38 @@ __global__ void sell_slot_records_kernel(int64_t n, int64_t nslices, const int64
     if (lane == 0 && expl) atomicAdd(n_explicit, expl);
 }
 
+// Right Jacobi preconditioning (NEXT-3, R-22).  d[r] := A(row0 + r, row0 + r)
+// (the stored diagonal; missing or zero -> bad |= 4).
+__global__ void diag_kernel(int64_t n, int64_t row0, const int32_t *rp, const int32_t *col, const double *val,
+                            double *d, int *bad) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        double v = 0.0;
+        for (int32_t k = rp[r]; k < rp[r + 1]; ++k)
+            if ((int64_t)col[k] == row0 + r) v = val[k];
+        d[r] = v;
+        if (v == 0.0) atomicOr(bad, 4);
+    }
+}
+
+// A' = A D^-1 on the sliced ELL: every stored entry divided (RN) by the
+// diagonal of its column, read from the padded x-layout copy of d (halo incl.)
+__global__ void sell_colscale_kernel(int64_t n, const int64_t *slice_off, const int32_t *row_len, double *sval,
+                                     const int32_t *scol, const double *dpad) {
+    for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < n;
+         pos += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t base = slice_off[pos >> 5] + (pos & 31);
+        const int len = row_len[pos];
+        for (int k = 0; k < len; ++k)
+            sval[base + 32 * k] = __ddiv_rn(sval[base + 32 * k], dpad[pos + scol[base + 32 * k]]);
+    }
+}
+
+// y := a op b elementwise (op 0: multiply, 1: divide), RN
+__global__ void vec_muldiv_kernel(int64_t n, const double *a, const double *b, double *y, int op) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = op ? __ddiv_rn(a[i], b[i]) : __dmul_rn(a[i], b[i]);
+}
+
 __global__ void nonfinite_scan_kernel(int64_t n, const double *v, int *bad) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         if (!isfinite(v[i])) atomicOr(bad, 2);

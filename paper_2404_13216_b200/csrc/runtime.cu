@@ -259,6 +259,7 @@ struct Rank {
     bool use_slots = true;
     int64_t nnz = 0, n_explicit = 0;  // stored nonzeros, column ids that stay explicit
     int spmv_kind = 0;                // SpMV kernel (set at setup)
+    double *dg = nullptr;             // Jacobi: diag(A) of this rank's rows
     double *part[NPH] = {};           // plain dot mode: CTA partials [PLAIN_GRID][4] per phase
     double *pdsum = nullptr;          // plain dot mode, NCCL ranks: local sums [NPH][4] (allreduced)
     // packed SELL-P chunks (rows <= 8 nonzeros): blob + byte offsets per chunk
@@ -280,6 +281,7 @@ struct pbcg_handle {
     bool comm = false;                // NCCL communicators exist (nranks > 1, or forced for testing)
     int64_t n_global = 0;
     bool comm_only = false;
+    int precond = PBCG_PRECOND_NONE;  // pbcg_dist.precond
     std::vector<Rank> R;
     ncclComm_t comm_halo = nullptr, comm_red = nullptr;
     long long **vgacc = nullptr;  // device array [NPH][V] of gacc pointers (virtual ranks)
@@ -319,7 +321,7 @@ struct Carver {
     }
 };
 
-static void carve_rank(Carver &C, Rank &R, int hist_cap, bool comm_only) {
+static void carve_rank(Carver &C, Rank &R, int hist_cap, bool comm_only, bool precond) {
     if (!comm_only) {
         R.slice_off = C.take<int64_t>(R.nslices + 16);      // + tail read by the TMA SpMV
         R.row_len = C.take<int32_t>((size_t)R.nslices * 32);  // whole slices, zero past n
@@ -341,6 +343,7 @@ static void carve_rank(Carver &C, Rank &R, int hist_cap, bool comm_only) {
         const size_t nb = (size_t)(R.buf_hi - R.buf_lo) + 2;
         R.zpad = C.take<double>(nb); R.wpad = C.take<double>(nb); R.xpad = C.take<double>(nb);
         R.hist = C.take<double>((size_t)hist_cap * H_COLS);
+        if (precond) R.dg = C.take<double>((size_t)R.n + 2);
     }
     for (int k = 0; k < NPH; ++k) R.gacc[k] = C.take<long long>(GW4);
     for (int k = 0; k < NPH; ++k) R.part[k] = C.take<double>((size_t)PLAIN_GRID * 4);
@@ -475,6 +478,8 @@ static int prepare(pbcg_handle *h, const pbcg_csr_local *A, const pbcg_dist *d, 
     h->rank = d ? d->rank : 0;
     h->V = (d && d->virtual_ranks > 1) ? d->virtual_ranks : 1;
     h->hist_cap = (d && d->history_capacity > 0) ? d->history_capacity : 10001;
+    h->precond = d ? d->precond : PBCG_PRECOND_NONE;
+    if (h->precond != PBCG_PRECOND_NONE && h->precond != PBCG_PRECOND_JACOBI) return fail(PBCG_EINVAL, "bad precond");
     if (h->nranks > 1 && h->V > 1) return fail(PBCG_EINVAL, "virtual ranks need nranks == 1");
     if (h->rank < 0 || h->rank >= h->nranks) return fail(PBCG_EINVAL, "bad rank");
     if (!A) {
@@ -513,7 +518,7 @@ static int prepare(pbcg_handle *h, const pbcg_csr_local *A, const pbcg_dist *d, 
 
 static size_t total_size(pbcg_handle *h) {
     Carver C{nullptr};
-    for (auto &R : h->R) carve_rank(C, R, h->hist_cap, h->comm_only);
+    for (auto &R : h->R) carve_rank(C, R, h->hist_cap, h->comm_only, h->precond == PBCG_PRECOND_JACOBI);
     return carve_handle_extra(C, h) + 256;
 }
 
@@ -932,6 +937,35 @@ static int build_sellp(pbcg_handle *h, Rank &R) {
     return PBCG_OK;
 }
 
+static int copy_own_to_pad(pbcg_handle *h, double *Rank::*src_member, int which);
+
+// Right Jacobi (NEXT-3, R-22): d = diag(A) per rank, d into the padded
+// x layout + halo (the columns' diagonals), then A' = A D^-1 in the SELL.
+static int jacobi_scale(pbcg_handle *h, const pbcg_csr_local *A) {
+    for (auto &R : h->R) {
+        if (R.n == 0) continue;
+        const int32_t *rp = A->row_ptr + (h->V > 1 ? R.rb : 0);
+        const int g = (int)std::min<int64_t>((R.n + 255) / 256, 65535);
+        diag_kernel<<<g, 256, 0, h->stream>>>(R.n, R.rb, rp, A->col_idx, A->values, R.dg, R.bad);
+        CUDA_TRY(cudaGetLastError());
+    }
+    RC_TRY(copy_own_to_pad(h, &Rank::dg, 2));
+    RC_TRY(halo(h, 2));
+    for (auto &R : h->R) {
+        if (R.n == 0) continue;
+        const int g = (int)std::min<int64_t>((R.n + 255) / 256, 65535);
+        sell_colscale_kernel<<<g, 256, 0, h->stream>>>(R.n, R.slice_off, R.row_len, R.sval, R.scol, R.xpad);
+        CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    for (auto &R : h->R) {
+        int bad = 0;
+        CUDA_TRY(cudaMemcpy(&bad, R.bad, sizeof(int), cudaMemcpyDeviceToHost));
+        if (bad & 4) return fail(PBCG_EINVAL, "jacobi: zero or missing diagonal entry");
+    }
+    return PBCG_OK;
+}
+
 extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void *stream, void *workspace,
                                size_t workspace_bytes, pbcg_handle **out) {
     if (!out) return fail(PBCG_EINVAL, "out == NULL");
@@ -987,7 +1021,7 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
     if (!workspace || workspace_bytes < need)
         return fail(PBCG_ENOMEM, "workspace too small: need %zu bytes, got %zu", need, workspace_bytes);
     Carver C{(char *)(((uintptr_t)workspace + 255) & ~uintptr_t(255))};
-    for (auto &R : h->R) carve_rank(C, R, h->hist_cap, h->comm_only);
+    for (auto &R : h->R) carve_rank(C, R, h->hist_cap, h->comm_only, h->precond == PBCG_PRECOND_JACOBI);
     carve_handle_extra(C, h);
     // zero reduction state
     for (auto &R : h->R) {
@@ -1038,6 +1072,7 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
             }
         }
         CUDA_TRY(cudaStreamSynchronize(h->stream));
+        if (h->precond == PBCG_PRECOND_JACOBI) RC_TRY(jacobi_scale(h, A));
         const char *es = getenv("PBCG_SELL_SLOTS");
         for (auto &R : h->R) {
             R.spmv_kind = spmv_kind_for(R, h->nsm);
@@ -1172,6 +1207,13 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
     }
     RC_TRY(scatter_in(h, b, &Rank::b, is_host_ptr(b)));
     RC_TRY(scatter_in(h, x0, &Rank::x, is_host_ptr(x0)));
+    if (h->precond == PBCG_PRECOND_JACOBI)  // y0 := D x0 (R-22)
+        for (auto &R : h->R)
+            if (R.n > 0) {
+                vec_muldiv_kernel<<<(int)std::min<int64_t>((R.n + 255) / 256, 4096), 256, 0, h->stream>>>(
+                    R.n, R.x, R.dg, R.x, 0);
+                CUDA_TRY(cudaGetLastError());
+            }
     for (auto &R : h->R) {
         if (R.n == 0) continue;
         const int grid = (int)std::min<int64_t>((R.n + 255) / 256, 4096);
@@ -1379,7 +1421,14 @@ extern "C" int pbicgstab_finish(pbcg_handle *h, double *x, pbcg_result *res) {
         const bool host = is_host_ptr(x);
         for (auto &R : h->R) {
             const int64_t off = h->V > 1 ? R.rb : 0;
-            CUDA_TRY(cudaMemcpyAsync(x + off, R.x, sizeof(double) * R.n,
+            const double *src = R.x;
+            if (h->precond == PBCG_PRECOND_JACOBI && R.n > 0) {  // x := D^-1 y (R-22)
+                vec_muldiv_kernel<<<(int)std::min<int64_t>((R.n + 255) / 256, 4096), 256, 0, h->stream>>>(
+                    R.n, R.x, R.dg, R.tmp, 1);
+                CUDA_TRY(cudaGetLastError());
+                src = R.tmp;
+            }
+            CUDA_TRY(cudaMemcpyAsync(x + off, src, sizeof(double) * R.n,
                                      host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, h->stream));
         }
     }

@@ -426,3 +426,34 @@ def test_residual_replacement_virtual_ranks(pb):
     x, r = S.solve(gpu_b(pb, S, A), tol=1e-10, max_iter=3000, rr_period=13)
     assert_same(O, x.cpu().numpy(), r, S.history(), A)
     S.close()
+
+
+# ------------------------------ right Jacobi preconditioning (NEXT-3, R-22) ---
+
+@pytest.mark.parametrize("name", ["c1", "rand", "small3d"])
+def test_jacobi_matches_oracle(pb, name):
+    import torch
+    A = {"c1": lambda: gen.make_config("c1_2d64"),
+         "rand": lambda: gen.random_banded(20_000, seed=9, band=1500),
+         "small3d": lambda: gen.stencil(3, 20, 100.0)}[name]()
+    S0 = solver(pb, A)
+    b = gpu_b(pb, S0, A)  # b of the original system
+    S0.close()
+    As, d = oracle.jacobi_right(A)
+    O = oracle.PBiCGStab(As, b=b.cpu().numpy(), tol=1e-10, max_iter=3000)
+    O.run()
+    for V in (1, 3):
+        S = solver(pb, A, history_capacity=3001, virtual_ranks=V, precond="jacobi")
+        x, r = S.solve(b, tol=1e-10, max_iter=3000)
+        assert r.iterations == O.iterations and r.status == O.status
+        assert np.array_equal(u64(S.history()), u64(O.history()))
+        assert np.array_equal(u64(S.vec("x")), u64(O.vec("x")))            # y
+        assert np.array_equal(u64(x.cpu().numpy()), u64(O.vec("x") / d))  # x = D^-1 y
+        S.close()
+
+
+def test_jacobi_rejects_zero_diagonal(pb):
+    A = gen.from_dense(np.array([[0.0, 1.0], [1.0, 2.0]]))
+    with pytest.raises(pb.PbcgError) as e:
+        solver(pb, A, precond="jacobi")
+    assert e.value.rc == 1
