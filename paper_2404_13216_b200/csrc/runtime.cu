@@ -715,7 +715,10 @@ static int multidot(pbcg_handle *h, int ph, int phase, int nd, const double *con
 #endif
 static constexpr int K2_NH = PBCG_K2_FPE;
 static constexpr int K3_NH = PBCG_K3_FPE;
-static constexpr int S_NCW = 7;  // warps per dot group (2*7+1 = 15 warps per CTA)
+#ifndef PBCG_S_NCW
+#define PBCG_S_NCW 7
+#endif
+static constexpr int S_NCW = PBCG_S_NCW;  // warps per dot group (2*7+1 = 15 warps per CTA)
 #ifndef PBCG_X_NCW
 #define PBCG_X_NCW 12
 #endif
