@@ -1,13 +1,14 @@
 // kernels.cuh -- the sm_100a kernels of the p-BiCGStab + ExBLAS hot path.
 //
-//   k2_kernel     Alg. 2 l.70-74 (p,s,z,q,y) + phase-A EXDOT partials
-//                 (q,y),(y,y),(r0,s),(r0,z)              [SURVEY §8(a) a2-a4, a6]
-//   spmv_sell     l.75 v = A z and l.80 t = A w, per-row ordered FMA chain
-//                 on a sliced-ELL (C = 32) layout         [a5, a10; reading R-6]
-//   k3_kernel     l.77-79 (x,r,w) + phase-B EXDOT partials
-//                 (r0,r'),(r0,w'),(r',r')                 [a7-a9, a11]
-//   multidot      generic fused EXDOTs (init, true residual, standalone exdot)
-//   finalize      normalise+round+scalars after a cross-rank allreduce
+//   phase_finalize   the scalar steps of Alg. 2 (and Alg. 1) from rounded dots
+//   multidot         generic fused EXDOTs (init, true residual, Alg. 1 phases)
+//   finalize         normalise + round + scalars (side stream / after allreduce)
+//   spmv_sell[_pipe] l.75 v = A z, l.80 t = A w: per-row ordered FMA chain on a
+//                    sliced-ELL (C = 32) layout         [a5, a10; reading R-6]
+//   a1_*, plain_*    the Alg. 1 and plain-dot arms
+//   setup helpers    SELL conversion, slot records, Jacobi scaling
+// The K2/K3 recurrences + dots, the EXDOT stream and the packed SELL-P SpMV
+// are the TMA kernels of stream.cuh.
 //
 // Every floating-point value op is an explicit __fma_rn/__dmul_rn/__dadd_rn or
 // an IEEE division/sqrt; the library is compiled with -fmad=false.
@@ -340,91 +341,6 @@ struct K2Args {
     double *part;  // plain dot mode: CTA partials [grid][ND] (exact mode: unused)
 };
 
-template <int NP, int NE>
-struct K2Row {
-    ExAcc<NP, NE> dqy, dyy, drs, drz;
-    double be, nom, nal;
-    bool first;
-    template <bool EARLY>
-    __device__ __forceinline__ void row(unsigned long long (*sw)[SACC_L], unsigned &flags, double r, double rh,
-                                        double w, double t, double v, double &p, double &s, double &z, double &q,
-                                        double &y) {
-        if (first) {  // beta_{-1} = 0: exact copies (R-3)
-            p = r; s = w; z = t;
-        } else {
-            p = __fma_rn(be, __fma_rn(nom, s, p), r);  // p := r + beta (p - omega s)   l.70
-            s = __fma_rn(be, __fma_rn(nom, z, s), w);  // s := w + beta (s - omega z)   l.71
-            z = __fma_rn(be, __fma_rn(nom, v, z), t);  // z := t + beta (z - omega v)   l.72
-        }
-        q = __fma_rn(nal, s, r);  // q := r - alpha s  l.73
-        y = __fma_rn(nal, z, w);  // y := w - alpha z  l.74
-        dqy.template add<EARLY>(q, y, sw[0], flags);
-        dyy.template add<EARLY>(y, y, sw[1], flags);
-        drs.template add<EARLY>(rh, s, sw[2], flags);
-        drz.template add<EARLY>(rh, z, sw[3], flags);
-    }
-};
-
-template <int NP, int NE, int BS, int U>
-__global__ void __launch_bounds__(BS) k2_kernel(K2Args a) {
-    __shared__ CtaSacc<4> S;
-    Scalars *sc = a.sc;
-    if (sc->done) return;
-    cta_sacc_zero<4>(S);
-    __syncthreads();
-    K2Row<NP, NE> R;
-    R.first = (sc->it == 0);
-    R.be = sc->beta;
-    R.nom = -sc->omega;
-    R.nal = -sc->alpha;
-    R.dqy.zero(); R.dyy.zero(); R.drs.zero(); R.drz.zero();
-    unsigned flags = 0;
-    const int64_t n = a.n, npair = n >> 1;
-    const int64_t stride = (int64_t)gridDim.x * BS;
-    const double2 *__restrict__ r2 = (const double2 *)a.r, *__restrict__ rh2 = (const double2 *)a.rh,
-                  *__restrict__ w2 = (const double2 *)a.w, *__restrict__ t2 = (const double2 *)a.t,
-                  *__restrict__ v2 = (const double2 *)a.v;
-    double2 *p2 = (double2 *)a.p, *ss2 = (double2 *)a.s, *z2 = (double2 *)a.z, *q2 = (double2 *)a.q,
-            *y2 = (double2 *)a.y;
-    int64_t k = (int64_t)blockIdx.x * BS + threadIdx.x;
-    // full groups: every lane of a warp runs the same trip count (warp-uniform early exits)
-    const int64_t full = (npair / (stride * U)) * (stride * U);
-    for (int64_t base = k; base < full; base += stride * U) {
-        double2 r[U], rh[U], w[U], t[U], p[U], s[U], z[U], v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = base + u * stride;
-            r[u] = __ldcs(r2 + i); rh[u] = __ldg(rh2 + i); w[u] = __ldcs(w2 + i); t[u] = __ldcs(t2 + i);
-            if (!R.first) { p[u] = __ldcs(p2 + i); s[u] = __ldcs(ss2 + i); z[u] = __ldcs(z2 + i); v[u] = __ldcs(v2 + i); }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = base + u * stride;
-            double2 q, y;
-            R.template row<true>(S.w, flags, r[u].x, rh[u].x, w[u].x, t[u].x, v[u].x, p[u].x, s[u].x, z[u].x, q.x, y.x);
-            R.template row<true>(S.w, flags, r[u].y, rh[u].y, w[u].y, t[u].y, v[u].y, p[u].y, s[u].y, z[u].y, q.y, y.y);
-            p2[i] = p[u]; ss2[i] = s[u]; z2[i] = z[u]; q2[i] = q; y2[i] = y;
-        }
-    }
-    for (int64_t i = full + k; i < npair; i += stride) {  // remainder pairs (lanes diverge: no early exit)
-        double2 r = r2[i], rh = rh2[i], w = w2[i], t = t2[i], p, s, z, v, q, y;
-        if (!R.first) { p = p2[i]; s = ss2[i]; z = z2[i]; v = v2[i]; }
-        R.template row<false>(S.w, flags, r.x, rh.x, w.x, t.x, v.x, p.x, s.x, z.x, q.x, y.x);
-        R.template row<false>(S.w, flags, r.y, rh.y, w.y, t.y, v.y, p.y, s.y, z.y, q.y, y.y);
-        p2[i] = p; ss2[i] = s; z2[i] = z; q2[i] = q; y2[i] = y;
-    }
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail row
-        const int64_t i = n - 1;
-        double p = 0, s = 0, z = 0, v = 0, q, y;
-        if (!R.first) { p = a.p[i]; s = a.s[i]; z = a.z[i]; v = a.v[i]; }
-        R.template row<false>(S.w, flags, a.r[i], a.rh[i], a.w[i], a.t[i], v, p, s, z, q, y);
-        a.p[i] = p; a.s[i] = s; a.z[i] = z; a.q[i] = q; a.y[i] = y;
-    }
-    R.dqy.warp_merge(S.w[0]); R.dyy.warp_merge(S.w[1]); R.drs.warp_merge(S.w[2]); R.drz.warp_merge(S.w[3]);
-    if (cta_sacc_publish<4>(S, flags, a.gacc, a.ticket))
-        last_cta_finish<4>(S, a.gacc, a.ticket, PH_A, a.finalize, sc, a.hist, nullptr, nullptr);
-}
-
 // ------------------------------------------------------------------------
 // K3: x,r,w + phase-B partial dots
 // ------------------------------------------------------------------------
@@ -439,78 +355,6 @@ struct K3Args {
     int finalize;
     double *part;  // plain dot mode: CTA partials [grid][ND] (exact mode: unused)
 };
-
-template <int NP, int NE>
-struct K3Row {
-    ExAcc<NP, NE> drr, drw, dnn;
-    double al, om, nal, nom;
-    template <bool EARLY>
-    __device__ __forceinline__ void row(unsigned long long (*sw)[SACC_L], unsigned &flags, double rh, double p,
-                                        double q, double y, double t, double v, double &x, double &r, double &w) {
-        x = __fma_rn(om, q, __fma_rn(al, p, x));    // x := x + alpha p + omega q      l.77
-        r = __fma_rn(nom, y, q);                    // r := q - omega y                l.78
-        w = __fma_rn(nom, __fma_rn(nal, v, t), y);  // w := y - omega (t - alpha v)    l.79
-        drr.template add<EARLY>(rh, r, sw[0], flags);
-        drw.template add<EARLY>(rh, w, sw[1], flags);
-        dnn.template add<EARLY>(r, r, sw[2], flags);
-    }
-};
-
-template <int NP, int NE, int BS, int U>
-__global__ void __launch_bounds__(BS) k3_kernel(K3Args a) {
-    __shared__ CtaSacc<3> S;
-    Scalars *sc = a.sc;
-    if (sc->done) return;
-    cta_sacc_zero<3>(S);
-    __syncthreads();
-    K3Row<NP, NE> R;
-    R.al = sc->alpha;
-    R.om = sc->omega;
-    R.nal = -R.al;
-    R.nom = -R.om;
-    R.drr.zero(); R.drw.zero(); R.dnn.zero();
-    unsigned flags = 0;
-    const int64_t n = a.n, npair = n >> 1;
-    const int64_t stride = (int64_t)gridDim.x * BS;
-    const double2 *__restrict__ rh2 = (const double2 *)a.rh, *__restrict__ p2 = (const double2 *)a.p,
-                  *__restrict__ q2 = (const double2 *)a.q, *__restrict__ y2 = (const double2 *)a.y,
-                  *__restrict__ t2 = (const double2 *)a.t, *__restrict__ v2 = (const double2 *)a.v;
-    double2 *x2 = (double2 *)a.x, *rr2 = (double2 *)a.r, *w2 = (double2 *)a.w;
-    int64_t k = (int64_t)blockIdx.x * BS + threadIdx.x;
-    const int64_t full = (npair / (stride * U)) * (stride * U);
-    for (int64_t base = k; base < full; base += stride * U) {
-        double2 rh[U], p[U], q[U], y[U], t[U], v[U], x[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = base + u * stride;
-            rh[u] = __ldg(rh2 + i); p[u] = __ldcs(p2 + i); q[u] = __ldcs(q2 + i); y[u] = __ldcs(y2 + i);
-            t[u] = __ldcs(t2 + i); v[u] = __ldcs(v2 + i); x[u] = __ldcs(x2 + i);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = base + u * stride;
-            double2 r, w;
-            R.template row<true>(S.w, flags, rh[u].x, p[u].x, q[u].x, y[u].x, t[u].x, v[u].x, x[u].x, r.x, w.x);
-            R.template row<true>(S.w, flags, rh[u].y, p[u].y, q[u].y, y[u].y, t[u].y, v[u].y, x[u].y, r.y, w.y);
-            x2[i] = x[u]; rr2[i] = r; w2[i] = w;
-        }
-    }
-    for (int64_t i = full + k; i < npair; i += stride) {
-        double2 rh = rh2[i], p = p2[i], q = q2[i], y = y2[i], t = t2[i], v = v2[i], x = x2[i], r, w;
-        R.template row<false>(S.w, flags, rh.x, p.x, q.x, y.x, t.x, v.x, x.x, r.x, w.x);
-        R.template row<false>(S.w, flags, rh.y, p.y, q.y, y.y, t.y, v.y, x.y, r.y, w.y);
-        x2[i] = x; rr2[i] = r; w2[i] = w;
-    }
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-        const int64_t i = n - 1;
-        double x = a.x[i], r, w;
-        R.template row<false>(S.w, flags, a.rh[i], a.p[i], a.q[i], a.y[i], a.t[i], a.v[i], x, r, w);
-        a.x[i] = x; a.r[i] = r; a.w[i] = w;
-    }
-    R.drr.warp_merge(S.w[0]); R.drw.warp_merge(S.w[1]); R.dnn.warp_merge(S.w[2]);
-    if (cta_sacc_publish<3>(S, flags, a.gacc, a.ticket))
-        last_cta_finish<3>(S, a.gacc, a.ticket, PH_B, a.finalize, sc, a.hist, nullptr, nullptr);
-}
 
 // ------------------------------------------------------------------------
 // multidot: up to 4 fused EXDOTs (init, true residual, standalone exdot)

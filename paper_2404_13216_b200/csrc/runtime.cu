@@ -214,7 +214,7 @@ static constexpr int NPH = 5;                        // reduction buffers: init,
 static constexpr int K_BS = 256;
 static constexpr int PLAIN_GRID = 1024;  // >= any K2/K3 stream grid (one CTA per SM)
 static constexpr int K_NP = 4, K_NE = 4;             // FPE depth for products / errors (performance only, R-16)
-static constexpr int U_K2 = 2, U_K3 = 2, U_MD4 = 2, U_MD1 = 4;  // row pairs in flight per thread
+static constexpr int U_MD4 = 2, U_MD1 = 4;  // row pairs in flight per thread (multidot)
 
 // packed SELL-P geometry (spmv_sellp_kernel): slices per chunk, slices per
 // consumer warp, ring stages
@@ -293,7 +293,7 @@ struct pbcg_handle {
     int g_mode = -1;                // dot mode + 2 method the captured graph was built with
     int hist_cap = 10001;
     Scalars *h_sc = nullptr;      // pinned mirror of rank 0's scalars
-    int grid_k2 = 0, grid_k3 = 0, grid_md = 0;
+    int grid_md = 0;
     cudaGraphExec_t gexec = nullptr;
     int g_iters = 0;
     cudaEvent_t ev[8] = {};
@@ -765,15 +765,7 @@ static constexpr size_t K3_SMEM = ring_bytes(7, S_NCW, K3_PPT, K3_ST);
 static constexpr size_t XD_SMEM = ring_bytes(2, X_NCW, XD_PPT, XD_ST);
 static constexpr int STREAM_THREADS = (X_NCW + 1) * 32;      // exdot: 1 dot group
 static constexpr int KSTREAM_THREADS = (2 * S_NCW + 1) * 32;  // K2/K3: 2 dot groups
-static int g_kernels_ldg = -1;  // 1: the register-pipelined (LDG) K2/K3 instead of the TMA ring (A/B runs)
 
-static bool use_ldg_kernels() {
-    if (g_kernels_ldg < 0) {
-        const char *e = getenv("PBCG_KERNELS");
-        g_kernels_ldg = (e && strcmp(e, "ldg") == 0) ? 1 : 0;
-    }
-    return g_kernels_ldg == 1;
-}
 
 static int stream_attrs() {
     static int done = 0;
@@ -806,9 +798,6 @@ static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     K2Args a{R.n, R.r, R.rh, R.w(), R.t, R.v, R.p, R.s, R.z(), R.q, R.y, R.sc, R.gacc[1], fin ? R.tickets + 1 : nullptr, R.hist, fin, R.part[1]};
     if (h->dot_mode == PBCG_DOT_PLAIN) {
         K2SP<<<stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T), KSTREAM_THREADS, K2_SMEM, st>>>(a);
-    } else if (use_ldg_kernels()) {
-        const int grid = std::max(1, std::min<int>(h->grid_k2, (int)((R.n / 2 + K_BS - 1) / K_BS)));
-        k2_kernel<K_NP, K_NE, K_BS, U_K2><<<grid, K_BS, 0, st>>>(a);
     } else if (R.n < LEAN_ROWS) {
         K2SL<<<stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T), KSTREAM_THREADS, K2_SMEM, st>>>(a);
     } else {
@@ -822,9 +811,6 @@ static int launch_k3(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     K3Args a{R.n, R.rh, R.p, R.q, R.y, R.t, R.v, R.x, R.r, R.w(), R.sc, R.gacc[2], fin ? R.tickets + 2 : nullptr, R.hist, fin, R.part[2]};
     if (h->dot_mode == PBCG_DOT_PLAIN) {
         K3SP<<<stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T), KSTREAM_THREADS, K3_SMEM, st>>>(a);
-    } else if (use_ldg_kernels()) {
-        const int grid = std::max(1, std::min<int>(h->grid_k3, (int)((R.n / 2 + K_BS - 1) / K_BS)));
-        k3_kernel<K_NP, K_NE, K_BS, U_K3><<<grid, K_BS, 0, st>>>(a);
     } else if (R.n < LEAN_ROWS) {
         K3SL<<<stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T), KSTREAM_THREADS, K3_SMEM, st>>>(a);
     } else {
@@ -1100,8 +1086,6 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
         }
     }
     RC_TRY(stream_attrs());
-    h->grid_k2 = grid_for((const void *)k2_kernel<K_NP, K_NE, K_BS, U_K2>, K_BS, h->nsm);
-    h->grid_k3 = grid_for((const void *)k3_kernel<K_NP, K_NE, K_BS, U_K3>, K_BS, h->nsm);
     h->grid_md = grid_for((const void *)multidot_kernel<4, K_NP, K_NE, K_BS, U_MD4>, K_BS, h->nsm);
     CUDA_TRY(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
     for (auto &e : h->ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
