@@ -58,6 +58,17 @@ __device__ unsigned long long g_dbg[16];
 #define PBCG_TS(k) ((void)0)
 #endif
 
+// Programmatic dependent launch: a kernel launched with programmatic stream
+// serialisation may start while the previous kernel of the stream finishes;
+// griddepcontrol.wait blocks until that kernel has completed and its memory
+// is visible, so everything before it (barrier init, smem zeroing, the CTA
+// getting resident) overlaps the previous kernel's tail.  launch_dependents
+// lets the next such kernel start likewise.  Both are no-ops without PDL.
+__device__ __forceinline__ void pdl_sync() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void two_sum(double a, double b, double &s, double &e) {
     // Knuth TwoSum, 6 DADD, exact for all finite a, b without overflow.
     s = __dadd_rn(a, b);

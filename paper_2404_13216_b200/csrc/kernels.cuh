@@ -503,6 +503,7 @@ __global__ void __launch_bounds__(256) spmv_sell_kernel(SellMat A, const double 
                                                         double *__restrict__ y2, const Scalars *sc) {
     // RPT positions per thread (pos0 + 256*u), loads of all of them in flight
     // before any fold: more memory-level parallelism per thread.
+    pdl_sync();
     if (sc && sc->done) return;
     const int64_t pos0 = (int64_t)blockIdx.x * (256 * RPT) + threadIdx.x;
     int64_t base[RPT];
@@ -570,6 +571,7 @@ template <int MODE, int UNR>
 __global__ void __launch_bounds__(256) spmv_sell_pipe_kernel(SellMat A, const double *__restrict__ x,
                                                              double *__restrict__ y, const double *__restrict__ b,
                                                              double *__restrict__ y2, const Scalars *sc) {
+    pdl_sync();
     if (sc && sc->done) return;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -628,6 +628,32 @@ static int spmv_kind_for(const Rank &R, int nsm) {  // at setup
     return strcmp(e, "pipe") == 0 ? SPMV_K_PIPE : strcmp(e, "tma") == 0 ? SPMV_K_TMA : SPMV_K_PLAIN;
 }
 
+// Launch with programmatic stream serialisation (PDL): the iteration kernels
+// call pdl_sync() after their prologue, so their launch and prologue overlap
+// the previous kernel's tail.  PBCG_PDL=0 turns it off (A/B runs).
+static int g_pdl = -1;
+static bool pdl_on() {
+    if (g_pdl < 0) {
+        const char *e = getenv("PBCG_PDL");
+        g_pdl = (e && e[0] == '0') ? 0 : 1;
+    }
+    return g_pdl == 1;
+}
+template <typename... KArgs, typename... Args>
+static void launch_ex(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, args...);  // errors surface in the caller's cudaGetLastError
+}
+
 template <int MODE>
 static void spmv_dispatch(pbcg_handle *h, const Rank &R, const double *xpad, double *y, const double *b, double *y2,
                           const Scalars *sc, cudaStream_t st) {
@@ -640,17 +666,17 @@ static void spmv_dispatch(pbcg_handle *h, const Rank &R, const double *xpad, dou
         }
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->nsm, R.nchunks));
         const size_t smem = (size_t)R.ps_stages * R.ps_stage + 2 * R.ps_stages * sizeof(uint64_t);
-        k<<<grid, (PS_SPS / PS_RPW + 1) * 32, smem, st>>>(R.n, R.nslices, R.blob, R.blob_off,
-                                                          R.h_perm.empty() ? nullptr : R.perm, xpad, y, b, y2, sc,
-                                                          R.ps_stage, R.ps_stages);
+        launch_ex(k, dim3(grid), dim3((PS_SPS / PS_RPW + 1) * 32), smem, st, R.n, R.nslices,
+                  (const unsigned char *)R.blob, (const int64_t *)R.blob_off,
+                  (const int32_t *)(R.h_perm.empty() ? nullptr : R.perm), xpad, y, b, y2, sc, R.ps_stage, R.ps_stages);
     } else if (R.spmv_kind == SPMV_K_PIPE) {
         static int grid_pipe = 0;
         if (!grid_pipe) grid_pipe = grid_for((const void *)spmv_sell_pipe_kernel<MODE, 8>, 256, h->nsm);
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid_pipe, (R.n + 255) / 256));
-        spmv_sell_pipe_kernel<MODE, 8><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
+        launch_ex(spmv_sell_pipe_kernel<MODE, 8>, dim3(grid), dim3(256), 0, st, R.mat(), xpad, y, b, y2, sc);
     } else {
         const int grid = (int)((R.n + 255) / 256);
-        spmv_sell_kernel<MODE, 8, 1><<<grid, 256, 0, st>>>(R.mat(), xpad, y, b, y2, sc);
+        launch_ex(spmv_sell_kernel<MODE, 8, 1>, dim3(grid), dim3(256), 0, st, R.mat(), xpad, y, b, y2, sc);
     }
 }
 
@@ -797,11 +823,11 @@ static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     // fin = 1: the last CTA rounds and runs the scalar step; fin = 0: publish only (finalize_kernel follows)
     K2Args a{R.n, R.r, R.rh, R.w(), R.t, R.v, R.p, R.s, R.z(), R.q, R.y, R.sc, R.gacc[1], fin ? R.tickets + 1 : nullptr, R.hist, fin, R.part[1]};
     if (h->dot_mode == PBCG_DOT_PLAIN) {
-        K2SP<<<stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T), KSTREAM_THREADS, K2_SMEM, st>>>(a);
+        launch_ex(K2SP, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T)), dim3(KSTREAM_THREADS), K2_SMEM, st, a);
     } else if (R.n < LEAN_ROWS) {
-        K2SL<<<stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T), KSTREAM_THREADS, K2_SMEM, st>>>(a);
+        launch_ex(K2SL, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T)), dim3(KSTREAM_THREADS), K2_SMEM, st, a);
     } else {
-        K2S<<<stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T), KSTREAM_THREADS, K2_SMEM, st>>>(a);
+        launch_ex(K2S, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T)), dim3(KSTREAM_THREADS), K2_SMEM, st, a);
     }
     CUDA_TRY(cudaGetLastError());
     return PBCG_OK;
@@ -810,11 +836,11 @@ static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
 static int launch_k3(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     K3Args a{R.n, R.rh, R.p, R.q, R.y, R.t, R.v, R.x, R.r, R.w(), R.sc, R.gacc[2], fin ? R.tickets + 2 : nullptr, R.hist, fin, R.part[2]};
     if (h->dot_mode == PBCG_DOT_PLAIN) {
-        K3SP<<<stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T), KSTREAM_THREADS, K3_SMEM, st>>>(a);
+        launch_ex(K3SP, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T)), dim3(KSTREAM_THREADS), K3_SMEM, st, a);
     } else if (R.n < LEAN_ROWS) {
-        K3SL<<<stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T), KSTREAM_THREADS, K3_SMEM, st>>>(a);
+        launch_ex(K3SL, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T)), dim3(KSTREAM_THREADS), K3_SMEM, st, a);
     } else {
-        K3S<<<stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T), KSTREAM_THREADS, K3_SMEM, st>>>(a);
+        launch_ex(K3S, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T)), dim3(KSTREAM_THREADS), K3_SMEM, st, a);
     }
     CUDA_TRY(cudaGetLastError());
     return PBCG_OK;

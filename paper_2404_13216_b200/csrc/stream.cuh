@@ -139,8 +139,6 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
     uint64_t *empty = full + STAGES;
     __shared__ CtaSacc<4> S;
     Scalars *sc = a.sc;
-    if (sc->done) return;
-    PBCG_TS(0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     cta_sacc_zero<4>(S);
     if (threadIdx.x == 0) {
@@ -148,6 +146,9 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
         mbar_fence_init();
     }
     __syncthreads();
+    pdl_sync();  // the previous kernel's vectors and scalars are complete from here on
+    if (sc->done) return;
+    PBCG_TS(0);
     const bool first = (sc->it == 0);
     const int64_t n = a.n;
     unsigned flags = 0;
@@ -291,7 +292,6 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
     uint64_t *empty = full + STAGES;
     __shared__ CtaSacc<3> S;
     Scalars *sc = a.sc;
-    if (sc->done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     cta_sacc_zero<3>(S);
     if (threadIdx.x == 0) {
@@ -299,6 +299,8 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
         mbar_fence_init();
     }
     __syncthreads();
+    pdl_sync();
+    if (sc->done) return;
     const int64_t n = a.n;
     unsigned flags = 0;
     K3Op<Acc> R;
@@ -610,7 +612,6 @@ __global__ void __launch_bounds__((SPS / RPW + 1) * 32, 1)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *full = (uint64_t *)(smem_raw + (size_t)STAGES * STAGE);
     uint64_t *empty = full + STAGES;
-    if (sc && sc->done) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -620,6 +621,8 @@ __global__ void __launch_bounds__((SPS / RPW + 1) * 32, 1)
         mbar_fence_init();
     }
     __syncthreads();
+    pdl_sync();
+    if (sc && sc->done) return;
     const int64_t nchunks = (nslices + SPS - 1) / SPS;
     if (warp == NCW) {  // producer warp
         sellp_produce(nchunks, blob, blob_off, smem_raw, STAGE, STAGES, full, empty);
