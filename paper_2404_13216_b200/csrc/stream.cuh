@@ -558,9 +558,14 @@ __global__ void sellp_fill_kernel(int64_t n, int64_t nslices, SellMat A, const u
 // Producer warp of the SELL-P kernels: the blob extents of 32 chunks per
 // batch are loaded one per lane (the next batch in flight during this one),
 // lane 0 moves each chunk of this CTA with ONE bulk copy into the ring.
+// `gate` (all lanes; returns false to abort) runs after the first `prefill`
+// chunks are issued: the SpMV's matrix stream is static, so the producer
+// starts it before waiting on the previous kernel (PDL); on abort it drains
+// the copies it issued, so none is in flight when the CTA exits.
+template <class Gate>
 __device__ __forceinline__ void sellp_produce(int64_t nchunks, const unsigned char *blob, const int64_t *blob_off,
                                               unsigned char *smem, int STAGE, int STAGES, uint64_t *full,
-                                              uint64_t *empty) {
+                                              uint64_t *empty, int prefill, Gate gate) {
     const int lane = threadIdx.x & 31;
     auto extents = [&](int64_t k, int64_t &c, int64_t &o0, int64_t &o1) {
         c = blockIdx.x + k * gridDim.x;
@@ -569,6 +574,16 @@ __device__ __forceinline__ void sellp_produce(int64_t nchunks, const unsigned ch
             o0 = __ldg(&blob_off[c]);
             o1 = __ldg(&blob_off[c + 1]);
         }
+    };
+    int issued = 0;
+    bool gated = false;
+    auto pass_gate = [&]() {
+        gated = true;
+        if (gate()) return true;
+        if (lane == 0)
+            for (int s = 0; s < issued; ++s) mbar_wait(&full[s], 0u);  // first pass only: issued <= STAGES
+        __syncwarp();
+        return false;
     };
     int64_t cc, c0, c1, nc, n0, n1;
     extents(lane, cc, c0, c1);
@@ -580,12 +595,14 @@ __device__ __forceinline__ void sellp_produce(int64_t nchunks, const unsigned ch
         for (int l = 0; l < 32; ++l) {
             const int64_t c = __shfl_sync(0xFFFFFFFFu, cc, l);
             if (c >= nchunks) break;
+            if (!gated && issued == prefill && !pass_gate()) return;
             const int64_t o0 = __shfl_sync(0xFFFFFFFFu, c0, l), o1 = __shfl_sync(0xFFFFFFFFu, c1, l);
             if (lane == 0) {
                 mbar_wait(&empty[st], ph ^ 1u);
                 mbar_expect_tx(&full[st], (uint32_t)(o1 - o0));
                 bulk_g2s(smem + (size_t)st * STAGE, blob + o0, (uint32_t)(o1 - o0), &full[st]);
             }
+            ++issued;
             if (++st == STAGES) {
                 st = 0;
                 ph ^= 1u;
@@ -596,6 +613,7 @@ __device__ __forceinline__ void sellp_produce(int64_t nchunks, const unsigned ch
         c0 = n0;
         c1 = n1;
     }
+    if (!gated) pass_gate();
 }
 
 // STAGE (bytes, multiple of 128) = the largest chunk blob of this matrix,
@@ -621,13 +639,16 @@ __global__ void __launch_bounds__((SPS / RPW + 1) * 32, 1)
         mbar_fence_init();
     }
     __syncthreads();
-    pdl_sync();
-    if (sc && sc->done) return;
     const int64_t nchunks = (nslices + SPS - 1) / SPS;
-    if (warp == NCW) {  // producer warp
-        sellp_produce(nchunks, blob, blob_off, smem_raw, STAGE, STAGES, full, empty);
+    if (warp == NCW) {  // producer warp: the first STAGES chunks go out before the PDL wait
+        sellp_produce(nchunks, blob, blob_off, smem_raw, STAGE, STAGES, full, empty, STAGES, [&]() {
+            pdl_sync();
+            return !(sc && sc->done);
+        });
         return;
     }
+    pdl_sync();
+    if (sc && sc->done) return;
     // gathers of a chunk's RPW slices of this warp (stage st)
     auto issue = [&](int64_t c, int st, int (&len)[RPW], double (&xv)[RPW][8]) {
         const unsigned char *sb = smem_raw + (size_t)st * STAGE;
