@@ -74,10 +74,64 @@ __device__ __forceinline__ void produce(const double *const *src, int nv_act, in
         const int rows = (int)min((int64_t)T, n - r0);
         const uint32_t bytes = (uint32_t)(rows & ~1) * 8u;
         mbar_expect_tx(&full[s], bytes * (uint32_t)nv_act);
-        if (bytes)
-            for (int v = 0; v < nv_act; ++v) bulk_g2s(buf + ((size_t)s * NV + v) * T, src[v] + r0, bytes, &full[s]);
+        if (bytes) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v)  // static indices keep src in registers
+                if (v < nv_act) bulk_g2s(buf + ((size_t)s * NV + v) * T, src[v] + r0, bytes, &full[s]);
+        }
         if (++s == STAGES) { s = 0; ph ^= 1u; }
     }
+}
+
+// The same, for a kernel launched with PDL: the first STAGES tiles of every
+// vector except `late` (the one the immediately preceding kernel writes) are
+// issued before `gate` (which waits on that kernel and returns false to
+// abort); every earlier kernel of the stream has completed by the time this
+// one launches.  The late vector's copies of those tiles follow the gate
+// (their bytes are already in the barrier's expected count); on abort they
+// are issued anyway and drained, so no copy is in flight at exit.
+template <int NV, int T, int STAGES, class Gate>
+__device__ __forceinline__ bool produce_gated(const double *const *src, int nv_act, int late, int64_t n, double *buf,
+                                              uint64_t *full, uint64_t *empty, Gate gate) {
+    const int64_t ntiles = (n + T - 1) / T;
+    int s = 0, issued = 0;
+    uint32_t ph = 0;
+    bool gated = false;
+    auto tile_bytes = [&](int64_t tile) { return (uint32_t)((int)min((int64_t)T, n - tile * T) & ~1) * 8u; };
+    auto open_gate = [&]() {
+        gated = true;
+        const bool ok = gate();
+        if (late >= 0 && late < nv_act) {
+            const double *sl = nullptr;
+#pragma unroll
+            for (int v = 0; v < NV; ++v)  // static indices keep src in registers
+                if (v == late) sl = src[v];
+            for (int k = 0; k < issued; ++k) {  // first pass: ring stage k holds tile blockIdx.x + k gridDim.x
+                const int64_t tile = blockIdx.x + (int64_t)k * gridDim.x;
+                const uint32_t by = tile_bytes(tile);
+                if (by) bulk_g2s(buf + ((size_t)k * NV + late) * T, sl + tile * T, by, &full[k]);
+            }
+        }
+        if (!ok)
+            for (int k = 0; k < issued; ++k) mbar_wait(&full[k], 0u);
+        return ok;
+    };
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        if (!gated && issued == STAGES && !open_gate()) return false;
+        mbar_wait(&empty[s], ph ^ 1u);
+        const int64_t r0 = tile * T;
+        const uint32_t bytes = tile_bytes(tile);
+        mbar_expect_tx(&full[s], bytes * (uint32_t)nv_act);
+        if (bytes) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v)  // static indices keep src in registers
+                if (v < nv_act && (gated || v != late))
+                    bulk_g2s(buf + ((size_t)s * NV + v) * T, src[v] + r0, bytes, &full[s]);
+        }
+        ++issued;
+        if (++s == STAGES) { s = 0; ph ^= 1u; }
+    }
+    return gated ? true : open_gate();
 }
 
 template <int NV, int T, int STAGES>
@@ -146,8 +200,23 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
         mbar_fence_init();
     }
     __syncthreads();
-    pdl_sync();  // the previous kernel's vectors and scalars are complete from here on
-    if (sc->done) return;
+    bool run;
+    if (warp == NCW) {  // producer: r, r^, w, p, s, z, v stream out before the PDL wait; t (the SpMV's) after
+        bool ok = true;
+        if (lane == 0) {
+            const bool first0 = (sc->it == 0);  // written by the previous finalize: complete (event dependency)
+            const double *src[NV] = {a.r, a.rh, a.w, a.t, a.p, a.s, a.z, a.v};
+            ok = produce_gated<NV, T, STAGES>(src, first0 ? 4 : 8, 3, a.n, buf, full, empty, [&]() {
+                pdl_sync();
+                return !sc->done;
+            });
+        }
+        run = __shfl_sync(0xFFFFFFFFu, ok, 0);
+    } else {
+        pdl_sync();  // the previous kernel's vectors and scalars are complete from here on
+        run = !sc->done;
+    }
+    if (!run) return;  // the whole CTA: done is the same value for every thread
     PBCG_TS(0);
     const bool first = (sc->it == 0);
     const int64_t n = a.n;
@@ -165,12 +234,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
         R.d1.slot = warp < NCW ? wg : -1;
     }
     unsigned long long *s0 = S.w[2 * g], *s1 = S.w[2 * g + 1];
-    if (warp == NCW) {
-        if (lane == 0) {
-            const double *src[NV] = {a.r, a.rh, a.w, a.t, a.p, a.s, a.z, a.v};
-            produce<NV, T, STAGES>(src, first ? 4 : 8, n, buf, full, empty);
-        }
-    } else {
+    if (warp < NCW) {  // consumers (the producer warp joins again for the merge)
         const int64_t ntiles = (n + T - 1) / T;
         int st = 0;
         uint32_t ph = 0;
@@ -299,8 +363,22 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
         mbar_fence_init();
     }
     __syncthreads();
-    pdl_sync();
-    if (sc->done) return;
+    bool run;
+    if (warp == NCW) {  // producer: everything but v (the SpMV's) streams out before the PDL wait
+        bool ok = true;
+        if (lane == 0) {
+            const double *src[NV] = {a.rh, a.p, a.q, a.y, a.t, a.v, a.x};
+            ok = produce_gated<NV, T, STAGES>(src, NV, 5, a.n, buf, full, empty, [&]() {
+                pdl_sync();
+                return !sc->done;
+            });
+        }
+        run = __shfl_sync(0xFFFFFFFFu, ok, 0);
+    } else {
+        pdl_sync();
+        run = !sc->done;
+    }
+    if (!run) return;
     const int64_t n = a.n;
     unsigned flags = 0;
     K3Op<Acc> R;
@@ -317,12 +395,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
     }
     // dot slots: (r0,r') -> 0, (r0,w') -> 1, (r',r') -> 2
     unsigned long long *s0 = S.w[g == 0 ? 0 : 1], *s1 = S.w[2];
-    if (warp == NCW) {
-        if (lane == 0) {
-            const double *src[NV] = {a.rh, a.p, a.q, a.y, a.t, a.v, a.x};
-            produce<NV, T, STAGES>(src, NV, n, buf, full, empty);
-        }
-    } else {
+    if (warp < NCW) {  // consumers (the producer warp joins again for the merge)
         const int64_t ntiles = (n + T - 1) / T;
         int st = 0;
         uint32_t ph = 0;
