@@ -676,7 +676,10 @@ static void spmv_dispatch(pbcg_handle *h, const Rank &R, const double *xpad, dou
         launch_ex(spmv_sell_pipe_kernel<MODE, 8>, dim3(grid), dim3(256), 0, st, R.mat(), xpad, y, b, y2, sc);
     } else {
         const int grid = (int)((R.n + 255) / 256);
-        launch_ex(spmv_sell_kernel<MODE, 8, 1>, dim3(grid), dim3(256), 0, st, R.mat(), xpad, y, b, y2, sc);
+#ifndef PBCG_PLAIN_UNR
+#define PBCG_PLAIN_UNR 8
+#endif
+        launch_ex(spmv_sell_kernel<MODE, PBCG_PLAIN_UNR, 1>, dim3(grid), dim3(256), 0, st, R.mat(), xpad, y, b, y2, sc);
     }
 }
 
