@@ -68,6 +68,10 @@ __device__ __forceinline__ void pdl_sync() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// wait only: for a kernel of many waves, an early trigger would let the next
+// (persistent, shared-memory-heavy) kernel occupy SMs its last waves need
+// (measured on C4: 1316 -> 1164 iter/s); dependents start at its exit instead
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ void two_sum(double a, double b, double &s, double &e) {
     // Knuth TwoSum, 6 DADD, exact for all finite a, b without overflow.

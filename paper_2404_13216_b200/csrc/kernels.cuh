@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(256) spmv_sell_kernel(SellMat A, const double 
                                                         double *__restrict__ y2, const Scalars *sc) {
     // RPT positions per thread (pos0 + 256*u), loads of all of them in flight
     // before any fold: more memory-level parallelism per thread.
-    pdl_sync();
+    pdl_wait();
     if (sc && sc->done) return;
     const int64_t pos0 = (int64_t)blockIdx.x * (256 * RPT) + threadIdx.x;
     int64_t base[RPT];

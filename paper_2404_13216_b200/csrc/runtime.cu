@@ -639,8 +639,13 @@ static bool pdl_on() {
     }
     return g_pdl == 1;
 }
+// PDL only where every kernel of the iteration is persistent (one CTA per SM):
+// with the many-wave row-per-thread SpMV (long rows, C4) the early launches
+// cost 10 % (1316 -> 1199 iter/s), so that path launches without it.
+static bool pdl_for(const Rank &R);
 template <typename... KArgs, typename... Args>
-static void launch_ex(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+static void launch_ex(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                      Args... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -648,11 +653,13 @@ static void launch_ex(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, c
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+    at[0].val.programmaticStreamSerializationAllowed = (pdl && pdl_on()) ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, k, args...);  // errors surface in the caller's cudaGetLastError
 }
+
+static bool pdl_for(const Rank &R) { return R.spmv_kind != SPMV_K_PLAIN; }
 
 template <int MODE>
 static void spmv_dispatch(pbcg_handle *h, const Rank &R, const double *xpad, double *y, const double *b, double *y2,
@@ -666,20 +673,22 @@ static void spmv_dispatch(pbcg_handle *h, const Rank &R, const double *xpad, dou
         }
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->nsm, R.nchunks));
         const size_t smem = (size_t)R.ps_stages * R.ps_stage + 2 * R.ps_stages * sizeof(uint64_t);
-        launch_ex(k, dim3(grid), dim3((PS_SPS / PS_RPW + 1) * 32), smem, st, R.n, R.nslices,
+        launch_ex(k, dim3(grid), dim3((PS_SPS / PS_RPW + 1) * 32), smem, st, pdl_for(R), R.n, R.nslices,
                   (const unsigned char *)R.blob, (const int64_t *)R.blob_off,
                   (const int32_t *)(R.h_perm.empty() ? nullptr : R.perm), xpad, y, b, y2, sc, R.ps_stage, R.ps_stages);
     } else if (R.spmv_kind == SPMV_K_PIPE) {
         static int grid_pipe = 0;
         if (!grid_pipe) grid_pipe = grid_for((const void *)spmv_sell_pipe_kernel<MODE, 8>, 256, h->nsm);
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid_pipe, (R.n + 255) / 256));
-        launch_ex(spmv_sell_pipe_kernel<MODE, 8>, dim3(grid), dim3(256), 0, st, R.mat(), xpad, y, b, y2, sc);
+        launch_ex(spmv_sell_pipe_kernel<MODE, 8>, dim3(grid), dim3(256), 0, st, pdl_for(R), R.mat(), xpad, y, b, y2,
+                  sc);
     } else {
         const int grid = (int)((R.n + 255) / 256);
 #ifndef PBCG_PLAIN_UNR
 #define PBCG_PLAIN_UNR 8
 #endif
-        launch_ex(spmv_sell_kernel<MODE, PBCG_PLAIN_UNR, 1>, dim3(grid), dim3(256), 0, st, R.mat(), xpad, y, b, y2, sc);
+        launch_ex(spmv_sell_kernel<MODE, PBCG_PLAIN_UNR, 1>, dim3(grid), dim3(256), 0, st, false, R.mat(), xpad, y, b,
+                  y2, sc);
     }
 }
 
@@ -826,11 +835,14 @@ static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     // fin = 1: the last CTA rounds and runs the scalar step; fin = 0: publish only (finalize_kernel follows)
     K2Args a{R.n, R.r, R.rh, R.w(), R.t, R.v, R.p, R.s, R.z(), R.q, R.y, R.sc, R.gacc[1], fin ? R.tickets + 1 : nullptr, R.hist, fin, R.part[1]};
     if (h->dot_mode == PBCG_DOT_PLAIN) {
-        launch_ex(K2SP, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T)), dim3(KSTREAM_THREADS), K2_SMEM, st, a);
+        launch_ex(K2SP, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T)), dim3(KSTREAM_THREADS), K2_SMEM, st,
+                  pdl_for(R), a);
     } else if (R.n < LEAN_ROWS) {
-        launch_ex(K2SL, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T)), dim3(KSTREAM_THREADS), K2_SMEM, st, a);
+        launch_ex(K2SL, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T)), dim3(KSTREAM_THREADS), K2_SMEM, st,
+                  pdl_for(R), a);
     } else {
-        launch_ex(K2S, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T)), dim3(KSTREAM_THREADS), K2_SMEM, st, a);
+        launch_ex(K2S, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T)), dim3(KSTREAM_THREADS), K2_SMEM, st,
+                  pdl_for(R), a);
     }
     CUDA_TRY(cudaGetLastError());
     return PBCG_OK;
@@ -839,11 +851,14 @@ static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
 static int launch_k3(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     K3Args a{R.n, R.rh, R.p, R.q, R.y, R.t, R.v, R.x, R.r, R.w(), R.sc, R.gacc[2], fin ? R.tickets + 2 : nullptr, R.hist, fin, R.part[2]};
     if (h->dot_mode == PBCG_DOT_PLAIN) {
-        launch_ex(K3SP, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T)), dim3(KSTREAM_THREADS), K3_SMEM, st, a);
+        launch_ex(K3SP, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T)), dim3(KSTREAM_THREADS), K3_SMEM, st,
+                  pdl_for(R), a);
     } else if (R.n < LEAN_ROWS) {
-        launch_ex(K3SL, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T)), dim3(KSTREAM_THREADS), K3_SMEM, st, a);
+        launch_ex(K3SL, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T)), dim3(KSTREAM_THREADS), K3_SMEM, st,
+                  pdl_for(R), a);
     } else {
-        launch_ex(K3S, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T)), dim3(KSTREAM_THREADS), K3_SMEM, st, a);
+        launch_ex(K3S, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T)), dim3(KSTREAM_THREADS), K3_SMEM, st,
+                  pdl_for(R), a);
     }
     CUDA_TRY(cudaGetLastError());
     return PBCG_OK;
