@@ -620,7 +620,7 @@ static bool multi(const pbcg_handle *h) { return h->V > 1 || h->comm; }
 // per thread (more warps in flight).  PBCG_SPMV_KERNEL=tma|pipe|plain
 // overrides (A/B runs).
 enum { SPMV_K_PLAIN = 0, SPMV_K_PIPE = 1, SPMV_K_TMA = 2 };
-static constexpr int64_t SELLP_MIN_SLICES_PER_SM = 512;  // C3 (443 per SM): the pipe kernel measured faster
+static constexpr int64_t SELLP_MIN_SLICES_PER_SM = 32;  // C3 (443/SM): TMA 7.17K vs 6.18K iter/s; C1 (1/SM): pipe
 static int spmv_kind_for(const Rank &R, int nsm) {  // at setup
     if (R.max_len > 8) return SPMV_K_PLAIN;
     const char *e = getenv("PBCG_SPMV_KERNEL");
