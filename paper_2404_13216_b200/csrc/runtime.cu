@@ -704,6 +704,7 @@ static int launch_spmv(pbcg_handle *h, Rank &R, int mode, const double *xpad, do
 
 // up-to-4 fused EXDOTs over every rank's rows (phase PH_INIT / PH_TRUE)
 static int launch_xd1(pbcg_handle *h, const MultiDotArgs &a);
+static int launch_xd2(pbcg_handle *h, const MultiDotArgs &a);
 
 static int multidot(pbcg_handle *h, int ph, int phase, int nd, const double *const *xs_per_rank[4],
                     const double *const *ys_per_rank[4]) {
@@ -723,8 +724,11 @@ static int multidot(pbcg_handle *h, int ph, int phase, int nd, const double *con
         a.phase = phase;
         a.finalize = fin;
         const int grid = std::max(1, std::min<int>(h->grid_md, (int)((R.n / 2 + K_BS - 1) / K_BS)));
-        if (nd == 1 && R.n > 0 && ((((uintptr_t)a.x[0]) | ((uintptr_t)a.y[0])) & 15) == 0) {
+        const bool aligned = ((((uintptr_t)a.x[0]) | ((uintptr_t)a.y[0])) & 15) == 0;
+        if (nd == 1 && R.n > 0 && aligned) {
             RC_TRY(launch_xd1(h, a));  // one dot over aligned vectors: the TMA-streamed EXDOT kernel
+        } else if (nd == 2 && R.n > 0 && aligned && a.x[1] == a.y[0] && a.y[1] == a.y[0]) {
+            RC_TRY(launch_xd2(h, a));  // (x,y), (y,y): the two-dot stream kernel
         } else if (nd == 4) multidot_kernel<4, K_NP, K_NE, K_BS, U_MD4><<<grid, K_BS, 0, h->stream>>>(a);
         else if (nd == 2) multidot_kernel<2, K_NP, K_NE, K_BS, U_MD4><<<grid, K_BS, 0, h->stream>>>(a);
         else multidot_kernel<1, K_NP, K_NE, K_BS, U_MD1><<<grid, K_BS, 0, h->stream>>>(a);
@@ -795,6 +799,7 @@ static constexpr int64_t LEAN_ROWS = 8 << 20;
 #define K2SP k2_stream<K2_NH, K2_NC, S_NCW, K2_PPT, K2_ST, K2_NHE, false>
 #define K3SP k3_stream<K3_NH, K3_NC, S_NCW, K3_PPT, K3_ST, K3_NHE, false>
 #define XDS exdot_stream<X_NH, X_NL, X_NCW, XD_PPT, XD_ST>
+#define XDS2 exdot_stream<X_NH, X_NL, X_NCW, XD_PPT, XD_ST, 2>
 static constexpr size_t ring_bytes(int nv, int ncw, int ppt, int stages) {
     return sizeof(double) * (size_t)stages * nv * (2 * ncw * 32 * ppt) + 2 * sizeof(uint64_t) * stages;
 }
@@ -815,6 +820,7 @@ static int stream_attrs() {
     CUDA_TRY(cudaFuncSetAttribute((const void *)K3SL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)K3SP, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)XDS, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XD_SMEM));
+    CUDA_TRY(cudaFuncSetAttribute((const void *)XDS2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XD_SMEM));
     done = 1;
     return PBCG_OK;
 }
@@ -827,6 +833,13 @@ static int stream_grid(pbcg_handle *h, int64_t n, int rows_per_tile) {
 static int launch_xd1(pbcg_handle *h, const MultiDotArgs &a) {
     RC_TRY(stream_attrs());
     XDS<<<stream_grid(h, a.n, TileGeo<X_NCW, XD_PPT>::T), STREAM_THREADS, XD_SMEM, h->stream>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    return PBCG_OK;
+}
+
+static int launch_xd2(pbcg_handle *h, const MultiDotArgs &a) {  // (x,y), (y,y)
+    RC_TRY(stream_attrs());
+    XDS2<<<stream_grid(h, a.n, TileGeo<X_NCW, XD_PPT>::T), STREAM_THREADS, XD_SMEM, h->stream>>>(a);
     CUDA_TRY(cudaGetLastError());
     return PBCG_OK;
 }

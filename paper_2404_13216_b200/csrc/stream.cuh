@@ -474,18 +474,22 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
 // ---------------------------------------------------------------------------
 // Standalone EXDOT (one dot, x and y 16-byte aligned)
 // ---------------------------------------------------------------------------
-template <int NH, int NL, int NCW, int PPT, int STAGES>
+// ND = 2: the dots (x,y) and (y,y) over the same two streams (Alg. 1's
+// (q,y),(y,y) and (r0,r),(r,r) phases); products alternate between the two
+// accumulators inside one batched cascade.
+template <int NH, int NL, int NCW, int PPT, int STAGES, int ND = 1>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a) {
+    static_assert(ND == 1 || ND == 2, "ND is 1 or 2");
     constexpr int NV = 2;
     constexpr int T = TileGeo<NCW, PPT>::T;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *buf = (double *)smem_raw;
     uint64_t *full = (uint64_t *)(buf + (size_t)STAGES * NV * T);
     uint64_t *empty = full + STAGES;
-    __shared__ CtaSacc<1> S;
+    __shared__ CtaSacc<ND> S;
     if (a.sc && a.sc->done && a.phase != PH_TRUE) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    cta_sacc_zero<1>(S);
+    cta_sacc_zero<ND>(S);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NCW); }
         mbar_fence_init();
@@ -493,8 +497,10 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a
     __syncthreads();
     const int64_t n = a.n;
     unsigned flags = 0;
-    ExAccT<NH, NL> acc;
+    ExAccT<NH, NL> acc, acc2;
     acc.zero();
+    acc2.zero();
+    unsigned long long *s1 = S.w[ND - 1];
     if (warp == NCW) {
         if (lane == 0) {
             const double *src[NV] = {a.x[0], a.y[0]};
@@ -521,15 +527,28 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);  // operands are in registers: free the slot early
+                if (ND == 1) {
 #pragma unroll
-                for (int u = 0; u < PPT; u += 2) {
-                    Prod P[4];
+                    for (int u = 0; u < PPT; u += 2) {
+                        Prod P[4];
 #pragma unroll
-                    for (int h = 0; h < 2 && u + h < PPT; ++h) {
-                        P[2 * h] = acc.prep(xv[u + h].x, yv[u + h].x, is_zero(xv[u + h].x) | is_zero(yv[u + h].x), flags);
-                        P[2 * h + 1] = acc.prep(xv[u + h].y, yv[u + h].y, is_zero(xv[u + h].y) | is_zero(yv[u + h].y), flags);
+                        for (int h = 0; h < 2 && u + h < PPT; ++h) {
+                            P[2 * h] = acc.prep(xv[u + h].x, yv[u + h].x, is_zero(xv[u + h].x) | is_zero(yv[u + h].x), flags);
+                            P[2 * h + 1] = acc.prep(xv[u + h].y, yv[u + h].y, is_zero(xv[u + h].y) | is_zero(yv[u + h].y), flags);
+                        }
+                        cascade_batch<4, false>(acc, acc, P, S.w[0], S.w[0]);
                     }
-                    cascade_batch<4, false>(acc, acc, P, S.w[0], S.w[0]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < PPT; ++u) {
+                        Prod P[4];  // (x,y) -> acc, (y,y) -> acc2, alternating
+                        const bool zy0 = is_zero(yv[u].x), zy1 = is_zero(yv[u].y);
+                        P[0] = acc.prep(xv[u].x, yv[u].x, is_zero(xv[u].x) | zy0, flags);
+                        P[1] = acc2.prep(yv[u].x, yv[u].x, zy0, flags);
+                        P[2] = acc.prep(xv[u].y, yv[u].y, is_zero(xv[u].y) | zy1, flags);
+                        P[3] = acc2.prep(yv[u].y, yv[u].y, zy1, flags);
+                        cascade_batch<4, true>(acc, acc2, P, S.w[0], s1);
+                    }
                 }
             } else {
 #pragma unroll
@@ -541,6 +560,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a
                         const bool m = lr < rows_even;
                         const double xv = m ? B[lr] : a.x[0][r0 + lr], yv = m ? B[T + lr] : a.y[0][r0 + lr];
                         cascade_one(acc, acc.prep(xv, yv, is_zero(xv) | is_zero(yv), flags), S.w[0]);
+                        if (ND == 2) cascade_one(acc2, acc2.prep(yv, yv, is_zero(yv), flags), s1);
                     }
                 }
                 __syncwarp();
@@ -551,9 +571,10 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a
     }
     __syncwarp();
     acc.warp_merge(S.w[0]);
-    if (cta_sacc_publish<1>(S, flags, a.gacc, a.ticket))
-        last_cta_finish<1>(S, a.gacc, a.ticket, a.phase, a.finalize, a.sc, a.hist, a.out, a.out_flags,
-                           a.phase == PH_EXDOT ? a.x[0] : nullptr, a.y[0], a.n);
+    if (ND == 2) acc2.warp_merge(s1);
+    if (cta_sacc_publish<ND>(S, flags, a.gacc, a.ticket))
+        last_cta_finish<ND>(S, a.gacc, a.ticket, a.phase, a.finalize, a.sc, a.hist, a.out, a.out_flags,
+                            (ND == 1 && a.phase == PH_EXDOT) ? a.x[0] : nullptr, a.y[0], a.n);
 }
 
 // ---------------------------------------------------------------------------
