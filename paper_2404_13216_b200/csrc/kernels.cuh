@@ -489,6 +489,9 @@ struct SellMat {
     // never read.  Slots k >= 15 are always explicit.  Null: every slot
     // explicit.  The same nonzeros are folded in the same order (R-6).
     const int32_t *slot_rec;
+    // positions [p0, p1) this launch folds (interior / boundary split of a
+    // rank's rows under multi-rank halo overlap; default: all rows)
+    int64_t p0, p1;
 };
 
 static constexpr int SELL_RS = 16, SELL_MASK = 15;
@@ -505,7 +508,7 @@ __global__ void __launch_bounds__(256) spmv_sell_kernel(SellMat A, const double 
     // before any fold: more memory-level parallelism per thread.
     pdl_wait();
     if (sc && sc->done) return;
-    const int64_t pos0 = (int64_t)blockIdx.x * (256 * RPT) + threadIdx.x;
+    const int64_t pos0 = A.p0 + (int64_t)blockIdx.x * (256 * RPT) + threadIdx.x;
     int64_t base[RPT];
     int len[RPT], lmax = 0;
 #pragma unroll
@@ -513,7 +516,7 @@ __global__ void __launch_bounds__(256) spmv_sell_kernel(SellMat A, const double 
         const int64_t pos = pos0 + 256 * u;
         base[u] = 0;
         len[u] = 0;
-        if (pos < A.n) {
+        if (pos < A.p1) {
             base[u] = __ldg(&A.slice_off[pos >> 5]) + (pos & 31);
             len[u] = __ldg(&A.row_len[pos]);
         }
@@ -547,7 +550,7 @@ __global__ void __launch_bounds__(256) spmv_sell_kernel(SellMat A, const double 
 #pragma unroll
     for (int u = 0; u < RPT; ++u) {
         const int64_t pos = pos0 + 256 * u;
-        if (pos >= A.n) continue;
+        if (pos >= A.p1) continue;
         const int64_t row = A.perm ? (int64_t)__ldg(&A.perm[pos]) : pos;
         if (MODE == SPMV_PLAIN) {
             y[row] = acc[u];
@@ -574,12 +577,12 @@ __global__ void __launch_bounds__(256) spmv_sell_pipe_kernel(SellMat A, const do
     pdl_sync();
     if (sc && sc->done) return;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t pos = A.p0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     // descriptor of a position: slot-0 offset and row length (0 past the end)
     auto desc = [&](int64_t p, int64_t &base, int &len) {
         base = 0;
         len = 0;
-        if (p < A.n) {
+        if (p < A.p1) {
             base = __ldg(&A.slice_off[p >> 5]) + (p & 31);
             len = __ldg(&A.row_len[p]);
         }
@@ -599,7 +602,7 @@ __global__ void __launch_bounds__(256) spmv_sell_pipe_kernel(SellMat A, const do
     double v[UNR], vn[UNR], xv[UNR];
     int c[UNR], cn[UNR];
     load_vc(cbase, 0, clen, v, c);
-    while (pos < A.n) {
+    while (pos < A.p1) {
         double acc = 0.0;
         for (int k0 = 0;; k0 += UNR) {
 #pragma unroll
@@ -822,6 +825,27 @@ __global__ void sell_colscale_kernel(int64_t n, const int64_t *slice_off, const 
 __global__ void vec_muldiv_kernel(int64_t n, const double *a, const double *b, double *y, int op) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         y[i] = op ? __ddiv_rn(a[i], b[i]) : __dmul_rn(a[i], b[i]);
+}
+
+// Multi-rank halo overlap: flag[s] = 1 if some stored entry of slice s reads
+// an x-buffer entry outside this rank's own rows [own_lo, own_hi) (a halo
+// entry), so the slice must wait for the exchange; one warp per slice.
+__global__ void sell_halo_flags_kernel(int64_t n, int64_t nslices, const int64_t *slice_off, const int32_t *row_len,
+                                       const int32_t *scol, int64_t own_lo, int64_t own_hi, uint8_t *flag) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < nslices; sl += nw) {
+        const int64_t pos = sl * 32 + lane;
+        const int len = pos < n ? row_len[pos] : 0;
+        const int64_t so = slice_off[sl];
+        bool out = false;
+        for (int k = 0; k < len; ++k) {
+            const int64_t c = pos + scol[so + 32 * k + lane];  // pos-relative column
+            out |= (c < own_lo) | (c >= own_hi);
+        }
+        const unsigned any = __ballot_sync(0xFFFFFFFFu, out);
+        if (lane == 0) flag[sl] = any ? 1 : 0;
+    }
 }
 
 __global__ void nonfinite_scan_kernel(int64_t n, const double *v, int *bad) {

@@ -268,15 +268,19 @@ struct Rank {
     int64_t *blob_off = nullptr;
     uint8_t *nexp = nullptr;
     int ps_stage = 0, ps_stages = 0;  // ring geometry of spmv_sellp_kernel (bytes per stage, stages)
-    SellMat mat() const {
+    // multi-rank halo overlap: the interior units [in_lo, in_hi) (chunks for
+    // the SELL-P kernel, slices otherwise) read no halo entry
+    bool split = false;
+    int64_t in_lo = 0, in_hi = 0;
+    SellMat mat(int64_t p0 = 0, int64_t p1 = -1) const {
         return SellMat{n, slice_off, row_len, sval, scol, h_perm.empty() ? nullptr : perm,
-                       use_slots ? slot_rec : nullptr};
+                       use_slots ? slot_rec : nullptr, p0, p1 < 0 ? n : std::min<int64_t>(p1, n)};
     }
 };
 
 struct pbcg_handle {
     int dev = 0, nsm = 148;
-    cudaStream_t stream = nullptr, side = nullptr;
+    cudaStream_t stream = nullptr, side = nullptr, cstream = nullptr;  // cstream: halo exchange (overlap)
     int nranks = 1, rank = 0, V = 1;  // real ranks, this rank, virtual ranks
     bool comm = false;                // NCCL communicators exist (nranks > 1, or forced for testing)
     int64_t n_global = 0;
@@ -297,6 +301,7 @@ struct pbcg_handle {
     cudaGraphExec_t gexec = nullptr;
     int g_iters = 0;
     cudaEvent_t ev[8] = {};
+    cudaEvent_t evh[4] = {};  // halo-overlap fork/join (multi-rank)
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     bool started = false;
     int max_iter = 0;
@@ -543,7 +548,8 @@ static int grid_for(const void *kern, int bs, int nsm, size_t smem = 0) {
 // padded buffer selector: 0 = z, 1 = w, 2 = x scratch
 static double *padbuf(Rank &R, int which) { return which == 0 ? R.zpad : which == 1 ? R.wpad : R.xpad; }
 
-static int halo(pbcg_handle *h, int which) {
+static int halo(pbcg_handle *h, int which, cudaStream_t st = nullptr) {
+    if (!st) st = h->stream;
     const int P = (int)h->R.size();
     if (h->V > 1) {
         for (int me = 0; me < P; ++me) {
@@ -553,7 +559,7 @@ static int halo(pbcg_handle *h, int which) {
                 if (hi <= lo) continue;
                 Rank &Q = h->R[q];
                 CUDA_TRY(cudaMemcpyAsync(padbuf(R, which) + (lo - R.buf_lo), padbuf(Q, which) + (lo - Q.buf_lo),
-                                         sizeof(double) * (hi - lo), cudaMemcpyDeviceToDevice, h->stream));
+                                         sizeof(double) * (hi - lo), cudaMemcpyDeviceToDevice, st));
             }
         }
         return PBCG_OK;
@@ -564,10 +570,10 @@ static int halo(pbcg_handle *h, int which) {
     for (int q = 0; q < h->nranks; ++q) {
         if (R.send_hi[q] > R.send_lo[q])
             NCCL_TRY(g_nccl.Send(padbuf(R, which) + (R.send_lo[q] - R.buf_lo), (size_t)(R.send_hi[q] - R.send_lo[q]),
-                                 ncclFloat64, q, h->comm_halo, h->stream));
+                                 ncclFloat64, q, h->comm_halo, st));
         if (R.recv_hi[q] > R.recv_lo[q])
             NCCL_TRY(g_nccl.Recv(padbuf(R, which) + (R.recv_lo[q] - R.buf_lo), (size_t)(R.recv_hi[q] - R.recv_lo[q]),
-                                 ncclFloat64, q, h->comm_halo, h->stream));
+                                 ncclFloat64, q, h->comm_halo, st));
     }
     NCCL_TRY(g_nccl.GroupEnd());
     return PBCG_OK;
@@ -620,6 +626,7 @@ static bool multi(const pbcg_handle *h) { return h->V > 1 || h->comm; }
 // per thread (more warps in flight).  PBCG_SPMV_KERNEL=tma|pipe|plain
 // overrides (A/B runs).
 enum { SPMV_K_PLAIN = 0, SPMV_K_PIPE = 1, SPMV_K_TMA = 2 };
+static constexpr int SPMV_COMM_SMS = 4;  // SMs the interior SpMV leaves to the halo's NCCL kernels
 static constexpr int64_t SELLP_MIN_SLICES_PER_SM = 32;  // C3 (443/SM): TMA 7.17K vs 6.18K iter/s; C1 (1/SM): pipe
 static int spmv_kind_for(const Rank &R, int nsm) {  // at setup
     if (R.max_len > 8) return SPMV_K_PLAIN;
@@ -661,43 +668,66 @@ static void launch_ex(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, c
 
 static bool pdl_for(const Rank &R) { return R.spmv_kind != SPMV_K_PLAIN; }
 
+// units [u0, u1): chunks for the SELL-P kernel, slices otherwise (u1 < 0: all);
+// reserve: SMs left free (the halo exchange's NCCL kernels during overlap)
 template <int MODE>
 static void spmv_dispatch(pbcg_handle *h, const Rank &R, const double *xpad, double *y, const double *b, double *y2,
-                          const Scalars *sc, cudaStream_t st) {
+                          const Scalars *sc, cudaStream_t st, int64_t u0, int64_t u1, int reserve) {
     if (R.spmv_kind == SPMV_K_TMA) {
+        if (u1 < 0) u1 = R.nchunks;
         auto *k = spmv_sellp_kernel<MODE, PS_SPS, PS_RPW>;
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute((const void *)k, cudaFuncAttributeMaxDynamicSharedMemorySize, PS_SMEM_MAX);
             attr = true;
         }
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->nsm, R.nchunks));
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->nsm - reserve, u1 - u0));
         const size_t smem = (size_t)R.ps_stages * R.ps_stage + 2 * R.ps_stages * sizeof(uint64_t);
         launch_ex(k, dim3(grid), dim3((PS_SPS / PS_RPW + 1) * 32), smem, st, pdl_for(R), R.n, R.nslices,
                   (const unsigned char *)R.blob, (const int64_t *)R.blob_off,
-                  (const int32_t *)(R.h_perm.empty() ? nullptr : R.perm), xpad, y, b, y2, sc, R.ps_stage, R.ps_stages);
-    } else if (R.spmv_kind == SPMV_K_PIPE) {
-        static int grid_pipe = 0;
-        if (!grid_pipe) grid_pipe = grid_for((const void *)spmv_sell_pipe_kernel<MODE, 8>, 256, h->nsm);
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid_pipe, (R.n + 255) / 256));
-        launch_ex(spmv_sell_pipe_kernel<MODE, 8>, dim3(grid), dim3(256), 0, st, pdl_for(R), R.mat(), xpad, y, b, y2,
-                  sc);
+                  (const int32_t *)(R.h_perm.empty() ? nullptr : R.perm), xpad, y, b, y2, sc, R.ps_stage, R.ps_stages,
+                  u0, u1);
+        return;
+    }
+    if (u1 < 0) u1 = R.nslices;
+    const SellMat M = R.mat(u0 * 32, u1 * 32);
+    const int64_t rows = M.p1 - M.p0;
+    if (rows <= 0) return;
+    if (R.spmv_kind == SPMV_K_PIPE) {
+        static int per_sm = 0;
+        if (!per_sm) per_sm = std::max(1, grid_for((const void *)spmv_sell_pipe_kernel<MODE, 8>, 256, 1));
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * (h->nsm - reserve), (rows + 255) / 256));
+        launch_ex(spmv_sell_pipe_kernel<MODE, 8>, dim3(grid), dim3(256), 0, st, pdl_for(R), M, xpad, y, b, y2, sc);
     } else {
-        const int grid = (int)((R.n + 255) / 256);
+        const int grid = (int)((rows + 255) / 256);
 #ifndef PBCG_PLAIN_UNR
 #define PBCG_PLAIN_UNR 8
 #endif
-        launch_ex(spmv_sell_kernel<MODE, PBCG_PLAIN_UNR, 1>, dim3(grid), dim3(256), 0, st, false, R.mat(), xpad, y, b,
-                  y2, sc);
+        launch_ex(spmv_sell_kernel<MODE, PBCG_PLAIN_UNR, 1>, dim3(grid), dim3(256), 0, st, false, M, xpad, y, b, y2,
+                  sc);
     }
 }
 
+// part: 0 = all rows, 1 = the interior (no halo entries), 2 = the boundary
+enum { SP_ALL = 0, SP_INTERIOR = 1, SP_BOUNDARY = 2 };
 static int launch_spmv(pbcg_handle *h, Rank &R, int mode, const double *xpad, double *y, const double *b, double *y2,
-                       bool predicated, cudaStream_t st) {
+                       bool predicated, cudaStream_t st, int part = SP_ALL, int reserve = 0) {
     if (R.n == 0) return PBCG_OK;
     const Scalars *sc = predicated ? R.sc : nullptr;
-    if (mode == SPMV_PLAIN) spmv_dispatch<SPMV_PLAIN>(h, R, xpad, y, b, y2, sc, st);
-    else spmv_dispatch<SPMV_RESID>(h, R, xpad, y, b, y2, sc, st);
+    auto go = [&](int64_t u0, int64_t u1, int rsv) {
+        if (u1 >= 0 && u1 <= u0) return;
+        if (mode == SPMV_PLAIN) spmv_dispatch<SPMV_PLAIN>(h, R, xpad, y, b, y2, sc, st, u0, u1, rsv);
+        else spmv_dispatch<SPMV_RESID>(h, R, xpad, y, b, y2, sc, st, u0, u1, rsv);
+    };
+    if (part == SP_ALL || !R.split) {
+        go(0, -1, 0);
+    } else if (part == SP_INTERIOR) {
+        go(R.in_lo, R.in_hi, reserve);
+    } else {
+        const int64_t units = R.spmv_kind == SPMV_K_TMA ? R.nchunks : R.nslices;
+        go(0, R.in_lo, 0);
+        go(R.in_hi, units, 0);
+    }
     CUDA_TRY(cudaGetLastError());
     return PBCG_OK;
 }
@@ -908,15 +938,43 @@ static int enqueue_iteration(pbcg_handle *h) {
         CUDA_TRY(cudaStreamWaitEvent(st, h->ev[7], 0));
         return PBCG_OK;
     }
-    if (h->V > 1) {  // virtual ranks: same dataflow, serialised on one stream
+    // halo + SpMV of padded buffer `which` into y: with a split, the interior
+    // rows run while the halo exchange runs on cstream (joined before the
+    // boundary rows; "communication hiding" applied to the halo too)
+    const int reserve = (h->comm && h->nranks > 1) ? SPMV_COMM_SMS : 0;
+    auto halo_spmv = [&](int which, double *Rank::*ymem, int evi) -> int {
+        bool split = false;
+        for (auto &R : h->R) split |= R.split;
+        if (!split) {
+            RC_TRY(halo(h, which));
+            for (auto &R : h->R) {
+                double *xp = which == 0 ? R.zpad : R.wpad;
+                RC_TRY(launch_spmv(h, R, SPMV_PLAIN, xp, R.*ymem, nullptr, nullptr, true, st));
+            }
+            return PBCG_OK;
+        }
+        CUDA_TRY(cudaEventRecord(h->evh[evi], st));  // the vector to exchange is complete
+        CUDA_TRY(cudaStreamWaitEvent(h->cstream, h->evh[evi], 0));
+        RC_TRY(halo(h, which, h->cstream));
+        CUDA_TRY(cudaEventRecord(h->evh[evi + 1], h->cstream));
+        for (auto &R : h->R) {
+            double *xp = which == 0 ? R.zpad : R.wpad;
+            RC_TRY(launch_spmv(h, R, SPMV_PLAIN, xp, R.*ymem, nullptr, nullptr, true, st, SP_INTERIOR, reserve));
+        }
+        CUDA_TRY(cudaStreamWaitEvent(st, h->evh[evi + 1], 0));
+        for (auto &R : h->R) {
+            double *xp = which == 0 ? R.zpad : R.wpad;
+            RC_TRY(launch_spmv(h, R, SPMV_PLAIN, xp, R.*ymem, nullptr, nullptr, true, st, SP_BOUNDARY));
+        }
+        return PBCG_OK;
+    };
+    if (h->V > 1) {  // virtual ranks: same dataflow, the reductions serialised on the main stream
         for (auto &R : h->R) RC_TRY(launch_k2(h, R, 0, st));
         RC_TRY(reduce_finalize<4>(h, 1, PH_A, st, nullptr, nullptr));
-        RC_TRY(halo(h, 0));
-        for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.zpad, R.v, nullptr, nullptr, true, st));
+        RC_TRY(halo_spmv(0, &Rank::v, 0));
         for (auto &R : h->R) RC_TRY(launch_k3(h, R, 0, st));
         RC_TRY(reduce_finalize<3>(h, 2, PH_B, st, nullptr, nullptr));
-        RC_TRY(halo(h, 1));
-        for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, true, st));
+        RC_TRY(halo_spmv(1, &Rank::t, 2));
         return PBCG_OK;
     }
     // real ranks: phase allreduce on the side stream overlaps halo + SpMV (l.90)
@@ -926,16 +984,14 @@ static int enqueue_iteration(pbcg_handle *h) {
     CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev[0], 0));
     RC_TRY(reduce_finalize<4>(h, 1, PH_A, h->side, nullptr, nullptr));
     CUDA_TRY(cudaEventRecord(h->ev[1], h->side));
-    RC_TRY(halo(h, 0));
-    RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.zpad, R.v, nullptr, nullptr, true, st));
+    RC_TRY(halo_spmv(0, &Rank::v, 0));
     CUDA_TRY(cudaStreamWaitEvent(st, h->ev[1], 0));
     RC_TRY(launch_k3(h, R, 0, st));
     CUDA_TRY(cudaEventRecord(h->ev[2], st));
     CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev[2], 0));
     RC_TRY(reduce_finalize<3>(h, 2, PH_B, h->side, nullptr, nullptr));
     CUDA_TRY(cudaEventRecord(h->ev[3], h->side));
-    RC_TRY(halo(h, 1));
-    RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, true, st));
+    RC_TRY(halo_spmv(1, &Rank::t, 2));
     CUDA_TRY(cudaStreamWaitEvent(st, h->ev[3], 0));
     return PBCG_OK;
 }
@@ -1008,6 +1064,49 @@ static int jacobi_scale(pbcg_handle *h, const pbcg_csr_local *A) {
         int bad = 0;
         CUDA_TRY(cudaMemcpy(&bad, R.bad, sizeof(int), cudaMemcpyDeviceToHost));
         if (bad & 4) return fail(PBCG_EINVAL, "jacobi: zero or missing diagonal entry");
+    }
+    return PBCG_OK;
+}
+
+// Multi-rank halo overlap: per rank, the longest run of slices that read no
+// halo entry is the interior (for the SELL-P kernel: whole chunks inside it).
+// PBCG_SPLIT=0 turns the overlap off.
+static int plan_split(pbcg_handle *h) {
+    const char *e = getenv("PBCG_SPLIT");
+    if (e && e[0] == '0') return PBCG_OK;
+    for (auto &R : h->R) {
+        R.split = false;
+        if (R.n == 0 || R.nslices < 4) continue;
+        uint8_t *d_flag = nullptr;
+        CUDA_TRY(cudaMalloc(&d_flag, (size_t)R.nslices));
+        const int g = (int)std::min<int64_t>((R.nslices + 7) / 8, 65535);
+        sell_halo_flags_kernel<<<g, 256, 0, h->stream>>>(R.n, R.nslices, R.slice_off, R.row_len, R.scol, R.own_off,
+                                                         R.own_off + R.n, d_flag);
+        std::vector<uint8_t> f(R.nslices);
+        cudaError_t ce = cudaGetLastError();
+        if (ce == cudaSuccess) ce = cudaMemcpyAsync(f.data(), d_flag, (size_t)R.nslices, cudaMemcpyDeviceToHost, h->stream);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(h->stream);
+        cudaFree(d_flag);
+        if (ce != cudaSuccess) return fail(PBCG_ECUDA, "plan_split: %s", cudaGetErrorString(ce));
+        int64_t best0 = 0, best1 = 0;
+        for (int64_t s0 = 0; s0 < R.nslices;) {  // longest run of interior slices
+            if (f[s0]) { ++s0; continue; }
+            int64_t s1 = s0;
+            while (s1 < R.nslices && !f[s1]) ++s1;
+            if (s1 - s0 > best1 - best0) { best0 = s0; best1 = s1; }
+            s0 = s1;
+        }
+        int64_t lo = best0, hi = best1, units = R.nslices;
+        if (R.spmv_kind == SPMV_K_TMA) {
+            lo = (best0 + PS_SPS - 1) / PS_SPS;
+            hi = best1 / PS_SPS;
+            units = R.nchunks;
+        }
+        if (hi - lo >= units / 4) {  // worth a second launch
+            R.split = true;
+            R.in_lo = lo;
+            R.in_hi = hi;
+        }
     }
     return PBCG_OK;
 }
@@ -1141,11 +1240,14 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
                 R.n_explicit = R.nnz;
             }
         }
+        if (multi(h)) RC_TRY(plan_split(h));
     }
     RC_TRY(stream_attrs());
     h->grid_md = grid_for((const void *)multidot_kernel<4, K_NP, K_NE, K_BS, U_MD4>, K_BS, h->nsm);
     CUDA_TRY(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
     for (auto &e : h->ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto &e : h->evh) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreate(&h->t0));
     CUDA_TRY(cudaEventCreate(&h->t1));
     CUDA_TRY(cudaMallocHost(&h->h_sc, sizeof(Scalars)));
@@ -1158,9 +1260,12 @@ extern "C" void pbicgstab_destroy(pbcg_handle *h) {
     if (h->gexec) cudaGraphExecDestroy(h->gexec);
     for (auto &e : h->ev)
         if (e) cudaEventDestroy(e);
+    for (auto &e : h->evh)
+        if (e) cudaEventDestroy(e);
     if (h->t0) cudaEventDestroy(h->t0);
     if (h->t1) cudaEventDestroy(h->t1);
     if (h->side) cudaStreamDestroy(h->side);
+    if (h->cstream) cudaStreamDestroy(h->cstream);
     if (h->h_sc) cudaFreeHost(h->h_sc);
     if (h->comm_halo && g_nccl.CommDestroy) g_nccl.CommDestroy(h->comm_halo);
     if (h->comm_red && g_nccl.CommDestroy) g_nccl.CommDestroy(h->comm_red);

@@ -657,12 +657,13 @@ __global__ void sellp_fill_kernel(int64_t n, int64_t nslices, SellMat A, const u
 // starts it before waiting on the previous kernel (PDL); on abort it drains
 // the copies it issued, so none is in flight when the CTA exits.
 template <class Gate>
-__device__ __forceinline__ void sellp_produce(int64_t nchunks, const unsigned char *blob, const int64_t *blob_off,
+__device__ __forceinline__ void sellp_produce(int64_t cbeg, int64_t nchunks, const unsigned char *blob,
+                                              const int64_t *blob_off,
                                               unsigned char *smem, int STAGE, int STAGES, uint64_t *full,
                                               uint64_t *empty, int prefill, Gate gate) {
     const int lane = threadIdx.x & 31;
     auto extents = [&](int64_t k, int64_t &c, int64_t &o0, int64_t &o1) {
-        c = blockIdx.x + k * gridDim.x;
+        c = cbeg + blockIdx.x + k * gridDim.x;
         o0 = o1 = 0;
         if (c < nchunks) {
             o0 = __ldg(&blob_off[c]);
@@ -717,7 +718,8 @@ __global__ void __launch_bounds__((SPS / RPW + 1) * 32, 1)
     spmv_sellp_kernel(int64_t n, int64_t nslices, const unsigned char *__restrict__ blob,
                       const int64_t *__restrict__ blob_off, const int32_t *__restrict__ perm,
                       const double *__restrict__ x, double *__restrict__ y, const double *__restrict__ b,
-                      double *__restrict__ y2, const Scalars *sc, int STAGE, int STAGES) {
+                      double *__restrict__ y2, const Scalars *sc, int STAGE, int STAGES, int64_t cbeg, int64_t cend) {
+    // chunks [cbeg, cend) (interior / boundary split under multi-rank halo overlap)
     using Geo = SellPGeo<SPS>;
     constexpr int NCW = SPS / RPW;  // consumer warps
     static_assert(SPS % RPW == 0, "SPS must be a multiple of RPW");
@@ -733,9 +735,9 @@ __global__ void __launch_bounds__((SPS / RPW + 1) * 32, 1)
         mbar_fence_init();
     }
     __syncthreads();
-    const int64_t nchunks = (nslices + SPS - 1) / SPS;
+    const int64_t nchunks = cend;
     if (warp == NCW) {  // producer warp: the first STAGES chunks go out before the PDL wait
-        sellp_produce(nchunks, blob, blob_off, smem_raw, STAGE, STAGES, full, empty, STAGES, [&]() {
+        sellp_produce(cbeg, nchunks, blob, blob_off, smem_raw, STAGE, STAGES, full, empty, STAGES, [&]() {
             pdl_sync();
             return !(sc && sc->done);
         });
@@ -802,7 +804,7 @@ __global__ void __launch_bounds__((SPS / RPW + 1) * 32, 1)
     uint32_t ph = 0;
     int len[RPW];
     double xv[RPW][8];
-    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    for (int64_t c = cbeg + blockIdx.x; c < nchunks; c += gridDim.x) {
         mbar_wait(&full[st], ph);
         issue(c, st, len, xv);
         fold(c, st, len, xv);
