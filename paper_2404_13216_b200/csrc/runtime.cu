@@ -1564,24 +1564,30 @@ static int true_residual(pbcg_handle *h) {
 
 extern "C" int pbicgstab_finish(pbcg_handle *h, double *x, pbcg_result *res) {
     if (!h || !h->started) return fail(PBCG_EINVAL, "finish before start");
-    if (h->h_sc->err == 0) RC_TRY(true_residual(h));
-    CUDA_TRY(cudaMemcpyAsync(h->h_sc, h->R[0].sc, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
+    // the copy-out of x (and Jacobi's x := D^-1 y) runs on the side stream
+    // while the true residual (which only reads x) runs on the main stream
+    cudaStream_t xs = x ? h->side : h->stream;
     if (x) {
+        CUDA_TRY(cudaEventRecord(h->ev[4], h->stream));
+        CUDA_TRY(cudaStreamWaitEvent(xs, h->ev[4], 0));
         const bool host = is_host_ptr(x);
         for (auto &R : h->R) {
             const int64_t off = h->V > 1 ? R.rb : 0;
             const double *src = R.x;
-            if (h->precond == PBCG_PRECOND_JACOBI && R.n > 0) {  // x := D^-1 y (R-22)
-                vec_muldiv_kernel<<<(int)std::min<int64_t>((R.n + 255) / 256, 4096), 256, 0, h->stream>>>(
-                    R.n, R.x, R.dg, R.tmp, 1);
+            if (h->precond == PBCG_PRECOND_JACOBI && R.n > 0) {  // x := D^-1 y (R-22), into q (free after the loop)
+                vec_muldiv_kernel<<<(int)std::min<int64_t>((R.n + 255) / 256, 4096), 256, 0, xs>>>(R.n, R.x, R.dg,
+                                                                                                  R.q, 1);
                 CUDA_TRY(cudaGetLastError());
-                src = R.tmp;
+                src = R.q;
             }
             CUDA_TRY(cudaMemcpyAsync(x + off, src, sizeof(double) * R.n,
-                                     host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, h->stream));
+                                     host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, xs));
         }
     }
+    if (h->h_sc->err == 0) RC_TRY(true_residual(h));
+    CUDA_TRY(cudaMemcpyAsync(h->h_sc, h->R[0].sc, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (xs != h->stream) CUDA_TRY(cudaStreamSynchronize(xs));
     if (res) {
         const Scalars &s = *h->h_sc;
         res->status = s.status == ST_RUNNING ? PBCG_MAXITER : s.status;
