@@ -540,7 +540,11 @@ __global__ void __launch_bounds__(256) spmv_sell_kernel(SellMat A, const double 
         for (int u = 0; u < RPT; ++u)
 #pragma unroll
             for (int j = 0; j < UNR; ++j)
+#ifdef PBCG_EXP_NOGATHER  // timing experiment only (wrong results): coalesced x reads
+                if (k + j < len[u]) xv[u][j] = __ldg(x + (pos0 + 256 * u + (c[u][j] & 1)));
+#else
                 if (k + j < len[u]) xv[u][j] = __ldg(x + (pos0 + 256 * u + c[u][j]));
+#endif
 #pragma unroll
         for (int u = 0; u < RPT; ++u)
 #pragma unroll

@@ -229,6 +229,29 @@ static constexpr int U_MD4 = 2, U_MD1 = 4;  // row pairs in flight per thread (m
 #endif
 static constexpr int PS_SPS = PBCG_PS_SPS, PS_RPW = PBCG_PS_RPW, PS_MAXSTAGES = PBCG_PS_MAXSTAGES;
 static constexpr int PS_SMEM_MAX = 227 * 1024;
+// SELL-V geometry (spmv_sellv_kernel, long rows): consumer warps (= most
+// slices per chunk), bytes per chunk, gathers in flight per lane, ring stages
+#ifndef PBCG_PV_NCW
+#define PBCG_PV_NCW 16
+#endif
+#ifndef PBCG_PV_CAP
+#define PBCG_PV_CAP 24576
+#endif
+#ifndef PBCG_PV_UNR
+#define PBCG_PV_UNR 8
+#endif
+#ifndef PBCG_PV_MAXSTAGES
+#define PBCG_PV_MAXSTAGES 8
+#endif
+#ifndef PBCG_PV_NCW_G
+#define PBCG_PV_NCW_G 30
+#endif
+#ifndef PBCG_PV_MIN_WIN_STAGES
+#define PBCG_PV_MIN_WIN_STAGES 6
+#endif
+static constexpr int PV_NCW = PBCG_PV_NCW, PV_CAP = PBCG_PV_CAP, PV_UNR = PBCG_PV_UNR,
+                     PV_MAXSTAGES = PBCG_PV_MAXSTAGES, PV_MIN_WIN_STAGES = PBCG_PV_MIN_WIN_STAGES,
+                     PV_NCW_G = PBCG_PV_NCW_G;
 
 struct Rank {
     int id = 0;
@@ -262,8 +285,13 @@ struct Rank {
     double *dg = nullptr;             // Jacobi: diag(A) of this rank's rows
     double *part[NPH] = {};           // plain dot mode: CTA partials [PLAIN_GRID][4] per phase
     double *pdsum = nullptr;          // plain dot mode, NCCL ranks: local sums [NPH][4] (allreduced)
-    // packed SELL-P chunks (rows <= 8 nonzeros): blob + byte offsets per chunk
+    // packed SELL-P chunks (rows <= 8 nonzeros) or SELL-V chunks (longer
+    // rows): blob + byte offsets per chunk; h_cs: first slice of each SELL-V chunk
     int64_t nchunks = 0, blob_cap = 0, blob_bytes = 0;
+    std::vector<int32_t> h_cs;
+    int32_t *cxlo = nullptr, *cxhi = nullptr;  // SELL-V: x-buffer index range [lo, hi) of each chunk
+    int ps_xr = 0;                             // SELL-V: x-window ring (doubles, power of two)
+    bool pv_gld = false;                       // SELL-V: matrix loaded from global (only headers in the ring)
     unsigned char *blob = nullptr;
     int64_t *blob_off = nullptr;
     uint8_t *nexp = nullptr;
@@ -339,6 +367,12 @@ static void carve_rank(Carver &C, Rank &R, int hist_cap, bool comm_only, bool pr
             R.blob = C.take<unsigned char>((size_t)R.blob_cap);
             R.blob_off = C.take<int64_t>((size_t)R.nchunks + 1);
             R.nexp = C.take<uint8_t>((size_t)R.nslices);
+        } else if (R.max_len <= 255) {  // SELL-V blob: every nonzero once + per-chunk headers
+            R.blob_cap = 12 * R.nnz + 96 * R.nslices + 256 + 2048;  // + header-copy slack past the last chunk
+            R.blob = C.take<unsigned char>((size_t)R.blob_cap);
+            R.blob_off = C.take<int64_t>((size_t)R.nslices + 1);
+            R.cxlo = C.take<int32_t>((size_t)R.nslices);
+            R.cxhi = C.take<int32_t>((size_t)R.nslices);
         }
         R.perm = C.take<int32_t>(R.h_perm.size());
         const size_t n = (size_t)R.n + 2;
@@ -625,12 +659,17 @@ static bool multi(const pbcg_handle *h) { return h->V > 1 || h->comm; }
 // register-pipelined persistent kernel (no ring to fill); long rows: one row
 // per thread (more warps in flight).  PBCG_SPMV_KERNEL=tma|pipe|plain
 // overrides (A/B runs).
-enum { SPMV_K_PLAIN = 0, SPMV_K_PIPE = 1, SPMV_K_TMA = 2 };
+enum { SPMV_K_PLAIN = 0, SPMV_K_PIPE = 1, SPMV_K_TMA = 2, SPMV_K_TMAV = 3 };
 static constexpr int SPMV_COMM_SMS = 4;  // SMs the interior SpMV leaves to the halo's NCCL kernels
 static constexpr int64_t SELLP_MIN_SLICES_PER_SM = 32;  // C3 (443/SM): TMA 7.17K vs 6.18K iter/s; C1 (1/SM): pipe
+static constexpr int64_t SELLV_MIN_SLICES_PER_SM = 16;
 static int spmv_kind_for(const Rank &R, int nsm) {  // at setup
-    if (R.max_len > 8) return SPMV_K_PLAIN;
     const char *e = getenv("PBCG_SPMV_KERNEL");
+    if (R.max_len > 8) {  // long rows: the SELL-V kernel (rows <= 255 nonzeros), else one row per thread
+        const bool v_ok = R.max_len <= 255 && R.blob;
+        if (e) return v_ok && (strcmp(e, "tma") == 0 || strcmp(e, "tmav") == 0) ? SPMV_K_TMAV : SPMV_K_PLAIN;
+        return v_ok && R.nslices >= SELLV_MIN_SLICES_PER_SM * nsm ? SPMV_K_TMAV : SPMV_K_PLAIN;
+    }
     if (!e) return R.nslices >= SELLP_MIN_SLICES_PER_SM * nsm ? SPMV_K_TMA : SPMV_K_PIPE;
     return strcmp(e, "pipe") == 0 ? SPMV_K_PIPE : strcmp(e, "tma") == 0 ? SPMV_K_TMA : SPMV_K_PLAIN;
 }
@@ -689,6 +728,26 @@ static void spmv_dispatch(pbcg_handle *h, const Rank &R, const double *xpad, dou
                   u0, u1);
         return;
     }
+    if (R.spmv_kind == SPMV_K_TMAV) {
+        if (u1 < 0) u1 = R.nchunks;
+        auto *k = R.pv_gld ? spmv_sellv_kernel<MODE, PV_NCW_G, PV_UNR, true> : spmv_sellv_kernel<MODE, PV_NCW, PV_UNR, false>;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute((const void *)spmv_sellv_kernel<MODE, PV_NCW_G, PV_UNR, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, PS_SMEM_MAX);
+            cudaFuncSetAttribute((const void *)spmv_sellv_kernel<MODE, PV_NCW, PV_UNR, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, PS_SMEM_MAX);
+            attr = true;
+        }
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->nsm - reserve, u1 - u0));
+        const size_t smem = (size_t)R.ps_stages * R.ps_stage + 8 * (size_t)R.ps_xr + 2 * R.ps_stages * sizeof(uint64_t);
+        launch_ex(k, dim3(grid), dim3(((R.pv_gld ? PV_NCW_G : PV_NCW) + 1) * 32), smem, st, pdl_for(R), R.n,
+                  (const unsigned char *)R.blob,
+                  (const int64_t *)R.blob_off, (const int32_t *)R.cxlo, (const int32_t *)R.cxhi,
+                  (const int32_t *)(R.h_perm.empty() ? nullptr : R.perm), xpad, y, b, y2, sc, R.ps_stage, R.ps_stages,
+                  R.ps_xr, u0, u1);
+        return;
+    }
     if (u1 < 0) u1 = R.nslices;
     const SellMat M = R.mat(u0 * 32, u1 * 32);
     const int64_t rows = M.p1 - M.p0;
@@ -724,7 +783,7 @@ static int launch_spmv(pbcg_handle *h, Rank &R, int mode, const double *xpad, do
     } else if (part == SP_INTERIOR) {
         go(R.in_lo, R.in_hi, reserve);
     } else {
-        const int64_t units = R.spmv_kind == SPMV_K_TMA ? R.nchunks : R.nslices;
+        const int64_t units = (R.spmv_kind == SPMV_K_TMA || R.spmv_kind == SPMV_K_TMAV) ? R.nchunks : R.nslices;
         go(0, R.in_lo, 0);
         go(R.in_hi, units, 0);
     }
@@ -1039,6 +1098,114 @@ static int build_sellp(pbcg_handle *h, Rank &R) {
     return PBCG_OK;
 }
 
+// SELL-V chunks (spmv_sellv_kernel): nonzeros per slice on the device, the
+// byte-bounded chunking on the host (at most PV_NCW slices and PV_CAP bytes
+// per chunk, or one slice), then the scatter.
+static int build_sellv(pbcg_handle *h, Rank &R) {
+    const int64_t ns = R.nslices;
+    int32_t *d_tmp = nullptr;  // [nnz per slice | cs | vs | x lo per slice | x hi per slice]
+    CUDA_TRY(cudaMalloc(&d_tmp, sizeof(int32_t) * (5 * ns + 2)));
+    int32_t *d_cnt = d_tmp, *d_cs = d_tmp + ns, *d_vs = d_tmp + 2 * ns + 1, *d_lo = d_tmp + 3 * ns + 2,
+            *d_hi = d_tmp + 4 * ns + 2;
+    std::vector<int32_t> cnt(ns), slo(ns), shi(ns);
+    {
+        const int g = (int)std::min<int64_t>((ns + 255) / 256, 65535);
+        sellv_count_kernel<<<g, 256, 0, h->stream>>>(R.n, ns, R.row_len, d_cnt);
+        const int gx = (int)std::min<int64_t>((ns + 7) / 8, 65535);
+        sellv_xrange_kernel<<<gx, 256, 0, h->stream>>>(R.n, ns, R.mat(), d_lo, d_hi);
+        cudaError_t ce = cudaGetLastError();
+        if (ce == cudaSuccess) ce = cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, h->stream);
+        if (ce == cudaSuccess) ce = cudaMemcpyAsync(slo.data(), d_lo, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, h->stream);
+        if (ce == cudaSuccess) ce = cudaMemcpyAsync(shi.data(), d_hi, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, h->stream);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(h->stream);
+        if (ce != cudaSuccess) {
+            cudaFree(d_tmp);
+            return fail(PBCG_ECUDA, "sellv: %s", cudaGetErrorString(ce));
+        }
+    }
+    auto bytes = [](int64_t nsl, int64_t nv) { return (sellv_hdr_bytes((int)nsl) + 12 * nv + 15) & ~int64_t(15); };
+    std::vector<int32_t> cs, vs(ns), clo, chi;
+    std::vector<int64_t> off;
+    // chunks of consecutive slices: at most `ncw` slices and `cap` bytes (or one
+    // slice); then each chunk's x range and the ring geometry: the most stages
+    // (>= min_st) whose x window fits next to `stage` bytes per stage
+    auto plan = [&](int64_t cap, int ncw, bool gld, int min_st) {
+        cs.assign(1, 0);
+        off.assign(1, 0);
+        int64_t mx = 0;
+        for (int64_t s0 = 0; s0 < ns;) {
+            int64_t s1 = s0, nv = 0;
+            while (s1 < ns && (s1 == s0 || (s1 - s0 < ncw && bytes(s1 + 1 - s0, nv + cnt[s1]) <= cap))) {
+                vs[s1] = (int32_t)nv;
+                nv += cnt[s1++];
+            }
+            const int64_t b = bytes(s1 - s0, nv);
+            mx = std::max(mx, b);
+            off.push_back(off.back() + b);
+            cs.push_back((int32_t)s1);
+            s0 = s1;
+        }
+        const int64_t nch = (int64_t)cs.size() - 1;
+        R.nchunks = nch;
+        R.blob_bytes = off.back();
+        R.ps_stage = gld ? (sellv_hdr_bytes(ncw) + 127) & ~127 : (int)((mx + 127) & ~int64_t(127));
+        clo.assign(nch, INT32_MAX);
+        chi.assign(nch, -1);
+        std::vector<int64_t> H(nch);  // running maximum of the chunks' even-rounded upper x index
+        for (int64_t c = 0; c < nch; ++c) {
+            for (int64_t q = cs[c]; q < cs[c + 1]; ++q) {
+                clo[c] = std::min(clo[c], slo[q]);
+                chi[c] = std::max(chi[c], shi[q]);
+            }
+            H[c] = std::max<int64_t>(c ? H[c - 1] : 0, (chi[c] + 1) & ~1);
+        }
+        R.ps_stages = 0;
+        R.ps_xr = 0;
+        R.pv_gld = gld;
+        for (int S = PV_MAXSTAGES; S >= min_st && !R.ps_stages; --S) {
+            int64_t span = 0;
+            for (int64_t c = 0; c < nch; ++c)
+                if (clo[c] != INT32_MAX) span = std::max<int64_t>(span, H[std::min<int64_t>(c + S - 1, nch - 1)] - clo[c]);
+            int64_t xr = 1024;
+            while (xr < span + 4) xr <<= 1;
+            if ((int64_t)S * R.ps_stage + 8 * xr + 16 * S + 256 <= PS_SMEM_MAX) {
+                R.ps_stages = S;
+                R.ps_xr = (int)xr;
+            }
+        }
+        return R.ps_stages > 0 && R.blob_bytes <= R.blob_cap - 2048;
+    };
+    // the matrix through the ring when the window leaves a deep one; else
+    // the matrix loaded by the consumers, only chunk headers in the ring
+    // (PBCG_SELLV_MODE=tma|gld forces one, for A/B runs)
+    const char *em = getenv("PBCG_SELLV_MODE");
+    bool ok = false;
+    if (!em || strcmp(em, "gld") != 0) ok = plan(PV_CAP, PV_NCW, false, PV_MIN_WIN_STAGES);
+    if (!ok && (!em || strcmp(em, "tma") != 0)) ok = plan(INT64_MAX / 4, PV_NCW_G, true, 2);
+    if (!ok) {  // x window wider than shared memory (not banded): one row per thread
+        cudaFree(d_tmp);
+        R.spmv_kind = SPMV_K_PLAIN;
+        return PBCG_OK;
+    }
+    R.h_cs = cs;
+    const int64_t nch = R.nchunks;
+    cudaError_t ce = cudaMemcpyAsync(R.blob_off, off.data(), sizeof(int64_t) * off.size(), cudaMemcpyHostToDevice, h->stream);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(R.cxlo, clo.data(), sizeof(int32_t) * nch, cudaMemcpyHostToDevice, h->stream);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(R.cxhi, chi.data(), sizeof(int32_t) * nch, cudaMemcpyHostToDevice, h->stream);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(d_cs, cs.data(), sizeof(int32_t) * cs.size(), cudaMemcpyHostToDevice, h->stream);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(d_vs, vs.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, h->stream);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(R.blob, 0, (size_t)R.blob_bytes + 2048, h->stream);
+    if (ce == cudaSuccess) {
+        const int gf = (int)std::min<int64_t>((ns + 7) / 8, 65535);
+        sellv_fill_kernel<<<gf, 256, 0, h->stream>>>(R.n, ns, R.mat(), d_cs, d_vs, R.nchunks, R.blob_off, R.blob);
+        ce = cudaGetLastError();
+    }
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(h->stream);  // host vectors must outlive the copies
+    cudaFree(d_tmp);
+    if (ce != cudaSuccess) return fail(PBCG_ECUDA, "sellv: %s", cudaGetErrorString(ce));
+    return PBCG_OK;
+}
+
 static int copy_own_to_pad(pbcg_handle *h, double *Rank::*src_member, int which);
 
 // Right Jacobi (NEXT-3, R-22): d = diag(A) per rank, d into the padded
@@ -1100,6 +1267,10 @@ static int plan_split(pbcg_handle *h) {
         if (R.spmv_kind == SPMV_K_TMA) {
             lo = (best0 + PS_SPS - 1) / PS_SPS;
             hi = best1 / PS_SPS;
+            units = R.nchunks;
+        } else if (R.spmv_kind == SPMV_K_TMAV) {  // whole chunks inside [best0, best1)
+            lo = std::lower_bound(R.h_cs.begin(), R.h_cs.end(), (int32_t)best0) - R.h_cs.begin();
+            hi = std::upper_bound(R.h_cs.begin(), R.h_cs.end(), (int32_t)best1) - R.h_cs.begin() - 1;
             units = R.nchunks;
         }
         if (hi - lo >= units / 4) {  // worth a second launch
@@ -1234,6 +1405,10 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
             if (R.spmv_kind == SPMV_K_TMA) {
                 if (R.blob && R.n > 0) RC_TRY(build_sellp(h, R));
                 else R.spmv_kind = SPMV_K_PIPE;
+            }
+            if (R.spmv_kind == SPMV_K_TMAV) {
+                if (R.n > 0) RC_TRY(build_sellv(h, R));
+                else R.spmv_kind = SPMV_K_PLAIN;
             }
             if (R.spmv_kind != SPMV_K_TMA) {
                 R.use_slots = false;
@@ -1846,7 +2021,7 @@ extern "C" int pbcg_spmv_format(pbcg_handle *h, int64_t *out8) {
         out8[2] += R.sell_nnz;
         out8[3] += R.n_explicit;
         out8[4] += slots;
-        if (R.spmv_kind == SPMV_K_TMA && R.blob)  // the packed chunks read once, x once, y
+        if ((R.spmv_kind == SPMV_K_TMA || R.spmv_kind == SPMV_K_TMAV) && R.blob)  // the packed chunks read once, x once, y
             out8[5] += R.blob_bytes + 8 * (R.nchunks + 1) + 16 * R.n + (R.h_perm.empty() ? 0 : 4 * R.n);
         else
             out8[5] += 8 * R.nnz + 4 * R.n_explicit + 4 * slots + 4 * R.n + 8 * R.nslices + 16 * R.n +

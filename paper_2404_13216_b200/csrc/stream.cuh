@@ -815,4 +815,276 @@ __global__ void __launch_bounds__((SPS / RPW + 1) * 32, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// SELL-V: the TMA-streamed SpMV for long rows (irregular matrices, C4).
+// The sliced ELL (C = 32, sigma-sorted) is cut into chunks of consecutive
+// slices bounded by BYTES (a chunk is at most one ring stage), not by slice
+// count, so a row may hold up to 255 nonzeros.  Within a slice the padding
+// is dropped: slot k stores only the lanes whose row has a k-th nonzero, in
+// lane order (a lane finds its entry by the popcount of the active lanes
+// below it), so the stream is exactly the nonzeros.  Chunk blob:
+//   int32 s0 (first slice), ns (slices), nval (entries), pad;
+//   int32 vo[ns] (entry offset of each slice); uint8 len[ns][32];
+//   (16-byte aligned) double val[nval]; int32 col[nval]  (pos-relative ids)
+// One bulk copy moves a chunk.  Slice j of a chunk goes to consumer warp
+// (rot + j) mod NCW, rot = the CTA's running slice count, so successive
+// chunks fill successive warps and every warp walks the ring (waiting on
+// each stage, arriving once per chunk): up to STAGES chunks of slices are
+// folded concurrently.  Lane = row: its ordered fma chain (R-6) over the
+// row's nonzeros, x gathered through L1/L2, UNR gathers in flight.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int sellv_hdr_bytes(int ns) { return (16 + 36 * ns + 15) & ~15; }
+
+// nonzeros per slice (the chunking runs on the host)
+__global__ void sellv_count_kernel(int64_t n, int64_t nslices, const int32_t *row_len, int32_t *nnz_slice) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nslices; s += (int64_t)gridDim.x * blockDim.x) {
+        int t = 0;
+        for (int l = 0; l < 32; ++l) t += (s * 32 + l < n) ? row_len[s * 32 + l] : 0;
+        nnz_slice[s] = t;
+    }
+}
+
+// one warp per slice: header entries, values and column ids of the slice into
+// its chunk (cs[c] = first slice of chunk c, vs[s] = entry offset of slice s
+// inside its chunk; blob zeroed beforehand)
+__global__ void sellv_fill_kernel(int64_t n, int64_t nslices, SellMat A, const int32_t *cs, const int32_t *vs,
+                                  int64_t nchunks, const int64_t *blob_off, unsigned char *blob) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nslices; s += nw) {
+        int64_t lo = 0, hi = nchunks;  // chunk c with cs[c] <= s < cs[c + 1]
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (cs[mid] <= s) lo = mid;
+            else hi = mid;
+        }
+        const int64_t c = lo;
+        const int ns = cs[c + 1] - cs[c];
+        const int j = (int)(s - cs[c]);
+        const int last = cs[c + 1] - 1;
+        unsigned char *bb = blob + blob_off[c];
+        int32_t *hd = (int32_t *)bb;
+        const int64_t pos = s * 32 + lane;
+        const int len = pos < n ? A.row_len[pos] : 0;
+        const int W = (int)((A.slice_off[s + 1] - A.slice_off[s]) >> 5);
+        const int vo = vs[s];
+        // entries of the chunk = offset of its last slice + that slice's nonzeros
+        int lastn = (last * 32LL + lane < n) ? A.row_len[last * 32LL + lane] : 0;
+        lastn = __reduce_add_sync(0xFFFFFFFFu, lastn);
+        const int64_t ent = vs[last] + lastn;
+        if (lane == 0) {
+            hd[4 + j] = vo;
+            if (j == 0) {
+                hd[0] = cs[c];
+                hd[1] = ns;
+                hd[2] = (int32_t)ent;
+            }
+        }
+        bb[16 + 4 * ns + 32 * j + lane] = (uint8_t)len;
+        double *bv = (double *)(bb + sellv_hdr_bytes(ns));
+        int32_t *bx = (int32_t *)(bv + ent);
+        const int64_t so = A.slice_off[s];
+        int off = vo;
+        for (int k = 0; k < W; ++k) {
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, k < len);
+            if (k < len) {
+                const int d = off + __popc(m & ((1u << lane) - 1u));
+                bv[d] = A.val[so + 32 * k + lane];
+                bx[d] = A.col[so + 32 * k + lane];
+            }
+            off += __popc(m);
+        }
+    }
+}
+
+// x-buffer index range of each slice's nonzeros (lo = INT32_MAX, hi = -1 if none)
+__global__ void sellv_xrange_kernel(int64_t n, int64_t nslices, SellMat A, int32_t *lo, int32_t *hi) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nslices; s += nw) {
+        const int64_t pos = s * 32 + lane, so = A.slice_off[s];
+        const int len = pos < n ? A.row_len[pos] : 0;
+        int mn = INT32_MAX, mx = -1;
+        for (int k = 0; k < len; ++k) {
+            const int i = (int)(pos + A.col[so + 32 * k + lane]);
+            mn = min(mn, i);
+            mx = max(mx, i);
+        }
+        mn = (int)__reduce_min_sync(0xFFFFFFFFu, (unsigned)mn);
+        mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+        if (lane == 0) {
+            lo[s] = mn;
+            hi[s] = mx < 0 ? -1 : mx + 1;
+        }
+    }
+}
+
+// The x window.  A CTA folds a contiguous run of chunks (the rows of a banded
+// matrix advance with it), so the x entries its chunks read form a sliding
+// window: the producer streams x into a ring of XR doubles (XR a power of
+// two; entry i at slot i mod XR) ahead of each chunk -- [loaded, hi'_c),
+// hi'_c = the running maximum of the chunks' upper x indices -- on the same
+// mbarrier as the chunk.  Setup checks that no chunk in flight can see its
+// entries overwritten (hi'_{c+STAGES-1} - lo_c <= XR - 4) with at least
+// PV_MIN_WIN_STAGES ring stages, else this kernel is not used.  The consumers
+// gather from shared memory: x crosses HBM/L2 about once instead of once per
+// nonzero.  Measured alternatives: the same ring with x
+// gathered through L1/L2 runs at 0.45-0.75x the row-per-thread kernel (16
+// warps cannot cover the gather latency); with C4's +-5000 band the window
+// takes 128 KB and leaves 4 stages: 340 us vs 308 us row-per-thread, so C4
+// stays on the row-per-thread kernel; a +-1000 band: 233 us vs 285 us.
+template <int MODE, int NCW, int UNR, bool GLD>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1)
+    spmv_sellv_kernel(int64_t n, const unsigned char *__restrict__ blob, const int64_t *__restrict__ blob_off,
+                      const int32_t *__restrict__ clo, const int32_t *__restrict__ chi,
+                      const int32_t *__restrict__ perm, const double *__restrict__ x, double *__restrict__ y,
+                      const double *__restrict__ b, double *__restrict__ y2, const Scalars *sc, int STAGE, int STAGES,
+                      int XR, int64_t cbeg, int64_t cend) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double *xw = (double *)(smem_raw + (size_t)STAGES * STAGE);
+    uint64_t *full = (uint64_t *)(xw + XR);
+    uint64_t *empty = full + STAGES;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int XM = XR - 1;
+    // this CTA's contiguous run of chunks
+    const int64_t U = cend - cbeg;
+    const int64_t c0 = cbeg + U * blockIdx.x / gridDim.x, c1 = cbeg + U * (blockIdx.x + 1) / gridDim.x;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (warp == NCW) {  // producer warp
+        int mn = INT32_MAX;
+        for (int64_t c = c0 + lane; c < c1; c += 32) mn = min(mn, __ldg(&clo[c]));
+        mn = (int)__reduce_min_sync(0xFFFFFFFFu, (unsigned)mn);
+        if (lane == 0) {
+            const int start = mn == INT32_MAX ? 0 : (mn & ~1);
+            int loaded = start;  // x entries [start, loaded) went out
+            // x range of chunk c given what went out before it (even bounds: 16-byte copies)
+            auto need = [&](int64_t c, int ld) { return max(ld, (__ldg(&chi[c]) + 1) & ~1); };
+            auto xcopy = [&](int a, int e, uint64_t *bar) {  // x[a, e) -> ring, split at the wrap
+                while (a < e) {
+                    const int sl = a & XM, m = min(e - a, XR - sl);
+                    bulk_g2s(xw + sl, x + a, (uint32_t)m * 8u, bar);
+                    a += m;
+                }
+            };
+            int st = 0, issued = 0;
+            uint32_t ph = 0;
+            bool ok = true, gated = false;
+            // the PDL wait, then the x ranges of the `cnt` chunks whose matrix
+            // went out before it (their bytes are already expected)
+            auto open_gate = [&](int cnt) {
+                gated = true;
+                pdl_sync();
+                ok = !(sc && sc->done);
+                int ld = start;
+                for (int k = 0; k < cnt; ++k) {
+                    const int e = need(c0 + k, ld);
+                    xcopy(ld, e, &full[k]);
+                    ld = e;
+                }
+            };
+            for (int64_t c = c0; c < c1; ++c) {
+                if (!gated && issued == STAGES) {
+                    open_gate(STAGES);
+                    if (!ok) break;
+                }
+                // GLD: the chunk's header only (STAGE bytes; the blob has that much slack)
+                const int64_t o0 = __ldg(&blob_off[c]), o1 = GLD ? o0 + STAGE : __ldg(&blob_off[c + 1]);
+                const int e = need(c, loaded);
+                mbar_wait(&empty[st], ph ^ 1u);
+                mbar_expect_tx(&full[st], (uint32_t)(o1 - o0) + (uint32_t)(e - loaded) * 8u);
+                bulk_g2s(smem_raw + (size_t)st * STAGE, blob + o0, (uint32_t)(o1 - o0), &full[st]);
+                if (gated) xcopy(loaded, e, &full[st]);
+                loaded = e;
+                ++issued;
+                if (++st == STAGES) {
+                    st = 0;
+                    ph ^= 1u;
+                }
+            }
+            if (!gated) open_gate(issued);  // run of at most STAGES chunks
+            if (!ok)  // aborted (solve already done): drain what went out
+                for (int k = 0; k < min(issued, STAGES); ++k) mbar_wait(&full[k], 0u);
+        }
+        __syncwarp();
+        return;
+    }
+    pdl_sync();
+    if (sc && sc->done) return;
+    int st = 0, rot = 0;
+    uint32_t ph = 0;
+    for (int64_t c = c0; c < c1; ++c) {
+        mbar_wait(&full[st], ph);
+        const unsigned char *sb = smem_raw + (size_t)st * STAGE;
+        const int32_t *hd = (const int32_t *)sb;
+        const int ns = hd[1];
+        int j = warp - rot;
+        if (j < 0) j += NCW;
+        if (j < ns) {
+            const int nval = hd[2];
+            const int len = sb[16 + 4 * ns + 32 * j + lane];
+            const int W = (int)__reduce_max_sync(0xFFFFFFFFu, (unsigned)len);
+            // values and column ids: in the stage, or (GLD) streamed from the blob
+            const double *vs = (const double *)((GLD ? blob + __ldg(&blob_off[c]) : sb) + sellv_hdr_bytes(ns));
+            const int32_t *xs = (const int32_t *)(vs + nval);
+            const int64_t pos = ((int64_t)hd[0] + j) * 32 + lane;
+            const int ipos = (int)pos;
+            int off = hd[4 + j];
+            double acc = 0.0;
+            for (int k = 0; k < W; k += UNR) {
+                double xv[UNR];
+                int d[UNR];
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {  // slot k+u: this lane's rank among the active lanes
+                    const unsigned m = __ballot_sync(0xFFFFFFFFu, k + u < len);
+                    d[u] = off + __popc(m & lt);
+                    off += __popc(m);
+                }
+                double vv[UNR];
+                int cc[UNR];
+#pragma unroll
+                for (int u = 0; u < UNR; ++u)
+                    if (k + u < len) {
+                        cc[u] = GLD ? __ldcs(xs + d[u]) : xs[d[u]];
+                        vv[u] = GLD ? __ldcs(vs + d[u]) : vs[d[u]];
+                    }
+#pragma unroll
+                for (int u = 0; u < UNR; ++u)
+                    if (k + u < len) xv[u] = xw[(ipos + cc[u]) & XM];
+#pragma unroll
+                for (int u = 0; u < UNR; ++u)
+                    if (k + u < len) acc = __fma_rn(vv[u], xv[u], acc);  // ordered chain, +0.0 start (R-6)
+            }
+            if (pos < n) {
+                const int64_t row = perm ? (int64_t)__ldg(&perm[pos]) : pos;
+                if (MODE == SPMV_PLAIN) {
+                    y[row] = acc;
+                } else {
+                    const double r = __dsub_rn(b[row], acc);  // r0 := b - A x0 (l.64)
+                    y[row] = r;
+                    if (y2) y2[row] = r;
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        // a full chunk shifts the assignment by one more warp: slice j of
+        // every sigma window (rows sorted by length) visits every warp
+        rot += ns == NCW ? ns + 1 : ns;
+        if (rot >= NCW) rot -= NCW;
+        if (rot >= NCW) rot -= NCW;
+        if (++st == STAGES) {
+            st = 0;
+            ph ^= 1u;
+        }
+    }
+}
+
 }  // namespace pbcg

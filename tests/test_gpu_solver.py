@@ -304,6 +304,75 @@ def test_spmv_format_random_keeps_explicit(pb):
     S.close()
 
 
+def ragged_long_rows(n, seed, lmax=255, wide_block=0, band=4000):
+    """Rows of 0..lmax nonzeros (uniform lengths, some empty), columns inside
+    +-band of the diagonal, loguniform values; rows [100, 100 + wide_block)
+    get lmax nonzeros (slices wider than a SELL-V chunk's byte budget)."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, lmax + 1, n)
+    lens[rng.random(n) < 0.05] = 0
+    lens[100:100 + wide_block] = lmax
+    rp = np.zeros(n + 1, np.int64)
+    cols = []
+    for i in range(n):
+        lo, hi = max(0, i - band), min(n, i + band + 1)
+        c = np.unique(rng.integers(lo, hi, 2 * int(lens[i])))[:int(lens[i])]
+        cols.append(c)
+        rp[i + 1] = rp[i] + c.size
+    col = np.concatenate(cols).astype(np.int32)
+    val = gen.loguniform(col.size, seed + 1, -3, 3)
+    return gen.CSR(n, rp.astype(np.int32), col, val, name=f"ragged{n}_{lmax}")
+
+
+@pytest.mark.parametrize("kind", ["rand", "ragged60", "ragged200", "over255", "unbanded"])
+def test_spmv_sellv(pb, kind, monkeypatch):
+    # the TMA-streamed SELL-V kernel (long rows, padding-free byte-bounded
+    # chunks, x window in shared memory): same bits as the oracle and as the
+    # row-per-thread kernel, for ragged lengths, empty rows, a ragged tail
+    # (n % 32 != 0), runs shorter than the ring, slices too wide for a deep
+    # ring (ragged200: the matrix is loaded by the consumers, only chunk
+    # headers pass through the ring).  Matrices it does not take fall back to
+    # the row-per-thread kernel: rows over 255 nonzeros, x windows wider than
+    # shared memory (unbanded)
+    import torch
+    A = {"rand": lambda: gen.random_banded(50_001, seed=3, band=2000),
+         "ragged60": lambda: ragged_long_rows(20_011, 5, lmax=60, band=1000),
+         "ragged200": lambda: ragged_long_rows(9_001, 6, lmax=200, wide_block=96, band=1000),
+         "over255": lambda: ragged_long_rows(4_003, 7, lmax=300, wide_block=40),
+         "unbanded": lambda: ragged_long_rows(60_007, 8, lmax=20, band=60_007)}[kind]()
+    x = gen.loguniform(A.n, 3, -20, 20)
+    xt = torch.from_numpy(x).cuda()
+    want = u64(oracle.spmv(A, x))
+    fmts = {}
+    for kern in ("tmav", "plain"):
+        monkeypatch.setenv("PBCG_SPMV_KERNEL", kern)
+        for V in (1, 3):
+            S = solver(pb, A, virtual_ranks=V)
+            fmts[kern, V] = S.spmv_format()
+            assert np.array_equal(u64(S.spmv(xt).cpu().numpy()), want), (kern, V)
+            S.close()
+    nnz = int(A.row_ptr[-1])
+    f, fp = fmts["tmav", 1], fmts["plain", 1]
+    assert f["explicit_cols"] == nnz and f["slot_records"] == 0
+    if kind in ("over255", "unbanded"):
+        assert f["bytes_per_spmv"] == fp["bytes_per_spmv"]  # the row-per-thread kernel ran
+    else:
+        # the chunks hold the nonzeros only (no ELL padding): about 12 B each
+        assert f["bytes_per_spmv"] != fp["bytes_per_spmv"]
+        assert 12 * nnz <= f["bytes_per_spmv"] - 16 * A.n <= 12 * nnz + 64 * (A.n // 32 + 1) + 8 * A.n
+
+
+@pytest.mark.parametrize("V", [1, 3])
+def test_sellv_solver_matches_oracle(pb, V, monkeypatch):
+    # whole trajectories with the SELL-V SpMV (also under the virtual-rank
+    # halo split: interior chunks, then the boundary ones)
+    monkeypatch.setenv("PBCG_SPMV_KERNEL", "tmav")
+    A = gen.random_banded(20_000, seed=9, band=1500)
+    S, O, x, r, H = run_both(pb, A, tol=1e-10, max_iter=3000, virtual_ranks=V)
+    assert r.status == pb.CONVERGED
+    assert_same(O, x, r, H, A)
+
+
 # ------------------------------------------------------ plain fp64 dots ---
 # SURVEY §8(f) NEXT-1: the paper's non-reproducible comparison arm.
 

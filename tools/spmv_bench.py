@@ -6,7 +6,10 @@ import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, gen, paper_2404_13216_b200 as pb
 name = sys.argv[1]; K = int(sys.argv[2]) if len(sys.argv) > 2 else 50
-A = gen.make_config(name)
+if name.startswith("c4band"):  # C4 with another band: c4band1000
+    A = gen.random_banded(1 << 22, seed=42, band=int(name[6:]))
+else:
+    A = gen.make_config(name)
 S = pb.Solver(A.row_ptr, A.col, A.val, A.n)
 x = torch.from_numpy(gen.uniform(A.n, 5)).cuda()
 for _ in range(3):
