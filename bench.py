@@ -326,11 +326,14 @@ def exdot_microbench(args, hbm):
     import paper_2404_13216_b200 as pb
     out = {}
     n = 1 << args.dot_log2
-    for kind in ("well", "ill"):
+    for kind in ("well", "ill", "range"):
         if kind == "well":
             x, y = gen.uniform(n, 1), gen.uniform(n, 2)
-        else:
+        elif kind == "ill":
             x, y = gen.ill_pair(n, seed=3)
+        else:  # |x|,|y| in 2^[-540, 1): 2.5 % of the products fall below 2^-960, in every CTA's share,
+            # so every CTA takes the full-range pass (NEXT-4): its worst case
+            x, y = gen.loguniform(n, 5, -540, 0), gen.loguniform(n, 6, -540, 0)
         xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
         del x, y
         res = torch.zeros(1, dtype=torch.float64, device="cuda")

@@ -197,9 +197,10 @@ int pbicgstab_spmv(pbcg_handle *h, const double *x_local, double *y_local);
  * flags: bit 1 (2) = some input is NaN/Inf (PBCG_ENONFINITE); otherwise
  * bit 0 (1) = some nonzero product has |fl(x*y)| < 2^-960 or >= 2^1000
  * (R-9), i.e. lies outside the fast pass's exact zone.  Single GPU
- * (h NULL, or one rank without NCCL): such a dot is recomputed by the
- * full-range pass (exact 106-bit products, accumulator down to 2^-2148;
- * SURVEY §8(f) NEXT-4), so the result is still the exactly rounded sum and
+ * (h NULL, or one rank without NCCL): the CTAs that met such a product
+ * correct it in the full-range pass (exact 106-bit products, accumulator
+ * down to 2^-2148), so the result is still the exactly
+ * rounded sum and
  * the call returns PBCG_OK unless that sum overflows binary64 (+-inf,
  * PBCG_ERANGE).  Distributed handles: PBCG_ERANGE, result unspecified.
  * When bit 1 is set, bit 0 is unspecified.  n_local = 0 gives +0.0

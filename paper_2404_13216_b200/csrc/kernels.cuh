@@ -198,14 +198,18 @@ __device__ void phase_finalize(int phase, Scalars *sc, const double *d, unsigned
 // ------------------------------------------------------------------------
 // Full-range EXDOT (closes reading R-9 for exdot).  The
 // fast kernels are exact for every product whose TwoProd is exact; a product
-// outside that zone raises FLAG_RANGE.  The last CTA of a flagged standalone
-// dot then recomputes it from the definition: each product formed exactly as
-// the 106-bit integer mx*my times 2^(ex+ey), ex+ey >= -2148, added into an
-// extended superaccumulator of XS_L 32-bit digits with LSB weight 2^-2148
-// (the binary64 product range), and rounded once (RN-even, subnormals,
-// overflow to +-inf).  One CTA: a rare, slow fallback.
+// outside that zone raises FLAG_RANGE.  In a standalone single-GPU dot, each
+// CTA that raised it corrects ITS OWN flagged products (cta_full_range): the
+// exact product -- the 106-bit integer mx*my times 2^(ex+ey), ex+ey >= -2148
+// -- minus what its FPE received, into an extended superaccumulator of XS_L
+// 32-bit digits with LSB weight 2^-2148 (the binary64 product range),
+// normalised and added into gacc[XS_OFF ..].  The last CTA adds the fast
+// words (2^-1074 = extended bit 1074) and rounds once (RN-even, subnormals,
+// overflow to +-inf).  Only the flagged CTAs pay, in parallel.
 // ------------------------------------------------------------------------
-constexpr int XS_L = 136;  // 4352 bits: 2^-2148 .. 2^2204 (products < 2^2048, sums of < 2^40 of them)
+constexpr int XS_L = 136;   // 4352 bits: 2^-2148 .. 2^2204 (products < 2^2048, sums of < 2^40 of them)
+constexpr int XS_OFF = 72;  // gacc word offset of the extended accumulator (PH_EXDOT, ND = 1)
+constexpr int XS_GW = XS_OFF + XS_L;  // gacc words a full-range EXDOT needs
 
 __device__ __forceinline__ void dbl_parts(double v, unsigned long long &m, int &e) {
     const unsigned long long b = (unsigned long long)__double_as_longlong(v);
@@ -214,71 +218,125 @@ __device__ __forceinline__ void dbl_parts(double v, unsigned long long &m, int &
     if (E) { m |= 1ull << 52; e = E - 1075; } else { e = -1074; }
 }
 
-// all threads of the CTA; returns the exactly rounded sum in every thread
-__device__ double full_range_dot_cta(int64_t n, const double *x, const double *y) {
-    __shared__ unsigned long long S[XS_L];
-    __shared__ double res;
-    for (int i = threadIdx.x; i < XS_L; i += blockDim.x) S[i] = 0ull;
-    __syncthreads();
-    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
-        const double a = x[k], b = y[k];
-        if (a == 0.0 || b == 0.0) continue;
-        unsigned long long ma, mb;
-        int ea, eb;
-        dbl_parts(a, ma, ea);
-        dbl_parts(b, mb, eb);
-        const unsigned long long lo = ma * mb, hi = __umul64hi(ma, mb);  // the 106-bit product
-        const int off = ea + eb + 2148;                                    // >= 0
-        const int w = off >> 5, sh = off & 31;
-        const unsigned long long l2 = lo << sh;
-        const unsigned long long h2 = (hi << sh) | (sh ? (lo >> (64 - sh)) : 0ull);
-        const unsigned long long top = sh ? (hi >> (64 - sh)) : 0ull;
-        const long long d[5] = {(long long)(l2 & 0xFFFFFFFFull), (long long)(l2 >> 32), (long long)(h2 & 0xFFFFFFFFull),
-                                (long long)(h2 >> 32), (long long)top};
-        const bool neg = (a < 0.0) != (b < 0.0);
+// the exact product a*b (finite) into the shared extended accumulator
+__device__ __forceinline__ void xs_add_product(unsigned long long *X, double a, double b) {
+    if (a == 0.0 || b == 0.0) return;
+    unsigned long long ma, mb;
+    int ea, eb;
+    dbl_parts(a, ma, ea);
+    dbl_parts(b, mb, eb);
+    const unsigned long long lo = ma * mb, hi = __umul64hi(ma, mb);  // the 106-bit product
+    const int off = ea + eb + 2148;                                    // >= 0
+    const int w = off >> 5, sh = off & 31;
+    const unsigned long long l2 = lo << sh;
+    const unsigned long long h2 = (hi << sh) | (sh ? (lo >> (64 - sh)) : 0ull);
+    const unsigned long long top = sh ? (hi >> (64 - sh)) : 0ull;
+    const long long d[5] = {(long long)(l2 & 0xFFFFFFFFull), (long long)(l2 >> 32), (long long)(h2 & 0xFFFFFFFFull),
+                            (long long)(h2 >> 32), (long long)top};
+    const bool neg = (a < 0.0) != (b < 0.0);
 #pragma unroll
-        for (int j = 0; j < 5; ++j)
-            if (d[j]) sacc_add_shared(&S[w + j], neg ? -d[j] : d[j]);
+    for (int j = 0; j < 5; ++j)
+        if (d[j]) sacc_add_shared(&X[w + j], neg ? -d[j] : d[j]);
+}
+
+// carry-propagate XS_L signed digits into [0, 2^32) (top word signed); one thread
+__device__ __forceinline__ void xs_normalize(long long *wd) {
+    long long carry = 0;
+    for (int i = 0; i < XS_L - 1; ++i) {
+        const long long v = wd[i] + carry;
+        carry = v >> 32;
+        wd[i] = v & 0xFFFFFFFFll;
+    }
+    wd[XS_L - 1] += carry;
+}
+
+// round the normalised extended value once (RN-even, subnormals, +-inf); one thread
+__device__ double xs_round(long long *wd) {
+    const bool neg = wd[XS_L - 1] < 0;
+    if (neg) {  // magnitude (two's complement negation over the digits)
+        unsigned long long c = 1;
+        for (int i = 0; i < XS_L; ++i) {
+            const unsigned long long v = (unsigned long long)(~(unsigned)wd[i]) + c;
+            wd[i] = (long long)(v & 0xFFFFFFFFull);
+            c = v >> 32;
+        }
+    }
+    int t = -1;  // highest set bit
+    for (int i = XS_L - 1; i >= 0 && t < 0; --i)
+        if (wd[i]) t = 32 * i + 31 - __clz((unsigned)wd[i]);
+    double r = 0.0;
+    if (t >= 0) {
+        auto bit = [&](int k) -> unsigned { return k < 0 ? 0u : (unsigned)(wd[k >> 5] >> (k & 31)) & 1u; };
+        const int q = max(t - 52, 1074);  // the result's LSB: 53 bits, or the subnormal quantum 2^-1074
+        unsigned long long M = 0;
+        for (int k = t; k >= q; --k) M = (M << 1) | bit(k);
+        const unsigned half = bit(q - 1);
+        bool sticky = false;
+        for (int k = q - 2; k >= 0 && !sticky; --k) sticky = bit(k) != 0u;
+        if (half && (sticky || (M & 1ull))) ++M;
+        r = scalbn((double)M, q - 2148);  // exact, or +inf on overflow
+        if (neg) r = -r;
+    }
+    return r;
+}
+
+// A CTA whose fast pass raised a flag, at its end (all threads; S.flags holds
+// the CTA's flags).  Its elements are read once more: a NaN/Inf input makes
+// the dot non-finite; a flagged product of finite operands
+// had entered the FPE as p + e with e inexact (|x y| < 2^-960), so the exact
+// correction x*y - p - e goes into the extended accumulator X.  If a product
+// is huge (|p| >= 2^1000: the FPE's sums may have overflowed), the CTA's fast
+// words are dropped and X takes all of its products exactly.  X is then added into
+// gacc[XS_OFF ..].  each(f) calls f(i) for every element index i of this CTA,
+// spread over its threads; X: NX * XS_L words of shared scratch (NX > 1: one
+// accumulator per warp, fewer same-address atomics, summed at the end).  The
+// hot loops are untouched: only flagged CTAs pay, one more read of their share.
+template <int NX, class Each>
+__device__ void cta_full_range(CtaSacc<1> &S, unsigned long long *X, long long *gacc, const double *x, const double *y,
+                               Each each) {
+    __shared__ int poisoned;
+    unsigned long long *Xw = X + ((threadIdx.x >> 5) % NX) * XS_L;
+    for (int i = threadIdx.x; i < NX * XS_L; i += blockDim.x) X[i] = 0ull;
+    if (threadIdx.x == 0) poisoned = 0;
+    __syncthreads();
+    each([&](int64_t i) {
+        const double a = x[i], b = y[i];
+        if (!isfinite(a) || !isfinite(b)) {
+            atomicOr(&S.flags, FLAG_NONFINITE);
+            return;
+        }
+        const double p = __dmul_rn(a, b), e = __fma_rn(a, b, -p);  // as the fast pass formed them
+        const unsigned ep = (unsigned)(__double2hiint(p) >> 20) & 0x7FFu;
+        if (((((ep - 63u) >= 1960u) & !(is_zero(a) | is_zero(b))) | (ep == 0x7FFu)) == 0u) return;  // not flagged
+        if (ep >= 63u) {  // |p| >= 2^1000: the FPE's TwoSums may have overflowed
+            poisoned = 1;
+            return;
+        }
+        xs_add_product(Xw, a, b);     // + the exact product
+        xs_add_product(Xw, -p, 1.0);  // - what the FPE received
+        xs_add_product(Xw, -e, 1.0);
+    });
+    __syncthreads();
+    if (S.flags & FLAG_NONFINITE) return;
+    if (poisoned) {  // the CTA's fast words are lost: all its products, exactly
+        for (int i = threadIdx.x; i < NX * XS_L; i += blockDim.x) X[i] = 0ull;
+        for (int i = threadIdx.x; i < SACC_L; i += blockDim.x) S.w[0][i] = 0ull;
+        __syncthreads();
+        each([&](int64_t i) { xs_add_product(Xw, x[i], y[i]); });
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        long long *wd = (long long *)S;
-        long long carry = 0;
-        for (int i = 0; i < XS_L - 1; ++i) {  // normalise
-            const long long v = wd[i] + carry;
-            carry = v >> 32;
-            wd[i] = v & 0xFFFFFFFFll;
+    if (NX > 1) {  // the warps' accumulators into X[0 .. XS_L) (each word < NX * 2^33 in magnitude)
+        for (int i = threadIdx.x; i < XS_L; i += blockDim.x) {
+            long long t = 0;
+            for (int k = 0; k < NX; ++k) t += (long long)X[k * XS_L + i];
+            X[i] = (unsigned long long)t;
         }
-        wd[XS_L - 1] += carry;
-        const bool neg = wd[XS_L - 1] < 0;
-        if (neg) {  // magnitude (two's complement negation over the digits)
-            unsigned long long c = 1;
-            for (int i = 0; i < XS_L; ++i) {
-                const unsigned long long v = (unsigned long long)(~(unsigned)wd[i]) + c;
-                wd[i] = (long long)(v & 0xFFFFFFFFull);
-                c = v >> 32;
-            }
-        }
-        int t = -1;  // highest set bit
-        for (int i = XS_L - 1; i >= 0 && t < 0; --i)
-            if (wd[i]) t = 32 * i + 31 - __clz((unsigned)wd[i]);
-        double r = 0.0;
-        if (t >= 0) {
-            auto bit = [&](int k) -> unsigned { return k < 0 ? 0u : (unsigned)(wd[k >> 5] >> (k & 31)) & 1u; };
-            const int q = max(t - 52, 1074);  // the result's LSB: 53 bits, or the subnormal quantum 2^-1074
-            unsigned long long M = 0;
-            for (int k = t; k >= q; --k) M = (M << 1) | bit(k);
-            const unsigned half = bit(q - 1);
-            bool sticky = false;
-            for (int k = q - 2; k >= 0 && !sticky; --k) sticky = bit(k) != 0u;
-            if (half && (sticky || (M & 1ull))) ++M;
-            r = scalbn((double)M, q - 2148);  // exact, or +inf on overflow
-            if (neg) r = -r;
-        }
-        res = r;
+        __syncthreads();
     }
+    if (threadIdx.x == 0) xs_normalize((long long *)X);
     __syncthreads();
-    return res;
+    for (int i = threadIdx.x; i < XS_L; i += blockDim.x)
+        if (X[i]) atomicAdd((unsigned long long *)&gacc[XS_OFF + i], X[i]);
 }
 
 // Last CTA of a dot kernel: collect + normalise gacc; then either round and
@@ -300,18 +358,22 @@ __device__ void last_cta_finish(CtaSacc<ND> &S, long long *gacc, unsigned *ticke
             }
         }
         __syncthreads();
-        // rare error path: a flagged standalone dot is classified as
-        // non-finite if any input is NaN/Inf, else range
-        if (gflags && cx) {
-            for (int64_t i = threadIdx.x; i < cn; i += blockDim.x)
-                if (!isfinite(cx[i]) || !isfinite(cy[i])) atomicOr(&S.flags, FLAG_NONFINITE);
-            __syncthreads();
-            // finite inputs, a product outside the fast zone: the full-range pass (NEXT-4)
-            if (!(S.flags & FLAG_NONFINITE)) {
-                const double r = full_range_dot_cta(cn, cx, cy);
-                if (threadIdx.x == 0) S.rounded[0] = r;
-                __syncthreads();
+        // a flagged standalone dot with finite inputs (the flagged CTAs have
+        // classified their elements): the fast words of the unflagged CTAs plus
+        // the flagged CTAs' extended sums, rounded once (NEXT-4)
+        if constexpr (ND == 1) if (cx && (gflags & FLAG_RANGE) && !(gflags & FLAG_NONFINITE)) {
+            __shared__ long long X[XS_L];
+            for (int i = threadIdx.x; i < XS_L; i += blockDim.x) {
+                X[i] = __ldcg(&gacc[XS_OFF + i]);
+                gacc[XS_OFF + i] = 0;
             }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int i = 0; i < SACC_L; ++i) X[i + 33] += w[i] * (1ll << 18);  // 2^-1074 = 2^(32*33+18) * 2^-2148
+                xs_normalize(X);
+                S.rounded[0] = xs_round(X);
+            }
+            __syncthreads();
         }
         if (threadIdx.x == 0) {
             unsigned f = gflags | (S.flags & (FLAG_RANGE | FLAG_NONFINITE));
@@ -427,6 +489,24 @@ __global__ void __launch_bounds__(BS) multidot_kernel(MultiDotArgs a) {
     }
 #pragma unroll
     for (int d = 0; d < ND; ++d) acc[d].warp_merge(S.w[d]);
+    if constexpr (ND == 1) {
+        if (a.finalize && a.phase == PH_EXDOT) {  // standalone dot: flagged CTAs take the full-range pass
+            __shared__ unsigned long long X[XS_L];
+            if (flags) atomicOr(&S.flags, flags);
+            flags = 0;
+            __syncthreads();
+            if (S.flags)
+                cta_full_range<1>(S, X, a.gacc, a.x[0], a.y[0], [&](auto f) {
+                    const bool al = ((((uintptr_t)a.x[0]) | ((uintptr_t)a.y[0])) & 15) == 0;
+                    const int64_t m = al ? n >> 1 : n;  // pairs (aligned) or elements, as the fast pass
+                    for (int64_t p0 = (int64_t)blockIdx.x * BS; p0 < m; p0 += stride)
+                        for (int64_t p = p0 + threadIdx.x; p < min(p0 + BS, m); p += blockDim.x) {
+                            if (al) { f(2 * p); f(2 * p + 1); } else f(p);
+                        }
+                    if (al && (n & 1) && blockIdx.x == 0 && threadIdx.x == 0) f(n - 1);
+                });
+        }
+    }
     if (cta_sacc_publish<ND>(S, flags, a.gacc, a.ticket)) {
         const bool cls = (ND == 1 && a.phase == PH_EXDOT);
         last_cta_finish<ND>(S, a.gacc, a.ticket, a.phase, a.finalize, a.sc, a.hist, a.out, a.out_flags,

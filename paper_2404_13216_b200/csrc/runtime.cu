@@ -210,6 +210,7 @@ extern "C" int pbcg_sacc_words(void) { return SACC_L; }
 // handle
 // ----------------------------------------------------------------------------
 static constexpr int GW4 = 4 * SACC_L + SACC_FLAGW;  // words of a 4-dot reduction buffer
+static_assert(GW4 >= XS_GW, "a phase buffer also holds the full-range EXDOT accumulator");
 static constexpr int NPH = 5;                        // reduction buffers: init, A, B, true, exdot
 static constexpr int K_BS = 256;
 static constexpr int PLAIN_GRID = 1024;  // >= any K2/K3 stream grid (one CTA per SM)
@@ -1850,13 +1851,13 @@ static int scratch(Scratch **out) {
         CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         S.grid1 = grid_for((const void *)multidot_kernel<1, K_NP, K_NE, K_BS, U_MD1>, K_BS, nsm);
         S.gridp = grid_for((const void *)plain_dot_kernel<K_BS>, K_BS, nsm);
-        CUDA_TRY(cudaMalloc(&S.gacc, sizeof(long long) * (SACC_L + SACC_FLAGW)));
+        CUDA_TRY(cudaMalloc(&S.gacc, sizeof(long long) * XS_GW));
         CUDA_TRY(cudaMalloc(&S.ticket, 64));
         CUDA_TRY(cudaMalloc(&S.out, 64));
         CUDA_TRY(cudaMalloc(&S.flags, 64));
         CUDA_TRY(cudaMalloc(&S.partials, sizeof(double) * (S.gridp + 1)));
         CUDA_TRY(cudaMalloc(&S.pticket, 64));
-        CUDA_TRY(cudaMemset(S.gacc, 0, sizeof(long long) * (SACC_L + SACC_FLAGW)));
+        CUDA_TRY(cudaMemset(S.gacc, 0, sizeof(long long) * XS_GW));
         CUDA_TRY(cudaMemset(S.ticket, 0, 64));
         CUDA_TRY(cudaMemset(S.pticket, 0, 64));
         CUDA_TRY(cudaDeviceSynchronize());

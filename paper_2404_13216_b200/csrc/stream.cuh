@@ -572,6 +572,20 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a
     __syncwarp();
     acc.warp_merge(S.w[0]);
     if (ND == 2) acc2.warp_merge(s1);
+    if constexpr (ND == 1) {
+        if (a.finalize && a.phase == PH_EXDOT) {  // standalone dot: a flagged CTA corrects its products (NEXT-4)
+            if (flags) atomicOr(&S.flags, flags);
+            flags = 0;
+            __syncthreads();  // the ring is drained: its memory is the scratch
+            if (S.flags)
+                cta_full_range<NCW + 1>(S, (unsigned long long *)buf, a.gacc, a.x[0], a.y[0], [&](auto f) {
+                    for (int64_t tile = blockIdx.x; tile * T < n; tile += gridDim.x) {
+                        const int64_t e = min(n, tile * T + T);
+                        for (int64_t i = tile * T + threadIdx.x; i < e; i += blockDim.x) f(i);
+                    }
+                });
+        }
+    }
     if (cta_sacc_publish<ND>(S, flags, a.gacc, a.ticket))
         last_cta_finish<ND>(S, a.gacc, a.ticket, a.phase, a.finalize, a.sc, a.hist, a.out, a.out_flags,
                             (ND == 1 && a.phase == PH_EXDOT) ? a.x[0] : nullptr, a.y[0], a.n);

@@ -208,3 +208,45 @@ def test_full_range_random(pb, seed):
         keep = (ex + ey) < -1000
         x, y = x[keep], y[keep]
     check(pb, x, y)
+
+
+@pytest.mark.parametrize("where", ["one", "spread", "all"])
+def test_full_range_many_ctas(pb, where):
+    # full-range pass across CTAs: the flagged CTAs recompute their own
+    # elements into the extended accumulator, the others keep their fast
+    # words; the last CTA adds both and rounds once
+    n = (1 << 21) + 37
+    x, y = gen.uniform(n, 11), gen.uniform(n, 12)
+    rng = np.random.default_rng(7)
+    if where == "all":
+        x, y = gen.loguniform(n, 5, -540, 0), gen.loguniform(n, 6, -540, 0)
+    else:
+        idx = [n // 3] if where == "one" else rng.choice(n, 40, replace=False)
+        for k, i in enumerate(idx):
+            x[i] = 2.0 ** -700 * (1 + k / 64)
+            y[i] = -(2.0 ** -300) if k % 2 else 2.0 ** -301
+        # the exact sum is tiny: cancel the fast part down to O(1e-300)
+        x[0] = 0.0
+    check(pb, x, y)
+    # the same through the general (unaligned) kernel: its CTAs walk strided pairs
+    import torch
+    xt = torch.from_numpy(np.concatenate([[0.0], x])).cuda()[1:]
+    yt = torch.from_numpy(np.concatenate([[0.0], y])).cuda()[1:]
+    want, wf = oracle.exdot(x, y)
+    got, gf = pb.exdot(xt, yt)
+    assert bits(got) == bits(want) and bool(gf & pb.FLAG_RANGE) == bool(wf & oracle.F_RANGE), (got, want, gf, wf)
+    # cancellation: the fast words and the extended sums meet in the low bits
+    x2 = np.concatenate([x, -x, [2.0 ** -600]])
+    y2 = np.concatenate([y, y, [-(2.0 ** -450)]])
+    assert check(pb, x2, y2) == -(2.0 ** -1050)
+
+
+def test_full_range_nonfinite_in_one_cta(pb):
+    n = 1 << 21
+    x, y = gen.uniform(n, 13), gen.uniform(n, 14)
+    x[n // 2] = 2.0 ** -700
+    y[n // 2] = 2.0 ** -400
+    x[n - 5] = np.inf
+    v, f = gpu_exdot(pb, x, y)
+    assert f & pb.FLAG_NONFINITE
+    check(pb, x, y)
