@@ -202,67 +202,38 @@ def run_gpu(args, rank, world, local_rank, dist):
         ok = bool(okt.item())
     clk = clocks.summary(tc0 - 0.05, tc1 + 0.05)
     out = {"ms": ms, "ok": ok, "iters": res.iterations, "clocks": clk}
-    # ---- the same K steps with plain fp64 dots (the
-    # paper's non-reproducible arm; its cost ratio is the ExBLAS overhead) ----
+    # ---- comparison arms, the same K steps each (SURVEY §8(f) NEXT-1..3) ----
+    def timed_arm(S_, **kw):
+        S_.start(b, tol=0.0, max_iter=W + K + 8, **kw)
+        S_.iterate(W)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record(S_.stream)
+        S_.iterate(K)
+        q1.record(S_.stream)
+        torch.cuda.synchronize()
+        tms = q0.elapsed_time(q1)
+        r_ = S_.finish(None)
+        if dist:
+            t = torch.tensor([tms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tms = float(t.item())
+        return {"value": K / (tms * 1e-3), "unit": "iter/s", "ms_per_step": tms / K, "valid": r_.iterations == W + K}
+
     if not args.no_extras:
-        S.start(b, tol=0.0, max_iter=W + K + 8, dot_mode="plain")
-        S.iterate(W)
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        p0.record(S.stream)
-        S.iterate(K)
-        p1.record(S.stream)
-        torch.cuda.synchronize()
-        pms = p0.elapsed_time(p1)
-        pres = S.finish(None)
-        if dist:
-            t = torch.tensor([pms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            pms = float(t.item())
-        out["plain"] = {"value": K / (pms * 1e-3), "unit": "iter/s", "ms_per_step": pms / K,
-                        "valid": pres.iterations == W + K}
-        # Algorithm 1 (classic BiCGStab, exact dots) on the same workload: the
-        # paper's other comparison column
-        S.start(b, tol=0.0, max_iter=W + K + 8, method="bicgstab")
-        S.iterate(W)
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        q0.record(S.stream)
-        S.iterate(K)
-        q1.record(S.stream)
-        torch.cuda.synchronize()
-        ams = q0.elapsed_time(q1)
-        ares = S.finish(None)
-        if dist:
-            t = torch.tensor([ams], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ams = float(t.item())
-        out["alg1"] = {"value": K / (ams * 1e-3), "unit": "iter/s", "ms_per_step": ams / K,
-                       "valid": ares.iterations == W + K}
-        # p-BiCGStab with residual replacement every 50 iterations (the paper's
-        # p-BiCGStabRR arm; 5 extra SpMVs per replacement)
-        S.start(b, tol=0.0, max_iter=W + K + 8, rr_period=50)
-        S.iterate(W)
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        q0.record(S.stream)
-        S.iterate(K)
-        q1.record(S.stream)
-        torch.cuda.synchronize()
-        rms = q0.elapsed_time(q1)
-        rres = S.finish(None)
-        if dist:
-            t = torch.tensor([rms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            rms = float(t.item())
-        out["rr"] = {"value": K / (rms * 1e-3), "unit": "iter/s", "ms_per_step": rms / K, "rr_period": 50,
-                     "valid": rres.iterations == W + K}
+        # plain fp64 dots: the paper's non-reproducible arm; its cost ratio is the ExBLAS overhead
+        out["plain"] = timed_arm(S, dot_mode="plain")
+        # Algorithm 1 (classic BiCGStab, exact dots): the paper's other comparison column
+        out["alg1"] = timed_arm(S, method="bicgstab")
+        # residual replacement every 50 iterations (p-BiCGStabRR; 5 extra SpMVs per replacement)
+        out["rr"] = dict(timed_arm(S, rr_period=50), rr_period=50)
+        # right Jacobi (NEXT-3): a column scaling of the stored matrix at setup, same kernels per iteration
+        Sj = pb.Solver(Al.row_ptr, Al.col, Al.val, A.n, row_begin=r0, row_end=r1, rank=rank, nranks=world,
+                       nccl_uid=uid, history_capacity=16, precond="jacobi")
+        out["jacobi"] = timed_arm(Sj)
+        Sj.close()
     # ---- per-kernel times: a second timed pass over the same K steps with
     # CUDA events around every launch (single rank) ----
     fmt = S.spmv_format()
@@ -497,6 +468,11 @@ def main():
         rr = out["rr"]
         rr["note"] = "same workload and K with residual replacement every 50 iterations (Alg. 2, exact dots; R-21)"
         line["pbicgstab_rr50"] = rr
+    if "jacobi" in out:
+        jc = out["jacobi"]
+        jc["note"] = ("same workload and K with right Jacobi (R-22: A D^-1 stored at setup, x = D^-1 y at the end); "
+                      "the iteration runs the same kernels on the scaled matrix")
+        line["pbicgstab_jacobi"] = jc
     line["bytes_per_iteration_per_gpu"] = by["iteration"]
     line["iteration_GBps_per_gpu"] = by["iteration"] / (ms_step * 1e-3) / 1e9
     line["iteration_frac_hbm"] = line["iteration_GBps_per_gpu"] / hbm
@@ -504,7 +480,8 @@ def main():
         sp_us = (kern["spmv_z"]["avg_us"] + kern["spmv_w"]["avg_us"]) / 2
         achieved = by["spmv"] / (sp_us * 1e-6) / 1e9
         tr = traffic_from_profiles(args.workload, "spmv")
-        line["roofline"] = {"kernel": "spmv (SpMV v=Az / t=Aw, 2 launches per step; C5: spmv_sellp_kernel)",
+        line["roofline"] = {"kernel": "spmv (SpMV v=Az / t=Aw, 2 launches per step; stencils: spmv_sellp_kernel, "
+                                      "C4: spmv_sellv_kernel)",
                             "bound": "hbm",
                             "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                             "traffic": tr, "peak_source": peak_src,
