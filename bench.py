@@ -176,6 +176,7 @@ def run_gpu(args, rank, world, local_rank, dist):
     time.sleep(0.3)
     # ---- timed region: K iterations replayed as CUDA-graph chunks ----
     S.start(b, tol=0.0, max_iter=W + K + 8)  # tol 0: every timed iteration does full work
+    exec_mode = S.exec_mode()  # 0: six kernels per iteration (graphs); 1: the fused small-system kernel
     S.iterate(W)  # warm-up (start() already captured the CUDA graph of one chunk)
     torch.cuda.synchronize()
     if dist:
@@ -201,7 +202,7 @@ def run_gpu(args, rank, world, local_rank, dist):
         dist.all_reduce(okt, op=dist.ReduceOp.MIN)
         ok = bool(okt.item())
     clk = clocks.summary(tc0 - 0.05, tc1 + 0.05)
-    out = {"ms": ms, "ok": ok, "iters": res.iterations, "clocks": clk}
+    out = {"ms": ms, "ok": ok, "iters": res.iterations, "clocks": clk, "exec_mode": exec_mode}
     # ---- comparison arms, the same K steps each (SURVEY §8(f) NEXT-1..3) ----
     def timed_arm(S_, **kw):
         S_.start(b, tol=0.0, max_iter=W + K + 8, **kw)
@@ -449,8 +450,11 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_config(args, A),
             "valid": out["ok"],
-            # K2, finalize A, SpMV, K3, finalize B, SpMV per iteration (per rank; NCCL kernels not counted)
-            "gpu_launches": 6 * K}
+            # six-kernel path: K2, finalize A, SpMV, K3, finalize B, SpMV per iteration (per rank; NCCL
+            # kernels not counted); fused small-system kernel: one cooperative launch runs the K iterations
+            "gpu_launches": 6 * K if out["exec_mode"] == 0 else 1,
+            "exec_mode": "six kernels per iteration, CUDA graphs" if out["exec_mode"] == 0
+            else "fused small-system kernel (one cooperative launch per iterate call)"}
     line["spmv_format"] = out["spmv_format"]
     if "plain" in out:
         pl = out["plain"]

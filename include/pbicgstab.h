@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define PBCG_ABI_VERSION 5
+#define PBCG_ABI_VERSION 6
 
 /* return codes of every entry point (never an abort across the ABI) */
 enum pbcg_rc {
@@ -253,6 +253,15 @@ int pbcg_get_vector(pbcg_handle *h, int32_t which, double *out);
  * are sigma-sorted.  The fold of every row is the CSR fma chain regardless
  * (R-6).  Host-only, no synchronisation. */
 int pbcg_spmv_format(pbcg_handle *h, int64_t *out8);
+
+/* How pbicgstab_iterate runs the iterations of the solve started last on
+ * this handle: *mode = 0: six kernels per iteration (K2, SpMV, K3, SpMV and
+ * the two side-stream finalizes), replayed from CUDA graphs; 1: the fused
+ * small-system kernel (single rank, n <= 131072 rows, exact dots, Algorithm 2
+ * without replacement), ONE cooperative launch per iterate
+ * call.  PBCG_SMALL=0 in the environment disables the fused kernel.
+ * Host-only. */
+int pbcg_exec_mode(const pbcg_handle *h, int32_t *mode);
 
 /* Spill counters of a -DPBCG_DEBUG_COUNTERS build (16 uint64; zeros in the
  * release build): [1] warp spill votes, [2] overflow-tier entries, [3]

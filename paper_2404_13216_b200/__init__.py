@@ -102,6 +102,7 @@ def lib(build_if_missing: bool = True) -> ctypes.CDLL:
         L.pbcg_profile_iterations.argtypes = [vp, i32, vp]
         L.pbcg_debug_counters.argtypes = [vp, i32]
         L.pbcg_spmv_format.argtypes = [vp, vp]
+        L.pbcg_exec_mode.argtypes = [vp, vp]
         L.pbcg_get_vector.argtypes = [vp, i32, vp]
         _lib = L
     return _lib
@@ -275,6 +276,13 @@ class Solver:
         keys = ("rows", "nnz", "sell_entries", "explicit_cols", "slot_records", "bytes_per_spmv", "max_row_len",
                 "sigma_sorted")
         return {k: int(v) for k, v in zip(keys, out)}
+
+    def exec_mode(self) -> int:
+        """0: six kernels per iteration (CUDA graphs); 1: the fused small-system
+        kernel, one launch per iterate call (include/pbicgstab.h pbcg_exec_mode)."""
+        m = ctypes.c_int32(0)
+        _check(lib().pbcg_exec_mode(self._h, ctypes.byref(m)))
+        return int(m.value)
 
     VEC = dict(b=0, x=1, r=2, rh=3, p=4, s=5, z=6, q=7, y=8, w=9, t=10, v=11)
 

@@ -31,6 +31,7 @@
 
 #include "../../include/pbicgstab.h"
 #include "kernels.cuh"
+#include "small.cuh"
 #include "stream.cuh"
 
 using namespace pbcg;
@@ -270,6 +271,8 @@ struct Rank {
            *t = nullptr, *v = nullptr, *b = nullptr, *tmp = nullptr;
     double *zpad = nullptr, *wpad = nullptr, *xpad = nullptr;
     long long *gacc[NPH] = {};
+    long long *gsm = nullptr;  // fused small-system kernel: phase buffers gA[2], gB[2] (GW4 words each)
+    unsigned *gbar = nullptr;  // its grid barrier
     unsigned *tickets = nullptr;
     Scalars *sc = nullptr;
     double *hist = nullptr;
@@ -327,6 +330,7 @@ struct pbcg_handle {
     int hist_cap = 10001;
     Scalars *h_sc = nullptr;      // pinned mirror of rank 0's scalars
     int grid_md = 0;
+    int small_grid = 0;  // fused small-system kernel: cooperative grid (0: not eligible)
     cudaGraphExec_t gexec = nullptr;
     int g_iters = 0;
     cudaEvent_t ev[8] = {};
@@ -389,6 +393,8 @@ static void carve_rank(Carver &C, Rank &R, int hist_cap, bool comm_only, bool pr
     for (int k = 0; k < NPH; ++k) R.part[k] = C.take<double>((size_t)PLAIN_GRID * 4);
     R.pdsum = C.take<double>((size_t)NPH * 4);
     R.tickets = C.take<unsigned>(16);
+    R.gsm = C.take<long long>(4 * (size_t)GW4);  // fused small-system kernel: gA[2], gB[2]
+    R.gbar = C.take<unsigned>(16);
     R.sc = C.take<Scalars>(1);
     R.bad = C.take<int>(4);
 }
@@ -1208,6 +1214,7 @@ static int build_sellv(pbcg_handle *h, Rank &R) {
 }
 
 static int copy_own_to_pad(pbcg_handle *h, double *Rank::*src_member, int which);
+static int small_grid_for(pbcg_handle *h);
 
 // Right Jacobi (NEXT-3, R-22): d = diag(A) per rank, d into the padded
 // x layout + halo (the columns' diagonals), then A' = A D^-1 in the SELL.
@@ -1420,6 +1427,7 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
     }
     RC_TRY(stream_attrs());
     h->grid_md = grid_for((const void *)multidot_kernel<4, K_NP, K_NE, K_BS, U_MD4>, K_BS, h->nsm);
+    h->small_grid = small_grid_for(h);
     CUDA_TRY(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
     for (auto &e : h->ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1526,6 +1534,8 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
     s0.hist_cap = h->hist_cap;
     s0.status = ST_RUNNING;
     for (auto &R : h->R) {
+        CUDA_TRY(cudaMemsetAsync(R.gsm, 0, sizeof(long long) * 4 * (size_t)GW4, h->stream));
+        CUDA_TRY(cudaMemsetAsync(R.gbar, 0, sizeof(unsigned) * 16, h->stream));
         CUDA_TRY(cudaMemcpyAsync(R.sc, &s0, sizeof(Scalars), cudaMemcpyHostToDevice, h->stream));
         CUDA_TRY(cudaMemsetAsync(R.hist, 0, sizeof(double) * (size_t)h->hist_cap * H_COLS, h->stream));
         CUDA_TRY(cudaMemsetAsync(R.bad, 0, sizeof(int) * 4, h->stream));
@@ -1697,7 +1707,63 @@ static int enqueue_replacement(pbcg_handle *h) {
     return PBCG_OK;
 }
 
+// Fused small-system kernel (csrc/small.cuh): single rank, exact dots,
+// Algorithm 2 without replacement, n <= SMALL_N_MAX rows, cooperative launch
+// available.  PBCG_SMALL=0 turns it off (A/B runs, and the six-kernel path's
+// own tests).
+static constexpr int SMALL_BS = 256;
+static constexpr int64_t SMALL_N_MAX = 1 << 17;
+static int small_grid_for(pbcg_handle *h) {
+    if (h->comm_only || h->V != 1 || h->comm || h->R.empty()) return 0;
+    const Rank &R = h->R[0];
+    if (R.n == 0 || R.n > SMALL_N_MAX) return 0;
+    int coop = 0, per_sm = 0;
+    if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->dev) != cudaSuccess || !coop) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pbcg_small_kernel<SMALL_BS>, SMALL_BS, 0) != cudaSuccess)
+        return 0;
+    const int64_t gran = R.h_perm.empty() ? 32 : 256;  // small.cuh: CTA row ranges
+    const int64_t windows = (R.n + gran - 1) / gran;
+    // at most 64 CTAs: C1 ran 55.1K iter/s at 64, 53.9K at 128 (one barrier counter, fewer arrivals)
+    int64_t g = std::min<int64_t>({windows, (int64_t)std::max(per_sm, 0) * h->nsm, (int64_t)64});
+    if (const char *e = getenv("PBCG_SMALL_GRID")) g = std::max<int64_t>(1, std::min<int64_t>(g, atoi(e)));  // A/B runs
+    return (int)g;
+}
+static bool small_on(const pbcg_handle *h) {
+    const char *e = getenv("PBCG_SMALL");
+    return !(e && e[0] == '0') && h->small_grid > 0 && h->method == PBCG_METHOD_PBICGSTAB && h->dot_mode == PBCG_DOT_EXACT &&
+           h->rr_period == 0;
+}
+static int launch_small(pbcg_handle *h, int32_t iters) {
+    Rank &R = h->R[0];
+    SmallArgs a{};
+    a.n = R.n;
+    a.slice_off = R.slice_off;
+    a.row_len = R.row_len;
+    a.val = R.sval;
+    a.col = R.scol;
+    a.perm = R.h_perm.empty() ? nullptr : R.perm;
+    a.x = R.x; a.r = R.r; a.rh = R.rh; a.p = R.p; a.s = R.s; a.q = R.q; a.y = R.y; a.t = R.t; a.v = R.v;
+    a.z = R.z();
+    a.w = R.w();
+    a.zpad = R.zpad;
+    a.wpad = R.wpad;
+    a.gA[0] = R.gsm; a.gA[1] = R.gsm + GW4; a.gB[0] = R.gsm + 2 * GW4; a.gB[1] = R.gsm + 3 * GW4;
+    a.bar = R.gbar;
+    a.sc = R.sc;
+    a.hist = R.hist;
+    a.iters = iters;
+    void *args[] = {&a};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void *)pbcg_small_kernel<SMALL_BS>, dim3(h->small_grid),
+                                         dim3(SMALL_BS), args, 0, h->stream));
+    return PBCG_OK;
+}
+
 static int iterate_impl(pbcg_handle *h, int32_t k, int chunk, bool graphs) {
+    if (small_on(h)) {  // the fused small-system kernel: one launch runs all k iterations (or stops when done)
+        if (k > 0) RC_TRY(launch_small(h, k));
+        h->it_enq += k;
+        return PBCG_OK;
+    }
     if (graphs && h->stream == nullptr) graphs = false;  // cannot capture the legacy stream
     while (k > 0) {
         // iterations until the next replacement boundary (all of k without replacement)
@@ -1949,6 +2015,12 @@ extern "C" int pbcg_nccl_unique_id(uint8_t *out128) {
 }
 
 extern "C" int pbcg_abi_version(void) { return PBCG_ABI_VERSION; }
+
+extern "C" int pbcg_exec_mode(const pbcg_handle *h, int32_t *mode) {
+    if (!h || !mode) return fail(PBCG_EINVAL, "exec_mode: null argument");
+    *mode = small_on(h) ? 1 : 0;
+    return PBCG_OK;
+}
 
 // Per-kernel device time of k more iterations (single rank): direct launches
 // bracketed by CUDA events on the handle's stream.  ms[0..3] = summed ms of

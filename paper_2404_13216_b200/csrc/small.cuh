@@ -1,0 +1,217 @@
+// small.cuh -- the whole p-BiCGStab iteration (Alg. 2 l.70-82) in ONE
+// persistent kernel, for systems small enough that the six-kernel iteration
+// is launch- and dependency-latency bound (C1: 4,096 rows).
+//
+// B200 design (DESIGN.md §5 "Fused small-system kernel"): a cooperative grid
+// of G CTAs (co-residency guaranteed by the cooperative launch), each owning
+// a contiguous range of 256-row sigma windows -- so the rows its K2/K3 part
+// updates are exactly the rows its SpMV part produces, and v, t never cross
+// CTAs (rows not permuted: whole 32-row slices, so up to one CTA per slice).
+// Per iteration:
+//   K2 rows + phase-A products (each lane deposits its own p and e: one or
+//     two rows per lane, no warp aggregation) -> CTA superaccumulator ->
+//     int64 red into gA
+//   grid barrier (z of every row and every CTA's words are complete)
+//   every CTA: normalise + round the 4 dots, the scalar step (omega) on its
+//     own copy of the scalars (CTA 0: the global ones + the history)
+//   SpMV v = A z over its rows; CTA barrier
+//   K3 rows + phase-B products -> gB; grid barrier; round, beta/alpha'/stop
+//   SpMV t = A w over its rows; CTA barrier
+// Two grid barriers per iteration instead of six launches and two
+// fork/joins.  The arithmetic is the same as the six-kernel path element by
+// element (FMA policy F, the per-row fma chain of the SpMV, exact dots), so
+// the trajectory is bit-identical to it and to the oracle.
+#pragma once
+#include "kernels.cuh"
+
+namespace pbcg {
+
+struct SmallArgs {
+    int64_t n;
+    const int64_t *slice_off;
+    const int32_t *row_len;
+    const double *val;
+    const int32_t *col;   // pos-relative x-buffer index
+    const int32_t *perm;  // position -> row, or null
+    double *x, *r, *rh, *p, *s, *q, *y, *t, *v;
+    double *z, *w;               // own rows of the padded buffers
+    const double *zpad, *wpad;   // padded bases (x-buffer index 0)
+    long long *gA[2], *gB[2];    // phase buffers, by iteration parity
+    unsigned *bar;               // grid barrier: [0] arrivals, [1] generation
+    Scalars *sc;
+    double *hist;
+    int iters;                   // at most this many iterations in this launch
+};
+
+// Sense-by-generation grid barrier (all CTAs co-resident: cooperative launch).
+__device__ __forceinline__ void grid_barrier(unsigned *bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *gen = bar + 1;
+        const unsigned g0 = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g0) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// this CTA's words into the phase buffer, not normalised: the whole grid adds
+// at most 2 n <= 2^18 signed 32-bit digits into any word (< 2^51, no int64
+// overflow); the readers normalise once (cta_sacc_collect)
+template <int ND>
+__device__ __forceinline__ void small_publish(CtaSacc<ND> &S, unsigned flags, long long *g) {
+    if (flags) atomicOr(&S.flags, flags);
+    __syncthreads();
+    for (int i = threadIdx.x; i < ND * SACC_L; i += blockDim.x) {
+        const long long v = (long long)(&S.w[0][0])[i];
+        if (v) atomicAdd((unsigned long long *)&g[i], (unsigned long long)v);
+    }
+    if (threadIdx.x == 0) {
+        if (S.flags & FLAG_RANGE) atomicAdd((unsigned long long *)&g[ND * SACC_L], 1ull);
+        if (S.flags & FLAG_NONFINITE) atomicAdd((unsigned long long *)&g[ND * SACC_L + 1], 1ull);
+    }
+}
+
+// all CTAs: the words of one phase -> rounded dots -> the scalar step
+template <int ND>
+__device__ void small_round(CtaSacc<ND> &S, long long *g, int phase, Scalars *scl, double *hist) {
+    if (threadIdx.x == 0) S.flags = 0u;
+    unsigned gflags;
+    cta_sacc_collect<ND>(S, g, gflags);
+    long long *w = (long long *)&S.w[0][0];
+    if ((threadIdx.x >> 5) < ND) {  // one warp per dot
+        bool ovf = false;
+        const double rv = sacc_round_warp(w + (threadIdx.x >> 5) * SACC_L, &ovf);
+        if ((threadIdx.x & 31) == 0) {
+            S.rounded[threadIdx.x >> 5] = rv;
+            if (ovf) atomicOr(&S.flags, FLAG_RANGE);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) phase_finalize(phase, scl, S.rounded, gflags | (S.flags & FLAG_RANGE), hist, nullptr, nullptr);
+    __syncthreads();
+}
+
+// this CTA's positions [P0, P1): y[row(pos)] = (A x)[row], the row's ordered fma chain (R-6)
+__device__ __forceinline__ void small_spmv(const SmallArgs &a, int64_t P0, int64_t P1, const double *xb, double *yv) {
+    for (int64_t pos = P0 + threadIdx.x; pos < P1; pos += blockDim.x) {
+        const int64_t base = a.slice_off[pos >> 5] + (pos & 31);
+        const int len = a.row_len[pos];
+        double acc = 0.0;
+        for (int k = 0; k < len; ++k) acc = __fma_rn(a.val[base + 32 * k], xb[pos + a.col[base + 32 * k]], acc);
+        yv[a.perm ? (int64_t)a.perm[pos] : pos] = acc;
+    }
+}
+
+template <int BS>
+__global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
+    __shared__ CtaSacc<4> SA;
+    __shared__ CtaSacc<3> SB;
+    __shared__ Scalars scs;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n = a.n;
+    // whole sigma windows (256 rows) when rows are permuted, else whole slices
+    const int64_t gran = a.perm ? 256 : 32, nw = (n + gran - 1) / gran;
+    const int64_t P0 = min(n, gran * (nw * blockIdx.x / gridDim.x));
+    const int64_t P1 = min(n, gran * (nw * (blockIdx.x + 1) / gridDim.x));
+    Scalars *scl = blockIdx.x == 0 ? a.sc : &scs;  // CTA 0 keeps the global scalars and the history
+    double *hist = blockIdx.x == 0 ? a.hist : nullptr;
+    if (threadIdx.x == 0 && blockIdx.x != 0) scs = *a.sc;
+    __syncthreads();
+    const ExAccT<1, 1, 1> tp{};  // TwoProd + R-9 flag only
+    for (int k = 0; k < a.iters && !scl->done; ++k) {
+        const int par = scl->it & 1;
+        // ---- K2 (l.70-74) + (q,y), (y,y), (r0,s), (r0,z) ----
+        {
+            const bool first = scl->it == 0;
+            const double be = scl->beta, nom = -scl->omega, nal = -scl->alpha;
+            unsigned flags = 0;
+            cta_sacc_zero<4>(SA);
+            __syncthreads();
+            for (int64_t b0 = P0 + 32 * warp; b0 < P1; b0 += BS) {  // whole warps: the deposits are warp-wide
+                const int64_t i = b0 + lane;
+                const bool on = i < P1;
+                Prod P[4] = {};
+                if (on) {
+                    const double r = a.r[i], w = a.w[i], t = a.t[i], rh = a.rh[i];
+                    double p = r, s = w, z = t;  // beta_{-1} = 0: exact copies (R-3)
+                    if (!first) {
+                        const double v = a.v[i];
+                        p = __fma_rn(be, __fma_rn(nom, a.s[i], a.p[i]), r);  // l.70
+                        s = __fma_rn(be, __fma_rn(nom, a.z[i], a.s[i]), w);  // l.71
+                        z = __fma_rn(be, __fma_rn(nom, v, a.z[i]), t);       // l.72
+                    }
+                    const double q = __fma_rn(nal, s, r), y = __fma_rn(nal, z, w);  // l.73-74
+                    a.p[i] = p; a.s[i] = s; a.z[i] = z; a.q[i] = q; a.y[i] = y;
+                    const bool zy = is_zero(y), zr = is_zero(rh);
+                    P[0] = tp.prep(q, y, is_zero(q) | zy, flags);
+                    P[1] = tp.prep(y, y, zy, flags);
+                    P[2] = tp.prep(rh, s, zr | is_zero(s), flags);
+                    P[3] = tp.prep(rh, z, zr | is_zero(z), flags);
+                }
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {  // one or two rows per lane: direct deposits (no warp aggregation chain)
+                    if (is_nonzero(P[d].p)) sacc_deposit(SA.w[d], P[d].p);
+                    if (is_nonzero(P[d].e)) sacc_deposit(SA.w[d], P[d].e);
+                }
+            }
+            small_publish<4>(SA, flags, a.gA[par]);
+        }
+        grid_barrier(a.bar);
+        if (blockIdx.x == 0) {  // every CTA has read gB of the previous iteration: clear it for the next one
+            for (int i = threadIdx.x; i < 3 * SACC_L + SACC_FLAGW; i += BS) a.gB[par ^ 1][i] = 0;
+        }
+        small_round<4>(SA, a.gA[par], PH_A, scl, hist);  // l.76
+        if (scl->done) break;
+        // ---- SpMV v = A z (l.75) over this CTA's rows ----
+        small_spmv(a, P0, P1, a.zpad, a.v);
+        __syncthreads();
+        // ---- K3 (l.77-79) + (r0,r'), (r0,w'), (r',r') ----
+        {
+            const double al = scl->alpha, om = scl->omega, nal = -al, nom = -om;
+            unsigned flags = 0;
+            cta_sacc_zero<3>(SB);
+            __syncthreads();
+            for (int64_t b0 = P0 + 32 * warp; b0 < P1; b0 += BS) {
+                const int64_t i = b0 + lane;
+                const bool on = i < P1;
+                Prod P[3] = {};
+                if (on) {
+                    const double rh = a.rh[i], q = a.q[i], y = a.y[i];
+                    const double x = __fma_rn(om, q, __fma_rn(al, a.p[i], a.x[i]));  // l.77
+                    const double r = __fma_rn(nom, y, q);                            // l.78
+                    const double w = __fma_rn(nom, __fma_rn(nal, a.v[i], a.t[i]), y);  // l.79
+                    a.x[i] = x; a.r[i] = r; a.w[i] = w;
+                    const bool zr = is_zero(r), zh = is_zero(rh);
+                    P[0] = tp.prep(rh, r, zh | zr, flags);
+                    P[1] = tp.prep(rh, w, zh | is_zero(w), flags);
+                    P[2] = tp.prep(r, r, zr, flags);
+                }
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    if (is_nonzero(P[d].p)) sacc_deposit(SB.w[d], P[d].p);
+                    if (is_nonzero(P[d].e)) sacc_deposit(SB.w[d], P[d].e);
+                }
+            }
+            small_publish<3>(SB, flags, a.gB[par]);
+        }
+        grid_barrier(a.bar);
+        if (blockIdx.x == 0) {  // every CTA has read gA of this iteration
+            for (int i = threadIdx.x; i < 4 * SACC_L + SACC_FLAGW; i += BS) a.gA[par][i] = 0;
+        }
+        small_round<3>(SB, a.gB[par], PH_B, scl, hist);  // l.81-82, stopping and breakdown rules
+        if (scl->done) break;
+        // ---- SpMV t = A w (l.80) ----
+        small_spmv(a, P0, P1, a.wpad, a.t);
+        __syncthreads();
+    }
+}
+
+}  // namespace pbcg

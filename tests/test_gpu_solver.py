@@ -526,3 +526,59 @@ def test_jacobi_rejects_zero_diagonal(pb):
     with pytest.raises(pb.PbcgError) as e:
         solver(pb, A, precond="jacobi")
     assert e.value.rc == 1
+
+
+# ----------------------------------------------- fused small-system kernel ---
+
+@pytest.mark.parametrize("name", ["c1", "rand", "stencil3d", "ragged"])
+def test_fused_small_kernel(pb, name, monkeypatch):
+    # n <= 131072 rows, single rank, exact dots: one cooperative kernel runs
+    # whole chunks of iterations (csrc/small.cuh).  Same bits as the
+    # six-kernel path and as the oracle, resumed across launches of varied
+    # length (the phase buffers alternate by iteration parity), sigma-sorted
+    # rows (rand), a ragged last window (n % 256 != 0)
+    import torch
+    A = {"c1": lambda: gen.make_config("c1_2d64"),
+         "rand": lambda: gen.random_banded(20_000, seed=9, band=1500),
+         "stencil3d": lambda: gen.stencil(3, 40, 100.0),
+         "ragged": lambda: gen.random_banded(3_001, seed=5, band=700)}[name]()
+    M = 400
+    got = {}
+    for env in ("1", "0"):
+        monkeypatch.setenv("PBCG_SMALL", env)
+        S = solver(pb, A, history_capacity=M + 1)
+        b = gpu_b(pb, S, A)
+        S.start(b, tol=1e-10, max_iter=M)
+        assert S.exec_mode() == int(env)
+        for k in (1, 3, 7, 16, M):
+            S.iterate(k)
+        x = torch.zeros(A.n, dtype=torch.float64, device="cuda")
+        r = S.finish(x)
+        got[env] = (u64(x.cpu().numpy()), u64(S.history()), r.iterations, r.status)
+        S.close()
+    assert got["1"][2] == got["0"][2] and got["1"][3] == got["0"][3]
+    assert np.array_equal(got["1"][0], got["0"][0]) and np.array_equal(got["1"][1], got["0"][1])
+    monkeypatch.delenv("PBCG_SMALL")
+    S, O, x, r, H = run_both(pb, A, tol=1e-10, max_iter=M)
+    assert_same(O, x, r, H, A)
+
+
+def test_fused_small_kernel_stops(pb):
+    # max_iter inside a launch, and the modes that keep the six-kernel path
+    import torch
+    A = gen.make_config("c1_2d64")
+    S, O, x, r, H = run_both(pb, A, tol=1e-30, max_iter=9)
+    assert r.iterations == 9 and r.status == pb.MAXITER
+    assert_same(O, x, r, H, A)
+    S = solver(pb, A)
+    b = gpu_b(pb, S, A)
+    for kw, mode in ((dict(), 1), (dict(dot_mode="plain"), 0), (dict(method="bicgstab"), 0), (dict(rr_period=5), 0)):
+        S.start(b, tol=1e-10, max_iter=20, **kw)
+        assert S.exec_mode() == mode, kw
+        S.iterate(3)
+        S.finish(None)
+    S.close()
+    S = solver(pb, A, virtual_ranks=2)
+    S.start(b, tol=1e-10, max_iter=20)
+    assert S.exec_mode() == 0
+    S.close()
