@@ -1712,7 +1712,7 @@ static int enqueue_replacement(pbcg_handle *h) {
 // available.  PBCG_SMALL=0 turns it off (A/B runs, and the six-kernel path's
 // own tests).
 static constexpr int SMALL_BS = 256;
-static constexpr int64_t SMALL_N_MAX = 1 << 17;
+static constexpr int64_t SMALL_N_MAX = 1 << 14;  // tools/small_ab.py: fused 50-55K vs 36-38K iter/s up to 16K rows, slower from 32K
 static int small_grid_for(pbcg_handle *h) {
     if (h->comm_only || h->V != 1 || h->comm || h->R.empty()) return 0;
     const Rank &R = h->R[0];

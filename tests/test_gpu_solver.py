@@ -532,15 +532,15 @@ def test_jacobi_rejects_zero_diagonal(pb):
 
 @pytest.mark.parametrize("name", ["c1", "rand", "stencil3d", "ragged"])
 def test_fused_small_kernel(pb, name, monkeypatch):
-    # n <= 131072 rows, single rank, exact dots: one cooperative kernel runs
+    # n <= 16384 rows, single rank, exact dots: one cooperative kernel runs
     # whole chunks of iterations (csrc/small.cuh).  Same bits as the
     # six-kernel path and as the oracle, resumed across launches of varied
     # length (the phase buffers alternate by iteration parity), sigma-sorted
     # rows (rand), a ragged last window (n % 256 != 0)
     import torch
     A = {"c1": lambda: gen.make_config("c1_2d64"),
-         "rand": lambda: gen.random_banded(20_000, seed=9, band=1500),
-         "stencil3d": lambda: gen.stencil(3, 40, 100.0),
+         "rand": lambda: gen.random_banded(16_000, seed=9, band=1500),
+         "stencil3d": lambda: gen.stencil(3, 25, 100.0),
          "ragged": lambda: gen.random_banded(3_001, seed=5, band=700)}[name]()
     M = 400
     got = {}
@@ -580,5 +580,10 @@ def test_fused_small_kernel_stops(pb):
     S.close()
     S = solver(pb, A, virtual_ranks=2)
     S.start(b, tol=1e-10, max_iter=20)
+    assert S.exec_mode() == 0
+    S.close()
+    A = gen.stencil(3, 26, 100.0)  # 17,576 rows: above the threshold
+    S = solver(pb, A)
+    S.start(gpu_b(pb, S, A), tol=1e-10, max_iter=20)
     assert S.exec_mode() == 0
     S.close()
