@@ -1,0 +1,31 @@
+#!/bin/bash
+# End-of-round measurement pass on one GPU (run under gpurun):
+#   bench lines for every workload + the reference (oracle) arm, the ncu launch
+#   list of the C5 bench, and one `ncu --set full` capture of the hot kernels
+#   (C5 iteration, C4 SELL-V SpMV, C1 fused small-system kernel).
+# Output: gpurun_out/$1/ (default r01d).  Each ncu pass runs after the same
+# command has exited 0 without ncu.
+OUT=gpurun_out/${1:-r01d}
+mkdir -p $OUT
+for w in c5_3d256 c4_rand4m c3_3d128 c1_2d64; do
+  timeout 900 python bench.py --workload $w > $OUT/bench_$w.json 2> $OUT/bench_$w.err || echo "bench $w failed"
+done
+timeout 900 python bench.py --impl reference > $OUT/bench_reference.json 2> $OUT/bench_reference.err || echo "reference failed"
+# launch list (cold, serialised; shares only)
+timeout 600 python bench.py --steps 20 --warmup 3 --no-extras --no-e2e > $OUT/b_nx.json 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_c5.csv \
+  python bench.py --steps 20 --warmup 3 --no-extras --no-e2e > $OUT/ncu_launch.log 2>&1 || echo "launch list failed"
+# full captures: C5 iteration kernels at iteration ~10
+timeout 1200 ncu --set full --clock-control none --import-source on \
+  -k regex:"k2_stream|k3_stream|spmv_sellp_kernel|finalize_kernel" --launch-skip 60 --launch-count 6 \
+  -o $OUT/ncu_full_c5 python bench.py --steps 20 --warmup 3 --no-extras --no-e2e > $OUT/ncu_full_c5.log 2>&1 || echo "c5 full failed"
+# C4 SELL-V SpMV
+timeout 300 python tools/spmv_bench.py c4_rand4m 5 > $OUT/spmv_c4.json 2>&1 && \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:spmv_sellv -s 3 -c 1 \
+  -o $OUT/ncu_full_c4_sellv python tools/spmv_bench.py c4_rand4m 5 > $OUT/ncu_full_c4.log 2>&1 || echo "c4 full failed"
+# C1 fused small-system kernel (the timed launch: 200 iterations)
+timeout 300 python bench.py --workload c1_2d64 --steps 200 --warmup 10 --no-extras --no-e2e > $OUT/b_c1_nx.json 2>&1 && \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:pbcg_small -s 1 -c 1 \
+  -o $OUT/ncu_full_c1_small python bench.py --workload c1_2d64 --steps 200 --warmup 10 --no-extras --no-e2e \
+  > $OUT/ncu_full_c1.log 2>&1 || echo "c1 full failed"
+ls -la $OUT
