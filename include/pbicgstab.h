@@ -257,7 +257,7 @@ int pbcg_spmv_format(pbcg_handle *h, int64_t *out8);
 /* How pbicgstab_iterate runs the iterations of the solve started last on
  * this handle: *mode = 0: six kernels per iteration (K2, SpMV, K3, SpMV and
  * the two side-stream finalizes), replayed from CUDA graphs; 1: the fused
- * small-system kernel (single rank, n <= 16384 rows, exact dots, Algorithm 2
+ * small-system kernel (single rank, n <= 16384 rows, exact or plain dots, Algorithm 2
  * without replacement), ONE cooperative launch per iterate
  * call.  PBCG_SMALL=0 in the environment disables the fused kernel.
  * Host-only. */

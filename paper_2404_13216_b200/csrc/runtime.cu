@@ -1707,8 +1707,8 @@ static int enqueue_replacement(pbcg_handle *h) {
     return PBCG_OK;
 }
 
-// Fused small-system kernel (csrc/small.cuh): single rank, exact dots,
-// Algorithm 2 without replacement, n <= SMALL_N_MAX rows, cooperative launch
+// Fused small-system kernel (csrc/small.cuh): single rank, exact or plain
+// dots, Algorithm 2 without replacement, n <= SMALL_N_MAX rows, cooperative launch
 // available.  PBCG_SMALL=0 turns it off (A/B runs, and the six-kernel path's
 // own tests).
 static constexpr int SMALL_BS = 256;
@@ -1719,7 +1719,8 @@ static int small_grid_for(pbcg_handle *h) {
     if (R.n == 0 || R.n > SMALL_N_MAX) return 0;
     int coop = 0, per_sm = 0;
     if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->dev) != cudaSuccess || !coop) return 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pbcg_small_kernel<SMALL_BS>, SMALL_BS, 0) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pbcg_small_kernel<SMALL_BS, true>, SMALL_BS, 0) !=
+        cudaSuccess)
         return 0;
     const int64_t gran = R.h_perm.empty() ? 32 : 256;  // small.cuh: CTA row ranges
     const int64_t windows = (R.n + gran - 1) / gran;
@@ -1730,8 +1731,7 @@ static int small_grid_for(pbcg_handle *h) {
 }
 static bool small_on(const pbcg_handle *h) {
     const char *e = getenv("PBCG_SMALL");
-    return !(e && e[0] == '0') && h->small_grid > 0 && h->method == PBCG_METHOD_PBICGSTAB && h->dot_mode == PBCG_DOT_EXACT &&
-           h->rr_period == 0;
+    return !(e && e[0] == '0') && h->small_grid > 0 && h->method == PBCG_METHOD_PBICGSTAB && h->rr_period == 0;
 }
 static int launch_small(pbcg_handle *h, int32_t iters) {
     Rank &R = h->R[0];
@@ -1753,8 +1753,9 @@ static int launch_small(pbcg_handle *h, int32_t iters) {
     a.hist = R.hist;
     a.iters = iters;
     void *args[] = {&a};
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void *)pbcg_small_kernel<SMALL_BS>, dim3(h->small_grid),
-                                         dim3(SMALL_BS), args, 0, h->stream));
+    const void *k = h->dot_mode == PBCG_DOT_PLAIN ? (const void *)pbcg_small_kernel<SMALL_BS, false>
+                                                  : (const void *)pbcg_small_kernel<SMALL_BS, true>;
+    CUDA_TRY(cudaLaunchCooperativeKernel(k, dim3(h->small_grid), dim3(SMALL_BS), args, 0, h->stream));
     return PBCG_OK;
 }
 

@@ -99,6 +99,38 @@ __device__ void small_round(CtaSacc<ND> &S, long long *g, int phase, Scalars *sc
     __syncthreads();
 }
 
+// Plain dot mode (the paper's non-reproducible arm, NEXT-1): per-thread fma
+// chains, a fixed xor-shuffle tree per warp, the warps summed in order into
+// this CTA's partial part[blockIdx.x * ND + d] ...
+template <int ND, int BS>
+__device__ __forceinline__ void small_plain_publish(const double (&acc)[4], double *ws, double *part) {
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+        double v = acc[d];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+        if ((threadIdx.x & 31) == 0) ws[(threadIdx.x >> 5) * 4 + d] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < ND) {
+        double t = 0.0;
+        for (int w = 0; w < BS / 32; ++w) t = __dadd_rn(t, ws[w * 4 + threadIdx.x]);
+        part[(size_t)blockIdx.x * ND + threadIdx.x] = t;
+    }
+}
+// ... and, after the grid barrier, every CTA sums the partials in grid order
+template <int ND>
+__device__ void small_plain_round(const double *part, double *dsum, int phase, Scalars *scl, double *hist) {
+    if (threadIdx.x < ND) {
+        double t = 0.0;
+        for (unsigned b = 0; b < gridDim.x; ++b) t = __dadd_rn(t, __ldcg(&part[(size_t)b * ND + threadIdx.x]));
+        dsum[threadIdx.x] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) phase_finalize(phase, scl, dsum, 0u, hist, nullptr, nullptr);
+    __syncthreads();
+}
+
 // this CTA's positions [P0, P1): y[row(pos)] = (A x)[row], the row's ordered fma chain (R-6)
 __device__ __forceinline__ void small_spmv(const SmallArgs &a, int64_t P0, int64_t P1, const double *xb, double *yv) {
     for (int64_t pos = P0 + threadIdx.x; pos < P1; pos += blockDim.x) {
@@ -110,11 +142,14 @@ __device__ __forceinline__ void small_spmv(const SmallArgs &a, int64_t P0, int64
     }
 }
 
-template <int BS>
+// EXACT = false: plain fp64 dots (dot_mode PBCG_DOT_PLAIN); the partials go to
+// gA[0] / gB[0] reinterpreted as doubles (G x 4 <= 256 of their 270 words)
+template <int BS, bool EXACT>
 __global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
     __shared__ CtaSacc<4> SA;
     __shared__ CtaSacc<3> SB;
     __shared__ Scalars scs;
+    __shared__ double ws[BS / 32 * 4], dsum[4];  // plain mode: warp sums, rounded dots
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n = a.n;
     // whole sigma windows (256 rows) when rows are permuted, else whole slices
@@ -133,7 +168,8 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
             const bool first = scl->it == 0;
             const double be = scl->beta, nom = -scl->omega, nal = -scl->alpha;
             unsigned flags = 0;
-            cta_sacc_zero<4>(SA);
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};  // plain mode
+            if (EXACT) cta_sacc_zero<4>(SA);
             __syncthreads();
             for (int64_t b0 = P0 + 32 * warp; b0 < P1; b0 += BS) {  // whole warps: the deposits are warp-wide
                 const int64_t i = b0 + lane;
@@ -150,25 +186,36 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
                     }
                     const double q = __fma_rn(nal, s, r), y = __fma_rn(nal, z, w);  // l.73-74
                     a.p[i] = p; a.s[i] = s; a.z[i] = z; a.q[i] = q; a.y[i] = y;
-                    const bool zy = is_zero(y), zr = is_zero(rh);
-                    P[0] = tp.prep(q, y, is_zero(q) | zy, flags);
-                    P[1] = tp.prep(y, y, zy, flags);
-                    P[2] = tp.prep(rh, s, zr | is_zero(s), flags);
-                    P[3] = tp.prep(rh, z, zr | is_zero(z), flags);
+                    if (EXACT) {
+                        const bool zy = is_zero(y), zr = is_zero(rh);
+                        P[0] = tp.prep(q, y, is_zero(q) | zy, flags);
+                        P[1] = tp.prep(y, y, zy, flags);
+                        P[2] = tp.prep(rh, s, zr | is_zero(s), flags);
+                        P[3] = tp.prep(rh, z, zr | is_zero(z), flags);
+                    } else {
+                        acc[0] = __fma_rn(q, y, acc[0]);
+                        acc[1] = __fma_rn(y, y, acc[1]);
+                        acc[2] = __fma_rn(rh, s, acc[2]);
+                        acc[3] = __fma_rn(rh, z, acc[3]);
+                    }
                 }
+                if (EXACT) {
 #pragma unroll
-                for (int d = 0; d < 4; ++d) {  // one or two rows per lane: direct deposits (no warp aggregation chain)
-                    if (is_nonzero(P[d].p)) sacc_deposit(SA.w[d], P[d].p);
-                    if (is_nonzero(P[d].e)) sacc_deposit(SA.w[d], P[d].e);
+                    for (int d = 0; d < 4; ++d) {  // one or two rows per lane: direct deposits (no warp aggregation chain)
+                        if (is_nonzero(P[d].p)) sacc_deposit(SA.w[d], P[d].p);
+                        if (is_nonzero(P[d].e)) sacc_deposit(SA.w[d], P[d].e);
+                    }
                 }
             }
-            small_publish<4>(SA, flags, a.gA[par]);
+            if (EXACT) small_publish<4>(SA, flags, a.gA[par]);
+            else small_plain_publish<4, BS>(acc, ws, (double *)a.gA[0]);
         }
         grid_barrier(a.bar);
-        if (blockIdx.x == 0) {  // every CTA has read gB of the previous iteration: clear it for the next one
+        if (EXACT && blockIdx.x == 0) {  // every CTA has read gB of the previous iteration: clear it for the next one
             for (int i = threadIdx.x; i < 3 * SACC_L + SACC_FLAGW; i += BS) a.gB[par ^ 1][i] = 0;
         }
-        small_round<4>(SA, a.gA[par], PH_A, scl, hist);  // l.76
+        if (EXACT) small_round<4>(SA, a.gA[par], PH_A, scl, hist);  // l.76
+        else small_plain_round<4>((const double *)a.gA[0], dsum, PH_A, scl, hist);
         if (scl->done) break;
         // ---- SpMV v = A z (l.75) over this CTA's rows ----
         small_spmv(a, P0, P1, a.zpad, a.v);
@@ -177,7 +224,8 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
         {
             const double al = scl->alpha, om = scl->omega, nal = -al, nom = -om;
             unsigned flags = 0;
-            cta_sacc_zero<3>(SB);
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};  // plain mode
+            if (EXACT) cta_sacc_zero<3>(SB);
             __syncthreads();
             for (int64_t b0 = P0 + 32 * warp; b0 < P1; b0 += BS) {
                 const int64_t i = b0 + lane;
@@ -189,24 +237,34 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
                     const double r = __fma_rn(nom, y, q);                            // l.78
                     const double w = __fma_rn(nom, __fma_rn(nal, a.v[i], a.t[i]), y);  // l.79
                     a.x[i] = x; a.r[i] = r; a.w[i] = w;
-                    const bool zr = is_zero(r), zh = is_zero(rh);
-                    P[0] = tp.prep(rh, r, zh | zr, flags);
-                    P[1] = tp.prep(rh, w, zh | is_zero(w), flags);
-                    P[2] = tp.prep(r, r, zr, flags);
+                    if (EXACT) {
+                        const bool zr = is_zero(r), zh = is_zero(rh);
+                        P[0] = tp.prep(rh, r, zh | zr, flags);
+                        P[1] = tp.prep(rh, w, zh | is_zero(w), flags);
+                        P[2] = tp.prep(r, r, zr, flags);
+                    } else {
+                        acc[0] = __fma_rn(rh, r, acc[0]);
+                        acc[1] = __fma_rn(rh, w, acc[1]);
+                        acc[2] = __fma_rn(r, r, acc[2]);
+                    }
                 }
+                if (EXACT) {
 #pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    if (is_nonzero(P[d].p)) sacc_deposit(SB.w[d], P[d].p);
-                    if (is_nonzero(P[d].e)) sacc_deposit(SB.w[d], P[d].e);
+                    for (int d = 0; d < 3; ++d) {
+                        if (is_nonzero(P[d].p)) sacc_deposit(SB.w[d], P[d].p);
+                        if (is_nonzero(P[d].e)) sacc_deposit(SB.w[d], P[d].e);
+                    }
                 }
             }
-            small_publish<3>(SB, flags, a.gB[par]);
+            if (EXACT) small_publish<3>(SB, flags, a.gB[par]);
+            else small_plain_publish<3, BS>(acc, ws, (double *)a.gB[0]);
         }
         grid_barrier(a.bar);
-        if (blockIdx.x == 0) {  // every CTA has read gA of this iteration
+        if (EXACT && blockIdx.x == 0) {  // every CTA has read gA of this iteration
             for (int i = threadIdx.x; i < 4 * SACC_L + SACC_FLAGW; i += BS) a.gA[par][i] = 0;
         }
-        small_round<3>(SB, a.gB[par], PH_B, scl, hist);  // l.81-82, stopping and breakdown rules
+        if (EXACT) small_round<3>(SB, a.gB[par], PH_B, scl, hist);  // l.81-82, stopping and breakdown rules
+        else small_plain_round<3>((const double *)a.gB[0], dsum, PH_B, scl, hist);
         if (scl->done) break;
         // ---- SpMV t = A w (l.80) ----
         small_spmv(a, P0, P1, a.wpad, a.t);

@@ -572,7 +572,7 @@ def test_fused_small_kernel_stops(pb):
     assert_same(O, x, r, H, A)
     S = solver(pb, A)
     b = gpu_b(pb, S, A)
-    for kw, mode in ((dict(), 1), (dict(dot_mode="plain"), 0), (dict(method="bicgstab"), 0), (dict(rr_period=5), 0)):
+    for kw, mode in ((dict(), 1), (dict(dot_mode="plain"), 1), (dict(method="bicgstab"), 0), (dict(rr_period=5), 0)):
         S.start(b, tol=1e-10, max_iter=20, **kw)
         assert S.exec_mode() == mode, kw
         S.iterate(3)
@@ -587,3 +587,26 @@ def test_fused_small_kernel_stops(pb):
     S.start(gpu_b(pb, S, A), tol=1e-10, max_iter=20)
     assert S.exec_mode() == 0
     S.close()
+
+
+def test_fused_small_kernel_plain_dots(pb, monkeypatch):
+    # plain fp64 dots in the fused kernel: per-thread fma chains, fixed warp
+    # trees, partials summed in grid order -- deterministic for one grid,
+    # converging like the exact solve; the six-kernel plain path groups the
+    # sums differently (the non-reproducibility the paper describes)
+    A = gen.make_config("c1_2d64")
+    runs = {}
+    for env in ("1", "1", "0"):
+        monkeypatch.setenv("PBCG_SMALL", env)
+        S = solver(pb, A, history_capacity=600)
+        b = gpu_b(pb, S, A)
+        x, r = S.solve(b, tol=1e-10, max_iter=500, dot_mode="plain")
+        assert S.exec_mode() == int(env)
+        assert r.status == pb.CONVERGED and r.relres_true <= 1e-9
+        runs.setdefault(env, []).append((u64(x.cpu().numpy()), u64(S.history()), r.iterations))
+        S.close()
+    (x1, h1, i1), (x2, h2, i2) = runs["1"]
+    assert i1 == i2 and np.array_equal(x1, x2) and np.array_equal(h1, h2)
+    O = oracle.PBiCGStab(A, tol=1e-10, max_iter=500)
+    O.run()
+    assert abs(i1 - O.iterations) <= max(3, O.iterations // 10), (i1, O.iterations)
