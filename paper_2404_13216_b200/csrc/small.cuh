@@ -26,6 +26,22 @@
 
 namespace pbcg {
 
+// Debug build (-DPBCG_DEBUG_COUNTERS): CTA 0 adds the globaltimer time of
+// each phase to g_dbg slots (tools/diag_small.py)
+#ifdef PBCG_DEBUG_COUNTERS
+#define SMALL_TS(slot)                                                                 \
+    do {                                                                               \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                                     \
+            unsigned long long t_;                                                     \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                     \
+            if ((slot) >= 0) g_dbg[(slot)] += t_ - ts_prev;                            \
+            ts_prev = t_;                                                              \
+        }                                                                              \
+    } while (0)
+#else
+#define SMALL_TS(slot) ((void)0)
+#endif
+
 struct SmallArgs {
     int64_t n;
     const int64_t *slice_off;
@@ -161,6 +177,9 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
     if (threadIdx.x == 0 && blockIdx.x != 0) scs = *a.sc;
     __syncthreads();
     const ExAccT<1, 1, 1> tp{};  // TwoProd + R-9 flag only
+    unsigned long long ts_prev = 0;
+    (void)ts_prev;
+    SMALL_TS(-1);
     for (int k = 0; k < a.iters && !scl->done; ++k) {
         const int par = scl->it & 1;
         // ---- K2 (l.70-74) + (q,y), (y,y), (r0,s), (r0,z) ----
@@ -210,16 +229,20 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
             if (EXACT) small_publish<4>(SA, flags, a.gA[par]);
             else small_plain_publish<4, BS>(acc, ws, (double *)a.gA[0]);
         }
+        SMALL_TS(4);  // K2 rows + publish
         grid_barrier(a.bar);
+        SMALL_TS(5);  // barrier A
         if (EXACT && blockIdx.x == 0) {  // every CTA has read gB of the previous iteration: clear it for the next one
             for (int i = threadIdx.x; i < 3 * SACC_L + SACC_FLAGW; i += BS) a.gB[par ^ 1][i] = 0;
         }
         if (EXACT) small_round<4>(SA, a.gA[par], PH_A, scl, hist);  // l.76
         else small_plain_round<4>((const double *)a.gA[0], dsum, PH_A, scl, hist);
+        SMALL_TS(6);  // round A
         if (scl->done) break;
         // ---- SpMV v = A z (l.75) over this CTA's rows ----
         small_spmv(a, P0, P1, a.zpad, a.v);
         __syncthreads();
+        SMALL_TS(7);  // SpMV v
         // ---- K3 (l.77-79) + (r0,r'), (r0,w'), (r',r') ----
         {
             const double al = scl->alpha, om = scl->omega, nal = -al, nom = -om;
@@ -259,7 +282,9 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
             if (EXACT) small_publish<3>(SB, flags, a.gB[par]);
             else small_plain_publish<3, BS>(acc, ws, (double *)a.gB[0]);
         }
+        SMALL_TS(13);  // K3 rows + publish
         grid_barrier(a.bar);
+        SMALL_TS(14);  // barrier B
         if (EXACT && blockIdx.x == 0) {  // every CTA has read gA of this iteration
             for (int i = threadIdx.x; i < 4 * SACC_L + SACC_FLAGW; i += BS) a.gA[par][i] = 0;
         }
@@ -269,6 +294,7 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
         // ---- SpMV t = A w (l.80) ----
         small_spmv(a, P0, P1, a.wpad, a.t);
         __syncthreads();
+        SMALL_TS(15);  // round B + SpMV t
     }
 }
 
