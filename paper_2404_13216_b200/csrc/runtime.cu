@@ -856,7 +856,11 @@ static constexpr int K3_NH = PBCG_K3_FPE;
 #ifndef PBCG_S_NCW
 #define PBCG_S_NCW 7
 #endif
-static constexpr int S_NCW = PBCG_S_NCW;  // warps per dot group (2*7+1 = 15 warps per CTA)
+static constexpr int S_NCW = PBCG_S_NCW;  // K2: warps per dot group (2*7+1 = 15 warps per CTA)
+#ifndef PBCG_K3_NCW
+#define PBCG_K3_NCW 8  // C5 K3 241 -> 228 us vs 7 warps per group (9: 238, 10: spills)
+#endif
+static constexpr int K3_NCW = PBCG_K3_NCW;  // K3: warps per dot group (3 dots: fewer registers than K2)
 #ifndef PBCG_X_NCW
 #define PBCG_X_NCW 12
 #endif
@@ -886,24 +890,25 @@ static constexpr int X_NH = PBCG_X_NH, X_NL = 2;  // standalone EXDOT: hot / col
 static constexpr int K2_PPT = PBCG_K2_PPT, K2_ST = PBCG_K2_ST, K3_PPT = PBCG_K3_PPT, K3_ST = PBCG_K3_ST,
                      XD_PPT = PBCG_XD_PPT, XD_ST = PBCG_XD_ST;
 #define K2S k2_stream<K2_NH, K2_NC, S_NCW, K2_PPT, K2_ST, K2_NHE>
-#define K3S k3_stream<K3_NH, K3_NC, S_NCW, K3_PPT, K3_ST, K3_NHE>
+#define K3S k3_stream<K3_NH, K3_NC, K3_NCW, K3_PPT, K3_ST, K3_NHE>
 // lean variants (one cold level less): less end-of-kernel drain, which is
 // what counts below LEAN_ROWS rows per rank (C1/C3/C4 measured faster, C5 slower)
 #define K2SL k2_stream<K2_NH, K2_NC - 1, S_NCW, K2_PPT, K2_ST, K2_NHE>
-#define K3SL k3_stream<K3_NH, K3_NC - 1, S_NCW, K3_PPT, K3_ST, K3_NHE>
+#define K3SL k3_stream<K3_NH, K3_NC - 1, K3_NCW, K3_PPT, K3_ST, K3_NHE>
 static constexpr int64_t LEAN_ROWS = 8 << 20;
 #define K2SP k2_stream<K2_NH, K2_NC, S_NCW, K2_PPT, K2_ST, K2_NHE, false>
-#define K3SP k3_stream<K3_NH, K3_NC, S_NCW, K3_PPT, K3_ST, K3_NHE, false>
+#define K3SP k3_stream<K3_NH, K3_NC, K3_NCW, K3_PPT, K3_ST, K3_NHE, false>
 #define XDS exdot_stream<X_NH, X_NL, X_NCW, XD_PPT, XD_ST>
 #define XDS2 exdot_stream<X_NH, X_NL, X_NCW, XD_PPT, XD_ST, 2>
 static constexpr size_t ring_bytes(int nv, int ncw, int ppt, int stages) {
     return sizeof(double) * (size_t)stages * nv * (2 * ncw * 32 * ppt) + 2 * sizeof(uint64_t) * stages;
 }
 static constexpr size_t K2_SMEM = ring_bytes(8, S_NCW, K2_PPT, K2_ST);
-static constexpr size_t K3_SMEM = ring_bytes(7, S_NCW, K3_PPT, K3_ST);
+static constexpr size_t K3_SMEM = ring_bytes(7, K3_NCW, K3_PPT, K3_ST);
 static constexpr size_t XD_SMEM = ring_bytes(2, X_NCW, XD_PPT, XD_ST);
 static constexpr int STREAM_THREADS = (X_NCW + 1) * 32;      // exdot: 1 dot group
-static constexpr int KSTREAM_THREADS = (2 * S_NCW + 1) * 32;  // K2/K3: 2 dot groups
+static constexpr int KSTREAM_THREADS = (2 * S_NCW + 1) * 32;  // K2: 2 dot groups
+static constexpr int K3_THREADS = (2 * K3_NCW + 1) * 32;       // K3: 2 dot groups
 
 
 static int stream_attrs() {
@@ -960,13 +965,13 @@ static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
 static int launch_k3(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     K3Args a{R.n, R.rh, R.p, R.q, R.y, R.t, R.v, R.x, R.r, R.w(), R.sc, R.gacc[2], fin ? R.tickets + 2 : nullptr, R.hist, fin, R.part[2]};
     if (h->dot_mode == PBCG_DOT_PLAIN) {
-        launch_ex(K3SP, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T)), dim3(KSTREAM_THREADS), K3_SMEM, st,
+        launch_ex(K3SP, dim3(stream_grid(h, R.n, TileGeo<K3_NCW, K3_PPT>::T)), dim3(K3_THREADS), K3_SMEM, st,
                   pdl_for(R), a);
     } else if (R.n < LEAN_ROWS) {
-        launch_ex(K3SL, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T)), dim3(KSTREAM_THREADS), K3_SMEM, st,
+        launch_ex(K3SL, dim3(stream_grid(h, R.n, TileGeo<K3_NCW, K3_PPT>::T)), dim3(K3_THREADS), K3_SMEM, st,
                   pdl_for(R), a);
     } else {
-        launch_ex(K3S, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T)), dim3(KSTREAM_THREADS), K3_SMEM, st,
+        launch_ex(K3S, dim3(stream_grid(h, R.n, TileGeo<K3_NCW, K3_PPT>::T)), dim3(K3_THREADS), K3_SMEM, st,
                   pdl_for(R), a);
     }
     CUDA_TRY(cudaGetLastError());
