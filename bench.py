@@ -235,6 +235,12 @@ def run_gpu(args, rank, world, local_rank, dist):
                        nccl_uid=uid, history_capacity=16, precond="jacobi")
         out["jacobi"] = timed_arm(Sj)
         Sj.close()
+        # right 2x2 point-block Jacobi (NEXT-3, R-23): B = A M^-1 stored (rows widened to whole column blocks)
+        if all(v % 2 == 0 for v in pb.plan_partition(A.n, world)[:-1]):
+            Sb = pb.Solver(Al.row_ptr, Al.col, Al.val, A.n, row_begin=r0, row_end=r1, rank=rank, nranks=world,
+                           nccl_uid=uid, history_capacity=16, precond="bjacobi2")
+            out["bjacobi2"] = dict(timed_arm(Sb), spmv_format=Sb.spmv_format())
+            Sb.close()
     # ---- per-kernel times: a second timed pass over the same K steps with
     # CUDA events around every launch (single rank) ----
     fmt = S.spmv_format()
@@ -477,6 +483,11 @@ def main():
         jc["note"] = ("same workload and K with right Jacobi (R-22: A D^-1 stored at setup, x = D^-1 y at the end); "
                       "the iteration runs the same kernels on the scaled matrix")
         line["pbicgstab_jacobi"] = jc
+    if "bjacobi2" in out:
+        bj = out["bjacobi2"]
+        bj["note"] = ("same workload and K with right 2x2 point-block Jacobi (R-23: B = A M^-1 stored, each row "
+                      "widened to whole column blocks, so more nonzeros per SpMV; x = M^-1 y at the end)")
+        line["pbicgstab_bjacobi2"] = bj
     line["bytes_per_iteration_per_gpu"] = by["iteration"]
     line["iteration_GBps_per_gpu"] = by["iteration"] / (ms_step * 1e-3) / 1e9
     line["iteration_frac_hbm"] = line["iteration_GBps_per_gpu"] / hbm

@@ -95,10 +95,15 @@ typedef struct {
                                  matrix at setup: A' = A D^-1 (one RN division per stored entry, D =
                                  diag(A), zero or missing diagonal -> PBCG_EINVAL); solves A' y = b with
                                  y0 = D x0 and returns x = D^-1 y.  Residuals (and history) are those of
-                                 A' y = b, i.e. of A x = b in exact arithmetic. */
+                                 A' y = b, i.e. of A x = b in exact arithmetic.
+                                 PBCG_PRECOND_BJACOBI2 (2): right 2x2 point-block Jacobi (R-23):
+                                 M = the 2x2 diagonal blocks of A (global rows 2m, 2m+1; 1x1 for the last
+                                 row when n is odd), B = A M^-1 stored explicitly (each row's pattern
+                                 widened to whole column blocks); y0 = M x0, x = M^-1 y.  Every rank's
+                                 first row must be even; a singular or non-finite block -> PBCG_EINVAL. */
 } pbcg_dist;
 
-enum pbcg_precond { PBCG_PRECOND_NONE = 0, PBCG_PRECOND_JACOBI = 1 };
+enum pbcg_precond { PBCG_PRECOND_NONE = 0, PBCG_PRECOND_JACOBI = 1, PBCG_PRECOND_BJACOBI2 = 2 };
 
 /* Solver options (SPEC.md l.214-217 SolverConfig subset). */
 typedef struct {

@@ -297,3 +297,104 @@ def jacobi_right(A):
     As = types.SimpleNamespace(n=A.n, row_ptr=A.row_ptr, col=A.col, val=val / d[col],
                                rhs=getattr(A, "rhs", "given"), b=getattr(A, "b", None))
     return As, d
+
+
+def _fma(a: float, b: float, c: float) -> float:
+    """fl(a*b + c), one rounding (RN-even), from exact rationals; an exact
+    zero takes IEEE 754's sign (-0 only for (-0) + (-0))."""
+    import math
+    from fractions import Fraction
+    r = Fraction(a) * Fraction(b) + Fraction(c)
+    if r == 0:
+        neg_p = (a == 0.0 or b == 0.0) and math.copysign(1.0, a) * math.copysign(1.0, b) < 0
+        return -0.0 if (neg_p and c == 0.0 and math.copysign(1.0, c) < 0) else 0.0
+    try:
+        return float(r)
+    except OverflowError:  # beyond the binary64 range: RN gives +-inf
+        return math.inf if r > 0 else -math.inf
+
+
+def block_jacobi_right(A):
+    """Right 2x2 point-block Jacobi (R-23).
+    M = the 2x2 diagonal blocks of A (rows 2m, 2m+1; 1x1 for the last row when
+    n is odd).  Per block (a b; c d): det = fma(a, d, -(b c)),
+    M^-1 = (d -b; -c a) / det, one RN division per entry.  B = A M^-1 stored
+    explicitly: row i's pattern widened to whole column blocks, A's values at
+    A's columns and 0 at the added ones, then per block
+    B_i,2m = fma(A_i,2m, m00, A_i,2m+1 m10), B_i,2m+1 = fma(A_i,2m, m01, A_i,2m+1 m11).
+    Returns (B, M, Minv): M and Minv as [nblocks, 4] row-major blocks.
+    Solve B y = b with Algorithm 2 (y0 = M x0), then x = M^-1 y (bj_apply)."""
+    import types
+    n = A.n
+    rp = np.asarray(A.row_ptr, np.int64)
+    col = np.asarray(A.col, np.int64)
+    val = _f64(A.val)
+    nb = (n + 1) // 2
+
+    def at(r, c):
+        s, e = rp[r], rp[r + 1]
+        k = np.searchsorted(col[s:e], c)
+        return float(val[s + k]) if k < e - s and col[s + k] == c else 0.0
+
+    M = np.zeros((nb, 4))
+    Mi = np.zeros((nb, 4))
+    for m in range(nb):
+        r0 = 2 * m
+        if r0 + 1 < n:
+            a, b, c, d = at(r0, r0), at(r0, r0 + 1), at(r0 + 1, r0), at(r0 + 1, r0 + 1)
+            det = _fma(a, d, -(b * c))
+            if det == 0.0:
+                raise ValueError("block jacobi: singular 2x2 diagonal block")
+            M[m] = (a, b, c, d)
+            Mi[m] = (d / det, -(b / det), -(c / det), a / det)
+        else:
+            a = at(r0, r0)
+            if a == 0.0:
+                raise ValueError("block jacobi: singular 1x1 tail block")
+            M[m] = (a, 0.0, 0.0, 0.0)
+            Mi[m] = (1.0 / a, 0.0, 0.0, 0.0)
+    if not np.all(np.isfinite(Mi)):
+        raise ValueError("block jacobi: non-finite inverse block")
+    brp, bcol, bval = [0], [], []
+    for i in range(n):
+        s, e = rp[i], rp[i + 1]
+        k = s
+        while k < e:
+            m = int(col[k]) >> 1
+            v0 = v1 = 0.0
+            while k < e and (int(col[k]) >> 1) == m:
+                if col[k] & 1:
+                    v1 = float(val[k])
+                else:
+                    v0 = float(val[k])
+                k += 1
+            m00, m01, m10, m11 = Mi[m]
+            if 2 * m + 1 < n:
+                bcol += [2 * m, 2 * m + 1]
+                bval += [_fma(v0, m00, v1 * m10), _fma(v0, m01, v1 * m11)]
+            else:
+                bcol.append(2 * m)
+                bval.append(v0 * m00)
+        brp.append(len(bcol))
+    B = types.SimpleNamespace(n=n, row_ptr=np.array(brp, np.int32), col=np.array(bcol, np.int32),
+                              val=np.array(bval, np.float64), rhs=getattr(A, "rhs", "given"),
+                              b=getattr(A, "b", None), nnz=len(bcol))
+    return B, M, Mi
+
+
+def bj_apply(Q, x):
+    """y = Q x per 2x2 block (Q: M or M^-1 from block_jacobi_right):
+    y_2m = fma(q00, x_2m, q01 x_2m+1), y_2m+1 = fma(q10, x_2m, q11 x_2m+1);
+    1x1 tail: y = q00 x."""
+    x = _f64(x)
+    n = x.size
+    y = np.empty(n)
+    for m in range(Q.shape[0]):
+        r0 = 2 * m
+        q00, q01, q10, q11 = Q[m]
+        if r0 + 1 < n:
+            y[r0] = _fma(q00, x[r0], q01 * x[r0 + 1])
+            y[r0 + 1] = _fma(q10, x[r0], q11 * x[r0 + 1])
+        else:
+            y[r0] = q00 * x[r0]
+    return y

@@ -173,7 +173,7 @@ class Solver:
             self._uid = ctypes.create_string_buffer(bytes(nccl_uid), 128)
         self._dist = _Dist(rank, nranks, ctypes.cast(self._uid, ctypes.c_void_p) if self._uid is not None else None,
                            virtual_ranks, history_capacity, 1 if force_nccl else 0,
-                           {"none": 0, "jacobi": 1}[precond])
+                           {"none": 0, "jacobi": 1, "bjacobi2": 2}[precond])
         nbytes = ctypes.c_size_t(0)
         torch.cuda.synchronize()
         _check(L.pbicgstab_workspace_size(ctypes.byref(self._csr), ctypes.byref(self._dist), ctypes.byref(nbytes)))

@@ -905,6 +905,130 @@ __global__ void sell_colscale_kernel(int64_t n, const int64_t *slice_off, const 
     }
 }
 
+// ------------------------------------------------------------------------
+// 2x2 point-block Jacobi, right preconditioning (SURVEY §8(f) NEXT-3,
+// DESIGN.md R-23): M = the 2x2 diagonal blocks of A (global rows 2m, 2m+1; a
+// 1x1 block for the last row when n is odd), B = A M^-1 stored explicitly.
+// B's pattern: every block a row touches contributes both its columns.
+// Per block (a b; c d): det = fma(a, d, -(b c)), M^-1 = (d -b; -c a) / det
+// (one RN division each); B_i,2m = fma(A_i,2m, m00, A_i,2m+1 m10),
+// B_i,2m+1 = fma(A_i,2m, m01, A_i,2m+1 m11); y = M x and x = M^-1 y per
+// block with the same shape of formula.
+// ------------------------------------------------------------------------
+// entries of row r of B: 2 per distinct column block (1 for the odd tail)
+__global__ void bj_count_kernel(int64_t nloc, const int32_t *rp, const int32_t *col, int64_t n, int32_t *cnt) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nloc; r += (int64_t)gridDim.x * blockDim.x) {
+        int c = 0;
+        int64_t last = -1;
+        for (int32_t k = rp[r]; k < rp[r + 1]; ++k) {
+            const int64_t m = col[k] >> 1;
+            if (m != last) c += (2 * m + 1 < n) ? 2 : 1;
+            last = m;
+        }
+        cnt[r] = c;
+    }
+}
+
+// B's pattern, with A's values at A's columns and +0.0 at the added ones
+__global__ void bj_fill_kernel(int64_t nloc, const int32_t *rp, const int32_t *col, const double *val, int64_t n,
+                               const int32_t *brp, int32_t *bcol, double *bval) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nloc; r += (int64_t)gridDim.x * blockDim.x) {
+        int32_t o = brp[r];
+        for (int32_t k = rp[r]; k < rp[r + 1];) {
+            const int64_t m = col[k] >> 1;
+            double v0 = 0.0, v1 = 0.0;
+            for (; k < rp[r + 1] && (col[k] >> 1) == m; ++k) {
+                if (col[k] & 1) v1 = val[k];
+                else v0 = val[k];
+            }
+            bcol[o] = (int32_t)(2 * m);
+            bval[o++] = v0;
+            if (2 * m + 1 < n) {
+                bcol[o] = (int32_t)(2 * m + 1);
+                bval[o++] = v1;
+            }
+        }
+    }
+}
+
+// value of A at (row r, global column c): 0 if not stored
+__device__ __forceinline__ double csr_at(const int32_t *rp, const int32_t *col, const double *val, int64_t r,
+                                         int64_t c) {
+    for (int32_t k = rp[r]; k < rp[r + 1]; ++k)
+        if (col[k] == c) return val[k];
+    return 0.0;
+}
+
+// per own block (rows rb+2j, rb+2j+1; rb even): M and M^-1 (4 doubles each,
+// row-major; the 1x1 tail block keeps one), and the columns of M^-1 in the
+// padded x layout: c0[k] = M^-1[2m][k], c1[k] = M^-1[2m+1][k] for k in block m
+__global__ void bj_blocks_kernel(int64_t nloc, int64_t rb, int64_t n, const int32_t *rp, const int32_t *col,
+                                 const double *val, double *bm, double *bi, double *c0, double *c1, int *bad) {
+    const int64_t nb = (nloc + 1) / 2;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nb; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r0 = 2 * j, g0 = rb + r0;
+        if (g0 + 1 < n) {
+            const double a = csr_at(rp, col, val, r0, g0), b = csr_at(rp, col, val, r0, g0 + 1);
+            const double c = csr_at(rp, col, val, r0 + 1, g0), d = csr_at(rp, col, val, r0 + 1, g0 + 1);
+            const double det = __fma_rn(a, d, -__dmul_rn(b, c));
+            const double m00 = __ddiv_rn(d, det), m01 = -__ddiv_rn(b, det), m10 = -__ddiv_rn(c, det),
+                         m11 = __ddiv_rn(a, det);
+            if (!(det != 0.0) || !isfinite(m00) || !isfinite(m01) || !isfinite(m10) || !isfinite(m11)) atomicOr(bad, 4);
+            bm[4 * j] = a; bm[4 * j + 1] = b; bm[4 * j + 2] = c; bm[4 * j + 3] = d;
+            bi[4 * j] = m00; bi[4 * j + 1] = m01; bi[4 * j + 2] = m10; bi[4 * j + 3] = m11;
+            c0[r0] = m00; c1[r0] = m10;
+            c0[r0 + 1] = m01; c1[r0 + 1] = m11;
+        } else {  // 1x1 tail block
+            const double a = csr_at(rp, col, val, r0, g0);
+            const double m = __ddiv_rn(1.0, a);
+            if (!(a != 0.0) || !isfinite(m)) atomicOr(bad, 4);
+            bm[4 * j] = a; bm[4 * j + 1] = 0.0; bm[4 * j + 2] = 0.0; bm[4 * j + 3] = 0.0;
+            bi[4 * j] = m; bi[4 * j + 1] = 0.0; bi[4 * j + 2] = 0.0; bi[4 * j + 3] = 0.0;
+            c0[r0] = m; c1[r0] = 0.0;
+        }
+    }
+}
+
+// B = A M^-1 in place on the sliced ELL of B's pattern (both columns of a
+// block sit in consecutive slots): c0/c1 in the padded x layout (halo incl.),
+// g = x-buffer index + buf_lo is the global column
+__global__ void bj_values_kernel(int64_t nloc, int64_t n, int64_t buf_lo, const int64_t *slice_off,
+                                 const int32_t *row_len, double *sval, const int32_t *scol, const double *c0,
+                                 const double *c1) {
+    for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < nloc;
+         pos += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t base = slice_off[pos >> 5] + (pos & 31);
+        const int len = row_len[pos];
+        for (int k = 0; k < len;) {
+            const int64_t xi = pos + scol[base + 32 * k], g = xi + buf_lo;
+            if (g + 1 < n) {  // a 2x2 block: slots k (column 2m) and k+1 (column 2m+1)
+                const double v0 = sval[base + 32 * k], v1 = sval[base + 32 * (k + 1)];
+                sval[base + 32 * k] = __fma_rn(v0, c0[xi], __dmul_rn(v1, c1[xi]));
+                sval[base + 32 * (k + 1)] = __fma_rn(v0, c0[xi + 1], __dmul_rn(v1, c1[xi + 1]));
+                k += 2;
+            } else {  // the 1x1 tail block
+                sval[base + 32 * k] = __dmul_rn(sval[base + 32 * k], c0[xi]);
+                k += 1;
+            }
+        }
+    }
+}
+
+// y = Q x per own block (Q = M or M^-1, 4 doubles per block), in place allowed
+__global__ void bj_apply_kernel(int64_t nloc, int64_t rb, int64_t n, const double *q, const double *x, double *y) {
+    const int64_t nb = (nloc + 1) / 2;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nb; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r0 = 2 * j;
+        if (rb + r0 + 1 < n) {
+            const double x0 = x[r0], x1 = x[r0 + 1];
+            y[r0] = __fma_rn(q[4 * j], x0, __dmul_rn(q[4 * j + 1], x1));
+            y[r0 + 1] = __fma_rn(q[4 * j + 2], x0, __dmul_rn(q[4 * j + 3], x1));
+        } else {
+            y[r0] = __dmul_rn(q[4 * j], x[r0]);
+        }
+    }
+}
+
 // y := a op b elementwise (op 0: multiply, 1: divide), RN
 __global__ void vec_muldiv_kernel(int64_t n, const double *a, const double *b, double *y, int op) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

@@ -287,6 +287,7 @@ struct Rank {
     int64_t nnz = 0, n_explicit = 0;  // stored nonzeros, column ids that stay explicit
     int spmv_kind = 0;                // SpMV kernel (set at setup)
     double *dg = nullptr;             // Jacobi: diag(A) of this rank's rows
+    double *bjm = nullptr, *bji = nullptr;  // 2x2 block Jacobi: M and M^-1 of this rank's blocks (4 doubles each)
     double *part[NPH] = {};           // plain dot mode: CTA partials [PLAIN_GRID][4] per phase
     double *pdsum = nullptr;          // plain dot mode, NCCL ranks: local sums [NPH][4] (allreduced)
     // packed SELL-P chunks (rows <= 8 nonzeros) or SELL-V chunks (longer
@@ -359,7 +360,7 @@ struct Carver {
     }
 };
 
-static void carve_rank(Carver &C, Rank &R, int hist_cap, bool comm_only, bool precond) {
+static void carve_rank(Carver &C, Rank &R, int hist_cap, bool comm_only, int precond) {
     if (!comm_only) {
         R.slice_off = C.take<int64_t>(R.nslices + 16);      // + tail read by the TMA SpMV
         R.row_len = C.take<int32_t>((size_t)R.nslices * 32);  // whole slices, zero past n
@@ -387,7 +388,11 @@ static void carve_rank(Carver &C, Rank &R, int hist_cap, bool comm_only, bool pr
         const size_t nb = (size_t)(R.buf_hi - R.buf_lo) + 2;
         R.zpad = C.take<double>(nb); R.wpad = C.take<double>(nb); R.xpad = C.take<double>(nb);
         R.hist = C.take<double>((size_t)hist_cap * H_COLS);
-        if (precond) R.dg = C.take<double>((size_t)R.n + 2);
+        if (precond == PBCG_PRECOND_JACOBI) R.dg = C.take<double>((size_t)R.n + 2);
+        if (precond == PBCG_PRECOND_BJACOBI2) {
+            R.bjm = C.take<double>(4 * (size_t)((R.n + 1) / 2 + 1));
+            R.bji = C.take<double>(4 * (size_t)((R.n + 1) / 2 + 1));
+        }
     }
     for (int k = 0; k < NPH; ++k) R.gacc[k] = C.take<long long>(GW4);
     for (int k = 0; k < NPH; ++k) R.part[k] = C.take<double>((size_t)PLAIN_GRID * 4);
@@ -525,7 +530,8 @@ static int prepare(pbcg_handle *h, const pbcg_csr_local *A, const pbcg_dist *d, 
     h->V = (d && d->virtual_ranks > 1) ? d->virtual_ranks : 1;
     h->hist_cap = (d && d->history_capacity > 0) ? d->history_capacity : 10001;
     h->precond = d ? d->precond : PBCG_PRECOND_NONE;
-    if (h->precond != PBCG_PRECOND_NONE && h->precond != PBCG_PRECOND_JACOBI) return fail(PBCG_EINVAL, "bad precond");
+    if (h->precond != PBCG_PRECOND_NONE && h->precond != PBCG_PRECOND_JACOBI && h->precond != PBCG_PRECOND_BJACOBI2)
+        return fail(PBCG_EINVAL, "bad precond");
     if (h->nranks > 1 && h->V > 1) return fail(PBCG_EINVAL, "virtual ranks need nranks == 1");
     if (h->rank < 0 || h->rank >= h->nranks) return fail(PBCG_EINVAL, "bad rank");
     if (!A) {
@@ -564,14 +570,59 @@ static int prepare(pbcg_handle *h, const pbcg_csr_local *A, const pbcg_dist *d, 
 
 static size_t total_size(pbcg_handle *h) {
     Carver C{nullptr};
-    for (auto &R : h->R) carve_rank(C, R, h->hist_cap, h->comm_only, h->precond == PBCG_PRECOND_JACOBI);
+    for (auto &R : h->R) carve_rank(C, R, h->hist_cap, h->comm_only, h->precond);
     return carve_handle_extra(C, h) + 256;
+}
+
+// 2x2 block Jacobi (R-23): the CSR of B's pattern (every column block a row
+// touches contributes both its columns; A's values there, +0.0 at the added
+// ones) in device memory owned by `own` (freed by its destructor), used in
+// place of A for the layout; B's values are formed after the SELL is built.
+struct BjCsr {
+    pbcg_csr_local B{};
+    int32_t *rp = nullptr, *col = nullptr;
+    double *val = nullptr;
+    ~BjCsr() { cudaFree(rp); cudaFree(col); cudaFree(val); }
+};
+static int bj_expand(const pbcg_csr_local *A, BjCsr &o) {
+    const int64_t nloc = A->row_end - A->row_begin;
+    if (nloc <= 0) { o.B = *A; return PBCG_OK; }
+    CUDA_TRY(cudaMalloc(&o.rp, sizeof(int32_t) * (nloc + 1)));
+    const int g = (int)std::min<int64_t>((nloc + 255) / 256, 65535);
+    bj_count_kernel<<<g, 256>>>(nloc, A->row_ptr, A->col_idx, A->n_global, o.rp + 1);
+    CUDA_TRY(cudaGetLastError());
+    std::vector<int32_t> cnt(nloc + 1, 0);
+    CUDA_TRY(cudaMemcpy(cnt.data() + 1, o.rp + 1, sizeof(int32_t) * nloc, cudaMemcpyDeviceToHost));
+    int64_t tot = 0;
+    for (int64_t r = 1; r <= nloc; ++r) {
+        tot += cnt[r];
+        if (tot > INT32_MAX) return fail(PBCG_EINVAL, "block jacobi: expanded matrix exceeds 2^31 entries");
+        cnt[r] = (int32_t)tot;
+    }
+    CUDA_TRY(cudaMemcpy(o.rp, cnt.data(), sizeof(int32_t) * (nloc + 1), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMalloc(&o.col, sizeof(int32_t) * std::max<int64_t>(tot, 1)));
+    CUDA_TRY(cudaMalloc(&o.val, sizeof(double) * std::max<int64_t>(tot, 1)));
+    bj_fill_kernel<<<g, 256>>>(nloc, A->row_ptr, A->col_idx, A->values, A->n_global, o.rp, o.col, o.val);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    o.B = *A;
+    o.B.nnz_local = tot;
+    o.B.row_ptr = o.rp;
+    o.B.col_idx = o.col;
+    o.B.values = o.val;
+    return PBCG_OK;
 }
 
 extern "C" int pbicgstab_workspace_size(const pbcg_csr_local *A, const pbcg_dist *d, size_t *bytes) {
     if (!bytes) return fail(PBCG_EINVAL, "bytes == NULL");
     pbcg_handle tmp;
     std::vector<int32_t> h_rp;
+    BjCsr bj;
+    if (A && d && d->precond == PBCG_PRECOND_BJACOBI2) {
+        RC_TRY(validate_csr(A, d));
+        RC_TRY(bj_expand(A, bj));
+        A = &bj.B;
+    }
     RC_TRY(prepare(&tmp, A, d, h_rp, nullptr));
     *bytes = total_size(&tmp);
     return PBCG_OK;
@@ -1223,6 +1274,39 @@ static int small_grid_for(pbcg_handle *h);
 
 // Right Jacobi (NEXT-3, R-22): d = diag(A) per rank, d into the padded
 // x layout + halo (the columns' diagonals), then A' = A D^-1 in the SELL.
+// 2x2 block Jacobi (R-23) after the SELL of B's pattern is built: M and M^-1
+// of every own block, the columns of M^-1 in the padded x layout (z / w
+// buffers, halo exchanged like a vector), then B = A M^-1 in place.
+static int bj_setup(pbcg_handle *h, const pbcg_csr_local *A0) {
+    for (auto &R : h->R) {
+        if (R.rb & 1) return fail(PBCG_EINVAL, "block jacobi: every rank's first row must be even (whole 2x2 blocks)");
+        if (R.n == 0) continue;
+        const int32_t *rp = A0->row_ptr + (h->V > 1 ? R.rb : 0);
+        const int g = (int)std::min<int64_t>((R.n + 511) / 512, 65535);
+        bj_blocks_kernel<<<g, 256, 0, h->stream>>>(R.n, R.rb, h->n_global, rp, A0->col_idx, A0->values, R.bjm,
+                                                   R.bji, R.zpad + R.own_off, R.wpad + R.own_off, R.bad);
+        CUDA_TRY(cudaGetLastError());
+    }
+    RC_TRY(halo(h, 0));
+    RC_TRY(halo(h, 1));
+    for (auto &R : h->R) {
+        if (R.n == 0) continue;
+        const int g = (int)std::min<int64_t>((R.n + 255) / 256, 65535);
+        bj_values_kernel<<<g, 256, 0, h->stream>>>(R.n, h->n_global, R.buf_lo, R.slice_off, R.row_len, R.sval,
+                                                   R.scol, R.zpad, R.wpad);
+        CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    for (auto &R : h->R) {
+        int bad = 0;
+        CUDA_TRY(cudaMemcpy(&bad, R.bad, sizeof(int), cudaMemcpyDeviceToHost));
+        if (bad & 4) return fail(PBCG_EINVAL, "block jacobi: singular or non-finite 2x2 diagonal block");
+        CUDA_TRY(cudaMemset(R.zpad, 0, sizeof(double) * (R.buf_hi - R.buf_lo)));
+        CUDA_TRY(cudaMemset(R.wpad, 0, sizeof(double) * (R.buf_hi - R.buf_lo)));
+    }
+    return PBCG_OK;
+}
+
 static int jacobi_scale(pbcg_handle *h, const pbcg_csr_local *A) {
     for (auto &R : h->R) {
         if (R.n == 0) continue;
@@ -1305,6 +1389,15 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
     CUDA_TRY(cudaGetDevice(&h->dev));
     CUDA_TRY(cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, h->dev));
     const int nranks = d ? std::max(1, d->nranks) : 1;
+    // 2x2 block Jacobi: the layout is B's (pattern expanded to whole column
+    // blocks); A0 keeps the caller's matrix for the blocks of M
+    const pbcg_csr_local *A0 = A;
+    BjCsr bj;
+    if (A && d && d->precond == PBCG_PRECOND_BJACOBI2) {
+        RC_TRY(validate_csr(A, d));
+        RC_TRY(bj_expand(A, bj));
+        A = &bj.B;
+    }
     // communicators first: real ranks need the allgathered row ranges + hulls
     std::vector<int64_t> all_ranges;
     std::vector<int32_t> h_rp;
@@ -1350,7 +1443,7 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
     if (!workspace || workspace_bytes < need)
         return fail(PBCG_ENOMEM, "workspace too small: need %zu bytes, got %zu", need, workspace_bytes);
     Carver C{(char *)(((uintptr_t)workspace + 255) & ~uintptr_t(255))};
-    for (auto &R : h->R) carve_rank(C, R, h->hist_cap, h->comm_only, h->precond == PBCG_PRECOND_JACOBI);
+    for (auto &R : h->R) carve_rank(C, R, h->hist_cap, h->comm_only, h->precond);
     carve_handle_extra(C, h);
     // zero reduction state
     for (auto &R : h->R) {
@@ -1402,6 +1495,7 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
         }
         CUDA_TRY(cudaStreamSynchronize(h->stream));
         if (h->precond == PBCG_PRECOND_JACOBI) RC_TRY(jacobi_scale(h, A));
+        if (h->precond == PBCG_PRECOND_BJACOBI2) RC_TRY(bj_setup(h, A0));
         const char *es = getenv("PBCG_SELL_SLOTS");
         for (auto &R : h->R) {
             R.spmv_kind = spmv_kind_for(R, h->nsm);
@@ -1547,6 +1641,13 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
     }
     RC_TRY(scatter_in(h, b, &Rank::b, is_host_ptr(b)));
     RC_TRY(scatter_in(h, x0, &Rank::x, is_host_ptr(x0)));
+    if (h->precond == PBCG_PRECOND_BJACOBI2)  // y0 := M x0 (R-23)
+        for (auto &R : h->R)
+            if (R.n > 0) {
+                bj_apply_kernel<<<(int)std::min<int64_t>((R.n + 511) / 512, 4096), 256, 0, h->stream>>>(
+                    R.n, R.rb, h->n_global, R.bjm, R.x, R.x);
+                CUDA_TRY(cudaGetLastError());
+            }
     if (h->precond == PBCG_PRECOND_JACOBI)  // y0 := D x0 (R-22)
         for (auto &R : h->R)
             if (R.n > 0) {
@@ -1822,6 +1923,12 @@ extern "C" int pbicgstab_finish(pbcg_handle *h, double *x, pbcg_result *res) {
         for (auto &R : h->R) {
             const int64_t off = h->V > 1 ? R.rb : 0;
             const double *src = R.x;
+            if (h->precond == PBCG_PRECOND_BJACOBI2 && R.n > 0) {  // x := M^-1 y (R-23), into q
+                bj_apply_kernel<<<(int)std::min<int64_t>((R.n + 511) / 512, 4096), 256, 0, xs>>>(
+                    R.n, R.rb, h->n_global, R.bji, R.x, R.q);
+                CUDA_TRY(cudaGetLastError());
+                src = R.q;
+            }
             if (h->precond == PBCG_PRECOND_JACOBI && R.n > 0) {  // x := D^-1 y (R-22), into q (free after the loop)
                 vec_muldiv_kernel<<<(int)std::min<int64_t>((R.n + 255) / 256, 4096), 256, 0, xs>>>(R.n, R.x, R.dg,
                                                                                                   R.q, 1);

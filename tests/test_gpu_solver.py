@@ -528,6 +528,55 @@ def test_jacobi_rejects_zero_diagonal(pb):
     assert e.value.rc == 1
 
 
+# ------------------------------------------- 2x2 point-block Jacobi (R-23) ---
+
+@pytest.mark.parametrize("name", ["c1", "rand", "small3d", "odd"])
+def test_block_jacobi_matches_oracle(pb, name, monkeypatch):
+    # B = A M^-1 formed on the GPU (pattern widened to whole column blocks,
+    # M^-1 columns halo-exchanged) bit for bit as the oracle forms it; the
+    # trajectory of B y = b, y (S.vec("x")) and x = M^-1 y; virtual ranks
+    # with even first rows; fused small kernel and six-kernel path; the 1x1
+    # tail block of an odd order
+    import torch
+    A = {"c1": lambda: gen.make_config("c1_2d64"),
+         "rand": lambda: gen.random_banded(20_000, seed=9, band=1500),
+         "small3d": lambda: gen.stencil(3, 20, 100.0),
+         "odd": lambda: gen.random_banded(3_001, seed=5, band=300)}[name]()
+    S0 = solver(pb, A)
+    b = gpu_b(pb, S0, A)
+    S0.close()
+    B, M, Mi = oracle.block_jacobi_right(A)
+    O = oracle.PBiCGStab(B, b=b.cpu().numpy(), tol=1e-10, max_iter=3000)
+    O.run()
+    assert O.status == oracle.CONVERGED
+    want_x = u64(oracle.bj_apply(Mi, O.vec("x")))
+    runs = [(1, "1"), (1, "0")] + ([(2, "1"), (4, "1")] if A.n % 8 == 0 else [])
+    for V, small in runs:
+        monkeypatch.setenv("PBCG_SMALL", small)
+        S = solver(pb, A, history_capacity=3001, virtual_ranks=V, precond="bjacobi2")
+        assert S.spmv_format()["nnz"] == B.nnz
+        x, r = S.solve(b, tol=1e-10, max_iter=3000)
+        assert r.iterations == O.iterations and r.status == O.status, (V, small)
+        assert np.array_equal(u64(S.history()), u64(O.history())), (V, small)
+        assert np.array_equal(u64(S.vec("x")), u64(O.vec("x")))  # y
+        assert np.array_equal(u64(x.cpu().numpy()), want_x)      # x = M^-1 y
+        S.close()
+
+
+def test_block_jacobi_rejects(pb):
+    # a singular 2x2 diagonal block; a rank whose first row is odd (3001 rows
+    # on 2 virtual ranks: 0 | 1501)
+    A = gen.from_dense(np.array([[1.0, 2.0, 0.0], [2.0, 4.0, 1.0], [0.0, 1.0, 3.0]]))
+    with pytest.raises(pb.PbcgError) as e:
+        solver(pb, A, precond="bjacobi2")
+    assert e.value.rc == 1
+    A = gen.random_banded(3_001, seed=5, band=300)
+    assert pb.plan_partition(A.n, 2)[1] % 2 == 1
+    with pytest.raises(pb.PbcgError) as e:
+        solver(pb, A, precond="bjacobi2", virtual_ranks=2)
+    assert e.value.rc == 1
+
+
 # ----------------------------------------------- fused small-system kernel ---
 
 @pytest.mark.parametrize("name", ["c1", "rand", "stencil3d", "ragged"])

@@ -410,3 +410,95 @@ def test_jacobi_helps_a_badly_scaled_system():
     assert S1.status == oracle.CONVERGED
     assert S0.status != oracle.CONVERGED or S1.iterations < S0.iterations
     assert np.abs(S1.vec("x") / d - 1.0).max() < 1e-5
+
+
+# ---- right 2x2 point-block Jacobi (R-23) ----
+
+def test_oracle_fma_matches_libm():
+    # the oracle's exact-rational fma against the C library's fma (glibc)
+    import ctypes
+    import ctypes.util
+    libm = ctypes.CDLL(ctypes.util.find_library("m"))
+    libm.fma.restype = ctypes.c_double
+    libm.fma.argtypes = [ctypes.c_double] * 3
+    rng = np.random.default_rng(5)
+    vals = list(rng.uniform(-4, 4, 300) * 2.0 ** rng.integers(-1080, 1000, 300)) + \
+        [0.0, -0.0, 1.0, -1.0, 2.0 ** -1074, -(2.0 ** -1074), 1.0 + 2.0 ** -52]
+    for _ in range(3000):
+        a, b, c = (vals[int(rng.integers(len(vals)))] for _ in range(3))
+        want = libm.fma(a, b, c)
+        got = oracle._fma(a, b, c)
+        assert np.float64(got).view(np.uint64) == np.float64(want).view(np.uint64), (a, b, c, got, want)
+
+
+def test_block_jacobi_identity_for_block_diagonal():
+    # A block diagonal with exactly invertible blocks: B = A M^-1 is exactly
+    # the identity (pattern widened to whole blocks), one iteration, x = M^-1 b
+    blocks = [((2.0, 1.0), (0.0, 4.0)), ((1.0, -1.0), (1.0, 1.0)), ((8.0, 0.0), (0.0, 0.5))]
+    n = 2 * len(blocks) + 1  # plus a 1x1 tail block
+    D = np.zeros((n, n))
+    for m, blk in enumerate(blocks):
+        D[2 * m:2 * m + 2, 2 * m:2 * m + 2] = blk
+    D[n - 1, n - 1] = 4.0
+    A = gen.from_dense(D)
+    B, M, Mi = oracle.block_jacobi_right(A)
+    dense_b = np.zeros((n, n))
+    for i in range(n):
+        dense_b[i, B.col[B.row_ptr[i]:B.row_ptr[i + 1]]] = B.val[B.row_ptr[i]:B.row_ptr[i + 1]]
+    assert np.array_equal(dense_b, np.eye(n))
+    b = np.arange(1.0, n + 1.0)
+    S = oracle.PBiCGStab(B, b=b, tol=1e-12, max_iter=5)
+    S.run()
+    assert S.status == oracle.CONVERGED and S.iterations == 1
+    x = oracle.bj_apply(Mi, S.vec("x"))
+    assert np.allclose(D @ x, b, rtol=0, atol=1e-14)
+
+
+def test_block_jacobi_product_and_inverse():
+    # B = A M^-1 entry by entry within a few ulps of the dense product, and
+    # M^-1 within a few ulps of numpy's inverse of each block
+    A = gen.random_banded(1001, seed=6, band=40)
+    B, M, Mi = oracle.block_jacobi_right(A)
+    for m in range(M.shape[0] - 1):
+        blk = M[m].reshape(2, 2)
+        assert np.allclose(Mi[m].reshape(2, 2), np.linalg.inv(blk), rtol=1e-14, atol=0)
+    assert M.shape[0] == 501 and Mi[-1, 0] == 1.0 / M[-1, 0]  # 1x1 tail block (n odd)
+    n = A.n
+    Ad = np.zeros((n, n))
+    for i in range(n):
+        Ad[i, A.col[A.row_ptr[i]:A.row_ptr[i + 1]]] = A.val[A.row_ptr[i]:A.row_ptr[i + 1]]
+    Mid = np.zeros((n, n))
+    for m in range(M.shape[0]):
+        r0 = 2 * m
+        if r0 + 1 < n:
+            Mid[r0:r0 + 2, r0:r0 + 2] = Mi[m].reshape(2, 2)
+        else:
+            Mid[r0, r0] = Mi[m, 0]
+    P = Ad @ Mid
+    Bd = np.zeros((n, n))
+    for i in range(n):
+        Bd[i, B.col[B.row_ptr[i]:B.row_ptr[i + 1]]] = B.val[B.row_ptr[i]:B.row_ptr[i + 1]]
+    assert np.all(np.abs(Bd - P) <= 4 * 2.0 ** -52 * (np.abs(Ad) @ np.abs(Mid)) + 1e-300)
+    # the widened pattern holds every nonzero of the product
+    assert np.all((P != 0) <= (Bd != 0) | (np.abs(P) < 1e-300))
+
+
+def test_block_jacobi_preconditioned_solves():
+    rng = np.random.default_rng(22)
+    for k in range(12):
+        n = int(rng.integers(8, 60))
+        A = gen.dense_as_sparse(n, seed=800 + k, density=0.5)
+        D = np.zeros((n, n))
+        for i in range(n):
+            D[i, A.col[A.row_ptr[i]:A.row_ptr[i + 1]]] = A.val[A.row_ptr[i]:A.row_ptr[i + 1]]
+        b = rng.uniform(-1, 1, n)
+        B, M, Mi = oracle.block_jacobi_right(A)
+        S = oracle.PBiCGStab(B, b=b, tol=1e-10, max_iter=1000)
+        S.run()
+        assert S.status == oracle.CONVERGED, (k, S.status)
+        x = oracle.bj_apply(Mi, S.vec("x"))
+        xs = np.linalg.solve(D, b)
+        assert np.linalg.norm(x - xs) <= 1e-6 * np.linalg.norm(xs)
+        # y0 = M x0 then x = M^-1 y round trip
+        y = oracle.bj_apply(M, xs)
+        assert np.allclose(oracle.bj_apply(Mi, y), xs, rtol=1e-13, atol=1e-15)
