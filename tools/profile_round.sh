@@ -5,7 +5,7 @@
 #   (C5 iteration, C4 SELL-V SpMV, C1 fused small-system kernel).
 # Output: gpurun_out/$1/ (default r01d).  Each ncu pass runs after the same
 # command has exited 0 without ncu.
-OUT=gpurun_out/${1:-r01d}
+OUT=gpurun_out/${1:-r01e}
 mkdir -p $OUT
 for w in c5_3d256 c4_rand4m c3_3d128 c1_2d64; do
   timeout 900 python bench.py --workload $w > $OUT/bench_$w.json 2> $OUT/bench_$w.err || echo "bench $w failed"
