@@ -231,6 +231,17 @@ def test_nccl_dataflow_single_rank(pb):
     A = gen.random_banded(30_000, seed=17, band=2500)
     S, O, x, r, H = run_both(pb, A, tol=1e-10, max_iter=400, force_nccl=True)
     assert_same(O, x, r, H, A)
+    # 2x2 block Jacobi through the same path (its setup exchanges the columns
+    # of M^-1 with the NCCL halo)
+    B, M, Mi = oracle.block_jacobi_right(A)
+    O = oracle.PBiCGStab(B, b=A.b, tol=1e-10, max_iter=400)
+    O.run()
+    S = solver(pb, A, history_capacity=401, force_nccl=True, precond="bjacobi2")
+    import torch
+    x, r = S.solve(torch.from_numpy(A.b).cuda(), tol=1e-10, max_iter=400)
+    assert r.iterations == O.iterations and np.array_equal(u64(S.history()), u64(O.history()))
+    assert np.array_equal(u64(x.cpu().numpy()), u64(oracle.bj_apply(Mi, O.vec("x"))))
+    S.close()
 
 
 def banded_with_holes(n, half, seed, holes_per_slice=0.3):
