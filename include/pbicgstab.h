@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define PBCG_ABI_VERSION 6
+#define PBCG_ABI_VERSION 7
 
 /* return codes of every entry point (never an abort across the ABI) */
 enum pbcg_rc {
@@ -127,6 +127,9 @@ typedef struct {
                                  §8(f) NEXT-2): after every rr_period-th iteration that leaves the solve
                                  running, r := b - A x, w := A r, s := A p, z := A s, t := A w (DESIGN.md
                                  R-21).  0 (default) = never. */
+    int32_t x0_zero;          /* 1: start from x0 = 0 without reading x0 (x0 may be NULL in pbicgstab_start;
+                                 in pbicgstab_solve x is then the output buffer only): no host->device copy
+                                 of the initial guess.  0 (default): x0 is read. */
 } pbcg_opts;
 
 enum pbcg_dot_mode { PBCG_DOT_EXACT = 0, PBCG_DOT_PLAIN = 1 };

@@ -57,7 +57,7 @@ METHODS = {"pbicgstab": 0, "bicgstab": 1}
 class _Opts(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("max_iter", ctypes.c_int32), ("breakdown_eps", ctypes.c_double),
                 ("poll_every", ctypes.c_int32), ("use_graphs", ctypes.c_int32), ("dot_mode", ctypes.c_int32),
-                ("method", ctypes.c_int32), ("rr_period", ctypes.c_int32)]
+                ("method", ctypes.c_int32), ("rr_period", ctypes.c_int32), ("x0_zero", ctypes.c_int32)]
 
 
 class _Result(ctypes.Structure):
@@ -187,9 +187,10 @@ class Solver:
         del rp, ci, va
 
     # -- helpers ------------------------------------------------------------
-    def _opts(self, tol, max_iter, eps, poll_every, use_graphs, dot_mode="exact", method="pbicgstab", rr_period=0):
+    def _opts(self, tol, max_iter, eps, poll_every, use_graphs, dot_mode="exact", method="pbicgstab", rr_period=0,
+              x0_zero=False):
         return _Opts(float(tol), int(max_iter), float(eps), int(poll_every), int(use_graphs), DOT_MODES[dot_mode],
-                     METHODS[method], int(rr_period))
+                     METHODS[method], int(rr_period), int(bool(x0_zero)))
 
     def _vec(self, v, allow_host: bool):
         torch = self.torch
@@ -214,22 +215,32 @@ class Solver:
 
     # -- API ------------------------------------------------------------------
     def solve(self, b, x0=None, tol=1e-10, max_iter=10000, eps=1e-30, poll_every=16, use_graphs=True,
-              dot_mode="exact", method="pbicgstab", rr_period=0):
+              dot_mode="exact", method="pbicgstab", rr_period=0, out=None):
         """Solve; b/x0 may be CUDA tensors or host arrays/tensors (host buffers
         go through the library's staging path).  Returns (x, Result) with x on
-        the same side as b."""
+        the same side as b.  x0=None starts from 0 without copying an initial
+        guess; `out` (optional, same side as b, e.g. a pinned host tensor)
+        receives x instead of a newly allocated buffer."""
         torch = self.torch
         self._sync_in()
         keep_b, bp = self._vec(b, allow_host=True)
         on_host = not (isinstance(keep_b, torch.Tensor) and keep_b.is_cuda)
-        if x0 is None:
+        if out is not None:
+            x, _ = self._vec(out, allow_host=on_host)
+            if x0 is not None:
+                src, _ = self._vec(x0, allow_host=on_host)
+                if isinstance(x, np.ndarray):
+                    np.copyto(x, src)
+                else:
+                    x.copy_(torch.as_tensor(src))
+        elif x0 is None:
             x = np.zeros(self.n_local_vec, np.float64) if on_host else torch.zeros(self.n_local_vec, dtype=torch.float64, device="cuda")
         else:
             x, _ = self._vec(x0, allow_host=on_host)
             x = x.copy() if isinstance(x, np.ndarray) else x.clone()
         xp = x.ctypes.data if isinstance(x, np.ndarray) else x.data_ptr()
         res = _Result()
-        opts = self._opts(tol, max_iter, eps, poll_every, use_graphs, dot_mode, method, rr_period)
+        opts = self._opts(tol, max_iter, eps, poll_every, use_graphs, dot_mode, method, rr_period, x0 is None)
         _check(lib().pbicgstab_solve(self._h, ctypes.c_void_p(bp), ctypes.c_void_p(xp), ctypes.byref(opts), ctypes.byref(res)))
         self._sync_out()
         return x, self._result(res)
@@ -243,10 +254,11 @@ class Solver:
         torch = self.torch
         self._sync_in()
         self._b, bp = self._vec(b, allow_host=True)
-        if x0 is None:
-            x0 = torch.zeros(self.n_local_vec, dtype=torch.float64, device="cuda")
-        self._x0, xp = self._vec(x0, allow_host=True)
-        opts = self._opts(tol, max_iter, eps, poll_every, use_graphs, dot_mode, method, rr_period)
+        if x0 is None:  # x0 = 0 on the device, nothing copied (pbcg_opts.x0_zero)
+            self._x0, xp = None, None
+        else:
+            self._x0, xp = self._vec(x0, allow_host=True)
+        opts = self._opts(tol, max_iter, eps, poll_every, use_graphs, dot_mode, method, rr_period, x0 is None)
         _check(lib().pbicgstab_start(self._h, ctypes.c_void_p(bp), ctypes.c_void_p(xp), ctypes.byref(opts)))
 
     def iterate(self, k: int):

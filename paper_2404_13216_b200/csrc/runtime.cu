@@ -330,6 +330,8 @@ struct pbcg_handle {
     int g_mode = -1;                // dot mode + 2 method the captured graph was built with
     int hist_cap = 10001;
     Scalars *h_sc = nullptr;      // pinned mirror of rank 0's scalars
+    Scalars *h_poll[2] = {};      // pinned scalars copies of the last two solve chunks
+    cudaEvent_t evp[2] = {};      // their copies done
     int grid_md = 0;
     int small_grid = 0;  // fused small-system kernel: cooperative grid (0: not eligible)
     cudaGraphExec_t gexec = nullptr;
@@ -1534,6 +1536,10 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
     CUDA_TRY(cudaEventCreate(&h->t0));
     CUDA_TRY(cudaEventCreate(&h->t1));
     CUDA_TRY(cudaMallocHost(&h->h_sc, sizeof(Scalars)));
+    for (int i = 0; i < 2; ++i) {
+        CUDA_TRY(cudaMallocHost(&h->h_poll[i], sizeof(Scalars)));
+        CUDA_TRY(cudaEventCreateWithFlags(&h->evp[i], cudaEventDisableTiming));
+    }
     *out = guard.release();
     return PBCG_OK;
 }
@@ -1550,6 +1556,10 @@ extern "C" void pbicgstab_destroy(pbcg_handle *h) {
     if (h->side) cudaStreamDestroy(h->side);
     if (h->cstream) cudaStreamDestroy(h->cstream);
     if (h->h_sc) cudaFreeHost(h->h_sc);
+    for (int i = 0; i < 2; ++i) {
+        if (h->h_poll[i]) cudaFreeHost(h->h_poll[i]);
+        if (h->evp[i]) cudaEventDestroy(h->evp[i]);
+    }
     if (h->comm_halo && g_nccl.CommDestroy) g_nccl.CommDestroy(h->comm_halo);
     if (h->comm_red && g_nccl.CommDestroy) g_nccl.CommDestroy(h->comm_red);
     delete h;
@@ -1592,6 +1602,7 @@ static void opts_defaults(const pbcg_opts *o, pbcg_opts &e) {
     e.dot_mode = PBCG_DOT_EXACT;
     e.method = PBCG_METHOD_PBICGSTAB;
     e.rr_period = 0;
+    e.x0_zero = 0;
     if (o) {
         e = *o;
         if (!(e.breakdown_eps > 0.0)) e.breakdown_eps = 1e-30;
@@ -1609,9 +1620,9 @@ static int g_default_chunk = 16;
 
 extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0, const pbcg_opts *o) {
     if (!h || h->comm_only) return fail(PBCG_EINVAL, "start: no matrix on this handle");
-    if (!b || !x0) return fail(PBCG_EINVAL, "start: b and x0 are required");
     pbcg_opts op;
     opts_defaults(o, op);
+    if (!b || (!x0 && !op.x0_zero)) return fail(PBCG_EINVAL, "start: b and x0 (or x0_zero) are required");
     if (!(op.tol >= 0.0) || op.max_iter < 0) return fail(PBCG_EINVAL, "start: bad tol / max_iter");
     if (op.dot_mode != PBCG_DOT_EXACT && op.dot_mode != PBCG_DOT_PLAIN) return fail(PBCG_EINVAL, "start: bad dot_mode");
     if (op.method != PBCG_METHOD_PBICGSTAB && op.method != PBCG_METHOD_BICGSTAB)
@@ -1640,7 +1651,11 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
         CUDA_TRY(cudaMemsetAsync(R.bad, 0, sizeof(int) * 4, h->stream));
     }
     RC_TRY(scatter_in(h, b, &Rank::b, is_host_ptr(b)));
-    RC_TRY(scatter_in(h, x0, &Rank::x, is_host_ptr(x0)));
+    if (op.x0_zero) {
+        for (auto &R : h->R) CUDA_TRY(cudaMemsetAsync(R.x, 0, sizeof(double) * R.n, h->stream));
+    } else {
+        RC_TRY(scatter_in(h, x0, &Rank::x, is_host_ptr(x0)));
+    }
     if (h->precond == PBCG_PRECOND_BJACOBI2)  // y0 := M x0 (R-23)
         for (auto &R : h->R)
             if (R.n > 0) {
@@ -1963,14 +1978,25 @@ extern "C" int pbicgstab_solve(pbcg_handle *h, const double *b, double *x, const
     RC_TRY(pbicgstab_start(h, b, x, &op));
     float ms = 0.f;
     CUDA_TRY(cudaEventRecord(h->t0, h->stream));
-    int done_iters = 0;
+    // Polls overlap the next chunk: chunk k+1 is enqueued before the host
+    // waits for the scalars copied after chunk k, so the GPU never idles on
+    // the round trip (iterations after done are device-side no-ops).
+    int done_iters = 0, k = 0;
     while (!h->h_sc->done && done_iters <= op.max_iter) {
         const int chunk = op.poll_every;
         RC_TRY(iterate_impl(h, chunk, chunk, op.use_graphs != 0));
         done_iters += chunk;
-        CUDA_TRY(cudaMemcpyAsync(h->h_sc, h->R[0].sc, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
-        CUDA_TRY(cudaStreamSynchronize(h->stream));
+        CUDA_TRY(cudaMemcpyAsync(h->h_poll[k & 1], h->R[0].sc, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
+        CUDA_TRY(cudaEventRecord(h->evp[k & 1], h->stream));
+        if (k > 0) {  // the previous chunk's scalars
+            CUDA_TRY(cudaEventSynchronize(h->evp[(k - 1) & 1]));
+            *h->h_sc = *h->h_poll[(k - 1) & 1];
+        }
+        ++k;
+        if (!(done_iters <= op.max_iter)) break;
     }
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (k > 0) *h->h_sc = *h->h_poll[(k - 1) & 1];
     CUDA_TRY(cudaEventRecord(h->t1, h->stream));
     CUDA_TRY(cudaEventSynchronize(h->t1));
     CUDA_TRY(cudaEventElapsedTime(&ms, h->t0, h->t1));

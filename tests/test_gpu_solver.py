@@ -670,3 +670,33 @@ def test_fused_small_kernel_plain_dots(pb, monkeypatch):
     O = oracle.PBiCGStab(A, tol=1e-10, max_iter=500)
     O.run()
     assert abs(i1 - O.iterations) <= max(3, O.iterations // 10), (i1, O.iterations)
+
+
+def test_solve_x0_zero_and_out_buffer(pb):
+    # x0=None starts from 0 on the device (pbcg_opts.x0_zero, no copy); out=
+    # receives x (a pinned host tensor here): the same bits as x0 = zeros;
+    # the polls overlap the next chunk, so the stop iteration is unchanged
+    import torch
+    A = gen.make_config("c1_2d64")
+    S = solver(pb, A, history_capacity=600)
+    b = gpu_b(pb, S, A)
+    for small in ("1", "0"):
+        import os
+        os.environ["PBCG_SMALL"] = small
+        xa, ra = S.solve(b, x0=torch.zeros(A.n, dtype=torch.float64, device="cuda"), tol=1e-10, max_iter=500)
+        Ha = S.history()
+        bh = b.cpu().pin_memory()
+        out = torch.empty(A.n, dtype=torch.float64).pin_memory()
+        xb, rb = S.solve(bh, x0=None, out=out, tol=1e-10, max_iter=500, poll_every=7)
+        assert xb.data_ptr() == out.data_ptr()
+        assert ra.iterations == rb.iterations and ra.status == rb.status
+        assert np.array_equal(u64(xa.cpu().numpy()), u64(out.numpy()))
+        assert np.array_equal(u64(Ha), u64(S.history()))
+        # a stop inside a chunk: max_iter not a multiple of poll_every
+        xc, rc = S.solve(b, x0=None, tol=1e-30, max_iter=23, poll_every=16)
+        assert rc.iterations == 23 and rc.status == pb.MAXITER
+    os.environ.pop("PBCG_SMALL")
+    O = oracle.PBiCGStab(A, tol=1e-10, max_iter=500)
+    O.run()
+    assert np.array_equal(u64(Ha), u64(O.history()))
+    S.close()
