@@ -921,7 +921,10 @@ static constexpr int X_NCW = PBCG_X_NCW;
 #ifndef PBCG_X_NH
 #define PBCG_X_NH 2
 #endif
-static constexpr int X_NH = PBCG_X_NH, X_NL = 2;  // standalone EXDOT: hot / cold levels
+#ifndef PBCG_X_NL
+#define PBCG_X_NL 2
+#endif
+static constexpr int X_NH = PBCG_X_NH, X_NL = PBCG_X_NL;  // standalone EXDOT: hot / cold levels
 #ifndef PBCG_K2_PPT
 #define PBCG_K2_PPT 1
 #endif
