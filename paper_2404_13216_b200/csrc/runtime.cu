@@ -1877,8 +1877,16 @@ static int launch_small(pbcg_handle *h, int32_t iters) {
     a.hist = R.hist;
     a.iters = iters;
     void *args[] = {&a};
-    const void *k = h->dot_mode == PBCG_DOT_PLAIN ? (const void *)pbcg_small_kernel<SMALL_BS, false>
-                                                  : (const void *)pbcg_small_kernel<SMALL_BS, true>;
+    // register-resident rows (small.cuh) when rows are not permuted, every CTA
+    // holds at most SMALL_BS rows and no row more than 8 nonzeros (C1)
+    const int64_t nw = (R.n + 31) / 32;
+    const bool reg = R.h_perm.empty() && R.max_len <= 8 && 32 * ((nw + h->small_grid - 1) / h->small_grid) <= SMALL_BS &&
+                     !(getenv("PBCG_SMALL_REG") && getenv("PBCG_SMALL_REG")[0] == '0');
+    const bool plain = h->dot_mode == PBCG_DOT_PLAIN;
+    const void *k = reg ? (plain ? (const void *)pbcg_small_reg_kernel<SMALL_BS, false>
+                                 : (const void *)pbcg_small_reg_kernel<SMALL_BS, true>)
+                        : (plain ? (const void *)pbcg_small_kernel<SMALL_BS, false>
+                                 : (const void *)pbcg_small_kernel<SMALL_BS, true>);
     CUDA_TRY(cudaLaunchCooperativeKernel(k, dim3(h->small_grid), dim3(SMALL_BS), args, 0, h->stream));
     return PBCG_OK;
 }

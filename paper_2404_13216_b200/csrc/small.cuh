@@ -153,7 +153,8 @@ __device__ __forceinline__ void small_spmv(const SmallArgs &a, int64_t P0, int64
         const int64_t base = a.slice_off[pos >> 5] + (pos & 31);
         const int len = a.row_len[pos];
         double acc = 0.0;
-        for (int k = 0; k < len; ++k) acc = __fma_rn(a.val[base + 32 * k], xb[pos + a.col[base + 32 * k]], acc);
+        for (int k = 0; k < len; ++k)  // x written by other CTAs before the grid barrier: read through L2
+            acc = __fma_rn(a.val[base + 32 * k], __ldcg(&xb[pos + a.col[base + 32 * k]]), acc);
         yv[a.perm ? (int64_t)a.perm[pos] : pos] = acc;
     }
 }
@@ -295,6 +296,164 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
         small_spmv(a, P0, P1, a.wpad, a.t);
         __syncthreads();
         SMALL_TS(15);  // round B + SpMV t
+    }
+}
+
+// Register-resident variant: rows not permuted, at most BS rows per CTA and at
+// most 8 nonzeros per row (C1).  Thread t owns row P0 + t for the whole launch:
+// its vector entries (x r r^ p s q y t v z w) and its SpMV row (values and
+// x-buffer indices) stay in registers, so an iteration reads global memory
+// only for the x gathers of the two SpMVs; z and w are stored as soon as they
+// are formed (other CTAs gather them after the grid barrier), everything else
+// once at exit.  Same arithmetic, same bits.
+template <int BS, bool EXACT>
+__global__ void __launch_bounds__(BS, 1) pbcg_small_reg_kernel(SmallArgs a) {
+    __shared__ CtaSacc<4> SA;
+    __shared__ CtaSacc<3> SB;
+    __shared__ Scalars scs;
+    __shared__ double ws[BS / 32 * 4], dsum[4];
+    const int64_t n = a.n, nw = (n + 31) / 32;
+    const int64_t P0 = min(n, 32 * (nw * blockIdx.x / gridDim.x));
+    const int64_t P1 = min(n, 32 * (nw * (blockIdx.x + 1) / gridDim.x));
+    Scalars *scl = blockIdx.x == 0 ? a.sc : &scs;
+    double *hist = blockIdx.x == 0 ? a.hist : nullptr;
+    if (threadIdx.x == 0 && blockIdx.x != 0) scs = *a.sc;
+    const int64_t i = P0 + threadIdx.x;
+    const bool on = i < P1;
+    double x = 0, r = 0, rh = 0, p = 0, s = 0, q = 0, y = 0, t = 0, v = 0, z = 0, w = 0;
+    double mv[8];
+    int64_t mx[8];
+    int len = 0;
+    if (on) {
+        x = a.x[i]; r = a.r[i]; rh = a.rh[i]; p = a.p[i]; s = a.s[i]; q = a.q[i]; y = a.y[i];
+        t = a.t[i]; v = a.v[i]; z = a.z[i]; w = a.w[i];
+        const int64_t base = a.slice_off[i >> 5] + (i & 31);
+        len = a.row_len[i];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            mv[k] = k < len ? a.val[base + 32 * k] : 0.0;
+            mx[k] = k < len ? i + a.col[base + 32 * k] : 0;
+        }
+    }
+    __syncthreads();
+    const ExAccT<1, 1, 1> tp{};
+    bool k3_done = true;  // the registers hold the state after K3 (or at entry)
+    for (int k = 0; k < a.iters && !scl->done; ++k) {
+        const int par = scl->it & 1;
+        // ---- K2 (l.70-74) ----
+        {
+            const bool first = scl->it == 0;
+            const double be = scl->beta, nom = -scl->omega, nal = -scl->alpha;
+            unsigned flags = 0;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            if (EXACT) cta_sacc_zero<4>(SA);
+            __syncthreads();
+            Prod P[4] = {};
+            if (on) {
+                if (first) {  // beta_{-1} = 0: exact copies (R-3)
+                    p = r; s = w; z = t;
+                } else {
+                    const double sp = s, zp = z;
+                    p = __fma_rn(be, __fma_rn(nom, sp, p), r);  // l.70
+                    s = __fma_rn(be, __fma_rn(nom, zp, sp), w);  // l.71
+                    z = __fma_rn(be, __fma_rn(nom, v, zp), t);   // l.72
+                }
+                q = __fma_rn(nal, s, r);  // l.73
+                y = __fma_rn(nal, z, w);  // l.74
+                a.z[i] = z;               // gathered by the SpMV of every CTA
+                if (EXACT) {
+                    const bool zy = is_zero(y), zr = is_zero(rh);
+                    P[0] = tp.prep(q, y, is_zero(q) | zy, flags);
+                    P[1] = tp.prep(y, y, zy, flags);
+                    P[2] = tp.prep(rh, s, zr | is_zero(s), flags);
+                    P[3] = tp.prep(rh, z, zr | is_zero(z), flags);
+                } else {
+                    acc[0] = __fma_rn(q, y, 0.0);
+                    acc[1] = __fma_rn(y, y, 0.0);
+                    acc[2] = __fma_rn(rh, s, 0.0);
+                    acc[3] = __fma_rn(rh, z, 0.0);
+                }
+            }
+            k3_done = false;
+            if (EXACT) {
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    if (is_nonzero(P[d].p)) sacc_deposit(SA.w[d], P[d].p);
+                    if (is_nonzero(P[d].e)) sacc_deposit(SA.w[d], P[d].e);
+                }
+                small_publish<4>(SA, flags, a.gA[par]);
+            } else {
+                small_plain_publish<4, BS>(acc, ws, (double *)a.gA[0]);
+            }
+        }
+        grid_barrier(a.bar);
+        if (EXACT && blockIdx.x == 0)
+            for (int j = threadIdx.x; j < 3 * SACC_L + SACC_FLAGW; j += BS) a.gB[par ^ 1][j] = 0;
+        if (EXACT) small_round<4>(SA, a.gA[par], PH_A, scl, hist);  // l.76
+        else small_plain_round<4>((const double *)a.gA[0], dsum, PH_A, scl, hist);
+        if (scl->done) break;
+        // ---- SpMV v = A z (l.75): the row's ordered fma chain (R-6) ----
+        if (on) {
+            double sum = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+                if (kk < len) sum = __fma_rn(mv[kk], __ldcg(&a.zpad[mx[kk]]), sum);  // other CTAs' z: L2
+            v = sum;
+        }
+        // ---- K3 (l.77-79) ----
+        {
+            const double al = scl->alpha, om = scl->omega, nal = -al, nom = -om;
+            unsigned flags = 0;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            if (EXACT) cta_sacc_zero<3>(SB);
+            __syncthreads();
+            Prod P[3] = {};
+            if (on) {
+                x = __fma_rn(om, q, __fma_rn(al, p, x));       // l.77
+                r = __fma_rn(nom, y, q);                        // l.78
+                w = __fma_rn(nom, __fma_rn(nal, v, t), y);      // l.79
+                a.w[i] = w;
+                if (EXACT) {
+                    const bool zr = is_zero(r), zh = is_zero(rh);
+                    P[0] = tp.prep(rh, r, zh | zr, flags);
+                    P[1] = tp.prep(rh, w, zh | is_zero(w), flags);
+                    P[2] = tp.prep(r, r, zr, flags);
+                } else {
+                    acc[0] = __fma_rn(rh, r, 0.0);
+                    acc[1] = __fma_rn(rh, w, 0.0);
+                    acc[2] = __fma_rn(r, r, 0.0);
+                }
+            }
+            k3_done = true;
+            if (EXACT) {
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    if (is_nonzero(P[d].p)) sacc_deposit(SB.w[d], P[d].p);
+                    if (is_nonzero(P[d].e)) sacc_deposit(SB.w[d], P[d].e);
+                }
+                small_publish<3>(SB, flags, a.gB[par]);
+            } else {
+                small_plain_publish<3, BS>(acc, ws, (double *)a.gB[0]);
+            }
+        }
+        grid_barrier(a.bar);
+        if (EXACT && blockIdx.x == 0)
+            for (int j = threadIdx.x; j < 4 * SACC_L + SACC_FLAGW; j += BS) a.gA[par][j] = 0;
+        if (EXACT) small_round<3>(SB, a.gB[par], PH_B, scl, hist);
+        else small_plain_round<3>((const double *)a.gB[0], dsum, PH_B, scl, hist);
+        if (scl->done) break;
+        // ---- SpMV t = A w (l.80) ----
+        if (on) {
+            double sum = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+                if (kk < len) sum = __fma_rn(mv[kk], __ldcg(&a.wpad[mx[kk]]), sum);
+            t = sum;
+        }
+    }
+    (void)k3_done;
+    if (on) {  // the state back to global memory (z and w are there already)
+        a.x[i] = x; a.r[i] = r; a.p[i] = p; a.s[i] = s; a.q[i] = q; a.y[i] = y; a.t[i] = t; a.v[i] = v;
     }
 }
 
