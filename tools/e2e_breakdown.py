@@ -14,7 +14,7 @@ for rep in range(3):
     torch.cuda.synchronize()
     w0 = time.time()
     ev[0].record(st)
-    S.start(bh, x0=xh, tol=1e-10, max_iter=K)
+    S.start(bh, x0=None, tol=1e-10, max_iter=K)
     ev[1].record(st)
     S.iterate(K)
     ev[2].record(st)
@@ -28,7 +28,7 @@ for rep in range(3):
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     f0.record(st)
-    x, r = S.solve(bh, x0=xh, tol=1e-10, max_iter=K, poll_every=16)
+    x, r = S.solve(bh, x0=None, out=xh, tol=1e-10, max_iter=K, poll_every=16)  # as bench.py's e2e
     f1.record(st)
     torch.cuda.synchronize()
     print(f"solve {f0.elapsed_time(f1):.2f} ms ({r.iterations} iterations)")
