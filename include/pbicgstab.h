@@ -109,7 +109,10 @@ enum pbcg_precond { PBCG_PRECOND_NONE = 0, PBCG_PRECOND_JACOBI = 1, PBCG_PRECOND
 typedef struct {
     double tol;               /* stop when ||r_{i+1}||/||b|| <= tol (>= 0; 0 never converges) */
     int32_t max_iter;         /* >= 0 */
-    double breakdown_eps;     /* relative breakdown threshold, default 1e-30; <= 0 -> 1e-30 */
+    double breakdown_eps;     /* relative breakdown threshold, default 1e-30; <= 0 -> 1e-30.
+                                 Algorithm 2: thr = max(eps NORM(r0) NORM(r'), 1e-300) for |rho'| and the
+                                 alpha denominator (R-11).  Ignored by
+                                 PBCG_METHOD_BICGSTAB, whose breakdowns are exact zeros (R-20). */
     int32_t poll_every;       /* iterations per CUDA-graph chunk / host poll; <= 0 -> 16 */
     int32_t use_graphs;       /* 1: replay captured CUDA graphs of poll_every iterations; 0: direct launches */
     int32_t dot_mode;         /* PBCG_DOT_EXACT (0, default): ExBLAS exactly rounded dots, reproducible;

@@ -207,6 +207,19 @@ class Solver:
         v = v.to(torch.float64).contiguous()
         return v, v.data_ptr()
 
+    def _check_out(self, out, on_host: bool):
+        """`out` receives x in place: it must be float64, contiguous, on the
+        same side as b and hold n_local_vec elements (no silent copies)."""
+        n = self.n_local_vec
+        if isinstance(out, np.ndarray):
+            ok = out.dtype == np.float64 and out.flags.c_contiguous and on_host and out.size == n
+        else:
+            ok = (out.dtype == self.torch.float64 and out.is_contiguous() and out.numel() == n
+                  and (out.device.type == "cpu") == on_host)
+        if not ok:
+            raise ValueError(f"solve(out=): need a contiguous float64 buffer of {n} elements on the "
+                             f"{'host' if on_host else 'device'} (the side of b)")
+
     def _sync_in(self):
         self.stream.wait_stream(self.torch.cuda.current_stream())
 
@@ -226,7 +239,8 @@ class Solver:
         keep_b, bp = self._vec(b, allow_host=True)
         on_host = not (isinstance(keep_b, torch.Tensor) and keep_b.is_cuda)
         if out is not None:
-            x, _ = self._vec(out, allow_host=on_host)
+            self._check_out(out, on_host)
+            x = out
             if x0 is not None:
                 src, _ = self._vec(x0, allow_host=on_host)
                 if isinstance(x, np.ndarray):

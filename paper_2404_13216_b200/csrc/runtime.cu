@@ -1843,9 +1843,17 @@ static int small_grid_for(pbcg_handle *h) {
     if (R.n == 0 || R.n > SMALL_N_MAX) return 0;
     int coop = 0, per_sm = 0;
     if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->dev) != cudaSuccess || !coop) return 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pbcg_small_kernel<SMALL_BS, true>, SMALL_BS, 0) !=
-        cudaSuccess)
-        return 0;
+    // launch_small may pick any of the four instantiations (the register-
+    // resident ones use more registers): the grid must be co-resident for all
+    per_sm = 1 << 30;
+    const void *kerns[] = {(const void *)pbcg_small_kernel<SMALL_BS, true>, (const void *)pbcg_small_kernel<SMALL_BS, false>,
+                           (const void *)pbcg_small_reg_kernel<SMALL_BS, true>,
+                           (const void *)pbcg_small_reg_kernel<SMALL_BS, false>};
+    for (const void *k : kerns) {
+        int b = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, SMALL_BS, 0) != cudaSuccess) return 0;
+        per_sm = std::min(per_sm, b);
+    }
     const int64_t gran = R.h_perm.empty() ? 32 : 256;  // small.cuh: CTA row ranges
     const int64_t windows = (R.n + gran - 1) / gran;
     // at most 64 CTAs: C1 ran 55.1K iter/s at 64, 53.9K at 128 (one barrier counter, fewer arrivals)

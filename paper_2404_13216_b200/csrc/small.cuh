@@ -312,6 +312,9 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_reg_kernel(SmallArgs a) {
     __shared__ CtaSacc<3> SB;
     __shared__ Scalars scs;
     __shared__ double ws[BS / 32 * 4], dsum[4];
+    // a launch enqueued after the solve stopped (the overlapped polls of
+    // pbicgstab_solve): no reload and store-back of the state
+    if (__ldcg(&a.sc->done)) return;
     const int64_t n = a.n, nw = (n + 31) / 32;
     const int64_t P0 = min(n, 32 * (nw * blockIdx.x / gridDim.x));
     const int64_t P1 = min(n, 32 * (nw * (blockIdx.x + 1) / gridDim.x));

@@ -672,7 +672,7 @@ def test_fused_small_kernel_plain_dots(pb, monkeypatch):
     assert abs(i1 - O.iterations) <= max(3, O.iterations // 10), (i1, O.iterations)
 
 
-def test_solve_x0_zero_and_out_buffer(pb):
+def test_solve_x0_zero_and_out_buffer(pb, monkeypatch):
     # x0=None starts from 0 on the device (pbcg_opts.x0_zero, no copy); out=
     # receives x (a pinned host tensor here): the same bits as x0 = zeros;
     # the polls overlap the next chunk, so the stop iteration is unchanged
@@ -681,8 +681,7 @@ def test_solve_x0_zero_and_out_buffer(pb):
     S = solver(pb, A, history_capacity=600)
     b = gpu_b(pb, S, A)
     for small in ("1", "0"):
-        import os
-        os.environ["PBCG_SMALL"] = small
+        monkeypatch.setenv("PBCG_SMALL", small)
         xa, ra = S.solve(b, x0=torch.zeros(A.n, dtype=torch.float64, device="cuda"), tol=1e-10, max_iter=500)
         Ha = S.history()
         bh = b.cpu().pin_memory()
@@ -695,8 +694,32 @@ def test_solve_x0_zero_and_out_buffer(pb):
         # a stop inside a chunk: max_iter not a multiple of poll_every
         xc, rc = S.solve(b, x0=None, tol=1e-30, max_iter=23, poll_every=16)
         assert rc.iterations == 23 and rc.status == pb.MAXITER
-    os.environ.pop("PBCG_SMALL")
+        # out= is written in place, never through a silent copy
+        for bad in (torch.empty(A.n, dtype=torch.float32).pin_memory(), torch.empty(A.n + 1, dtype=torch.float64),
+                    torch.empty(2 * A.n, dtype=torch.float64)[::2], torch.empty(A.n, dtype=torch.float64, device="cuda")):
+            with pytest.raises(ValueError):
+                S.solve(bh, x0=None, out=bad, tol=1e-10, max_iter=5)
+    monkeypatch.delenv("PBCG_SMALL")
     O = oracle.PBiCGStab(A, tol=1e-10, max_iter=500)
     O.run()
     assert np.array_equal(u64(Ha), u64(O.history()))
     S.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "stencil3d"])
+@pytest.mark.parametrize("dot_mode", ["exact", "plain"])
+def test_fused_register_variant_same_bits(pb, name, dot_mode, monkeypatch):
+    # the register-resident fused kernel (PBCG_SMALL_REG=1, the default where
+    # it applies) and the shared-memory fused kernel give the same bits
+    A = {"c1": lambda: gen.make_config("c1_2d64"), "stencil3d": lambda: gen.stencil(3, 24, 100.0)}[name]()
+    got = {}
+    for reg in ("1", "0"):
+        monkeypatch.setenv("PBCG_SMALL_REG", reg)
+        S = solver(pb, A, history_capacity=601)
+        b = gpu_b(pb, S, A)
+        x, r = S.solve(b, tol=1e-10, max_iter=600, dot_mode=dot_mode)
+        assert S.exec_mode() == 1
+        got[reg] = (u64(x.cpu().numpy()), u64(S.history()), r.iterations, r.status)
+        S.close()
+    assert got["1"][2:] == got["0"][2:]
+    assert np.array_equal(got["1"][0], got["0"][0]) and np.array_equal(got["1"][1], got["0"][1])
