@@ -174,8 +174,10 @@ def run_gpu(args, rank, world, local_rank, dist):
     clocks = Clocks(local_rank)
     clocks.start()
     time.sleep(0.3)
-    # ---- timed region: K iterations replayed as CUDA-graph chunks ----
-    S.start(b, tol=0.0, max_iter=W + K + 8)  # tol 0: every timed iteration does full work
+    # ---- timed region: the K iterations replayed as ONE captured CUDA graph
+    # (start() captures the K-iteration chunk; the W warm-ups run as one
+    # graph of their own length, captured before the timed region) ----
+    S.start(b, tol=0.0, max_iter=W + K + 8, poll_every=K)  # tol 0: every timed iteration does full work
     exec_mode = S.exec_mode()  # 0: six kernels per iteration (graphs); 1: the fused small-system kernel
     S.iterate(W)  # warm-up (start() already captured the CUDA graph of one chunk)
     torch.cuda.synchronize()
@@ -205,7 +207,7 @@ def run_gpu(args, rank, world, local_rank, dist):
     out = {"ms": ms, "ok": ok, "iters": res.iterations, "clocks": clk, "exec_mode": exec_mode}
     # ---- comparison arms, the same K steps each (SURVEY §8(f) NEXT-1..3) ----
     def timed_arm(S_, **kw):
-        S_.start(b, tol=0.0, max_iter=W + K + 8, **kw)
+        S_.start(b, tol=0.0, max_iter=W + K + 8, poll_every=K, **kw)
         S_.iterate(W)
         torch.cuda.synchronize()
         if dist:
@@ -249,7 +251,7 @@ def run_gpu(args, rank, world, local_rank, dist):
     out["by"] = by
     kern = None
     if world == 1:
-        S.start(b, tol=0.0, max_iter=W + K + 8)
+        S.start(b, tol=0.0, max_iter=W + K + 8, poll_every=K)
         S.iterate(W)
         kms = S.profile(K)
         res2 = S.finish(None)
@@ -271,6 +273,10 @@ def run_gpu(args, rank, world, local_rank, dist):
         bh = torch.empty(nloc, dtype=torch.float64, pin_memory=True)
         bh.copy_(b.cpu())
         xh = torch.zeros(nloc, dtype=torch.float64, pin_memory=True)
+        e2e_iters = args.e2e_max_iter or args.steps
+        # one untimed solve with the same options first: the handle captures its
+        # CUDA graph of poll_every iterations once and replays it in later solves
+        S.solve(bh, x0=None, out=xh, tol=1e-10, max_iter=min(e2e_iters, 32), poll_every=16)
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
@@ -278,7 +284,7 @@ def run_gpu(args, rank, world, local_rank, dist):
         tw0 = time.time()
         f0.record(S.stream)
         # x0 = 0 (the workload's initial guess) is set on the device; x lands in the pinned buffer xh
-        x, r = S.solve(bh, x0=None, out=xh, tol=1e-10, max_iter=args.e2e_max_iter or args.steps, poll_every=16)
+        x, r = S.solve(bh, x0=None, out=xh, tol=1e-10, max_iter=e2e_iters, poll_every=16)
         f1.record(S.stream)
         torch.cuda.synchronize()
         tw1 = time.time()
@@ -293,20 +299,29 @@ def run_gpu(args, rank, world, local_rank, dist):
                "h2d_bytes_per_step": (nloc * 8 * world) / it, "d2h_bytes_per_step": (nloc * 8 * world) / it,
                "h2d_bytes_per_solve": nloc * 8 * world, "d2h_bytes_per_solve": nloc * 8 * world,
                "note": ("pbicgstab_solve with pinned host b -> pinned host x (x0 = 0 set on the device, "
-                        "pbcg_opts.x0_zero); copies, init, polls and true residual inside the timed region")}
+                        "pbcg_opts.x0_zero); copies, init, polls and true residual inside the timed region; the "
+                        "handle's 16-iteration CUDA graph was captured by an untimed warm-up solve")}
     S.close()
     return out, kern, e2e, A, by, hbm, peak_src, t_gen
 
 
 def exdot_microbench(args, hbm):
-    """BASELINE.json configs[1]: EXDOT vs plain fp64 dot vs torch.dot, GB/s."""
+    """BASELINE.json configs[1]: EXDOT vs plain fp64 dot vs torch.dot, GB/s,
+    at n = 2^26 (WELL, ILL, RANGE) and 2^28 (WELL, ILL)."""
+    out = {}
+    for lg in [int(v) for v in str(args.dot_log2).split(",")]:
+        out[f"2^{lg}"] = exdot_size(lg, hbm, ("well", "ill", "range") if lg <= 26 else ("well", "ill"))
+    return out
+
+
+def exdot_size(lg, hbm, kinds):
     import torch
 
     import gen
     import paper_2404_13216_b200 as pb
     out = {}
-    n = 1 << args.dot_log2
-    for kind in ("well", "ill", "range"):
+    n = 1 << lg
+    for kind in kinds:
         if kind == "well":
             x, y = gen.uniform(n, 1), gen.uniform(n, 2)
         elif kind == "ill":
@@ -377,13 +392,15 @@ def host_cpu():
 
 
 def traffic_from_profiles(workload: str, kernel: str):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
+    of `kernel` from the committed ncu --set full capture (profiles/traffic.json)."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
             t = json.load(f)
-        return t.get(workload, {}).get(kernel)
+        return t.get(workload, {}).get(kernel), t.get("_source")
     except Exception:
-        return None
+        return None, None
 
 
 # ---------------------------------------------------------------- reference --
@@ -424,7 +441,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the exdot microbench and the CPU baseline")
-    ap.add_argument("--dot-log2", type=int, default=26)
+    ap.add_argument("--dot-log2", default="26,28", help="comma-separated log2 sizes of the EXDOT microbench")
     ap.add_argument("--e2e-max-iter", type=int, default=0, help="0: --steps")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-budget", type=float, default=90.0)
@@ -496,13 +513,19 @@ def main():
     if kern:
         sp_us = (kern["spmv_z"]["avg_us"] + kern["spmv_w"]["avg_us"]) / 2
         achieved = by["spmv"] / (sp_us * 1e-6) / 1e9
-        tr = traffic_from_profiles(args.workload, "spmv")
+        achieved_csr = by["spmv_csr"] / (sp_us * 1e-6) / 1e9
+        tr, tr_src = traffic_from_profiles(args.workload, "spmv")
         line["roofline"] = {"kernel": "spmv (SpMV v=Az / t=Aw, 2 launches per step; stencils: spmv_sellp_kernel, "
                                       "C4: spmv_sellv_kernel)",
                             "bound": "hbm",
                             "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                            "traffic": tr, "peak_source": peak_src,
+                            "traffic": tr, "traffic_source": tr_src, "peak_source": peak_src,
+                            "numerator": ("bytes the stored format must move per launch (pbcg_spmv_format[5]: "
+                                          "values, explicit column ids, slot records, headers, x once, y); "
+                                          "frac_csr uses SURVEY §8(d)'s CSR bytes 12 nnz + 4(n+1) + 16 n instead"),
                             "alg_bytes_per_launch": by["spmv"],
+                            "alg_bytes_per_launch_csr": by["spmv_csr"],
+                            "achieved_csr": achieved_csr, "frac_csr": achieved_csr / hbm, "frac_format": achieved / hbm,
                             "share_of_step": 2 * sp_us / kern["iteration_sum_us"]}
         if not args.no_extras:
             rp = read_peak_live()

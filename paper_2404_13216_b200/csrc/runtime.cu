@@ -327,15 +327,18 @@ struct pbcg_handle {
     int method = PBCG_METHOD_PBICGSTAB;  // of the running solve (pbcg_opts.method)
     int rr_period = 0;                   // residual replacement period of the running solve (0: never)
     int64_t it_enq = 0;                  // iterations enqueued since start (host-side count)
-    int g_mode = -1;                // dot mode + 2 method the captured graph was built with
+    int g_mode[2] = {-1, -1};       // dot mode + 2 method each captured graph was built with
     int hist_cap = 10001;
     Scalars *h_sc = nullptr;      // pinned mirror of rank 0's scalars
     Scalars *h_poll[2] = {};      // pinned scalars copies of the last two solve chunks
     cudaEvent_t evp[2] = {};      // their copies done
     int grid_md = 0;
     int small_grid = 0;  // fused small-system kernel: cooperative grid (0: not eligible)
-    cudaGraphExec_t gexec = nullptr;
-    int g_iters = 0;
+    // captured iteration graphs: [0] one chunk of `chunk` iterations, [1] the
+    // last remainder length (iterate(k) = k / chunk replays of [0] + one of [1])
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    int g_iters[2] = {0, 0};
+    int chunk = 16;                 // iterations per graph chunk (pbcg_opts.poll_every of the last start)
     cudaEvent_t ev[8] = {};
     cudaEvent_t evh[4] = {};  // halo-overlap fork/join (multi-rank)
     cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -1549,7 +1552,8 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
 
 extern "C" void pbicgstab_destroy(pbcg_handle *h) {
     if (!h) return;
-    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    for (auto &g : h->gexec)
+        if (g) cudaGraphExecDestroy(g);
     for (auto &e : h->ev)
         if (e) cudaEventDestroy(e);
     for (auto &e : h->evh)
@@ -1616,7 +1620,8 @@ static void opts_defaults(const pbcg_opts *o, pbcg_opts &e) {
 // ----------------------------------------------------------------------------
 // start / iterate / finish / solve
 // ----------------------------------------------------------------------------
-static int capture_chunk(pbcg_handle *h, int iters);
+static int capture_chunk(pbcg_handle *h, int iters, int slot);
+static bool small_on(const pbcg_handle *h);
 static int start_alg1(pbcg_handle *h);
 static int start_alg2_rest(pbcg_handle *h);
 static int g_default_chunk = 16;
@@ -1699,7 +1704,8 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
     if (h->h_sc->err) return fail(PBCG_EINVAL, "start: ||b|| = 0");
     // capture the iteration graph now (nothing runs), so that the first
     // iterate()/solve() chunk does not pay for capture + instantiation
-    if (op.use_graphs && h->stream) RC_TRY(capture_chunk(h, o ? op.poll_every : g_default_chunk));
+    h->chunk = o ? op.poll_every : g_default_chunk;
+    if (op.use_graphs && h->stream && !small_on(h)) RC_TRY(capture_chunk(h, h->chunk, 0));
     return PBCG_OK;
 }
 
@@ -1792,9 +1798,10 @@ static int enqueue_alg1(pbcg_handle *h) {
     return PBCG_OK;
 }
 
-static int capture_chunk(pbcg_handle *h, int iters) {
-    if (h->gexec && h->g_iters == iters && h->g_mode == h->dot_mode + 2 * h->method) return PBCG_OK;
-    if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+static int capture_chunk(pbcg_handle *h, int iters, int slot) {
+    cudaGraphExec_t &gx = h->gexec[slot];
+    if (gx && h->g_iters[slot] == iters && h->g_mode[slot] == h->dot_mode + 2 * h->method) return PBCG_OK;
+    if (gx) { cudaGraphExecDestroy(gx); gx = nullptr; }
     cudaGraph_t g;
     CUDA_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
     int rc = PBCG_OK;
@@ -1802,10 +1809,10 @@ static int capture_chunk(pbcg_handle *h, int iters) {
     cudaError_t e = cudaStreamEndCapture(h->stream, &g);
     if (rc != PBCG_OK) return rc;
     if (e != cudaSuccess) return fail(PBCG_ECUDA, "graph capture: %s", cudaGetErrorString(e));
-    CUDA_TRY(cudaGraphInstantiate(&h->gexec, g, 0));
+    CUDA_TRY(cudaGraphInstantiate(&gx, g, 0));
     cudaGraphDestroy(g);
-    h->g_iters = iters;
-    h->g_mode = h->dot_mode + 2 * h->method;
+    h->g_iters[slot] = iters;
+    h->g_mode[slot] = h->dot_mode + 2 * h->method;
     return PBCG_OK;
 }
 
@@ -1913,10 +1920,15 @@ static int iterate_impl(pbcg_handle *h, int32_t k, int chunk, bool graphs) {
         k -= run;
         while (run > 0) {
             if (graphs && run >= chunk) {
-                RC_TRY(capture_chunk(h, chunk));
-                CUDA_TRY(cudaGraphLaunch(h->gexec, h->stream));
+                RC_TRY(capture_chunk(h, chunk, 0));
+                CUDA_TRY(cudaGraphLaunch(h->gexec[0], h->stream));
                 run -= chunk;
                 h->it_enq += chunk;
+            } else if (graphs && h->rr_period == 0) {  // the remainder: one graph of its own length
+                RC_TRY(capture_chunk(h, run, 1));
+                CUDA_TRY(cudaGraphLaunch(h->gexec[1], h->stream));
+                h->it_enq += run;
+                run = 0;
             } else {
                 RC_TRY(enqueue_iteration(h));
                 run -= 1;
@@ -1931,7 +1943,7 @@ static int iterate_impl(pbcg_handle *h, int32_t k, int chunk, bool graphs) {
 extern "C" int pbicgstab_iterate(pbcg_handle *h, int32_t k) {
     if (!h || !h->started) return fail(PBCG_EINVAL, "iterate before start");
     if (k < 0) return fail(PBCG_EINVAL, "iterate: k < 0");
-    return iterate_impl(h, k, g_default_chunk, true);
+    return iterate_impl(h, k, h->chunk, true);
 }
 
 static int true_residual(pbcg_handle *h) {

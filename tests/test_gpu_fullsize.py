@@ -71,3 +71,31 @@ def test_exdot_2_28_well(pb):
     want, wf = oracle.exdot(x, y)
     got, gf = pb.exdot(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
     assert wf == 0 and gf == 0 and u64(got)[()] == u64(want)[()]
+
+
+def test_exdot_2_28_ill(pb):
+    # BASELINE.json configs[1] at its larger size, ill-conditioned (cond ~1e30)
+    import torch
+    n = 1 << 28
+    x, y = gen.ill_pair(n, seed=3)
+    want, wf = oracle.exdot(x, y)
+    got, gf = pb.exdot(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
+    assert wf == 0 and gf == 0 and u64(got)[()] == u64(want)[()]
+
+
+def test_c4_north_star_vs_plain_alg1(pb):
+    # north_star: the final ||b - Ax||/||b|| agrees with a plain-double
+    # BiCGStab (Alg. 1, the oracle's sequential dots) within 1e-10 --
+    # on the full C4 config, solved to convergence on the GPU
+    import torch
+    A = gen.make_config("c4_rand4m")
+    S = pb.Solver(A.row_ptr, A.col, A.val, A.n, history_capacity=256)
+    x, r = S.solve(torch.from_numpy(A.b).cuda(), tol=1e-10, max_iter=250)
+    S.close()
+    assert r.status == pb.CONVERGED, r
+    st, it, xb, _ = oracle.bicgstab(A, A.b, tol=1e-10, max_iter=250)
+    assert st == oracle.CONVERGED
+    tb = oracle.true_relres(A, A.b, xb)[0]
+    tg = oracle.true_relres(A, A.b, x.cpu().numpy())[0]
+    assert tg == r.relres_true  # the GPU's own true residual, bit for bit
+    assert abs(r.relres_true - tb) <= 1e-10, (r.relres_true, tb, r.iterations, it)
