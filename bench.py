@@ -156,11 +156,16 @@ def run_gpu(args, rank, world, local_rank, dist):
     t_gen = time.time() - t_gen
     r0, r1 = local_rows(A, rank, world)
     Al = A.rows(r0, r1)
-    uid = None
-    if world > 1:
+    def fresh_uid():
+        """a new NCCL unique id from rank 0 for every communicator (an id
+        bootstraps exactly one ncclCommInitRank)"""
+        if world == 1:
+            return None
         obj = [pb.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
+        return obj[0]
+
+    uid = fresh_uid()
     S = pb.Solver(Al.row_ptr, Al.col, Al.val, A.n, row_begin=r0, row_end=r1, rank=rank, nranks=world,
                   nccl_uid=uid, history_capacity=16)
     nloc = r1 - r0
@@ -234,13 +239,13 @@ def run_gpu(args, rank, world, local_rank, dist):
         out["rr"] = dict(timed_arm(S, rr_period=50), rr_period=50)
         # right Jacobi (NEXT-3): a column scaling of the stored matrix at setup, same kernels per iteration
         Sj = pb.Solver(Al.row_ptr, Al.col, Al.val, A.n, row_begin=r0, row_end=r1, rank=rank, nranks=world,
-                       nccl_uid=uid, history_capacity=16, precond="jacobi")
+                       nccl_uid=fresh_uid(), history_capacity=16, precond="jacobi")
         out["jacobi"] = timed_arm(Sj)
         Sj.close()
         # right 2x2 point-block Jacobi (NEXT-3, R-23): B = A M^-1 stored (rows widened to whole column blocks)
         if all(v % 2 == 0 for v in pb.plan_partition(A.n, world)[:-1]):
             Sb = pb.Solver(Al.row_ptr, Al.col, Al.val, A.n, row_begin=r0, row_end=r1, rank=rank, nranks=world,
-                           nccl_uid=uid, history_capacity=16, precond="bjacobi2")
+                           nccl_uid=fresh_uid(), history_capacity=16, precond="bjacobi2")
             out["bjacobi2"] = dict(timed_arm(Sb), spmv_format=Sb.spmv_format())
             Sb.close()
     # ---- per-kernel times: a second timed pass over the same K steps with
@@ -302,7 +307,7 @@ def run_gpu(args, rank, world, local_rank, dist):
                         "pbcg_opts.x0_zero); copies, init, polls and true residual inside the timed region; the "
                         "handle's 16-iteration CUDA graph was captured by an untimed warm-up solve")}
     S.close()
-    return out, kern, e2e, A, by, hbm, peak_src, t_gen
+    return out, kern, e2e, A, by, hbm, peak_src, t_gen, fresh_uid()
 
 
 def exdot_microbench(args, hbm):
@@ -360,6 +365,59 @@ def exdot_size(lg, hbm, kinds):
         del xt, yt
         torch.cuda.empty_cache()
     out["n"] = n
+    return out
+
+
+def exdot_distributed(args, rank, world, dist, uid, hbm):
+    """BASELINE.json configs[1] at N GPUs: each rank holds a
+    contiguous slice of x, y (n = 2^26 in total); a comm-only handle reduces
+    its slice with the TMA EXDOT kernel, allreduces the int64 words over NCCL
+    and rounds once on every rank.  Time = max over ranks of the median of
+    10 calls (CUDA events on the handle's stream); GB/s over all 16 n bytes."""
+    import torch
+
+    import gen
+    import paper_2404_13216_b200 as pb
+    n = 1 << 26
+    b = pb.plan_partition(n, world)
+    lo, hi = int(b[rank]), int(b[rank + 1])
+    out = {"n": n}
+    C = pb.Comm(rank=rank, nranks=world, nccl_uid=uid)
+    for kind in ("well", "ill"):
+        if kind == "well":
+            x, y = gen.uniform(n, 1), gen.uniform(n, 2)
+        else:
+            x, y = gen.ill_pair(n, seed=3)
+        xt, yt = torch.from_numpy(x[lo:hi].copy()).cuda(), torch.from_numpy(y[lo:hi].copy()).cuda()
+        del x, y
+        res = torch.zeros(1, dtype=torch.float64, device="cuda")
+        fl = torch.zeros(1, dtype=torch.int32, device="cuda")
+        for _ in range(3):
+            C.exdot(xt, yt, on_device=True, out=res, flags_out=fl)
+        torch.cuda.synchronize()
+        dist.barrier()
+        es = [torch.cuda.Event(enable_timing=True) for _ in range(11)]
+        for i in range(10):
+            es[i].record(C.stream)
+            C.exdot(xt, yt, on_device=True, out=res, flags_out=fl)
+            es[i + 1].record(C.stream)
+        torch.cuda.synchronize()
+        med = float(np.median([es[i].elapsed_time(es[i + 1]) for i in range(10)]))
+        t = torch.tensor([med], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        med = float(t.item())
+        # every rank rounded the same allreduced words: identical bits
+        r = torch.tensor([res.view(torch.int64).item()], dtype=torch.int64, device="cuda")
+        rmin, rmax = r.clone(), r.clone()
+        dist.all_reduce(rmin, op=dist.ReduceOp.MIN)
+        dist.all_reduce(rmax, op=dist.ReduceOp.MAX)
+        out[kind] = {"median_us": med * 1e3, "GBps": 16 * n / (med * 1e-3) / 1e9,
+                     "GBps_per_gpu": 16 * n / (med * 1e-3) / 1e9 / world,
+                     "frac_hbm_per_gpu": 16 * n / (med * 1e-3) / 1e9 / world / hbm,
+                     "identical_on_all_ranks": bool(rmin.item() == rmax.item()), "flags": int(fl.item())}
+        del xt, yt
+        torch.cuda.empty_cache()
+    C.close()
     return out
 
 
@@ -467,7 +525,7 @@ def main():
         print(json.dumps({"error": "--gpus > 1 needs torchrun (one process per GPU)"}))
         sys.exit(2)
 
-    out, kern, e2e, A, by, hbm, peak_src, t_gen = run_gpu(args, rank, world, local_rank, dist)
+    out, kern, e2e, A, by, hbm, peak_src, t_gen, uid = run_gpu(args, rank, world, local_rank, dist)
     K = args.steps
     ms_step = out["ms"] / K
     value = K / (out["ms"] * 1e-3)
@@ -539,8 +597,11 @@ def main():
     if rank == 0 and not args.no_extras and args.gpus == 1:
         line["exdot_microbench"] = exdot_microbench(args, hbm)
         line["cpu_baseline"] = cpu_baseline(A, budget_s=args.cpu_budget, max_iters=50)
-    elif rank == 0 and not args.no_extras:
-        line["cpu_baseline"] = cpu_baseline(A, budget_s=args.cpu_budget, max_iters=50)
+    elif not args.no_extras:
+        xd = exdot_distributed(args, rank, world, dist, uid, hbm)
+        if rank == 0:
+            line["exdot_distributed"] = xd
+            line["cpu_baseline"] = cpu_baseline(A, budget_s=args.cpu_budget, max_iters=50)
     line["gen_seconds"] = t_gen
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define PBCG_ABI_VERSION 7
+#define PBCG_ABI_VERSION 8
 
 /* return codes of every entry point (never an abort across the ABI) */
 enum pbcg_rc {
@@ -165,7 +165,13 @@ int pbicgstab_workspace_size(const pbcg_csr_local *A, const pbcg_dist *dist, siz
  * device memory of >= workspace_bytes that must outlive the handle (the
  * library makes no cudaMalloc after setup).  Converts A to the internal
  * sliced-ELL layout, plans the halo exchange, creates the NCCL communicators
- * (nranks > 1), scans A for NaN/Inf (-> PBCG_ENONFINITE).  Collective. */
+ * (nranks > 1, each limited to a few CTAs through ncclConfig_t.maxCTAs so that
+ * they run beside the interior SpMV), scans A for NaN/Inf (-> PBCG_ENONFINITE).
+ * Collective: with nranks > 1 every rank allgathers
+ * (row_begin, row_end, column hull, pbcg_config_hash) and checks them with
+ * pbcg_check_ranks; a mismatch returns PBCG_EINVAL on every rank.
+ * A == NULL: a comm-only handle (any nranks) for the distributed exdot; each
+ * rank then passes its own contiguous slice of x and y. */
 int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *dist, void *stream, void *workspace,
                     size_t workspace_bytes, pbcg_handle **out);
 
@@ -213,7 +219,8 @@ int pbicgstab_spmv(pbcg_handle *h, const double *x_local, double *y_local);
  * down to 2^-2148), so the result is still the exactly
  * rounded sum and
  * the call returns PBCG_OK unless that sum overflows binary64 (+-inf,
- * PBCG_ERANGE).  Distributed handles: PBCG_ERANGE, result unspecified.
+ * PBCG_ERANGE).  Distributed handles (virtual ranks, NCCL ranks, comm-only
+ * handles of any nranks): PBCG_ERANGE, result unspecified.
  * When bit 1 is set, bit 0 is unspecified.  n_local = 0 gives +0.0
  * (SPEC.md l.69). */
 int exdot(pbcg_handle *h, int64_t n_local, const double *x, const double *y, double *result, int32_t *flags,
@@ -280,6 +287,18 @@ int pbcg_exec_mode(const pbcg_handle *h, int32_t *mode);
 int pbcg_debug_counters(uint64_t *out16, int32_t reset);
 
 /* ---- host-only planning helpers (no GPU needed; CPU-testable) ------------ */
+
+/* FNV-1a hash of the setup arguments every rank must agree on: ABI version,
+ * n_global (-1 for a comm-only handle), nranks, virtual_ranks, precond,
+ * comm_mode. */
+int pbcg_config_hash(const pbcg_csr_local *A, const pbcg_dist *dist, uint64_t *out);
+
+/* The check setup runs on the allgathered records, PBCG_RANK_REC int64 per
+ * rank: (row_begin, row_end, cmin, cmax, config hash).  PBCG_EINVAL (with a
+ * message naming the rank) if a hash differs from rank 0's or, with a
+ * matrix, if the row blocks do not tile [0, n_global) in rank order. */
+#define PBCG_RANK_REC 5
+int pbcg_check_ranks(int32_t nranks, const int64_t *records, int64_t n_global, int32_t has_matrix);
 
 /* Balanced contiguous partition of n rows over p ranks (SPEC.md l.148,
  * l.185-187): the first n mod p ranks get one extra row.  begins: p+1 entries. */

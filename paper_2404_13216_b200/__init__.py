@@ -104,6 +104,8 @@ def lib(build_if_missing: bool = True) -> ctypes.CDLL:
         L.pbcg_spmv_format.argtypes = [vp, vp]
         L.pbcg_exec_mode.argtypes = [vp, vp]
         L.pbcg_get_vector.argtypes = [vp, i32, vp]
+        L.pbcg_config_hash.argtypes = [P(_Csr), P(_Dist), P(ctypes.c_uint64)]
+        L.pbcg_check_ranks.argtypes = [i32, vp, i64, i32]
         _lib = L
     return _lib
 
@@ -386,6 +388,66 @@ def dot_plain(x, y, out=None, stream=None):
     _check(lib().pbcg_dot_plain(x.numel(), ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()),
                                 ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(st.cuda_stream)))
     return out
+
+
+class Comm:
+    """Comm-only handle (pbicgstab_setup with A = NULL; include/pbicgstab.h):
+    the distributed EXDOT of SURVEY §8(b)/(e).  Every rank passes its own
+    contiguous slice of x and y; the superaccumulators are allreduced as
+    int64 over NCCL and rounded once, identically on every rank."""
+
+    def __init__(self, rank: int = 0, nranks: int = 1, nccl_uid: bytes | None = None, stream=None,
+                 force_nccl: bool = False):
+        torch = _torch()
+        L = lib()
+        self.torch = torch
+        self.stream = stream if stream is not None else torch.cuda.Stream()
+        self._uid = ctypes.create_string_buffer(bytes(nccl_uid), 128) if nccl_uid is not None else None
+        self._dist = _Dist(rank, nranks, ctypes.cast(self._uid, ctypes.c_void_p) if self._uid is not None else None,
+                           1, 0, 1 if force_nccl else 0, 0)
+        nbytes = ctypes.c_size_t(0)
+        _check(L.pbicgstab_workspace_size(None, ctypes.byref(self._dist), ctypes.byref(nbytes)))
+        self.workspace = torch.empty(int(nbytes.value) + 256, dtype=torch.uint8, device="cuda")
+        h = ctypes.c_void_p()
+        torch.cuda.synchronize()
+        _check(L.pbicgstab_setup(None, ctypes.byref(self._dist), ctypes.c_void_p(self.stream.cuda_stream),
+                                 ctypes.c_void_p(self.workspace.data_ptr()), ctypes.c_size_t(self.workspace.numel()),
+                                 ctypes.byref(h)))
+        self._h = h
+
+    def exdot(self, x, y, on_device: bool = False, out=None, flags_out=None):
+        return exdot(x, y, handle=self, on_device=on_device, stream=self.stream, out=out, flags_out=flags_out)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.torch.cuda.synchronize()
+            lib().pbicgstab_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def config_hash(n_global: int | None, nranks: int = 1, virtual_ranks: int = 1, precond: str = "none",
+                comm_mode: int = 0) -> int:
+    """pbcg_config_hash of these setup arguments (n_global None: comm-only)."""
+    csr = _Csr(n_global or 0, 0, n_global or 0, 0, None, None, None)
+    d = _Dist(0, nranks, None, virtual_ranks, 0, comm_mode, {"none": 0, "jacobi": 1, "bjacobi2": 2}[precond])
+    out = ctypes.c_uint64(0)
+    _check(lib().pbcg_config_hash(ctypes.byref(csr) if n_global is not None else None, ctypes.byref(d),
+                                  ctypes.byref(out)))
+    return int(out.value)
+
+
+def check_ranks(records, n_global: int, has_matrix: bool = True) -> tuple[int, str]:
+    """pbcg_check_ranks on allgathered records [(row_begin, row_end, cmin,
+    cmax, hash), ...]: (rc, message)."""
+    rec = np.ascontiguousarray(np.asarray(records, dtype=np.uint64).view(np.int64), np.int64)
+    rc = lib().pbcg_check_ranks(rec.shape[0], ctypes.c_void_p(rec.ctypes.data), int(n_global), int(bool(has_matrix)))
+    return rc, (lib().pbicgstab_last_error().decode() if rc else "")
 
 
 def nccl_unique_id() -> bytes:

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/pbicgstab.h"
 #include "kernels.cuh"
@@ -64,6 +65,14 @@ static int fail(int rc, const char *fmt, ...) {
         if (rc_ != PBCG_OK) return rc_; \
     } while (0)
 
+// NVTX ranges around the host entry points (setup, start, iterate, finish,
+// exdot, allreduce enqueue): one nsys capture of a multi-rank run shows the
+// reductions beside the SpMV (header-only NVTX 3; no cost without a tool)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 // ----------------------------------------------------------------------------
 // NCCL (resolved at run time: the library works without NCCL on one GPU)
 // ----------------------------------------------------------------------------
@@ -71,6 +80,7 @@ struct NcclApi {
     bool ok = false;
     ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
     ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommInitRankConfig)(ncclComm_t *, int, ncclUniqueId, int, ncclConfig_t *) = nullptr;  // optional
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t *, ncclConfig_t *) = nullptr;
     ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
@@ -99,6 +109,7 @@ static void nccl_load() {
 #define SYM(f, s) g_nccl.f = (decltype(g_nccl.f))dlsym(h, s)
     SYM(GetUniqueId, "ncclGetUniqueId");
     SYM(CommInitRank, "ncclCommInitRank");
+    SYM(CommInitRankConfig, "ncclCommInitRankConfig");
     SYM(CommDestroy, "ncclCommDestroy");
     SYM(CommSplit, "ncclCommSplit");
     SYM(AllReduce, "ncclAllReduce");
@@ -118,12 +129,60 @@ static bool nccl_available() {
     return g_nccl.ok;
 }
 
+// CTAs per NCCL communicator (ncclConfig_t.maxCTAs): the halo and the
+// reduction communicators together fit the SMs the interior SpMV leaves free
+static int nccl_ctas() {
+    const char *e = getenv("PBCG_NCCL_CTAS");
+    return e ? std::max(1, atoi(e)) : 2;
+}
+
 #define NCCL_TRY(x)                                                                                          \
     do {                                                                                                     \
         ncclResult_t e_ = (x);                                                                               \
         if (e_ != ncclSuccess)                                                                               \
             return fail(PBCG_ENCCL, "%s: %s", #x, g_nccl.GetErrorString ? g_nccl.GetErrorString(e_) : "?"); \
     } while (0)
+
+// ----------------------------------------------------------------------------
+// collective contract of setup: every rank hashes the setup
+// arguments that must agree; setup allgathers (row_begin, row_end, hull,
+// hash) and every rank checks the same records, so all return the same code
+// ----------------------------------------------------------------------------
+extern "C" int pbcg_config_hash(const pbcg_csr_local *A, const pbcg_dist *d, uint64_t *out) {
+    if (!out) return fail(PBCG_EINVAL, "config_hash: out == NULL");
+    uint64_t hsh = 1469598103934665603ull;  // FNV-1a 64
+    auto mix = [&](int64_t v) {
+        for (int k = 0; k < 8; ++k) {
+            hsh ^= (uint64_t)((v >> (8 * k)) & 0xFF);
+            hsh *= 1099511628211ull;
+        }
+    };
+    mix(PBCG_ABI_VERSION);
+    mix(A ? A->n_global : -1);  // comm-only handles: no matrix
+    mix(d ? std::max(1, d->nranks) : 1);
+    mix(d ? std::max(1, d->virtual_ranks) : 1);
+    mix(d ? d->precond : 0);
+    mix(d ? d->comm_mode : 0);
+    *out = hsh;
+    return PBCG_OK;
+}
+
+// rec: nranks records of PBCG_RANK_REC int64 (row_begin, row_end, cmin, cmax,
+// hash); with a matrix the row blocks must tile [0, n_global) in rank order
+extern "C" int pbcg_check_ranks(int32_t nranks, const int64_t *rec, int64_t n_global, int32_t has_matrix) {
+    if (nranks < 1 || !rec) return fail(PBCG_EINVAL, "check_ranks: bad arguments");
+    for (int k = 1; k < nranks; ++k)
+        if (rec[PBCG_RANK_REC * k + 4] != rec[4])
+            return fail(PBCG_EINVAL, "setup arguments differ between rank 0 and rank %d (config hash)", k);
+    if (!has_matrix) return PBCG_OK;
+    if (rec[0] != 0) return fail(PBCG_EINVAL, "rank 0 does not start at row 0");
+    for (int k = 0; k + 1 < nranks; ++k)
+        if (rec[PBCG_RANK_REC * k + 1] != rec[PBCG_RANK_REC * (k + 1)])
+            return fail(PBCG_EINVAL, "row blocks of ranks %d and %d are not contiguous", k, k + 1);
+    if (rec[PBCG_RANK_REC * (nranks - 1) + 1] != n_global)
+        return fail(PBCG_EINVAL, "row blocks of the ranks do not cover [0, n_global)");
+    return PBCG_OK;
+}
 
 // ----------------------------------------------------------------------------
 // host-only planning (exported; CPU-testable)
@@ -679,6 +738,7 @@ static int halo(pbcg_handle *h, int which, cudaStream_t st = nullptr) {
 // sum the phase-`ph` superaccumulators over ranks, then round + finalise
 template <int ND>
 static int reduce_finalize(pbcg_handle *h, int ph, int phase, cudaStream_t st, double *out, int32_t *oflags) {
+    NvtxRange nvtx_("pbcg.allreduce+finalize");
     if (h->dot_mode == PBCG_DOT_PLAIN && (phase == PH_A || phase == PH_B)) {
         // plain dots: every rank sums all partials in the same order (virtual
         // ranks), or its own and then an fp64 allreduce (NCCL: order chosen by NCCL)
@@ -1389,6 +1449,7 @@ static int plan_split(pbcg_handle *h) {
 
 extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void *stream, void *workspace,
                                size_t workspace_bytes, pbcg_handle **out) {
+    NvtxRange nvtx_("pbcg.setup");
     if (!out) return fail(PBCG_EINVAL, "out == NULL");
     *out = nullptr;
     auto *h = new pbcg_handle();
@@ -1419,29 +1480,46 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
         h->comm = true;
         // two communicators (halo on the main stream, reductions on the side
         // stream, so they can run concurrently); one unique id bootstraps one
-        // communicator, the second is split from it
-        NCCL_TRY(g_nccl.CommInitRank(&h->comm_halo, nranks, uid, d->rank));
-        NCCL_TRY(g_nccl.CommSplit(h->comm_halo, 0, d->rank, &h->comm_red, nullptr));
-        // hull of my rows, then allgather (rb, re, cmin, cmax) of every rank
+        // communicator, the second is split from it.  Each may use at most
+        // NCCL_CTAS CTAs: the interior SpMV they overlap leaves SPMV_COMM_SMS
+        // SMs free
+        ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+        cfg.blocking = 1;
+        cfg.minCTAs = 1;
+        cfg.maxCTAs = nccl_ctas();
+        cfg.commName = "pbcg_halo";
+        ncclConfig_t cfg2 = cfg;
+        cfg2.commName = "pbcg_reduce";
+        if (g_nccl.CommInitRankConfig)
+            NCCL_TRY(g_nccl.CommInitRankConfig(&h->comm_halo, nranks, uid, d->rank, &cfg));
+        else
+            NCCL_TRY(g_nccl.CommInitRank(&h->comm_halo, nranks, uid, d->rank));
+        NCCL_TRY(g_nccl.CommSplit(h->comm_halo, 0, d->rank, &h->comm_red, &cfg2));
+        // hull of my rows and the config hash, then allgather every rank's record
         RC_TRY(validate_csr(A, d));
-        if (!A) return fail(PBCG_EINVAL, "nranks > 1 needs a matrix (comm-only handles are single-rank)");
-        int64_t mine[4] = {A->row_begin, A->row_end, 0, -1};
-        {
+        if (A && d->virtual_ranks > 1) return fail(PBCG_EINVAL, "virtual ranks need nranks == 1");
+        int64_t mine[PBCG_RANK_REC] = {A ? A->row_begin : 0, A ? A->row_end : 0, 0, -1, 0};
+        uint64_t hsh = 0;
+        RC_TRY(pbcg_config_hash(A, d, &hsh));
+        mine[4] = (int64_t)hsh;
+        if (A) {
             std::vector<int64_t> b1 = {0, A->row_end - A->row_begin};
             std::vector<long long> hull;
             RC_TRY(compute_hulls(A, 1, b1, hull));
             if (hull[1] >= hull[0]) { mine[2] = hull[0]; mine[3] = hull[1]; }
         }
         int64_t *dbuf = nullptr;
-        CUDA_TRY(cudaMalloc(&dbuf, sizeof(int64_t) * 4 * (nranks + 1)));
+        CUDA_TRY(cudaMalloc(&dbuf, sizeof(int64_t) * PBCG_RANK_REC * (nranks + 1)));
         CUDA_TRY(cudaMemcpy(dbuf, mine, sizeof(mine), cudaMemcpyHostToDevice));
-        NCCL_TRY(g_nccl.AllGather(dbuf, dbuf + 4, 4, ncclInt64, h->comm_red, h->stream));
+        NCCL_TRY(g_nccl.AllGather(dbuf, dbuf + PBCG_RANK_REC, PBCG_RANK_REC, ncclInt64, h->comm_red, h->stream));
         CUDA_TRY(cudaStreamSynchronize(h->stream));
-        all_ranges.resize(4 * nranks);
-        CUDA_TRY(cudaMemcpy(all_ranges.data(), dbuf + 4, sizeof(int64_t) * 4 * nranks, cudaMemcpyDeviceToHost));
+        std::vector<int64_t> rec((size_t)PBCG_RANK_REC * nranks);
+        CUDA_TRY(cudaMemcpy(rec.data(), dbuf + PBCG_RANK_REC, sizeof(int64_t) * rec.size(), cudaMemcpyDeviceToHost));
         cudaFree(dbuf);
-        if (all_ranges[0] != 0 || all_ranges[4 * (nranks - 1) + 1] != A->n_global)
-            return fail(PBCG_EINVAL, "row blocks of the ranks do not cover [0, n_global)");
+        RC_TRY(pbcg_check_ranks(nranks, rec.data(), A ? A->n_global : 0, A ? 1 : 0));
+        all_ranges.resize(4 * (size_t)nranks);
+        for (int k = 0; k < nranks; ++k)
+            for (int j = 0; j < 4; ++j) all_ranges[4 * k + j] = rec[(size_t)PBCG_RANK_REC * k + j];
     }
     RC_TRY(prepare(h, A, d, h_rp, h->comm ? &all_ranges : nullptr));
     h->nranks = nranks;
@@ -1627,6 +1705,7 @@ static int start_alg2_rest(pbcg_handle *h);
 static int g_default_chunk = 16;
 
 extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0, const pbcg_opts *o) {
+    NvtxRange nvtx_("pbcg.start (I1-I4)");
     if (!h || h->comm_only) return fail(PBCG_EINVAL, "start: no matrix on this handle");
     pbcg_opts op;
     opts_defaults(o, op);
@@ -1907,6 +1986,7 @@ static int launch_small(pbcg_handle *h, int32_t iters) {
 }
 
 static int iterate_impl(pbcg_handle *h, int32_t k, int chunk, bool graphs) {
+    NvtxRange nvtx_("pbcg.iterate");
     if (small_on(h)) {  // the fused small-system kernel: one launch runs all k iterations (or stops when done)
         if (k > 0) RC_TRY(launch_small(h, k));
         h->it_enq += k;
@@ -1958,6 +2038,7 @@ static int true_residual(pbcg_handle *h) {
 }
 
 extern "C" int pbicgstab_finish(pbcg_handle *h, double *x, pbcg_result *res) {
+    NvtxRange nvtx_("pbcg.finish (true residual)");
     if (!h || !h->started) return fail(PBCG_EINVAL, "finish before start");
     // the copy-out of x (and Jacobi's x := D^-1 y) runs on the side stream
     // while the true residual (which only reads x) runs on the main stream
@@ -2104,6 +2185,7 @@ static int scratch(Scratch **out) {
 
 extern "C" int exdot(pbcg_handle *h, int64_t n, const double *x, const double *y, double *result, int32_t *flags,
                      int on_device, void *stream) {
+    NvtxRange nvtx_("pbcg.exdot");
     if (n < 0 || !result || (n > 0 && (!x || !y))) return fail(PBCG_EINVAL, "exdot: bad arguments");
     cudaStream_t st = (cudaStream_t)stream;
     Scratch *S = nullptr;
@@ -2142,9 +2224,14 @@ extern "C" int exdot(pbcg_handle *h, int64_t n, const double *x, const double *y
             a.gacc = h->R[v].gacc[4];
             a.ticket = h->R[v].tickets + 4;
             a.phase = PH_EXDOT;
-            a.finalize = 0;
-            const int grid = std::max(1, std::min<int>(S->grid1, (int)(((hi - lo) / 2 + K_BS - 1) / K_BS)));
-            multidot_kernel<1, K_NP, K_NE, K_BS, U_MD1><<<grid, K_BS, 0, st>>>(a);
+            a.finalize = 0;  // the last CTA leaves normalised words for the allreduce
+            if (((((uintptr_t)a.x[0]) | ((uintptr_t)a.y[0])) & 15) == 0 && a.n > 0) {
+                RC_TRY(stream_attrs());
+                XDS<<<stream_grid(h, a.n, TileGeo<X_NCW, XD_PPT>::T), STREAM_THREADS, XD_SMEM, st>>>(a);
+            } else {
+                const int grid = std::max(1, std::min<int>(S->grid1, (int)(((hi - lo) / 2 + K_BS - 1) / K_BS)));
+                multidot_kernel<1, K_NP, K_NE, K_BS, U_MD1><<<grid, K_BS, 0, st>>>(a);
+            }
             CUDA_TRY(cudaGetLastError());
         }
         RC_TRY(reduce_finalize<1>(h, 4, PH_EXDOT, st, out, ofl));

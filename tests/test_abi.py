@@ -32,7 +32,7 @@ def test_library_exports_every_header_symbol():
     assert len(names) >= 15, names
     for nm in names:
         assert hasattr(L, nm), nm
-    assert L.pbcg_abi_version() == 7
+    assert L.pbcg_abi_version() == 8
 
 
 def test_plan_partition_spec_examples():
@@ -166,3 +166,64 @@ def test_gloo_world2_superacc_allreduce_and_halo():
     for rank, r, ok in out:
         assert bits(r) == bits(want), rank
         assert ok
+
+
+# ---- collective contract of setup: config hash + rank records ----
+
+def test_config_hash_and_rank_check():
+    h = pb.config_hash(1000, nranks=4)
+    assert h == pb.config_hash(1000, nranks=4)
+    for other in (pb.config_hash(1001, nranks=4), pb.config_hash(1000, nranks=2), pb.config_hash(None, nranks=4),
+                  pb.config_hash(1000, nranks=4, precond="jacobi"), pb.config_hash(1000, nranks=4, comm_mode=1)):
+        assert other != h
+    b = pb.plan_partition(1000, 4)
+    rec = [[b[k], b[k + 1], 0, 999, h] for k in range(4)]
+    assert pb.check_ranks(rec, 1000)[0] == 0
+    bad = [list(r) for r in rec]
+    bad[2][4] = pb.config_hash(1000, nranks=4, precond="jacobi")
+    rc, msg = pb.check_ranks(bad, 1000)
+    assert rc == 1 and "rank 2" in msg
+    gap = [list(r) for r in rec]
+    gap[1][1] -= 1  # rows [b2 - 1, b2) owned by nobody
+    assert pb.check_ranks(gap, 1000)[0] == 1
+    assert pb.check_ranks(gap, 1000, has_matrix=False)[0] == 0  # comm-only: rows are not checked
+    short = [list(r) for r in rec]
+    short[3][1] = 999
+    assert pb.check_ranks(short, 1000)[0] == 1
+
+
+def _gloo_contract_worker(rank, world, port, n_mine, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b = pb.plan_partition(1000, world)
+    rec = torch.tensor([[int(b[rank]), int(b[rank + 1]), 0, 999,
+                         np.uint64(pb.config_hash(n_mine, nranks=world)).view(np.int64)]], dtype=torch.int64)
+    outs = [torch.zeros_like(rec) for _ in range(world)]
+    dist.all_gather(outs, rec)
+    rc, msg = pb.check_ranks(torch.cat(outs).numpy(), 1000)
+    q.put((rank, rc))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mismatch", [False, True])
+def test_gloo_world2_setup_contract(mismatch):
+    # the setup check as two processes run it: every rank sees the same
+    # gathered records and returns the same code
+    import multiprocessing as mp
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ns = [1000, 1001 if mismatch else 1000]
+    ps = [ctx.Process(target=_gloo_contract_worker, args=(r, 2, port, ns[r], q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert out[0] == out[1] == (1 if mismatch else 0)

@@ -173,6 +173,28 @@ def test_nccl_single_rank_handle(pb):
     S.close()
 
 
+@pytest.mark.parametrize("kind,n", [("well", 1 << 22), ("ill", 1 << 20), ("ragged", 100_003), ("unaligned", 4_097)])
+def test_comm_only_handle(pb, kind, n):
+    # comm-only handle (pbicgstab_setup with A = NULL) through
+    # the NCCL dataflow (1-rank communicator): the rank's slice goes through
+    # the TMA stream kernel (finalize = 0), the words through ncclAllReduce
+    # int64, then one rounding -- bit-exact; and without NCCL (local handle)
+    import torch
+    if kind == "ill":
+        x, y = gen.ill_pair(n, seed=9, block=1 << 12)
+    else:
+        x, y = gen.uniform(n, 3), gen.uniform(n, 4)
+    want = oracle.exdot(x, y)[0]
+    for force in (True, False):
+        C = pb.Comm(force_nccl=force)
+        xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        if kind == "unaligned":  # 8-byte aligned slices: the generic kernel
+            xt, yt = torch.from_numpy(np.concatenate([[0.0], x])).cuda()[1:], torch.from_numpy(np.concatenate([[0.0], y])).cuda()[1:]
+        got, f = C.exdot(xt, yt)
+        assert f == 0 and bits(got) == bits(want), (kind, force)
+        C.close()
+
+
 # ---- full-range EXDOT: products outside the fast zone ----
 
 def test_full_range_underflow_zone(pb):
