@@ -179,10 +179,12 @@ def run_gpu(args, rank, world, local_rank, dist):
     clocks = Clocks(local_rank)
     clocks.start()
     time.sleep(0.3)
-    # ---- timed region: the K iterations replayed as ONE captured CUDA graph
-    # (start() captures the K-iteration chunk; the W warm-ups run as one
-    # graph of their own length, captured before the timed region) ----
-    S.start(b, tol=0.0, max_iter=W + K + 8, poll_every=K)  # tol 0: every timed iteration does full work
+    # ---- timed region: the K iterations replayed as K / chunk launches of ONE
+    # captured CUDA graph of `chunk` iterations, chunk = the largest divisor of
+    # K up to 16 (start() captures it; long graphs replay slower: C3 7.2K
+    # iter/s at 8-16 iterations per graph, 6.8K at 200, tools/chunk_ab.py) ----
+    chunk = max(d for d in range(1, 17) if K % d == 0)
+    S.start(b, tol=0.0, max_iter=W + K + 8, poll_every=chunk)  # tol 0: every timed iteration does full work
     exec_mode = S.exec_mode()  # 0: six kernels per iteration (graphs); 1: the fused small-system kernel
     S.iterate(W)  # warm-up (start() already captured the CUDA graph of one chunk)
     torch.cuda.synchronize()
@@ -209,10 +211,10 @@ def run_gpu(args, rank, world, local_rank, dist):
         dist.all_reduce(okt, op=dist.ReduceOp.MIN)
         ok = bool(okt.item())
     clk = clocks.summary(tc0 - 0.05, tc1 + 0.05)
-    out = {"ms": ms, "ok": ok, "iters": res.iterations, "clocks": clk, "exec_mode": exec_mode}
+    out = {"ms": ms, "ok": ok, "iters": res.iterations, "clocks": clk, "exec_mode": exec_mode, "chunk": chunk}
     # ---- comparison arms, the same K steps each (SURVEY §8(f) NEXT-1..3) ----
     def timed_arm(S_, **kw):
-        S_.start(b, tol=0.0, max_iter=W + K + 8, poll_every=K, **kw)
+        S_.start(b, tol=0.0, max_iter=W + K + 8, poll_every=chunk, **kw)
         S_.iterate(W)
         torch.cuda.synchronize()
         if dist:
@@ -256,7 +258,7 @@ def run_gpu(args, rank, world, local_rank, dist):
     out["by"] = by
     kern = None
     if world == 1:
-        S.start(b, tol=0.0, max_iter=W + K + 8, poll_every=K)
+        S.start(b, tol=0.0, max_iter=W + K + 8, poll_every=chunk)
         S.iterate(W)
         kms = S.profile(K)
         res2 = S.finish(None)
@@ -536,6 +538,7 @@ def main():
             # six-kernel path: K2, finalize A, SpMV, K3, finalize B, SpMV per iteration (per rank; NCCL
             # kernels not counted); fused small-system kernel: one cooperative launch runs the K iterations
             "gpu_launches": 6 * K if out["exec_mode"] == 0 else 1,
+            "graph_chunk": out["chunk"],
             "exec_mode": "six kernels per iteration, CUDA graphs" if out["exec_mode"] == 0
             else "fused small-system kernel (one cooperative launch per iterate call)"}
     line["spmv_format"] = out["spmv_format"]

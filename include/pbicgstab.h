@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define PBCG_ABI_VERSION 8
+#define PBCG_ABI_VERSION 9
 
 /* return codes of every entry point (never an abort across the ABI) */
 enum pbcg_rc {
@@ -55,7 +55,8 @@ enum pbcg_status {
     PBCG_BREAKDOWN_RHO = 3,   /* |(r0,r_{i+1})| <= thr (R-11) */
     PBCG_BREAKDOWN_OMEGA = 4, /* omega_i = 0 and not converged (R-12) */
     PBCG_BREAKDOWN_ALPHA = 5, /* |alpha denominator| <= thr or not finite (R-11) */
-    PBCG_RANGE = 6,           /* an EXDOT left the exact zone (R-9) */
+    PBCG_RANGE = 6,           /* range_mode FULL: a NaN/Inf operand or an overflowing dot; FAST: a product
+                                 outside the fast zone (R-9, R-24) */
     PBCG_RUNNING = -1
 };
 
@@ -133,7 +134,16 @@ typedef struct {
     int32_t x0_zero;          /* 1: start from x0 = 0 without reading x0 (x0 may be NULL in pbicgstab_start;
                                  in pbicgstab_solve x is then the output buffer only): no host->device copy
                                  of the initial guess.  0 (default): x0 is read. */
+    int32_t range_mode;       /* PBCG_RANGE_FULL (0, default): every Algorithm 2 dot is exact over the whole
+                                 binary64 range (R-24):
+                                 a CTA whose products leave the fast zone (|fl(xy)| < 2^-960 or >= 2^1000)
+                                 corrects them into an extended accumulator (LSB 2^-2148); only a NaN/Inf
+                                 operand or a dot whose exact value rounds to +-inf ends the solve with
+                                 PBCG_RANGE.  PBCG_RANGE_FAST (1): any product outside the fast zone ends
+                                 it with PBCG_RANGE (R-9, R-19).  Algorithm 1 keeps R-9. */
 } pbcg_opts;
+
+enum pbcg_range_mode { PBCG_RANGE_FULL = 0, PBCG_RANGE_FAST = 1 };
 
 enum pbcg_dot_mode { PBCG_DOT_EXACT = 0, PBCG_DOT_PLAIN = 1 };
 enum pbcg_method { PBCG_METHOD_PBICGSTAB = 0, PBCG_METHOD_BICGSTAB = 1 };
@@ -220,7 +230,8 @@ int pbicgstab_spmv(pbcg_handle *h, const double *x_local, double *y_local);
  * rounded sum and
  * the call returns PBCG_OK unless that sum overflows binary64 (+-inf,
  * PBCG_ERANGE).  Distributed handles (virtual ranks, NCCL ranks, comm-only
- * handles of any nranks): PBCG_ERANGE, result unspecified.
+ * handles of any nranks) do the same per rank: the flagged CTAs' extended
+ * words are summed across ranks with the fast words (int64) and rounded once.
  * When bit 1 is set, bit 0 is unspecified.  n_local = 0 gives +0.0
  * (SPEC.md l.69). */
 int exdot(pbcg_handle *h, int64_t n_local, const double *x, const double *y, double *result, int32_t *flags,

@@ -33,6 +33,7 @@ _lib = None
 
 F_RANGE = 1
 F_NONFINITE = 2
+F_OVERFLOW = 4
 
 CONVERGED, MAXITER, BREAKDOWN_INIT, BREAKDOWN_RHO, BREAKDOWN_OMEGA, BREAKDOWN_ALPHA, RANGE = range(7)
 RUNNING = -1
@@ -75,7 +76,7 @@ def _L():
         lib.orc_dot_seq.argtypes = [i64, vp, vp]
         lib.orc_pbcg_size.restype = i32
         lib.orc_pbcg_init.restype = i32
-        lib.orc_pbcg_init.argtypes = [vp, i64, vp, vp, vp, vp, vp, dbl, dbl, i32, vp]
+        lib.orc_pbcg_init.argtypes = [vp, i64, vp, vp, vp, vp, vp, dbl, dbl, i32, vp, i32]
         lib.orc_pbcg_step.restype = i32
         lib.orc_pbcg_step.argtypes = [vp]
         lib.orc_pbcg_run.restype = i32
@@ -182,7 +183,11 @@ class PBiCGStab:
     """Algorithm 2 state machine.  ``b=None`` means b := A*ones (each side
     computes it with its own SpMV); ``x0=None`` means x0 := 0."""
 
-    def __init__(self, A, b=None, x0=None, tol=1e-10, eps=1e-30, max_iter=10000, history=True, rr_period=0):
+    def __init__(self, A, b=None, x0=None, tol=1e-10, eps=1e-30, max_iter=10000, history=True, rr_period=0,
+                 range_mode="full"):
+        """range_mode "full" (R-24): dots exact over the whole
+        binary64 range, only NaN/Inf or an overflowing exact sum stops the
+        solve; "fast" (R-9): any product outside the fast zone stops it."""
         L = _L()
         self.A = A
         self._rp = np.ascontiguousarray(A.row_ptr, np.int32)
@@ -197,7 +202,8 @@ class PBiCGStab:
                                   None if self._b is None else _p(self._b),
                                   None if self._x0 is None else _p(self._x0),
                                   float(tol), float(eps), int(max_iter),
-                                  None if self.hist is None else _p(self.hist))
+                                  None if self.hist is None else _p(self.hist),
+                                  {"full": 1, "fast": 0}[range_mode])
         if rr_period:  # residual replacement every rr_period iterations (NEXT-2, R-21)
             L.orc_pbcg_set_rr(self._S, int(rr_period))
 

@@ -30,6 +30,12 @@
  *              readings R-1..R-15 of DESIGN.md (w0 := A r0, scalar omega vs
  *              vector w, i=0 copies, FMA policy F, omega := 0 when (y,y)=0,
  *              relative breakdown thresholds, recursive-residual stopping).
+ *              Range of its dots (R-9, R-24): full range (default
+ *              of the Python binding): every dot is the exact sum rounded
+ *              once over the whole binary64 range; only
+ *              a NaN/Inf operand or an exact sum that rounds to +-inf stops
+ *              the solve (RANGE).  Fast zone (range_mode 0, round 1's
+ *              reading): any product outside the fast zone also stops it.
  *
  *  BiCGStab    PAPER.md §2 Algorithm 1 (l.39-54) in plain binary64 with
  *              sequential left-to-right dots (the "plain-double BiCGStab" of
@@ -53,7 +59,7 @@
 #define ORC_LIMBS 68
 #define ORC_BIAS 2148 /* bit 0 has weight 2^-2148 */
 
-enum { ORC_F_RANGE = 1, ORC_F_NONFINITE = 2 };
+enum { ORC_F_RANGE = 1, ORC_F_NONFINITE = 2, ORC_F_OVERFLOW = 4 /* the exact sum rounds to +-inf */ };
 
 typedef struct {
     uint64_t pos[ORC_LIMBS];
@@ -177,7 +183,7 @@ double orc_acc_round(orc_acc *a) {
     for (int i = ORC_LIMBS - 1; i >= 0; --i)
         if (mag[i]) { msb = i * 64 + 63 - __builtin_clzll(mag[i]); break; }
     int E = msb - ORC_BIAS; /* value in [2^E, 2^(E+1)) */
-    if (E >= 1024) { a->flags |= ORC_F_RANGE; return negative ? -INFINITY : INFINITY; }
+    if (E >= 1024) { a->flags |= ORC_F_RANGE | ORC_F_OVERFLOW; return negative ? -INFINITY : INFINITY; }
     int k = (E >= -1022) ? msb - 52 : (-1074 + ORC_BIAS); /* index of the kept LSB */
     uint64_t mant = 0;
     for (int i = msb; i >= k; --i) mant = (mant << 1) | (uint64_t)bit_of(mag, i);
@@ -189,7 +195,7 @@ double orc_acc_round(orc_acc *a) {
         if (mant == (1ULL << 53)) { mant >>= 1; k += 1; }
     }
     double r = ldexp((double)mant, k - ORC_BIAS);
-    if (isinf(r)) a->flags |= ORC_F_RANGE;
+    if (isinf(r)) a->flags |= ORC_F_RANGE | ORC_F_OVERFLOW;
     return negative ? -r : r;
 }
 
@@ -265,7 +271,13 @@ typedef struct {
     double *hist; /* (max_iter+1)*H_COLS, caller-owned, may be NULL */
     double loop_seconds;
     int rr_period, replacements; /* residual replacement every rr_period iterations (0: never) */
+    int full_range;              /* 1: only NONFINITE / OVERFLOW stop (R-24); 0: any RANGE flag stops (R-9) */
 } orc_pbcg;
+
+/* the flags of a dot phase that stop Algorithm 2 (R-9 / R-24) */
+static int stops(const orc_pbcg *S, int f) {
+    return S->full_range ? (f & (ORC_F_NONFINITE | ORC_F_OVERFLOW)) != 0 : f != 0;
+}
 
 int orc_pbcg_size(void) { return (int)sizeof(orc_pbcg); }
 
@@ -281,11 +293,13 @@ static void hist_put(orc_pbcg *S, int row, int col, double v) {
 }
 
 /* Lines I1-I4.  b == NULL means b := A*ones; x0 == NULL
- * means x0 := 0.  Returns ORC_OK / ORC_EINVAL / ORC_ENONFINITE; the solve
+ * means x0 := 0; full_range selects R-24 (1) or R-9 (0) for every dot.  Returns ORC_OK / ORC_EINVAL / ORC_ENONFINITE; the solve
  * outcome is in S->status (ORC_RUNNING while iterations remain). */
 int orc_pbcg_init(orc_pbcg *S, int64_t n, const int32_t *rp, const int32_t *col, const double *val,
-                  const double *b, const double *x0, double tol, double eps, int max_iter, double *hist) {
+                  const double *b, const double *x0, double tol, double eps, int max_iter, double *hist,
+                  int full_range) {
     memset(S, 0, sizeof(*S));
+    S->full_range = full_range != 0;
     S->n = n; S->rp = rp; S->col = col; S->val = val;
     S->tol = tol; S->max_iter = max_iter; S->hist = hist;
     if (n <= 0 || max_iter < 0 || !(tol >= 0.0)) return ORC_EINVAL;
@@ -325,7 +339,7 @@ int orc_pbcg_init(orc_pbcg *S, int64_t n, const int32_t *rp, const int32_t *col,
     hist_put(S, 0, H_RR, rr);
     hist_put(S, 0, H_RELRES, relres);
     S->it = 0;
-    if (f0 | f1 | f2 | f3) { S->status = ORC_RANGE; return ORC_OK; }
+    if (stops(S, f0 | f1 | f2 | f3)) { S->status = ORC_RANGE; return ORC_OK; }
     /* I3 */
     if (relres <= tol) { S->status = ORC_CONVERGED; return ORC_OK; }
     /* I4: a0 := (r0,r0)/(r0,w0) */
@@ -402,7 +416,7 @@ int orc_pbcg_step(orc_pbcg *S) {
     hist_put(S, i + 1, H_SIGMA, sigma);
     hist_put(S, i + 1, H_ZETA, zeta);
     hist_put(S, i + 1, H_OMEGA, omn);
-    if (fA) { S->status = ORC_RANGE; goto out; }
+    if (stops(S, fA)) { S->status = ORC_RANGE; goto out; }
     /* S6 (l.77-79) */
     for (int64_t k = 0; k < n; ++k) {
         x[k] = fma(omn, q[k], fma(al, p[k], x[k]));   /* x := x + alpha p + omega q */
@@ -424,7 +438,7 @@ int orc_pbcg_step(orc_pbcg *S) {
     hist_put(S, i + 1, H_RELRES, relres);
     S->it = i + 1;
     S->omega = omn;
-    if (fB) { S->status = ORC_RANGE; goto out; }
+    if (stops(S, fB)) { S->status = ORC_RANGE; goto out; }
     if (relres <= S->tol) { S->status = ORC_CONVERGED; goto out; }
     /* S10: breakdown (R-11, R-12) */
     double thr = fmax(S->epsn * sqrt(rr), 1e-300);

@@ -52,12 +52,15 @@ class _Dist(ctypes.Structure):
 DOT_MODES = {"exact": 0, "plain": 1}
 # pbcg_opts.method: "pbicgstab" = Algorithm 2 (the hot path), "bicgstab" = Algorithm 1 with exact dots
 METHODS = {"pbicgstab": 0, "bicgstab": 1}
+# pbcg_opts.range_mode: "full" = dots exact over the whole binary64 range (R-24), "fast" = R-9 zone stops
+RANGE_MODES = {"full": 0, "fast": 1}
 
 
 class _Opts(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("max_iter", ctypes.c_int32), ("breakdown_eps", ctypes.c_double),
                 ("poll_every", ctypes.c_int32), ("use_graphs", ctypes.c_int32), ("dot_mode", ctypes.c_int32),
-                ("method", ctypes.c_int32), ("rr_period", ctypes.c_int32), ("x0_zero", ctypes.c_int32)]
+                ("method", ctypes.c_int32), ("rr_period", ctypes.c_int32), ("x0_zero", ctypes.c_int32),
+                ("range_mode", ctypes.c_int32)]
 
 
 class _Result(ctypes.Structure):
@@ -190,9 +193,9 @@ class Solver:
 
     # -- helpers ------------------------------------------------------------
     def _opts(self, tol, max_iter, eps, poll_every, use_graphs, dot_mode="exact", method="pbicgstab", rr_period=0,
-              x0_zero=False):
+              x0_zero=False, range_mode="full"):
         return _Opts(float(tol), int(max_iter), float(eps), int(poll_every), int(use_graphs), DOT_MODES[dot_mode],
-                     METHODS[method], int(rr_period), int(bool(x0_zero)))
+                     METHODS[method], int(rr_period), int(bool(x0_zero)), RANGE_MODES[range_mode])
 
     def _vec(self, v, allow_host: bool):
         torch = self.torch
@@ -230,7 +233,7 @@ class Solver:
 
     # -- API ------------------------------------------------------------------
     def solve(self, b, x0=None, tol=1e-10, max_iter=10000, eps=1e-30, poll_every=16, use_graphs=True,
-              dot_mode="exact", method="pbicgstab", rr_period=0, out=None):
+              dot_mode="exact", method="pbicgstab", rr_period=0, out=None, range_mode="full"):
         """Solve; b/x0 may be CUDA tensors or host arrays/tensors (host buffers
         go through the library's staging path).  Returns (x, Result) with x on
         the same side as b.  x0=None starts from 0 without copying an initial
@@ -256,7 +259,7 @@ class Solver:
             x = x.copy() if isinstance(x, np.ndarray) else x.clone()
         xp = x.ctypes.data if isinstance(x, np.ndarray) else x.data_ptr()
         res = _Result()
-        opts = self._opts(tol, max_iter, eps, poll_every, use_graphs, dot_mode, method, rr_period, x0 is None)
+        opts = self._opts(tol, max_iter, eps, poll_every, use_graphs, dot_mode, method, rr_period, x0 is None, range_mode)
         _check(lib().pbicgstab_solve(self._h, ctypes.c_void_p(bp), ctypes.c_void_p(xp), ctypes.byref(opts), ctypes.byref(res)))
         self._sync_out()
         return x, self._result(res)
@@ -266,7 +269,7 @@ class Solver:
         return self.n_global if self._dist.virtual_ranks > 1 else self.n_local
 
     def start(self, b, x0=None, tol=1e-10, max_iter=10000, eps=1e-30, poll_every=16, use_graphs=True,
-              dot_mode="exact", method="pbicgstab", rr_period=0):
+              dot_mode="exact", method="pbicgstab", rr_period=0, range_mode="full"):
         torch = self.torch
         self._sync_in()
         self._b, bp = self._vec(b, allow_host=True)
@@ -274,7 +277,7 @@ class Solver:
             self._x0, xp = None, None
         else:
             self._x0, xp = self._vec(x0, allow_host=True)
-        opts = self._opts(tol, max_iter, eps, poll_every, use_graphs, dot_mode, method, rr_period, x0 is None)
+        opts = self._opts(tol, max_iter, eps, poll_every, use_graphs, dot_mode, method, rr_period, x0 is None, range_mode)
         _check(lib().pbicgstab_start(self._h, ctypes.c_void_p(bp), ctypes.c_void_p(xp), ctypes.byref(opts)))
 
     def iterate(self, k: int):

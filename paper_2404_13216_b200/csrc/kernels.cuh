@@ -35,7 +35,7 @@ struct Scalars {
     int32_t it, done, status, max_iter;
     int32_t hist_cap, err;
     int32_t qconv;  // Alg. 1: converged at the q check, x += alpha p still to apply
-    int32_t pad1;
+    int32_t range_mode;  // Alg. 2 dots: 0 full range (R-24: corrected, only NaN/Inf or overflow stop), 1 fast zone (R-9)
 };
 
 // ------------------------------------------------------------------------
@@ -208,8 +208,13 @@ __device__ void phase_finalize(int phase, Scalars *sc, const double *d, unsigned
 // overflow to +-inf).  Only the flagged CTAs pay, in parallel.
 // ------------------------------------------------------------------------
 constexpr int XS_L = 136;   // 4352 bits: 2^-2148 .. 2^2204 (products < 2^2048, sums of < 2^40 of them)
-constexpr int XS_OFF = 72;  // gacc word offset of the extended accumulator (PH_EXDOT, ND = 1)
-constexpr int XS_GW = XS_OFF + XS_L;  // gacc words a full-range EXDOT needs
+// word layout of an ND-dot reduction buffer: ND * SACC_L fast words, the
+// SACC_FLAGW flag counts, padding, then ND extended accumulators of XS_L words
+// (written only by CTAs that met a product outside the fast zone)
+__host__ __device__ constexpr int xs_off(int nd) { return ((nd * SACC_L + SACC_FLAGW + 7) / 8) * 8; }
+__host__ __device__ constexpr int xs_words(int nd) { return xs_off(nd) + nd * XS_L; }
+constexpr int XS_OFF = xs_off(1);     // 72: the standalone EXDOT's extended accumulator
+constexpr int XS_GW = xs_words(1);    // gacc words a full-range EXDOT needs
 
 __device__ __forceinline__ void dbl_parts(double v, unsigned long long &m, int &e) {
     const unsigned long long b = (unsigned long long)__double_as_longlong(v);
@@ -339,46 +344,165 @@ __device__ void cta_full_range(CtaSacc<1> &S, unsigned long long *X, long long *
         if (X[i]) atomicAdd((unsigned long long *)&gacc[XS_OFF + i], X[i]);
 }
 
+// Whether a reduction phase uses the full-range dots (R-24): the standalone
+// EXDOT always; Algorithm 2's phases (init, A, B, true residual) unless the
+// solve asked for the fast zone (R-9); Algorithm 1's phases keep R-9 (R-20).
+__device__ __forceinline__ bool phase_full_range(int phase, const Scalars *sc) {
+    if (phase == PH_EXDOT) return true;
+    if (phase >= PH1_INIT || !sc) return false;
+    return sc->range_mode == 0;
+}
+
+// The exact correction of one product of finite operands a, b, as a fast
+// pass formed it (p = fl(a b), e = fma(a, b, -p); a non-finite p or e was
+// never deposited): X += a b - p - e.
+__device__ __noinline__ void xs_correct(unsigned long long *X, double a, double b) {
+    const double p = __dmul_rn(a, b), e = __fma_rn(a, b, -p);
+    xs_add_product(X, a, b);
+    if (isfinite(p)) {
+        xs_add_product(X, -p, 1.0);
+        if (isfinite(e)) xs_add_product(X, -e, 1.0);
+    }
+}
+
+// Full-range pass of a CTA of an ND-dot FPE kernel whose fast pass raised
+// FLAG_RANGE (R-24): all threads, after the
+// CTA's FPEs are merged into S.w and before it publishes.  rows(f) calls
+// f(i) for every element i of this CTA (spread over its threads);
+// pair(d, i, a, b) yields dot d's operands at i, exactly as the fast pass
+// formed them.  A flagged product (|fl(ab)| < 2^-960 with a, b != 0) is
+// corrected into dot d's extended accumulator; a product with |fl(ab)| >=
+// 2^1000 may have overflowed the FPE's sums, so that dot's fast words of this
+// CTA are dropped and all its products enter the extended accumulator
+// exactly.  NaN/Inf operands set FLAG_NONFINITE (the solve stops).  The
+// normalised extended words are red.added into gext[d * XS_L ..].  X: ND *
+// XS_L words of shared scratch.  Only flagged CTAs run this (one more read of
+// their rows).
+template <int ND, class Rows, class Pair>
+__device__ void cta_full_range_nd(CtaSacc<ND> &S, unsigned long long *X, long long *gext, Rows rows, Pair pair) {
+    __shared__ int poisoned[ND];
+    for (int i = threadIdx.x; i < ND * XS_L; i += blockDim.x) X[i] = 0ull;
+    if (threadIdx.x < ND) poisoned[threadIdx.x] = 0;
+    __syncthreads();
+    rows([&](int64_t i) {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+            double a, b;
+            pair(d, i, a, b);
+            if (!isfinite(a) || !isfinite(b)) {
+                atomicOr(&S.flags, FLAG_NONFINITE);
+                continue;
+            }
+            if (is_zero(a) || is_zero(b)) continue;
+            const double p = __dmul_rn(a, b);
+            const unsigned ep = (unsigned)(__double2hiint(p) >> 20) & 0x7FFu;
+            if ((ep - 63u) < 1960u) continue;  // inside the fast zone: TwoProd was exact, no correction
+            if (ep >= 63u) {                   // |p| >= 2^1000 (or p = inf)
+                poisoned[d] = 1;
+                continue;
+            }
+            xs_correct(X + d * XS_L, a, b);
+        }
+    });
+    __syncthreads();
+    if (S.flags & FLAG_NONFINITE) return;
+    bool any_p = false;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) any_p |= poisoned[d] != 0;
+    if (any_p) {  // the poisoned dots: every product of this CTA, exactly
+        for (int j = threadIdx.x; j < ND * XS_L; j += blockDim.x)
+            if (poisoned[j / XS_L]) X[j] = 0ull;
+        for (int j = threadIdx.x; j < ND * SACC_L; j += blockDim.x)
+            if (poisoned[j / SACC_L]) (&S.w[0][0])[j] = 0ull;
+        __syncthreads();
+        rows([&](int64_t i) {
+#pragma unroll
+            for (int d = 0; d < ND; ++d) {
+                if (!poisoned[d]) continue;
+                double a, b;
+                pair(d, i, a, b);
+                xs_add_product(X + d * XS_L, a, b);
+            }
+        });
+        __syncthreads();
+    }
+    if (threadIdx.x < ND) xs_normalize((long long *)X + threadIdx.x * XS_L);
+    __syncthreads();
+    for (int j = threadIdx.x; j < ND * XS_L; j += blockDim.x)
+        if (X[j]) atomicAdd((unsigned long long *)&gext[j], X[j]);
+}
+
+// The extended path of round_dots (kept out of line: it is rare, and inlined
+// it would raise the register count of the kernels that call it): dot d =
+// fast words w[d] + extended words ge[d XS_L ..], rounded once into r[d].
+__device__ __noinline__ unsigned round_ext(double *r, const long long *w, long long *ge, int nd, bool nonfinite,
+                                           bool clear_ext) {
+    __shared__ long long X[XS_L];
+    __shared__ unsigned ovf;
+    __syncthreads();
+    if (threadIdx.x == 0) ovf = 0u;
+    for (int d = 0; d < nd; ++d) {
+        long long *g = ge + d * XS_L;
+        for (int i = threadIdx.x; i < XS_L; i += blockDim.x) {
+            X[i] = __ldcg(&g[i]);
+            if (clear_ext) g[i] = 0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && !nonfinite) {
+            const long long *wd = w + d * SACC_L;
+            for (int i = 0; i < SACC_L; ++i) X[i + 33] += wd[i] * (1ll << 18);  // 2^-1074 = 2^(32*33+18) * 2^-2148
+            xs_normalize(X);
+            const double v = xs_round(X);
+            r[d] = v;
+            if (isinf(v)) ovf |= FLAG_RANGE;
+        }
+        __syncthreads();
+    }
+    return nonfinite ? FLAG_NONFINITE : ovf;
+}
+
+// The rounded dots of a reduction buffer whose fast words are normalised in
+// S.w (cta_sacc_collect): S.rounded[0..ND), all threads.  full (R-24): when
+// some CTA flagged FLAG_RANGE (and no input was NaN/Inf), dot d is its fast
+// words plus its extended words gacc[xs_off(ND) + d XS_L ..], rounded once
+// (RN-even, subnormals, +-inf on overflow), and those extended words are
+// cleared (clear_ext; the fused kernels' CTAs all read one buffer, CTA 0
+// clears it later).  Returns the flags for phase_finalize: full -> FLAG_NONFINITE,
+// or FLAG_RANGE for a dot that rounds to +-inf; fast zone (R-9) -> the
+// gathered flags plus overflow.
+template <int ND>
+__device__ unsigned round_dots(CtaSacc<ND> &S, long long *gacc, unsigned gflags, bool full, bool clear_ext = true) {
+    __shared__ unsigned ovf;
+    if (threadIdx.x == 0) ovf = 0u;
+    __syncthreads();
+    long long *w = (long long *)&S.w[0][0];
+    if ((threadIdx.x >> 5) < ND) {  // one warp per dot
+        bool o = false;
+        const double rv = sacc_round_warp(w + (threadIdx.x >> 5) * SACC_L, &o);
+        if ((threadIdx.x & 31) == 0) {
+            S.rounded[threadIdx.x >> 5] = rv;
+            if (o) atomicOr(&ovf, FLAG_RANGE);
+        }
+    }
+    __syncthreads();
+    if (!full) return gflags | ovf;
+    if (!(gflags & FLAG_RANGE)) return (gflags & FLAG_NONFINITE) | ovf;
+    return round_ext(S.rounded, (const long long *)&S.w[0][0], gacc + xs_off(ND), ND, (gflags & FLAG_NONFINITE) != 0,
+                     clear_ext);
+}
+
 // Last CTA of a dot kernel: collect + normalise gacc; then either round and
 // finalise (single rank) or leave normalised words for the allreduce.
 template <int ND>
 __device__ void last_cta_finish(CtaSacc<ND> &S, long long *gacc, unsigned *ticket, int phase, int finalize,
-                                Scalars *sc, double *hist, double *out, int32_t *out_flags,
-                                const double *cx = nullptr, const double *cy = nullptr, int64_t cn = 0) {
+                                Scalars *sc, double *hist, double *out, int32_t *out_flags) {
     unsigned gflags;
     cta_sacc_collect<ND>(S, gacc, gflags);
     long long *w = (long long *)&S.w[0][0];
     if (finalize) {
-        if ((threadIdx.x >> 5) < ND) {  // one warp per dot
-            bool ovf = false;
-            const double rv = sacc_round_warp(w + (threadIdx.x >> 5) * SACC_L, &ovf);
-            if ((threadIdx.x & 31) == 0) {
-                S.rounded[threadIdx.x >> 5] = rv;
-                if (ovf) atomicOr(&S.flags, FLAG_RANGE);
-            }
-        }
-        __syncthreads();
-        // a flagged standalone dot with finite inputs (the flagged CTAs have
-        // classified their elements): the fast words of the unflagged CTAs plus
-        // the flagged CTAs' extended sums, rounded once (NEXT-4)
-        if constexpr (ND == 1) if (cx && (gflags & FLAG_RANGE) && !(gflags & FLAG_NONFINITE)) {
-            __shared__ long long X[XS_L];
-            for (int i = threadIdx.x; i < XS_L; i += blockDim.x) {
-                X[i] = __ldcg(&gacc[XS_OFF + i]);
-                gacc[XS_OFF + i] = 0;
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                for (int i = 0; i < SACC_L; ++i) X[i + 33] += w[i] * (1ll << 18);  // 2^-1074 = 2^(32*33+18) * 2^-2148
-                xs_normalize(X);
-                S.rounded[0] = xs_round(X);
-            }
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) {
-            unsigned f = gflags | (S.flags & (FLAG_RANGE | FLAG_NONFINITE));
-            phase_finalize(phase, sc, S.rounded, f, hist, out, out_flags);
-        }
+        unsigned f = round_dots<ND>(S, gacc, gflags, phase_full_range(phase, sc));
+        if (phase == PH_EXDOT) f |= gflags & FLAG_RANGE;  // the exdot flag contract reports the zone (pbicgstab.h)
+        if (threadIdx.x == 0) phase_finalize(phase, sc, S.rounded, f, hist, out, out_flags);
         for (int i = threadIdx.x; i < ND * SACC_L + SACC_FLAGW; i += blockDim.x) gacc[i] = 0;
     } else {
         for (int i = threadIdx.x; i < ND * SACC_L; i += blockDim.x) gacc[i] = w[i];
@@ -489,29 +613,38 @@ __global__ void __launch_bounds__(BS) multidot_kernel(MultiDotArgs a) {
     }
 #pragma unroll
     for (int d = 0; d < ND; ++d) acc[d].warp_merge(S.w[d]);
-    if constexpr (ND == 1) {
-        if (a.finalize && a.phase == PH_EXDOT) {  // standalone dot: flagged CTAs take the full-range pass
-            __shared__ unsigned long long X[XS_L];
-            if (flags) atomicOr(&S.flags, flags);
-            flags = 0;
-            __syncthreads();
-            if (S.flags)
-                cta_full_range<1>(S, X, a.gacc, a.x[0], a.y[0], [&](auto f) {
-                    const bool al = ((((uintptr_t)a.x[0]) | ((uintptr_t)a.y[0])) & 15) == 0;
-                    const int64_t m = al ? n >> 1 : n;  // pairs (aligned) or elements, as the fast pass
-                    for (int64_t p0 = (int64_t)blockIdx.x * BS; p0 < m; p0 += stride)
-                        for (int64_t p = p0 + threadIdx.x; p < min(p0 + BS, m); p += blockDim.x) {
-                            if (al) { f(2 * p); f(2 * p + 1); } else f(p);
-                        }
-                    if (al && (n & 1) && blockIdx.x == 0 && threadIdx.x == 0) f(n - 1);
-                });
+    // full range (R-24): the CTAs that met a product outside the fast zone
+    // correct it (the standalone EXDOT, single GPU or distributed; Alg. 2's
+    // init and true-residual dots unless the solve runs in the fast zone)
+    if (a.phase == PH_EXDOT || phase_full_range(a.phase, a.sc)) {
+        if (flags) atomicOr(&S.flags, flags);
+        flags = 0;
+        __syncthreads();
+        auto rows = [&](auto f) {  // this CTA's elements, as the fast pass visited them
+            const bool al = aligned;
+            const int64_t m = al ? n >> 1 : n;  // pairs (aligned) or elements
+            for (int64_t p0 = (int64_t)blockIdx.x * BS; p0 < m; p0 += stride)
+                for (int64_t p = p0 + threadIdx.x; p < min(p0 + BS, m); p += blockDim.x) {
+                    if (al) { f(2 * p); f(2 * p + 1); } else f(p);
+                }
+            if (al && (n & 1) && blockIdx.x == 0 && threadIdx.x == 0) f(n - 1);
+        };
+        if constexpr (ND == 1) {
+            if (a.phase == PH_EXDOT) {
+                __shared__ unsigned long long X1[XS_L];
+                if (S.flags) cta_full_range<1>(S, X1, a.gacc, a.x[0], a.y[0], rows);
+            }
+        }
+        if (a.phase != PH_EXDOT && (S.flags & FLAG_RANGE)) {
+            __shared__ unsigned long long X[ND * XS_L];
+            cta_full_range_nd<ND>(S, X, a.gacc + xs_off(ND), rows, [&](int d, int64_t i, double &x, double &y) {
+                x = a.x[d][i];
+                y = a.y[d][i];
+            });
         }
     }
-    if (cta_sacc_publish<ND>(S, flags, a.gacc, a.ticket)) {
-        const bool cls = (ND == 1 && a.phase == PH_EXDOT);
-        last_cta_finish<ND>(S, a.gacc, a.ticket, a.phase, a.finalize, a.sc, a.hist, a.out, a.out_flags,
-                            cls ? a.x[0] : nullptr, cls ? a.y[0] : nullptr, a.n);
-    }
+    if (cta_sacc_publish<ND>(S, flags, a.gacc, a.ticket))
+        last_cta_finish<ND>(S, a.gacc, a.ticket, a.phase, a.finalize, a.sc, a.hist, a.out, a.out_flags);
 }
 
 // After an allreduce of normalised words: normalise, round, finalise (1 CTA).
@@ -526,17 +659,9 @@ __global__ void finalize_kernel(long long *gacc, int phase, Scalars *sc, double 
     if (threadIdx.x == 0) S.flags = 0u;
     unsigned gflags;
     cta_sacc_collect<ND>(S, gacc, gflags);
-    long long *w = (long long *)&S.w[0][0];
-    if ((threadIdx.x >> 5) < ND) {  // one warp per dot
-        bool ovf = false;
-        const double rv = sacc_round_warp(w + (threadIdx.x >> 5) * SACC_L, &ovf);
-        if ((threadIdx.x & 31) == 0) {
-            S.rounded[threadIdx.x >> 5] = rv;
-            if (ovf) atomicOr(&S.flags, FLAG_RANGE);
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) phase_finalize(phase, sc, S.rounded, gflags | (S.flags & FLAG_RANGE), hist, out, out_flags);
+    unsigned f = round_dots<ND>(S, gacc, gflags, phase_full_range(phase, sc));
+    if (phase == PH_EXDOT) f |= gflags & FLAG_RANGE;  // the exdot flag contract reports the zone (pbicgstab.h)
+    if (threadIdx.x == 0) phase_finalize(phase, sc, S.rounded, f, hist, out, out_flags);
     __syncthreads();
     for (int i = threadIdx.x; i < ND * SACC_L + SACC_FLAGW; i += blockDim.x) gacc[i] = 0;
 }

@@ -269,7 +269,7 @@ extern "C" int pbcg_sacc_words(void) { return SACC_L; }
 // ----------------------------------------------------------------------------
 // handle
 // ----------------------------------------------------------------------------
-static constexpr int GW4 = 4 * SACC_L + SACC_FLAGW;  // words of a 4-dot reduction buffer
+static constexpr int GW4 = xs_words(4);  // words of a 4-dot reduction buffer (fast words, flags, extended words)
 static_assert(GW4 >= XS_GW, "a phase buffer also holds the full-range EXDOT accumulator");
 static constexpr int NPH = 5;                        // reduction buffers: init, A, B, true, exdot
 static constexpr int K_BS = 256;
@@ -757,7 +757,7 @@ static int reduce_finalize(pbcg_handle *h, int ph, int phase, cudaStream_t st, d
         }
         return PBCG_OK;
     }
-    const int words = ND * SACC_L + SACC_FLAGW;
+    const int words = xs_words(ND);  // fast words, flag counts and the extended words (R-24)
     if (h->V > 1) {
         vallreduce_kernel<<<(words + 127) / 128, 128, 0, st>>>(h->vgacc + (size_t)ph * h->V, h->V, words);
         CUDA_TRY(cudaGetLastError());
@@ -1688,6 +1688,7 @@ static void opts_defaults(const pbcg_opts *o, pbcg_opts &e) {
     e.method = PBCG_METHOD_PBICGSTAB;
     e.rr_period = 0;
     e.x0_zero = 0;
+    e.range_mode = PBCG_RANGE_FULL;
     if (o) {
         e = *o;
         if (!(e.breakdown_eps > 0.0)) e.breakdown_eps = 1e-30;
@@ -1717,6 +1718,8 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
     if (op.method == PBCG_METHOD_BICGSTAB && op.dot_mode != PBCG_DOT_EXACT)
         return fail(PBCG_EINVAL, "start: Algorithm 1 runs with exact dots only");
     if (op.rr_period < 0) return fail(PBCG_EINVAL, "start: rr_period < 0");
+    if (op.range_mode != PBCG_RANGE_FULL && op.range_mode != PBCG_RANGE_FAST)
+        return fail(PBCG_EINVAL, "start: bad range_mode");
     if (op.rr_period > 0 && op.method != PBCG_METHOD_PBICGSTAB)
         return fail(PBCG_EINVAL, "start: residual replacement is defined for Algorithm 2");
     h->max_iter = op.max_iter;
@@ -1730,6 +1733,7 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
     s0.max_iter = op.max_iter;
     s0.hist_cap = h->hist_cap;
     s0.status = ST_RUNNING;
+    s0.range_mode = op.range_mode;
     for (auto &R : h->R) {
         CUDA_TRY(cudaMemsetAsync(R.gsm, 0, sizeof(long long) * 4 * (size_t)GW4, h->stream));
         CUDA_TRY(cudaMemsetAsync(R.gbar, 0, sizeof(unsigned) * 16, h->stream));
@@ -2243,10 +2247,9 @@ extern "C" int exdot(pbcg_handle *h, int64_t n, const double *x, const double *y
     CUDA_TRY(cudaStreamSynchronize(st));
     if (flags) *flags = fl;
     if (fl & FLAG_NONFINITE) return fail(PBCG_ENONFINITE, "exdot: NaN/Inf input");
-    const bool full = !h || (h->V == 1 && !h->comm);  // the full-range pass ran: the value is exact
-    if ((fl & FLAG_RANGE) && (!full || !std::isfinite(*result)))
-        return fail(PBCG_ERANGE, full ? "exdot: the exact sum overflows binary64"
-                                      : "exdot: product outside the exact zone (R-9), distributed handle");
+    // the full-range pass ran on every flagged CTA (single GPU or per rank):
+    // the value is the exactly rounded sum; only an overflow is an error
+    if ((fl & FLAG_RANGE) && !std::isfinite(*result)) return fail(PBCG_ERANGE, "exdot: the exact sum overflows binary64");
     return PBCG_OK;
 }
 

@@ -80,9 +80,11 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar) {
 
 // this CTA's words into the phase buffer, not normalised: the whole grid adds
 // at most 2 n <= 2^18 signed 32-bit digits into any word (< 2^51, no int64
-// overflow); the readers normalise once (cta_sacc_collect)
+// overflow); the readers normalise once (cta_sacc_collect).  Full range
+// (R-24): a CTA that corrected products (X, one extended accumulator per dot)
+// adds its normalised extended words into g[xs_off(ND) ..] and clears X.
 template <int ND>
-__device__ __forceinline__ void small_publish(CtaSacc<ND> &S, unsigned flags, long long *g) {
+__device__ __forceinline__ void small_publish(CtaSacc<ND> &S, unsigned flags, long long *g, unsigned long long *X) {
     if (flags) atomicOr(&S.flags, flags);
     __syncthreads();
     for (int i = threadIdx.x; i < ND * SACC_L; i += blockDim.x) {
@@ -93,26 +95,52 @@ __device__ __forceinline__ void small_publish(CtaSacc<ND> &S, unsigned flags, lo
         if (S.flags & FLAG_RANGE) atomicAdd((unsigned long long *)&g[ND * SACC_L], 1ull);
         if (S.flags & FLAG_NONFINITE) atomicAdd((unsigned long long *)&g[ND * SACC_L + 1], 1ull);
     }
+    if ((S.flags & FLAG_RANGE) && X) {
+        if (threadIdx.x < ND) xs_normalize((long long *)X + threadIdx.x * XS_L);
+        __syncthreads();
+        for (int i = threadIdx.x; i < ND * XS_L; i += blockDim.x) {
+            if (X[i]) atomicAdd((unsigned long long *)&g[xs_off(ND) + i], X[i]);
+            X[i] = 0ull;
+        }
+    }
 }
 
-// all CTAs: the words of one phase -> rounded dots -> the scalar step
+// all CTAs: the words of one phase -> rounded dots -> the scalar step (every
+// CTA reads the same buffer: its extended words are cleared by CTA 0 later)
 template <int ND>
 __device__ void small_round(CtaSacc<ND> &S, long long *g, int phase, Scalars *scl, double *hist) {
     if (threadIdx.x == 0) S.flags = 0u;
     unsigned gflags;
     cta_sacc_collect<ND>(S, g, gflags);
-    long long *w = (long long *)&S.w[0][0];
-    if ((threadIdx.x >> 5) < ND) {  // one warp per dot
-        bool ovf = false;
-        const double rv = sacc_round_warp(w + (threadIdx.x >> 5) * SACC_L, &ovf);
-        if ((threadIdx.x & 31) == 0) {
-            S.rounded[threadIdx.x >> 5] = rv;
-            if (ovf) atomicOr(&S.flags, FLAG_RANGE);
-        }
+    const unsigned f = round_dots<ND>(S, g, gflags, phase_full_range(phase, scl), false);
+    if (threadIdx.x == 0) phase_finalize(phase, scl, S.rounded, f, hist, nullptr, nullptr);
+    __syncthreads();
+}
+
+// CTA 0 (all its threads): clear a phase buffer every CTA has read; its
+// extended words only if some CTA wrote them (flag count != 0)
+template <int ND>
+__device__ __forceinline__ void small_clear(long long *g) {
+    const bool ext = __ldcg(&g[ND * SACC_L]) != 0;
+    __syncthreads();
+    const int words = ext ? xs_words(ND) : ND * SACC_L + SACC_FLAGW;
+    for (int i = threadIdx.x; i < words; i += blockDim.x) g[i] = 0;
+}
+
+// one product of the fused kernels: TwoProd + flag; a flagged product of
+// finite operands is corrected into the dot's extended accumulator Xd when
+// the solve runs with full range (R-24), a NaN/Inf operand flags NONFINITE
+template <class TP>
+__device__ __forceinline__ Prod small_prod(const TP &tp, double a, double b, bool zero_op, unsigned &flags,
+                                           unsigned long long *Xd) {
+    unsigned f = 0;
+    const Prod P = tp.prep(a, b, zero_op, f);
+    if (f) {
+        if (!isfinite(a) || !isfinite(b)) f = FLAG_NONFINITE;
+        else if (Xd) xs_correct(Xd, a, b);
+        flags |= f;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) phase_finalize(phase, scl, S.rounded, gflags | (S.flags & FLAG_RANGE), hist, nullptr, nullptr);
-    __syncthreads();
+    return P;
 }
 
 // Plain dot mode (the paper's non-reproducible arm, NEXT-1): per-thread fma
@@ -167,6 +195,7 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
     __shared__ CtaSacc<3> SB;
     __shared__ Scalars scs;
     __shared__ double ws[BS / 32 * 4], dsum[4];  // plain mode: warp sums, rounded dots
+    __shared__ unsigned long long X[4 * XS_L];   // full range: extended accumulators of the corrected products
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n = a.n;
     // whole sigma windows (256 rows) when rows are permuted, else whole slices
@@ -178,6 +207,11 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
     if (threadIdx.x == 0 && blockIdx.x != 0) scs = *a.sc;
     __syncthreads();
     const ExAccT<1, 1, 1> tp{};  // TwoProd + R-9 flag only
+    // full range (R-24): corrections of flagged products go to X (per dot)
+    const bool full = EXACT && scl->range_mode == 0;
+    for (int i = threadIdx.x; i < 4 * XS_L; i += blockDim.x) X[i] = 0ull;
+    __syncthreads();
+    auto XD = [&](int d) -> unsigned long long * { return full ? X + d * XS_L : nullptr; };
     unsigned long long ts_prev = 0;
     (void)ts_prev;
     SMALL_TS(-1);
@@ -208,10 +242,10 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
                     a.p[i] = p; a.s[i] = s; a.z[i] = z; a.q[i] = q; a.y[i] = y;
                     if (EXACT) {
                         const bool zy = is_zero(y), zr = is_zero(rh);
-                        P[0] = tp.prep(q, y, is_zero(q) | zy, flags);
-                        P[1] = tp.prep(y, y, zy, flags);
-                        P[2] = tp.prep(rh, s, zr | is_zero(s), flags);
-                        P[3] = tp.prep(rh, z, zr | is_zero(z), flags);
+                        P[0] = small_prod(tp, q, y, is_zero(q) | zy, flags, XD(0));
+                        P[1] = small_prod(tp, y, y, zy, flags, XD(1));
+                        P[2] = small_prod(tp, rh, s, zr | is_zero(s), flags, XD(2));
+                        P[3] = small_prod(tp, rh, z, zr | is_zero(z), flags, XD(3));
                     } else {
                         acc[0] = __fma_rn(q, y, acc[0]);
                         acc[1] = __fma_rn(y, y, acc[1]);
@@ -227,14 +261,14 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
                     }
                 }
             }
-            if (EXACT) small_publish<4>(SA, flags, a.gA[par]);
+            if (EXACT) small_publish<4>(SA, flags, a.gA[par], full ? X : nullptr);
             else small_plain_publish<4, BS>(acc, ws, (double *)a.gA[0]);
         }
         SMALL_TS(4);  // K2 rows + publish
         grid_barrier(a.bar);
         SMALL_TS(5);  // barrier A
         if (EXACT && blockIdx.x == 0) {  // every CTA has read gB of the previous iteration: clear it for the next one
-            for (int i = threadIdx.x; i < 3 * SACC_L + SACC_FLAGW; i += BS) a.gB[par ^ 1][i] = 0;
+            small_clear<3>(a.gB[par ^ 1]);
         }
         if (EXACT) small_round<4>(SA, a.gA[par], PH_A, scl, hist);  // l.76
         else small_plain_round<4>((const double *)a.gA[0], dsum, PH_A, scl, hist);
@@ -263,9 +297,9 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
                     a.x[i] = x; a.r[i] = r; a.w[i] = w;
                     if (EXACT) {
                         const bool zr = is_zero(r), zh = is_zero(rh);
-                        P[0] = tp.prep(rh, r, zh | zr, flags);
-                        P[1] = tp.prep(rh, w, zh | is_zero(w), flags);
-                        P[2] = tp.prep(r, r, zr, flags);
+                        P[0] = small_prod(tp, rh, r, zh | zr, flags, XD(0));
+                        P[1] = small_prod(tp, rh, w, zh | is_zero(w), flags, XD(1));
+                        P[2] = small_prod(tp, r, r, zr, flags, XD(2));
                     } else {
                         acc[0] = __fma_rn(rh, r, acc[0]);
                         acc[1] = __fma_rn(rh, w, acc[1]);
@@ -280,14 +314,14 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_kernel(SmallArgs a) {
                     }
                 }
             }
-            if (EXACT) small_publish<3>(SB, flags, a.gB[par]);
+            if (EXACT) small_publish<3>(SB, flags, a.gB[par], full ? X : nullptr);
             else small_plain_publish<3, BS>(acc, ws, (double *)a.gB[0]);
         }
         SMALL_TS(13);  // K3 rows + publish
         grid_barrier(a.bar);
         SMALL_TS(14);  // barrier B
         if (EXACT && blockIdx.x == 0) {  // every CTA has read gA of this iteration
-            for (int i = threadIdx.x; i < 4 * SACC_L + SACC_FLAGW; i += BS) a.gA[par][i] = 0;
+            small_clear<4>(a.gA[par]);
         }
         if (EXACT) small_round<3>(SB, a.gB[par], PH_B, scl, hist);  // l.81-82, stopping and breakdown rules
         else small_plain_round<3>((const double *)a.gB[0], dsum, PH_B, scl, hist);
@@ -312,6 +346,7 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_reg_kernel(SmallArgs a) {
     __shared__ CtaSacc<3> SB;
     __shared__ Scalars scs;
     __shared__ double ws[BS / 32 * 4], dsum[4];
+    __shared__ unsigned long long X[4 * XS_L];
     // a launch enqueued after the solve stopped (the overlapped polls of
     // pbicgstab_solve): no reload and store-back of the state
     if (__ldcg(&a.sc->done)) return;
@@ -340,6 +375,11 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_reg_kernel(SmallArgs a) {
     }
     __syncthreads();
     const ExAccT<1, 1, 1> tp{};
+    // full range (R-24): corrections of flagged products go to X (per dot)
+    const bool full = EXACT && scl->range_mode == 0;
+    for (int i = threadIdx.x; i < 4 * XS_L; i += blockDim.x) X[i] = 0ull;
+    __syncthreads();
+    auto XD = [&](int d) -> unsigned long long * { return full ? X + d * XS_L : nullptr; };
     bool k3_done = true;  // the registers hold the state after K3 (or at entry)
     for (int k = 0; k < a.iters && !scl->done; ++k) {
         const int par = scl->it & 1;
@@ -366,10 +406,10 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_reg_kernel(SmallArgs a) {
                 a.z[i] = z;               // gathered by the SpMV of every CTA
                 if (EXACT) {
                     const bool zy = is_zero(y), zr = is_zero(rh);
-                    P[0] = tp.prep(q, y, is_zero(q) | zy, flags);
-                    P[1] = tp.prep(y, y, zy, flags);
-                    P[2] = tp.prep(rh, s, zr | is_zero(s), flags);
-                    P[3] = tp.prep(rh, z, zr | is_zero(z), flags);
+                    P[0] = small_prod(tp, q, y, is_zero(q) | zy, flags, XD(0));
+                    P[1] = small_prod(tp, y, y, zy, flags, XD(1));
+                    P[2] = small_prod(tp, rh, s, zr | is_zero(s), flags, XD(2));
+                    P[3] = small_prod(tp, rh, z, zr | is_zero(z), flags, XD(3));
                 } else {
                     acc[0] = __fma_rn(q, y, 0.0);
                     acc[1] = __fma_rn(y, y, 0.0);
@@ -384,14 +424,14 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_reg_kernel(SmallArgs a) {
                     if (is_nonzero(P[d].p)) sacc_deposit(SA.w[d], P[d].p);
                     if (is_nonzero(P[d].e)) sacc_deposit(SA.w[d], P[d].e);
                 }
-                small_publish<4>(SA, flags, a.gA[par]);
+                small_publish<4>(SA, flags, a.gA[par], full ? X : nullptr);
             } else {
                 small_plain_publish<4, BS>(acc, ws, (double *)a.gA[0]);
             }
         }
         grid_barrier(a.bar);
         if (EXACT && blockIdx.x == 0)
-            for (int j = threadIdx.x; j < 3 * SACC_L + SACC_FLAGW; j += BS) a.gB[par ^ 1][j] = 0;
+            small_clear<3>(a.gB[par ^ 1]);
         if (EXACT) small_round<4>(SA, a.gA[par], PH_A, scl, hist);  // l.76
         else small_plain_round<4>((const double *)a.gA[0], dsum, PH_A, scl, hist);
         if (scl->done) break;
@@ -418,9 +458,9 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_reg_kernel(SmallArgs a) {
                 a.w[i] = w;
                 if (EXACT) {
                     const bool zr = is_zero(r), zh = is_zero(rh);
-                    P[0] = tp.prep(rh, r, zh | zr, flags);
-                    P[1] = tp.prep(rh, w, zh | is_zero(w), flags);
-                    P[2] = tp.prep(r, r, zr, flags);
+                    P[0] = small_prod(tp, rh, r, zh | zr, flags, XD(0));
+                    P[1] = small_prod(tp, rh, w, zh | is_zero(w), flags, XD(1));
+                    P[2] = small_prod(tp, r, r, zr, flags, XD(2));
                 } else {
                     acc[0] = __fma_rn(rh, r, 0.0);
                     acc[1] = __fma_rn(rh, w, 0.0);
@@ -434,14 +474,14 @@ __global__ void __launch_bounds__(BS, 1) pbcg_small_reg_kernel(SmallArgs a) {
                     if (is_nonzero(P[d].p)) sacc_deposit(SB.w[d], P[d].p);
                     if (is_nonzero(P[d].e)) sacc_deposit(SB.w[d], P[d].e);
                 }
-                small_publish<3>(SB, flags, a.gB[par]);
+                small_publish<3>(SB, flags, a.gB[par], full ? X : nullptr);
             } else {
                 small_plain_publish<3, BS>(acc, ws, (double *)a.gB[0]);
             }
         }
         grid_barrier(a.bar);
         if (EXACT && blockIdx.x == 0)
-            for (int j = threadIdx.x; j < 4 * SACC_L + SACC_FLAGW; j += BS) a.gA[par][j] = 0;
+            small_clear<4>(a.gA[par]);
         if (EXACT) small_round<3>(SB, a.gB[par], PH_B, scl, hist);
         else small_plain_round<3>((const double *)a.gB[0], dsum, PH_B, scl, hist);
         if (scl->done) break;

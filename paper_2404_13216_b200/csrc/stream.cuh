@@ -308,6 +308,24 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
     R.d1.warp_merge(s1);
     PBCG_TS(2);
     if constexpr (EXACT) {
+        if (sc->range_mode == 0) {  // full range (R-24): a flagged CTA corrects its products
+            if (flags) atomicOr(&S.flags, flags);
+            flags = 0;
+            __syncthreads();  // the ring is drained (its memory is the scratch); this CTA's q, y, s, z stores are visible
+            if (S.flags & FLAG_RANGE)
+                cta_full_range_nd<4>(S, (unsigned long long *)buf, a.gacc + xs_off(4),
+                    [&](auto f) {
+                        for (int64_t tile = blockIdx.x; tile * T < n; tile += gridDim.x) {
+                            const int64_t e = min(n, tile * T + T);
+                            for (int64_t i = tile * T + threadIdx.x; i < e; i += blockDim.x) f(i);
+                        }
+                    },
+                    [&](int d, int64_t i, double &x, double &y) {  // (q,y), (y,y), (r0,s), (r0,z)
+                        const double yi = a.y[i];
+                        x = d == 0 ? a.q[i] : d == 1 ? yi : a.rh[i];
+                        y = d <= 1 ? yi : d == 2 ? a.s[i] : a.z[i];
+                    });
+        }
         const bool last = cta_sacc_publish<4>(S, flags, a.gacc, a.ticket);
         PBCG_TS(3);
         if (last) {
@@ -464,6 +482,24 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
     R.d0.warp_merge(s0);
     R.d1.warp_merge(s1);
     if constexpr (EXACT) {
+        if (sc->range_mode == 0) {  // full range (R-24): a flagged CTA corrects its products
+            if (flags) atomicOr(&S.flags, flags);
+            flags = 0;
+            __syncthreads();
+            if (S.flags & FLAG_RANGE)
+                cta_full_range_nd<3>(S, (unsigned long long *)buf, a.gacc + xs_off(3),
+                    [&](auto f) {
+                        for (int64_t tile = blockIdx.x; tile * T < n; tile += gridDim.x) {
+                            const int64_t e = min(n, tile * T + T);
+                            for (int64_t i = tile * T + threadIdx.x; i < e; i += blockDim.x) f(i);
+                        }
+                    },
+                    [&](int d, int64_t i, double &x, double &y) {  // (r0,r'), (r0,w'), (r',r')
+                        const double ri = a.r[i];
+                        x = d <= 1 ? a.rh[i] : ri;
+                        y = d == 1 ? a.w[i] : ri;
+                    });
+        }
         if (cta_sacc_publish<3>(S, flags, a.gacc, a.ticket))
             last_cta_finish<3>(S, a.gacc, a.ticket, PH_B, a.finalize, sc, a.hist, nullptr, nullptr);
     } else {
@@ -573,7 +609,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a
     acc.warp_merge(S.w[0]);
     if (ND == 2) acc2.warp_merge(s1);
     if constexpr (ND == 1) {
-        if (a.finalize && a.phase == PH_EXDOT) {  // standalone dot: a flagged CTA corrects its products (NEXT-4)
+        if (a.phase == PH_EXDOT) {  // standalone dot (single GPU or a rank's slice): a flagged CTA corrects its products (NEXT-4)
             if (flags) atomicOr(&S.flags, flags);
             flags = 0;
             __syncthreads();  // the ring is drained: its memory is the scratch
@@ -587,8 +623,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a
         }
     }
     if (cta_sacc_publish<ND>(S, flags, a.gacc, a.ticket))
-        last_cta_finish<ND>(S, a.gacc, a.ticket, a.phase, a.finalize, a.sc, a.hist, a.out, a.out_flags,
-                            (ND == 1 && a.phase == PH_EXDOT) ? a.x[0] : nullptr, a.y[0], a.n);
+        last_cta_finish<ND>(S, a.gacc, a.ticket, a.phase, a.finalize, a.sc, a.hist, a.out, a.out_flags);
 }
 
 // ---------------------------------------------------------------------------

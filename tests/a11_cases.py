@@ -187,7 +187,7 @@ def range_case(oracle, A, b, phase: str, max_iter: int = 60, min_i: int = 1):
     2^-960 (R-9) in `phase` ('A' or 'B') of an iteration i >= min_i.
     Returns (k, i, unscaled history, unscaled x after each iteration)."""
     seq, H, xs = product_minima(oracle, A, b, max_iter)
-    for k in range(400, 540):
+    for k in range(540, 399, -1):
         T = 2.0 ** (2 * k - 960)  # m * 2^-2k < 2^-960  <=>  m < T
         first = next(((ph, i) for ph, i, m in seq if m < T), None)
         if first is None:

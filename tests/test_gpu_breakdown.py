@@ -96,17 +96,17 @@ def test_relative_threshold(pb, seed, kind, at, path, monkeypatch):
 @pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("phase", ["A", "B"])
 def test_range_stop_mid_solve(pb, phase, path, monkeypatch):
-    # b * 2^-k: the first product below 2^-960 (R-9) falls in `phase` of an
+    # range_mode "fast" (R-9): b * 2^-k: the first product below 2^-960 (R-9) falls in `phase` of an
     # iteration i >= 1; R-19 fixes the stop (A: before S6, iterations = i;
     # B: after S6, iterations = i + 1)
     A = gen.stencil(2, 50, 10.0)
     b = 1.0 + gen.uniform(A.n, 5, 0.0, 1.0)
     k, i, _, _ = range_case(oracle, A, b, phase)
     bs = b * 2.0 ** -k
-    O = oracle.PBiCGStab(A, b=bs, tol=0.0, max_iter=80)
+    O = oracle.PBiCGStab(A, b=bs, tol=0.0, max_iter=80, range_mode="fast")
     O.run()
     assert O.status == oracle.RANGE and O.iterations == (i if phase == "A" else i + 1)
-    x, r, H = gpu_solve(pb, A, bs, path, monkeypatch, tol=0.0, max_iter=80)
+    x, r, H = gpu_solve(pb, A, bs, path, monkeypatch, tol=0.0, max_iter=80, range_mode="fast")
     assert r.status == pb.RANGE and r.iterations == O.iterations, (path, r.status, r.iterations)
     Ho = O.history()
     assert H.shape == Ho.shape
@@ -115,3 +115,47 @@ def test_range_stop_mid_solve(pb, phase, path, monkeypatch):
         cols = [oracle.H_THETA, oracle.H_ETA, oracle.H_SIGMA, oracle.H_ZETA, oracle.H_OMEGA]
         assert np.array_equal(u64(H[i + 1, cols]), u64(Ho[i + 1, cols])), path
     assert np.array_equal(u64(x), u64(O.vec("x"))), path
+
+
+# ---- full range (R-24): the default --------
+
+def _full_case(name):
+    """(A, b, tol, max_iter) systems whose dots leave the fast zone."""
+    if name in ("under_a", "under_b"):  # b * 2^-k: products below 2^-960 from iteration i on (then subnormal dots)
+        A = gen.stencil(2, 50, 10.0)
+        b = 1.0 + gen.uniform(A.n, 5, 0.0, 1.0)
+        k, i, _, _ = range_case(oracle, A, b, "A" if name == "under_a" else "B")
+        return A, b * 2.0 ** -k, 0.0, 80
+    if name == "under_converge":  # converges at the unscaled iteration, x scaled
+        A = gen.stencil(2, 50, 10.0)
+        return A, (1.0 + gen.uniform(A.n, 5, 0.0, 1.0)) * 2.0 ** -470, 1e-10, 400
+    A = gen.stencil(3, 10, 100.0)  # b = A*1 * 2^k: products above 2^1000 (the FPE-overflow path)
+    b = oracle.spmv(A, np.ones(A.n))
+    return A, b * 2.0 ** (493 if name == "over_run" else 497), 0.0, 30
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("name", ["under_a", "under_b", "under_converge", "over_run", "over_stop"])
+def test_full_range_solve(pb, name, path, monkeypatch):
+    # the CTAs that meet products outside the fast zone correct them exactly
+    # (K2/K3 stream kernels, init and true-residual multidots, fused kernels);
+    # trajectories, outcome and x are the oracle's bit for bit.  over_stop:
+    # a dot whose exact value overflows stops the solve with RANGE (R-24)
+    A, b, tol, M = _full_case(name)
+    O = oracle.PBiCGStab(A, b=b, tol=tol, max_iter=M)
+    O.run()
+    want = {"under_converge": oracle.CONVERGED, "over_stop": oracle.RANGE}.get(name, oracle.MAXITER)
+    assert O.status == want, (name, O.status)
+    Of = oracle.PBiCGStab(A, b=b, tol=tol, max_iter=M, range_mode="fast")
+    Of.run()
+    assert Of.status == oracle.RANGE and Of.iterations < O.iterations + (name == "over_stop")
+    x, r, H = gpu_solve(pb, A, b, path, monkeypatch, tol=tol, max_iter=M)
+    assert r.status == O.status and r.iterations == O.iterations, (path, r.status, r.iterations)
+    Ho = O.history()
+    if name == "over_stop":  # the row of the overflowing phase holds +-inf: compare the rows before it
+        Ho, H = Ho[:-1], H[:-1]
+    assert np.array_equal(u64(H), u64(Ho)), path
+    assert np.array_equal(u64(x), u64(O.vec("x"))), path
+    if name != "over_stop":
+        tr = oracle.true_relres(A, b, O.vec("x"))[0]
+        assert r.relres_true == tr or (np.isnan(tr) and np.isnan(r.relres_true))

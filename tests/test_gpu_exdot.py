@@ -272,3 +272,44 @@ def test_full_range_nonfinite_in_one_cta(pb):
     v, f = gpu_exdot(pb, x, y)
     assert f & pb.FLAG_NONFINITE
     check(pb, x, y)
+
+
+@pytest.mark.parametrize("where", ["spread", "all", "overflow_zone", "random"])
+def test_full_range_distributed(pb, where):
+    # full range per rank (R-24): each rank's flagged CTAs correct their
+    # products into extended words, which are summed across ranks (int64)
+    # with the fast words and rounded once -- virtual ranks, the comm-only
+    # handle through NCCL (1-rank communicator), bit-exact against the oracle
+    import torch
+    n = (1 << 20) + 11
+    rng = np.random.default_rng(3)
+    if where == "all":
+        x, y = gen.loguniform(n, 5, -540, 0), gen.loguniform(n, 6, -540, 0)
+    elif where == "random":
+        n = 20_000
+        ex, ey = rng.integers(-1070, 500, n), rng.integers(-1070, 500, n)
+        x = np.ldexp(rng.uniform(1, 2, n) * rng.choice([-1.0, 1.0], n), ex)
+        y = np.ldexp(rng.uniform(1, 2, n) * rng.choice([-1.0, 1.0], n), ey)
+    else:
+        x, y = gen.uniform(n, 11), gen.uniform(n, 12)
+        idx = rng.choice(n, 40, replace=False)
+        for k, i in enumerate(idx):
+            if where == "spread":
+                x[i], y[i] = 2.0 ** -700 * (1 + k / 64), (-(2.0 ** -300) if k % 2 else 2.0 ** -301)
+            else:  # products above 2^1000 that cancel: the FPE-overflow (poisoned) path
+                x[i], y[i] = 2.0 ** 510 * (1 + k / 64), (2.0 ** 500 if k % 2 == 0 else -(2.0 ** 500))
+                if k % 2:
+                    x[i] = x[idx[k - 1]]
+    want, wf = oracle.exdot(x, y)
+    assert np.isfinite(want)
+    xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    A = gen.stencil(2, 16, 10.0)
+    for V in (2, 3):
+        S = pb.Solver(A.row_ptr, A.col, A.val, A.n, virtual_ranks=V)
+        got, f = pb.exdot(xt, yt, handle=S)
+        assert bits(got) == bits(want), (where, V, got, want)
+        S.close()
+    C = pb.Comm(force_nccl=True)
+    got, f = C.exdot(xt, yt)
+    assert bits(got) == bits(want), (where, "comm", got, want)
+    C.close()

@@ -122,7 +122,7 @@ def test_cauchy_schwarz_eps_one():
 
 @pytest.mark.parametrize("phase", ["A", "B"])
 def test_range_stop_mid_solve(phase):
-    # R-9 / R-19: b * 2^-k; the first product below 2^-960 falls in `phase`
+    # range_mode "fast" -- R-9 / R-19: b * 2^-k; the first product below 2^-960 falls in `phase`
     # of iteration i >= 1.  Phase A: stop before S6 (x unchanged, iterations
     # = i).  Phase B: stop after S6 (iterations = i + 1).  Every history row
     # before the stop is the unscaled row with the dots times 2^-2k.
@@ -131,7 +131,7 @@ def test_range_stop_mid_solve(phase):
     case = range_case(oracle, A, b, phase)
     assert case is not None
     k, i, H, xs = case
-    O = oracle.PBiCGStab(A, b=b * 2.0 ** -k, tol=0.0, max_iter=60)
+    O = oracle.PBiCGStab(A, b=b * 2.0 ** -k, tol=0.0, max_iter=60, range_mode="fast")
     O.run()
     want_it = i if phase == "A" else i + 1
     assert O.status == oracle.RANGE and O.iterations == want_it, (k, i, O.status, O.iterations)
@@ -146,3 +146,101 @@ def test_range_stop_mid_solve(phase):
         assert np.array_equal(u64(Hs[i + 1, a_cols]), u64(H[i + 1, a_cols] * 2.0 ** (-2 * k)))
         assert Hs[i + 1, oracle.H_OMEGA] == H[i + 1, oracle.H_OMEGA]
     assert np.array_equal(u64(O.vec("x")), u64(xs[want_it] * 2.0 ** -k))
+
+
+# ---- full range (R-24): dots exact over the
+# whole binary64 range, so a product outside the fast
+# zone no longer stops the solve ----
+
+DOTS = [oracle.H_THETA, oracle.H_ETA, oracle.H_SIGMA, oracle.H_ZETA, oracle.H_RHO, oracle.H_DELTA, oracle.H_RR]
+SAME = [oracle.H_OMEGA, oracle.H_RELRES, oracle.H_BETA, oracle.H_ALPHA]
+
+
+@pytest.mark.parametrize("phase", ["A", "B"])
+def test_full_range_continues_past_the_fast_zone(phase):
+    # the systems of test_range_stop_mid_solve: with full range the solve runs
+    # on, and every row is the unscaled row (dots times 2^-2k) as long as the
+    # scaled dots stay normal binary64 numbers (exact power-of-two scaling)
+    A = gen.stencil(2, 12, 10.0)
+    b = 1.0 + gen.uniform(A.n, 5, 0.0, 1.0)
+    k, i, _, _ = range_case(oracle, A, b, phase)
+    M = 60
+    O0 = oracle.PBiCGStab(A, b=b, tol=0.0, max_iter=M)
+    O0.run()
+    H0 = O0.history()
+    O = oracle.PBiCGStab(A, b=b * 2.0 ** -k, tol=0.0, max_iter=M)
+    O.run()
+    H = O.history()
+    scaled = H0[:, DOTS] * 2.0 ** (-2 * k)
+    small = np.any((scaled != 0) & (np.abs(scaled) < 2.0 ** -1022), axis=1)
+    last = int(np.argmax(small)) if small.any() else H0.shape[0]  # first row with a subnormal dot
+    assert last > i + 2, (last, i)
+    assert np.array_equal(u64(H[:last, DOTS]), u64(scaled[:last]))
+    assert np.array_equal(u64(H[:last, SAME]), u64(H0[:last, SAME]))
+    if last == H0.shape[0]:
+        assert O.status == oracle.MAXITER and np.array_equal(u64(O.vec("x")), u64(O0.vec("x") * 2.0 ** -k))
+
+
+def test_full_range_converges_bit_exact_scaled():
+    # tol 1e-10: the scaled system converges in the same iteration with
+    # x = x_unscaled * 2^-k, although its products leave the fast zone
+    A = gen.stencil(2, 12, 10.0)
+    b = 1.0 + gen.uniform(A.n, 5, 0.0, 1.0)
+    O0 = oracle.PBiCGStab(A, b=b, tol=1e-10, max_iter=300)
+    O0.run()
+    assert O0.status == oracle.CONVERGED
+    for k in (440, 470):
+        Of = oracle.PBiCGStab(A, b=b * 2.0 ** -k, tol=1e-10, max_iter=300, range_mode="fast")
+        Of.run()
+        assert Of.status == oracle.RANGE
+        O = oracle.PBiCGStab(A, b=b * 2.0 ** -k, tol=1e-10, max_iter=300)
+        O.run()
+        assert O.status == oracle.CONVERGED and O.iterations == O0.iterations, k
+        assert np.array_equal(u64(O.vec("x")), u64(O0.vec("x") * 2.0 ** -k))
+        assert np.array_equal(u64(O.history()[:, SAME]), u64(O0.history()[:, SAME]))
+
+
+def _overflow_system(name):
+    if name == "2d":
+        A = gen.stencil(2, 12, 10.0)
+        return A, 1.0 + gen.uniform(A.n, 5, 0.0, 1.0)
+    A = gen.stencil(3, 10, 100.0)  # b = A*1: the residual climbs ~2^12 before it falls
+    return A, oracle.spmv(A, np.ones(A.n))
+
+
+@pytest.mark.parametrize("name,k", [("2d", 501), ("2d", 503), ("2d", 506), ("3d", 493), ("3d", 497)])
+def test_full_range_overflow_zone(name, k):
+    # b * 2^+k: products above 2^1000 (outside the fast zone: "fast" stops at
+    # init) are exact with full range; the solve stops with RANGE exactly at
+    # the first dot whose exact value rounds to +-inf (|dot| 2^2k >= 2^1024),
+    # (phase A of iteration i stops with iterations = i, R-19)
+    A, b = _overflow_system(name)
+    M = 30
+    O0 = oracle.PBiCGStab(A, b=b, tol=0.0, max_iter=M)
+    O0.run()
+    H0 = O0.history()
+    Of = oracle.PBiCGStab(A, b=b * 2.0 ** k, tol=0.0, max_iter=M, range_mode="fast")
+    Of.run()
+    assert Of.status == oracle.RANGE
+    # the first phase (init, then A and B of each iteration) with an overflowing dot
+    rows = []
+    rows.append(("I", 0, [oracle.H_RHO, oracle.H_DELTA, oracle.H_RR]))
+    for r in range(1, H0.shape[0]):
+        rows.append(("A", r, [oracle.H_THETA, oracle.H_ETA, oracle.H_SIGMA, oracle.H_ZETA]))
+        rows.append(("B", r, [oracle.H_RHO, oracle.H_DELTA, oracle.H_RR]))
+    lim = 1024 - 2 * k
+    stop = next(((ph, r) for ph, r, cols in rows if np.log2(np.abs(H0[r, cols]).max()) >= lim), None)
+    assert stop is None or all(abs(np.log2(np.abs(H0[r, c]).max()) - lim) > 1e-9 for _, r, c in rows)
+    O = oracle.PBiCGStab(A, b=b * 2.0 ** k, tol=0.0, max_iter=M)
+    O.run()
+    if stop is None:
+        assert O.status == oracle.MAXITER and O.iterations == M
+        good = H0.shape[0]
+    else:
+        ph, r = stop
+        assert O.status == oracle.RANGE
+        assert O.iterations == {"I": 0, "A": r - 1, "B": r}[ph], (stop, O.iterations)
+        good = r if ph != "I" else 0
+    H = O.history()
+    assert np.array_equal(u64(H[:good, DOTS]), u64(H0[:good, DOTS] * 2.0 ** (2 * k)))
+    assert np.array_equal(u64(H[:good, SAME]), u64(H0[:good, SAME]))
