@@ -250,6 +250,11 @@ def run_gpu(args, rank, world, local_rank, dist):
                            nccl_uid=fresh_uid(), history_capacity=16, precond="bjacobi2")
             out["bjacobi2"] = dict(timed_arm(Sb), spmv_format=Sb.spmv_format())
             Sb.close()
+            # the same M applied inside the iteration (R-25): K2 / K3 write M^-1 z, M^-1 w; SpMVs on A
+            Sp = pb.Solver(Al.row_ptr, Al.col, Al.val, A.n, row_begin=r0, row_end=r1, rank=rank, nranks=world,
+                           nccl_uid=fresh_uid(), history_capacity=16, precond="bjacobi2_pipe")
+            out["bjacobi2_pipe"] = timed_arm(Sp)
+            Sp.close()
     # ---- per-kernel times: a second timed pass over the same K steps with
     # CUDA events around every launch (single rank) ----
     fmt = S.spmv_format()
@@ -568,6 +573,12 @@ def main():
         bj["note"] = ("same workload and K with right 2x2 point-block Jacobi (R-23: B = A M^-1 stored, each row "
                       "widened to whole column blocks, so more nonzeros per SpMV; x = M^-1 y at the end)")
         line["pbicgstab_bjacobi2"] = bj
+    if "bjacobi2_pipe" in out:
+        bp = out["bjacobi2_pipe"]
+        bp["over_unpreconditioned"] = bp["value"] / value
+        bp["note"] = ("same workload and K with the 2x2 point-block Jacobi applied inside the iteration (R-25: K2 "
+                      "writes M^-1 z, K3 M^-1 w, +48 B/row; the SpMVs run on A in its SELL-P / SELL-V format)")
+        line["pbicgstab_bjacobi2_pipe"] = bp
     line["bytes_per_iteration_per_gpu"] = by["iteration"]
     line["iteration_GBps_per_gpu"] = by["iteration"] / (ms_step * 1e-3) / 1e9
     line["iteration_frac_hbm"] = line["iteration_GBps_per_gpu"] / hbm

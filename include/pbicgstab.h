@@ -101,10 +101,17 @@ typedef struct {
                                  M = the 2x2 diagonal blocks of A (global rows 2m, 2m+1; 1x1 for the last
                                  row when n is odd), B = A M^-1 stored explicitly (each row's pattern
                                  widened to whole column blocks); y0 = M x0, x = M^-1 y.  Every rank's
-                                 first row must be even; a singular or non-finite block -> PBCG_EINVAL. */
+                                 first row must be even; a singular or non-finite block -> PBCG_EINVAL.
+                                 PBCG_PRECOND_BJACOBI2_PIPE (3): the same M applied INSIDE the iteration
+                                 (R-25): A is stored as given; K2 writes
+                                 z_hat = M^-1 z and K3 w_hat = M^-1 w beside z and w, and the SpMVs compute
+                                 v = A z_hat, t = A w_hat (every product of Algorithm 2 is A (M^-1 u)).
+                                 y0 = M x0, x = M^-1 y.  Algorithm 2 only; the fused small kernel is off;
+                                 pbicgstab_spmv computes A x. */
 } pbcg_dist;
 
-enum pbcg_precond { PBCG_PRECOND_NONE = 0, PBCG_PRECOND_JACOBI = 1, PBCG_PRECOND_BJACOBI2 = 2 };
+enum pbcg_precond { PBCG_PRECOND_NONE = 0, PBCG_PRECOND_JACOBI = 1, PBCG_PRECOND_BJACOBI2 = 2,
+                    PBCG_PRECOND_BJACOBI2_PIPE = 3 };
 
 /* Solver options (SPEC.md l.214-217 SolverConfig subset). */
 typedef struct {

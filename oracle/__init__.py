@@ -76,7 +76,10 @@ def _L():
         lib.orc_dot_seq.argtypes = [i64, vp, vp]
         lib.orc_pbcg_size.restype = i32
         lib.orc_pbcg_init.restype = i32
-        lib.orc_pbcg_init.argtypes = [vp, i64, vp, vp, vp, vp, vp, dbl, dbl, i32, vp, i32]
+        lib.orc_pbcg_init.argtypes = [vp, i64, vp, vp, vp, vp, vp, dbl, dbl, i32, vp, i32, vp]
+        lib.orc_bj_apply.argtypes = [i64, vp, vp, vp]
+        lib.orc_bj_blocks.restype = i32
+        lib.orc_bj_blocks.argtypes = [i64, vp, vp, vp, vp, vp]
         lib.orc_pbcg_step.restype = i32
         lib.orc_pbcg_step.argtypes = [vp]
         lib.orc_pbcg_run.restype = i32
@@ -184,10 +187,13 @@ class PBiCGStab:
     computes it with its own SpMV); ``x0=None`` means x0 := 0."""
 
     def __init__(self, A, b=None, x0=None, tol=1e-10, eps=1e-30, max_iter=10000, history=True, rr_period=0,
-                 range_mode="full"):
+                 range_mode="full", minv=None):
         """range_mode "full" (R-24): dots exact over the whole
         binary64 range, only NaN/Inf or an overflowing exact sum stops the
-        solve; "fast" (R-9): any product outside the fast zone stops it."""
+        solve; "fast" (R-9): any product outside the fast zone stops it.
+        minv: [nb, 4] M^-1 blocks (block_jacobi_right): the pipelined right
+        2x2 block Jacobi of R-25 -- every product of the iteration is
+        A (M^-1 u); x0 is then y0 = M x0 and vec("x") the final y."""
         L = _L()
         self.A = A
         self._rp = np.ascontiguousarray(A.row_ptr, np.int32)
@@ -195,6 +201,7 @@ class PBiCGStab:
         self._val = _f64(A.val)
         self._b = None if b is None else _f64(b)
         self._x0 = None if x0 is None else _f64(x0)
+        self._minv = None if minv is None else np.ascontiguousarray(minv, np.float64).reshape(-1)
         self.max_iter = max_iter
         self.hist = np.zeros((max_iter + 1, H_COLS), np.float64) if history else None
         self._S = ctypes.create_string_buffer(L.orc_pbcg_size())
@@ -203,7 +210,8 @@ class PBiCGStab:
                                   None if self._x0 is None else _p(self._x0),
                                   float(tol), float(eps), int(max_iter),
                                   None if self.hist is None else _p(self.hist),
-                                  {"full": 1, "fast": 0}[range_mode])
+                                  {"full": 1, "fast": 0}[range_mode],
+                                  None if self._minv is None else _p(self._minv))
         if rr_period:  # residual replacement every rr_period iterations (NEXT-2, R-21)
             L.orc_pbcg_set_rr(self._S, int(rr_period))
 
@@ -386,6 +394,30 @@ def block_jacobi_right(A):
                               val=np.array(bval, np.float64), rhs=getattr(A, "rhs", "given"),
                               b=getattr(A, "b", None), nnz=len(bcol))
     return B, M, Mi
+
+
+def bj_blocks_c(A):
+    """(M, M^-1) of A's 2x2 diagonal blocks by orc_bj_blocks (the C twin of
+    block_jacobi_right's blocks, for full-size systems); ValueError if a
+    block is singular or its inverse not finite."""
+    nb = (A.n + 1) // 2
+    M = np.zeros((nb, 4))
+    Mi = np.zeros((nb, 4))
+    rp = np.ascontiguousarray(A.row_ptr, np.int32)
+    col = np.ascontiguousarray(A.col, np.int32)
+    val = _f64(A.val)
+    if _L().orc_bj_blocks(A.n, _p(rp), _p(col), _p(val), _p(M), _p(Mi)):
+        raise ValueError("block jacobi: singular or non-finite 2x2 diagonal block")
+    return M, Mi
+
+
+def bj_apply_c(Q, x) -> np.ndarray:
+    """orc_bj_apply (the C twin used inside the pipelined preconditioner)."""
+    x = _f64(x)
+    Q = np.ascontiguousarray(Q, np.float64)
+    y = np.empty_like(x)
+    _L().orc_bj_apply(x.size, _p(Q), _p(x), _p(y))
+    return y
 
 
 def bj_apply(Q, x):

@@ -243,6 +243,57 @@ void orc_spmv(int64_t nrows, const int32_t *rp, const int32_t *col, const double
     }
 }
 
+/* y = Q x per 2x2 diagonal block (R-23): Q given as [nb][4]
+ * row-major blocks over global rows (2m, 2m+1); y_2m = fma(q00, x_2m, q01 x_2m+1),
+ * y_2m+1 = fma(q10, x_2m, q11 x_2m+1); the 1x1 tail block of an odd order:
+ * y = q00 x.  (The C twin of oracle.bj_apply, pinned against it.) */
+void orc_bj_apply(int64_t n, const double *Q, const double *x, double *y) {
+    for (int64_t m = 0; 2 * m < n; ++m) {
+        const double *q = Q + 4 * m;
+        if (2 * m + 1 < n) {
+            const double x0 = x[2 * m], x1 = x[2 * m + 1];
+            y[2 * m] = fma(q[0], x0, q[1] * x1);
+            y[2 * m + 1] = fma(q[2], x0, q[3] * x1);
+        } else {
+            y[2 * m] = q[0] * x[2 * m];
+        }
+    }
+}
+
+/* The 2x2 diagonal blocks of A and their inverses (R-23): rows
+ * (2m, 2m+1), block (a b; c d), det = fma(a, d, -(b c)), M^-1 = (d -b; -c a)
+ * / det with one RN division per entry; the 1x1 tail block of an odd order:
+ * (a), 1/a.  M, Mi: [nb][4].  Returns 0, or 1 for a singular / non-finite
+ * block.  (The C twin of oracle.block_jacobi_right's blocks, pinned against it.) */
+static double csr_entry(const int32_t *rp, const int32_t *col, const double *val, int64_t r, int64_t c) {
+    for (int32_t k = rp[r]; k < rp[r + 1]; ++k)
+        if (col[k] == c) return val[k];
+    return 0.0;
+}
+int orc_bj_blocks(int64_t n, const int32_t *rp, const int32_t *col, const double *val, double *M, double *Mi) {
+    int bad = 0;
+    for (int64_t m = 0; 2 * m < n; ++m) {
+        const int64_t r0 = 2 * m;
+        double *q = M + 4 * m, *qi = Mi + 4 * m;
+        if (r0 + 1 < n) {
+            const double a = csr_entry(rp, col, val, r0, r0), b = csr_entry(rp, col, val, r0, r0 + 1);
+            const double c = csr_entry(rp, col, val, r0 + 1, r0), d = csr_entry(rp, col, val, r0 + 1, r0 + 1);
+            const double det = fma(a, d, -(b * c));
+            q[0] = a; q[1] = b; q[2] = c; q[3] = d;
+            qi[0] = d / det; qi[1] = -(b / det); qi[2] = -(c / det); qi[3] = a / det;
+            if (det == 0.0) bad = 1;
+        } else {
+            const double a = csr_entry(rp, col, val, r0, r0);
+            q[0] = a; q[1] = 0.0; q[2] = 0.0; q[3] = 0.0;
+            qi[0] = 1.0 / a; qi[1] = 0.0; qi[2] = 0.0; qi[3] = 0.0;
+            if (a == 0.0) bad = 1;
+        }
+        for (int k = 0; k < 4; ++k)
+            if (!isfinite(qi[k])) bad = 1;
+    }
+    return bad;
+}
+
 /* plain sequential fp64 dot (Algorithm 1 baseline; "Sequential") */
 double orc_dot_seq(int64_t n, const double *x, const double *y) {
     double s = 0.0;
@@ -272,7 +323,22 @@ typedef struct {
     double loop_seconds;
     int rr_period, replacements; /* residual replacement every rr_period iterations (0: never) */
     int full_range;              /* 1: only NONFINITE / OVERFLOW stop (R-24); 0: any RANGE flag stops (R-9) */
+    const double *minv;          /* pipelined 2x2 block Jacobi (R-25): M^-1 blocks [nb][4], or NULL */
+    double *tmp;                 /* M^-1 u scratch (n) */
 } orc_pbcg;
+
+/* The operator Algorithm 2 runs on: out = A u, or with the pipelined right
+ * 2x2 block Jacobi preconditioner (R-25; PAPER.md l.90, l.93:
+ * the preconditioner is applied inside the iteration) out = A (M^-1 u):
+ * u_hat = M^-1 u by orc_bj_apply, then the per-row fma chain of A over u_hat. */
+static void op_apply(orc_pbcg *S, const double *u, double *out) {
+    if (S->minv) {
+        orc_bj_apply(S->n, S->minv, u, S->tmp);
+        orc_spmv(S->n, S->rp, S->col, S->val, S->tmp, out);
+    } else {
+        orc_spmv(S->n, S->rp, S->col, S->val, u, out);
+    }
+}
 
 /* the flags of a dot phase that stop Algorithm 2 (R-9 / R-24) */
 static int stops(const orc_pbcg *S, int f) {
@@ -293,20 +359,23 @@ static void hist_put(orc_pbcg *S, int row, int col, double v) {
 }
 
 /* Lines I1-I4.  b == NULL means b := A*ones; x0 == NULL
- * means x0 := 0; full_range selects R-24 (1) or R-9 (0) for every dot.  Returns ORC_OK / ORC_EINVAL / ORC_ENONFINITE; the solve
+ * means x0 := 0; full_range selects R-24 (1) or R-9 (0) for every dot;
+ * minv != NULL: the iteration runs on B = A M^-1 applied as op_apply (R-25),
+ * x0 is then the initial y0 = M x0 and x the final y (x = M^-1 y).  Returns ORC_OK / ORC_EINVAL / ORC_ENONFINITE; the solve
  * outcome is in S->status (ORC_RUNNING while iterations remain). */
 int orc_pbcg_init(orc_pbcg *S, int64_t n, const int32_t *rp, const int32_t *col, const double *val,
                   const double *b, const double *x0, double tol, double eps, int max_iter, double *hist,
-                  int full_range) {
+                  int full_range, const double *minv) {
     memset(S, 0, sizeof(*S));
     S->full_range = full_range != 0;
+    S->minv = minv;
     S->n = n; S->rp = rp; S->col = col; S->val = val;
     S->tol = tol; S->max_iter = max_iter; S->hist = hist;
     if (n <= 0 || max_iter < 0 || !(tol >= 0.0)) return ORC_EINVAL;
     if (any_nonfinite(rp[n], val)) return ORC_ENONFINITE;
     S->b = vnew(n); S->x = vnew(n); S->r = vnew(n); S->rh = vnew(n); S->p = vnew(n);
     S->s = vnew(n); S->z = vnew(n); S->q = vnew(n); S->y = vnew(n); S->w = vnew(n);
-    S->t = vnew(n); S->v = vnew(n);
+    S->t = vnew(n); S->v = vnew(n); S->tmp = vnew(n);
     if (b) memcpy(S->b, b, sizeof(double) * (size_t)n);
     else {
         double *ones = vnew(n);
@@ -317,12 +386,12 @@ int orc_pbcg_init(orc_pbcg *S, int64_t n, const int32_t *rp, const int32_t *col,
     if (x0) memcpy(S->x, x0, sizeof(double) * (size_t)n);
     if (any_nonfinite(n, S->b) || any_nonfinite(n, S->x)) return ORC_ENONFINITE;
     /* I1: r0 := b - A x0 ; r^ := r0 ; w0 := A r0 ; t0 := A w0 */
-    orc_spmv(n, rp, col, val, S->x, S->v); /* v used as scratch for A x0 */
+    op_apply(S, S->x, S->v); /* v used as scratch for A x0 */
     for (int64_t i = 0; i < n; ++i) S->r[i] = S->b[i] - S->v[i];
     memset(S->v, 0, sizeof(double) * (size_t)n);
     memcpy(S->rh, S->r, sizeof(double) * (size_t)n);
-    orc_spmv(n, rp, col, val, S->r, S->w);
-    orc_spmv(n, rp, col, val, S->w, S->t);
+    op_apply(S, S->r, S->w);
+    op_apply(S, S->w, S->t);
     /* I2: norms and the first two inner products */
     int f0 = 0, f1 = 0, f2 = 0, f3 = 0;
     double bb = orc_exdot(n, S->b, S->b, &f0);
@@ -361,13 +430,13 @@ int orc_pbcg_init(orc_pbcg *S, int64_t n, const int32_t *rp, const int32_t *col,
 int orc_pbcg_replace(orc_pbcg *S) {
     const int64_t n = S->n;
     double *ax = vnew(n);
-    orc_spmv(n, S->rp, S->col, S->val, S->x, ax);
+    op_apply(S, S->x, ax);
     for (int64_t k = 0; k < n; ++k) S->r[k] = S->b[k] - ax[k];
     free(ax);
-    orc_spmv(n, S->rp, S->col, S->val, S->r, S->w);
-    orc_spmv(n, S->rp, S->col, S->val, S->p, S->s);
-    orc_spmv(n, S->rp, S->col, S->val, S->s, S->z);
-    orc_spmv(n, S->rp, S->col, S->val, S->w, S->t);
+    op_apply(S, S->r, S->w);
+    op_apply(S, S->p, S->s);
+    op_apply(S, S->s, S->z);
+    op_apply(S, S->w, S->t);
     S->replacements += 1;
     return ORC_OK;
 }
@@ -408,7 +477,7 @@ int orc_pbcg_step(orc_pbcg *S) {
     double sigma = orc_exdot(n, rh, s, &f); fA |= f;
     double zeta = orc_exdot(n, rh, z, &f); fA |= f;
     /* S4 (l.75): v := A z */
-    orc_spmv(n, S->rp, S->col, S->val, z, v);
+    op_apply(S, z, v);
     /* S5 (l.76): omega := (q,y)/(y,y), and 0 when (y,y) = 0 (R-12) */
     double omn = (eta == 0.0) ? 0.0 : theta / eta;
     hist_put(S, i + 1, H_THETA, theta);
@@ -429,7 +498,7 @@ int orc_pbcg_step(orc_pbcg *S) {
     double deltan = orc_exdot(n, rh, w, &f); fB |= f;
     double rr = orc_exdot(n, r, r, &f); fB |= f;
     /* S8 (l.80): t := A w */
-    orc_spmv(n, S->rp, S->col, S->val, w, t);
+    op_apply(S, w, t);
     /* S9: recursive relative residual and the stopping rule (R-10) */
     double relres = sqrt(rr) / S->nb;
     hist_put(S, i + 1, H_RHO, rhon);
@@ -510,6 +579,7 @@ const double *orc_pbcg_vec(const orc_pbcg *S, int which) {
 void orc_pbcg_free(orc_pbcg *S) {
     double *tab[12] = {S->b, S->x, S->r, S->rh, S->p, S->s, S->z, S->q, S->y, S->w, S->t, S->v};
     for (int k = 0; k < 12; ++k) free(tab[k]);
+    free(S->tmp);
     memset(S, 0, sizeof(*S));
 }
 

@@ -52,6 +52,8 @@ class _Dist(ctypes.Structure):
 DOT_MODES = {"exact": 0, "plain": 1}
 # pbcg_opts.method: "pbicgstab" = Algorithm 2 (the hot path), "bicgstab" = Algorithm 1 with exact dots
 METHODS = {"pbicgstab": 0, "bicgstab": 1}
+# pbcg_dist.precond: "bjacobi2" = B = A M^-1 stored (R-23); "bjacobi2_pipe" = M^-1 applied inside K2/K3 (R-25)
+PRECONDS = {"none": 0, "jacobi": 1, "bjacobi2": 2, "bjacobi2_pipe": 3}
 # pbcg_opts.range_mode: "full" = dots exact over the whole binary64 range (R-24), "fast" = R-9 zone stops
 RANGE_MODES = {"full": 0, "fast": 1}
 
@@ -178,7 +180,7 @@ class Solver:
             self._uid = ctypes.create_string_buffer(bytes(nccl_uid), 128)
         self._dist = _Dist(rank, nranks, ctypes.cast(self._uid, ctypes.c_void_p) if self._uid is not None else None,
                            virtual_ranks, history_capacity, 1 if force_nccl else 0,
-                           {"none": 0, "jacobi": 1, "bjacobi2": 2}[precond])
+                           PRECONDS[precond])
         nbytes = ctypes.c_size_t(0)
         torch.cuda.synchronize()
         _check(L.pbicgstab_workspace_size(ctypes.byref(self._csr), ctypes.byref(self._dist), ctypes.byref(nbytes)))
@@ -438,7 +440,7 @@ def config_hash(n_global: int | None, nranks: int = 1, virtual_ranks: int = 1, p
                 comm_mode: int = 0) -> int:
     """pbcg_config_hash of these setup arguments (n_global None: comm-only)."""
     csr = _Csr(n_global or 0, 0, n_global or 0, 0, None, None, None)
-    d = _Dist(0, nranks, None, virtual_ranks, 0, comm_mode, {"none": 0, "jacobi": 1, "bjacobi2": 2}[precond])
+    d = _Dist(0, nranks, None, virtual_ranks, 0, comm_mode, PRECONDS[precond])
     out = ctypes.c_uint64(0)
     _check(lib().pbcg_config_hash(ctypes.byref(csr) if n_global is not None else None, ctypes.byref(d),
                                   ctypes.byref(out)))

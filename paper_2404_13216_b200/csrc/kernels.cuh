@@ -525,6 +525,9 @@ struct K2Args {
     double *hist;
     int finalize;
     double *part;  // plain dot mode: CTA partials [grid][ND] (exact mode: unused)
+    const double *minv;  // pipelined block Jacobi (R-25): M^-1 blocks of the own rows, or null
+    double *zh;          // ... z_hat = M^-1 z (own part of its padded buffer)
+    int last_rank;       // this rank holds the global last row (a 1x1 tail block when n is odd)
 };
 
 // ------------------------------------------------------------------------
@@ -540,7 +543,17 @@ struct K3Args {
     double *hist;
     int finalize;
     double *part;  // plain dot mode: CTA partials [grid][ND] (exact mode: unused)
+    const double *minv;  // pipelined block Jacobi (R-25), or null
+    double *wh;          // w_hat = M^-1 w
+    int last_rank;
 };
+
+// pipelined 2x2 block Jacobi (R-25): u_hat of the block (u0, u1) = rows
+// (2m, 2m+1) with the formula of bj_apply_kernel / orc_bj_apply
+__device__ __forceinline__ double2 bj_pair(const double *minv, int64_t m, double u0, double u1) {
+    const double2 q01 = __ldg((const double2 *)minv + 2 * m), q23 = __ldg((const double2 *)minv + 2 * m + 1);
+    return make_double2(__fma_rn(q01.x, u0, __dmul_rn(q01.y, u1)), __fma_rn(q23.x, u0, __dmul_rn(q23.y, u1)));
+}
 
 // ------------------------------------------------------------------------
 // multidot: up to 4 fused EXDOTs (init, true residual, standalone exdot)

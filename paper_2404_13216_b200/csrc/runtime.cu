@@ -347,6 +347,11 @@ struct Rank {
     int spmv_kind = 0;                // SpMV kernel (set at setup)
     double *dg = nullptr;             // Jacobi: diag(A) of this rank's rows
     double *bjm = nullptr, *bji = nullptr;  // 2x2 block Jacobi: M and M^-1 of this rank's blocks (4 doubles each)
+    // pipelined 2x2 block Jacobi (R-25): the SpMV inputs z_hat = M^-1 z and
+    // w_hat = M^-1 w (padded like z, w; halo-exchanged instead of them)
+    bool pipe = false;
+    int64_t ng = 0;  // global order (block of the last row)
+    double *zhpad = nullptr, *whpad = nullptr;
     double *part[NPH] = {};           // plain dot mode: CTA partials [PLAIN_GRID][4] per phase
     double *pdsum = nullptr;          // plain dot mode, NCCL ranks: local sums [NPH][4] (allreduced)
     // packed SELL-P chunks (rows <= 8 nonzeros) or SELL-V chunks (longer
@@ -453,9 +458,13 @@ static void carve_rank(Carver &C, Rank &R, int hist_cap, bool comm_only, int pre
         R.zpad = C.take<double>(nb); R.wpad = C.take<double>(nb); R.xpad = C.take<double>(nb);
         R.hist = C.take<double>((size_t)hist_cap * H_COLS);
         if (precond == PBCG_PRECOND_JACOBI) R.dg = C.take<double>((size_t)R.n + 2);
-        if (precond == PBCG_PRECOND_BJACOBI2) {
+        if (precond == PBCG_PRECOND_BJACOBI2 || precond == PBCG_PRECOND_BJACOBI2_PIPE) {
             R.bjm = C.take<double>(4 * (size_t)((R.n + 1) / 2 + 1));
             R.bji = C.take<double>(4 * (size_t)((R.n + 1) / 2 + 1));
+        }
+        if (precond == PBCG_PRECOND_BJACOBI2_PIPE) {
+            R.zhpad = C.take<double>(nb);
+            R.whpad = C.take<double>(nb);
         }
     }
     for (int k = 0; k < NPH; ++k) R.gacc[k] = C.take<long long>(GW4);
@@ -594,7 +603,8 @@ static int prepare(pbcg_handle *h, const pbcg_csr_local *A, const pbcg_dist *d, 
     h->V = (d && d->virtual_ranks > 1) ? d->virtual_ranks : 1;
     h->hist_cap = (d && d->history_capacity > 0) ? d->history_capacity : 10001;
     h->precond = d ? d->precond : PBCG_PRECOND_NONE;
-    if (h->precond != PBCG_PRECOND_NONE && h->precond != PBCG_PRECOND_JACOBI && h->precond != PBCG_PRECOND_BJACOBI2)
+    if (h->precond != PBCG_PRECOND_NONE && h->precond != PBCG_PRECOND_JACOBI && h->precond != PBCG_PRECOND_BJACOBI2 &&
+        h->precond != PBCG_PRECOND_BJACOBI2_PIPE)
         return fail(PBCG_EINVAL, "bad precond");
     if (h->nranks > 1 && h->V > 1) return fail(PBCG_EINVAL, "virtual ranks need nranks == 1");
     if (h->rank < 0 || h->rank >= h->nranks) return fail(PBCG_EINVAL, "bad rank");
@@ -702,7 +712,10 @@ static int grid_for(const void *kern, int bs, int nsm, size_t smem = 0) {
 // halo exchange and cross-rank reduction
 // ----------------------------------------------------------------------------
 // padded buffer selector: 0 = z, 1 = w, 2 = x scratch
-static double *padbuf(Rank &R, int which) { return which == 0 ? R.zpad : which == 1 ? R.wpad : R.xpad; }
+// (pipelined block Jacobi: the SpMV inputs are z_hat, w_hat; z, w stay own-only)
+static double *padbuf(Rank &R, int which) {
+    return which == 0 ? (R.pipe ? R.zhpad : R.zpad) : which == 1 ? (R.pipe ? R.whpad : R.wpad) : R.xpad;
+}
 
 static int halo(pbcg_handle *h, int which, cudaStream_t st = nullptr) {
     if (!st) st = h->stream;
@@ -1066,7 +1079,8 @@ static int launch_xd2(pbcg_handle *h, const MultiDotArgs &a) {  // (x,y), (y,y)
 
 static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     // fin = 1: the last CTA rounds and runs the scalar step; fin = 0: publish only (finalize_kernel follows)
-    K2Args a{R.n, R.r, R.rh, R.w(), R.t, R.v, R.p, R.s, R.z(), R.q, R.y, R.sc, R.gacc[1], fin ? R.tickets + 1 : nullptr, R.hist, fin, R.part[1]};
+    K2Args a{R.n, R.r, R.rh, R.w(), R.t, R.v, R.p, R.s, R.z(), R.q, R.y, R.sc, R.gacc[1], fin ? R.tickets + 1 : nullptr, R.hist, fin, R.part[1],
+             R.pipe ? R.bji : nullptr, R.pipe ? R.zhpad + R.own_off : nullptr, R.rb + R.n == R.ng};
     if (h->dot_mode == PBCG_DOT_PLAIN) {
         launch_ex(K2SP, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T)), dim3(KSTREAM_THREADS), K2_SMEM, st,
                   pdl_for(R), a);
@@ -1082,7 +1096,8 @@ static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
 }
 
 static int launch_k3(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
-    K3Args a{R.n, R.rh, R.p, R.q, R.y, R.t, R.v, R.x, R.r, R.w(), R.sc, R.gacc[2], fin ? R.tickets + 2 : nullptr, R.hist, fin, R.part[2]};
+    K3Args a{R.n, R.rh, R.p, R.q, R.y, R.t, R.v, R.x, R.r, R.w(), R.sc, R.gacc[2], fin ? R.tickets + 2 : nullptr, R.hist, fin, R.part[2],
+             R.pipe ? R.bji : nullptr, R.pipe ? R.whpad + R.own_off : nullptr, R.rb + R.n == R.ng};
     if (h->dot_mode == PBCG_DOT_PLAIN) {
         launch_ex(K3SP, dim3(stream_grid(h, R.n, TileGeo<K3_NCW, K3_PPT>::T)), dim3(K3_THREADS), K3_SMEM, st,
                   pdl_for(R), a);
@@ -1115,7 +1130,7 @@ static int enqueue_iteration(pbcg_handle *h) {
         else finalize_kernel<4><<<1, 128, 0, h->side>>>(R.gacc[1], PH_A, R.sc, R.hist, nullptr, nullptr);
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaEventRecord(h->ev[5], h->side));
-        RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.zpad, R.v, nullptr, nullptr, true, st));
+        RC_TRY(launch_spmv(h, R, SPMV_PLAIN, padbuf(R, 0), R.v, nullptr, nullptr, true, st));
         CUDA_TRY(cudaStreamWaitEvent(st, h->ev[5], 0));
         RC_TRY(launch_k3(h, R, 0, st));
         CUDA_TRY(cudaEventRecord(h->ev[6], st));
@@ -1124,7 +1139,7 @@ static int enqueue_iteration(pbcg_handle *h) {
         else finalize_kernel<3><<<1, 128, 0, h->side>>>(R.gacc[2], PH_B, R.sc, R.hist, nullptr, nullptr);
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaEventRecord(h->ev[7], h->side));
-        RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, true, st));
+        RC_TRY(launch_spmv(h, R, SPMV_PLAIN, padbuf(R, 1), R.t, nullptr, nullptr, true, st));
         CUDA_TRY(cudaStreamWaitEvent(st, h->ev[7], 0));
         return PBCG_OK;
     }
@@ -1138,7 +1153,7 @@ static int enqueue_iteration(pbcg_handle *h) {
         if (!split) {
             RC_TRY(halo(h, which));
             for (auto &R : h->R) {
-                double *xp = which == 0 ? R.zpad : R.wpad;
+                double *xp = padbuf(R, which);
                 RC_TRY(launch_spmv(h, R, SPMV_PLAIN, xp, R.*ymem, nullptr, nullptr, true, st));
             }
             return PBCG_OK;
@@ -1148,12 +1163,12 @@ static int enqueue_iteration(pbcg_handle *h) {
         RC_TRY(halo(h, which, h->cstream));
         CUDA_TRY(cudaEventRecord(h->evh[evi + 1], h->cstream));
         for (auto &R : h->R) {
-            double *xp = which == 0 ? R.zpad : R.wpad;
+            double *xp = padbuf(R, which);
             RC_TRY(launch_spmv(h, R, SPMV_PLAIN, xp, R.*ymem, nullptr, nullptr, true, st, SP_INTERIOR, reserve));
         }
         CUDA_TRY(cudaStreamWaitEvent(st, h->evh[evi + 1], 0));
         for (auto &R : h->R) {
-            double *xp = which == 0 ? R.zpad : R.wpad;
+            double *xp = padbuf(R, which);
             RC_TRY(launch_spmv(h, R, SPMV_PLAIN, xp, R.*ymem, nullptr, nullptr, true, st, SP_BOUNDARY));
         }
         return PBCG_OK;
@@ -1375,6 +1390,33 @@ static int bj_setup(pbcg_handle *h, const pbcg_csr_local *A0) {
     return PBCG_OK;
 }
 
+// Pipelined 2x2 block Jacobi (R-25): M and M^-1 of every own block; the
+// matrix stays A (the iteration applies M^-1 to z and w in K2 / K3).
+static int bj_pipe_setup(pbcg_handle *h, const pbcg_csr_local *A0) {
+    for (auto &R : h->R) {
+        if (R.rb & 1) return fail(PBCG_EINVAL, "block jacobi: every rank's first row must be even (whole 2x2 blocks)");
+        R.pipe = true;
+        R.ng = h->n_global;
+        CUDA_TRY(cudaMemsetAsync(R.zhpad, 0, sizeof(double) * (R.buf_hi - R.buf_lo), h->stream));
+        CUDA_TRY(cudaMemsetAsync(R.whpad, 0, sizeof(double) * (R.buf_hi - R.buf_lo), h->stream));
+        if (R.n == 0) continue;
+        const int32_t *rp = A0->row_ptr + (h->V > 1 ? R.rb : 0);
+        const int g = (int)std::min<int64_t>((R.n + 511) / 512, 65535);
+        // the M^-1 column outputs (stored-B mode) land in the unused own part of xpad
+        bj_blocks_kernel<<<g, 256, 0, h->stream>>>(R.n, R.rb, h->n_global, rp, A0->col_idx, A0->values, R.bjm,
+                                                   R.bji, R.xpad + R.own_off, R.tmp, R.bad);
+        CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    for (auto &R : h->R) {
+        int bad = 0;
+        CUDA_TRY(cudaMemcpy(&bad, R.bad, sizeof(int), cudaMemcpyDeviceToHost));
+        if (bad & 4) return fail(PBCG_EINVAL, "block jacobi: singular or non-finite 2x2 diagonal block");
+        CUDA_TRY(cudaMemset(R.xpad, 0, sizeof(double) * (R.buf_hi - R.buf_lo)));
+    }
+    return PBCG_OK;
+}
+
 static int jacobi_scale(pbcg_handle *h, const pbcg_csr_local *A) {
     for (auto &R : h->R) {
         if (R.n == 0) continue;
@@ -1582,6 +1624,7 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
         CUDA_TRY(cudaStreamSynchronize(h->stream));
         if (h->precond == PBCG_PRECOND_JACOBI) RC_TRY(jacobi_scale(h, A));
         if (h->precond == PBCG_PRECOND_BJACOBI2) RC_TRY(bj_setup(h, A0));
+        if (h->precond == PBCG_PRECOND_BJACOBI2_PIPE) RC_TRY(bj_pipe_setup(h, A0));
         const char *es = getenv("PBCG_SELL_SLOTS");
         for (auto &R : h->R) {
             R.spmv_kind = spmv_kind_for(R, h->nsm);
@@ -1671,10 +1714,32 @@ static int scatter_in(pbcg_handle *h, const double *src, double *Rank::*dst_memb
     return PBCG_OK;
 }
 
+// The own part of the SpMV input for the product "B u": u itself, or with the
+// pipelined block Jacobi (R-25) u_hat = M^-1 u (bj_apply_kernel, the
+// oracle's orc_bj_apply formula) -- the SpMV then computes A (M^-1 u).
+static int own_to_pad(pbcg_handle *h, Rank &R, const double *src, int which) {
+    if (R.pipe) {
+        if (R.n == 0) return PBCG_OK;
+        bj_apply_kernel<<<(int)std::min<int64_t>((R.n + 511) / 512, 4096), 256, 0, h->stream>>>(
+            R.n, R.rb, R.ng, R.bji, src, padbuf(R, which) + R.own_off);
+        CUDA_TRY(cudaGetLastError());
+        return PBCG_OK;
+    }
+    if (src != padbuf(R, which) + R.own_off)
+        CUDA_TRY(cudaMemcpyAsync(padbuf(R, which) + R.own_off, src, sizeof(double) * R.n, cudaMemcpyDeviceToDevice,
+                                 h->stream));
+    return PBCG_OK;
+}
+
 static int copy_own_to_pad(pbcg_handle *h, double *Rank::*src_member, int which) {
+    for (auto &R : h->R) RC_TRY(own_to_pad(h, R, R.*src_member, which));
+    return PBCG_OK;
+}
+
+// w (already the own part of wpad) as the SpMV input of t = B w
+static int w_to_pad(pbcg_handle *h) {
     for (auto &R : h->R)
-        CUDA_TRY(cudaMemcpyAsync(padbuf(R, which) + R.own_off, R.*src_member, sizeof(double) * R.n,
-                                 cudaMemcpyDeviceToDevice, h->stream));
+        if (R.pipe) RC_TRY(own_to_pad(h, R, R.w(), 1));
     return PBCG_OK;
 }
 
@@ -1718,6 +1783,8 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
     if (op.method == PBCG_METHOD_BICGSTAB && op.dot_mode != PBCG_DOT_EXACT)
         return fail(PBCG_EINVAL, "start: Algorithm 1 runs with exact dots only");
     if (op.rr_period < 0) return fail(PBCG_EINVAL, "start: rr_period < 0");
+    if (op.method == PBCG_METHOD_BICGSTAB && h->precond == PBCG_PRECOND_BJACOBI2_PIPE)
+        return fail(PBCG_EINVAL, "start: the pipelined block Jacobi is defined for Algorithm 2");
     if (op.range_mode != PBCG_RANGE_FULL && op.range_mode != PBCG_RANGE_FAST)
         return fail(PBCG_EINVAL, "start: bad range_mode");
     if (op.rr_period > 0 && op.method != PBCG_METHOD_PBICGSTAB)
@@ -1747,7 +1814,7 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
     } else {
         RC_TRY(scatter_in(h, x0, &Rank::x, is_host_ptr(x0)));
     }
-    if (h->precond == PBCG_PRECOND_BJACOBI2)  // y0 := M x0 (R-23)
+    if (h->precond == PBCG_PRECOND_BJACOBI2 || h->precond == PBCG_PRECOND_BJACOBI2_PIPE)  // y0 := M x0 (R-23, R-25)
         for (auto &R : h->R)
             if (R.n > 0) {
                 bj_apply_kernel<<<(int)std::min<int64_t>((R.n + 511) / 512, 4096), 256, 0, h->stream>>>(
@@ -1797,8 +1864,9 @@ static int start_alg2_rest(pbcg_handle *h) {
     RC_TRY(copy_own_to_pad(h, &Rank::r, 2));
     RC_TRY(halo(h, 2));
     for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.xpad, R.w(), nullptr, nullptr, false, h->stream));
+    RC_TRY(w_to_pad(h));
     RC_TRY(halo(h, 1));
-    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, false, h->stream));
+    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, padbuf(R, 1), R.t, nullptr, nullptr, false, h->stream));
     // I2-I4: ||b||, rho0 = (r^,r0), delta0 = (r^,w0), (r0,r0); alpha0
     std::vector<const double *> xb, yb, xr, yr, xw, yw, xn, yn;
     for (auto &R : h->R) {
@@ -1916,8 +1984,9 @@ static int enqueue_replacement(pbcg_handle *h) {
     RC_TRY(copy_own_to_pad(h, &Rank::s, 2));
     RC_TRY(halo(h, 2));
     for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.xpad, R.z(), nullptr, nullptr, true, st));
+    RC_TRY(w_to_pad(h));
     RC_TRY(halo(h, 1));
-    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, true, st));
+    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, padbuf(R, 1), R.t, nullptr, nullptr, true, st));
     return PBCG_OK;
 }
 
@@ -1928,7 +1997,7 @@ static int enqueue_replacement(pbcg_handle *h) {
 static constexpr int SMALL_BS = 256;
 static constexpr int64_t SMALL_N_MAX = 1 << 14;  // tools/small_ab.py: fused 50-55K vs 36-38K iter/s up to 16K rows, slower from 32K
 static int small_grid_for(pbcg_handle *h) {
-    if (h->comm_only || h->V != 1 || h->comm || h->R.empty()) return 0;
+    if (h->comm_only || h->V != 1 || h->comm || h->R.empty() || h->precond == PBCG_PRECOND_BJACOBI2_PIPE) return 0;
     const Rank &R = h->R[0];
     if (R.n == 0 || R.n > SMALL_N_MAX) return 0;
     int coop = 0, per_sm = 0;
@@ -2054,7 +2123,7 @@ extern "C" int pbicgstab_finish(pbcg_handle *h, double *x, pbcg_result *res) {
         for (auto &R : h->R) {
             const int64_t off = h->V > 1 ? R.rb : 0;
             const double *src = R.x;
-            if (h->precond == PBCG_PRECOND_BJACOBI2 && R.n > 0) {  // x := M^-1 y (R-23), into q
+            if ((h->precond == PBCG_PRECOND_BJACOBI2 || h->precond == PBCG_PRECOND_BJACOBI2_PIPE) && R.n > 0) {  // x := M^-1 y (R-23, R-25), into q
                 bj_apply_kernel<<<(int)std::min<int64_t>((R.n + 511) / 512, 4096), 256, 0, xs>>>(
                     R.n, R.rb, h->n_global, R.bji, R.x, R.q);
                 CUDA_TRY(cudaGetLastError());
@@ -2303,14 +2372,14 @@ extern "C" int pbcg_profile_iterations(pbcg_handle *h, int32_t k, double *ms) {
         if (h->dot_mode == PBCG_DOT_PLAIN) rc = reduce_finalize<4>(h, 1, PH_A, st, nullptr, nullptr);
         else finalize_kernel<4><<<1, 128, 0, st>>>(R.gacc[1], PH_A, R.sc, R.hist, nullptr, nullptr);
         cudaEventRecord(e[2], st);
-        if (rc == PBCG_OK) rc = launch_spmv(h, R, SPMV_PLAIN, R.zpad, R.v, nullptr, nullptr, true, st);
+        if (rc == PBCG_OK) rc = launch_spmv(h, R, SPMV_PLAIN, padbuf(R, 0), R.v, nullptr, nullptr, true, st);
         cudaEventRecord(e[3], st);
         if (rc == PBCG_OK) rc = launch_k3(h, R, 0, st);
         cudaEventRecord(e[4], st);
         if (rc == PBCG_OK && h->dot_mode == PBCG_DOT_PLAIN) rc = reduce_finalize<3>(h, 2, PH_B, st, nullptr, nullptr);
         else if (h->dot_mode != PBCG_DOT_PLAIN) finalize_kernel<3><<<1, 128, 0, st>>>(R.gacc[2], PH_B, R.sc, R.hist, nullptr, nullptr);
         cudaEventRecord(e[5], st);
-        if (rc == PBCG_OK) rc = launch_spmv(h, R, SPMV_PLAIN, R.wpad, R.t, nullptr, nullptr, true, st);
+        if (rc == PBCG_OK) rc = launch_spmv(h, R, SPMV_PLAIN, padbuf(R, 1), R.t, nullptr, nullptr, true, st);
         cudaEventRecord(e[6], st);
     }
     cudaError_t se = cudaStreamSynchronize(st);

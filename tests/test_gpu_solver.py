@@ -723,3 +723,62 @@ def test_fused_register_variant_same_bits(pb, name, dot_mode, monkeypatch):
         S.close()
     assert got["1"][2:] == got["0"][2:]
     assert np.array_equal(got["1"][0], got["0"][0]) and np.array_equal(got["1"][1], got["0"][1])
+
+
+# ---------------- pipelined 2x2 block Jacobi (R-25) ---
+
+@pytest.mark.parametrize("name", ["c1", "rand", "small3d", "odd"])
+def test_pipelined_block_jacobi_matches_oracle(pb, name):
+    # M^-1 applied inside K2 (z_hat) and K3 (w_hat); the SpMVs run on A:
+    # trajectory of A M^-1 y = b, y and x = M^-1 y bit for bit against the
+    # oracle's op_apply, at 1 rank, 2/4 virtual ranks and the NCCL vehicle;
+    # the odd order has a 1x1 tail block in the last rank's tail tile
+    import torch
+    A = {"c1": lambda: gen.make_config("c1_2d64"),
+         "rand": lambda: gen.random_banded(20_000, seed=9, band=1500),
+         "small3d": lambda: gen.stencil(3, 20, 100.0),
+         "odd": lambda: gen.random_banded(3_001, seed=5, band=300)}[name]()
+    S0 = solver(pb, A)
+    b = gpu_b(pb, S0, A)
+    S0.close()
+    M, Mi = oracle.bj_blocks_c(A)
+    O = oracle.PBiCGStab(A, b=b.cpu().numpy(), tol=1e-10, max_iter=3000, minv=Mi)
+    O.run()
+    assert O.status == oracle.CONVERGED
+    want_x = u64(oracle.bj_apply(Mi, O.vec("x")))
+    runs = [dict(), dict(force_nccl=True)] + ([dict(virtual_ranks=2), dict(virtual_ranks=4)] if A.n % 8 == 0 else [])
+    for kw in runs:
+        S = solver(pb, A, history_capacity=3001, precond="bjacobi2_pipe", **kw)
+        assert S.spmv_format()["nnz"] == A.nnz  # A is stored as given
+        x, r = S.solve(b, tol=1e-10, max_iter=3000)
+        assert S.exec_mode() == 0
+        assert r.iterations == O.iterations and r.status == O.status, kw
+        assert np.array_equal(u64(S.history()), u64(O.history())), kw
+        assert np.array_equal(u64(S.vec("x")), u64(O.vec("x"))), kw  # y
+        assert np.array_equal(u64(x.cpu().numpy()), want_x), kw      # x = M^-1 y
+        tr = oracle.true_relres(A, b.cpu().numpy(), oracle.bj_apply(Mi, O.vec("x")))[0]
+        assert r.relres_true == tr, kw
+        S.close()
+
+
+def test_pipelined_block_jacobi_full_size_and_rejects(pb):
+    # full C3 in the bench's launch configuration: first iterations bit-exact
+    # (SELL-P SpMV on A, z_hat / w_hat from the stream kernels); Alg. 1 with
+    # the pipelined preconditioner is EINVAL
+    import torch
+    A = gen.make_config("c3_3d128")
+    M, Mi = oracle.bj_blocks_c(A)
+    S = solver(pb, A, history_capacity=16, precond="bjacobi2_pipe")
+    b = S.spmv(torch.ones(A.n, dtype=torch.float64, device="cuda"))
+    O = oracle.PBiCGStab(A, b=b.cpu().numpy(), tol=0.0, max_iter=8, minv=Mi)
+    O.run(4)
+    S.start(b, tol=0.0, max_iter=8)
+    S.iterate(4)
+    S.finish(None)
+    assert np.array_equal(u64(S.history()), u64(O.history()))
+    for k in ("z", "w", "t", "v", "x"):
+        assert np.array_equal(u64(S.vec(k)), u64(O.vec(k))), k
+    with pytest.raises(pb.PbcgError) as e:
+        S.solve(b, method="bicgstab")
+    assert e.value.rc == 1
+    S.close()

@@ -502,3 +502,114 @@ def test_block_jacobi_preconditioned_solves():
         # y0 = M x0 then x = M^-1 y round trip
         y = oracle.bj_apply(M, xs)
         assert np.allclose(oracle.bj_apply(Mi, y), xs, rtol=1e-13, atol=1e-15)
+
+
+# ---- pipelined right 2x2 block Jacobi (R-25) ----
+# Algorithm 2 on B = A M^-1 where every product B u is evaluated inside the
+# iteration as A (M^-1 u): u_hat = M^-1 u (orc_bj_apply), then A's fma chain.
+
+def _dense(A):
+    D = np.zeros((A.n, A.n))
+    for i in range(A.n):
+        D[i, A.col[A.row_ptr[i]:A.row_ptr[i + 1]]] = A.val[A.row_ptr[i]:A.row_ptr[i + 1]]
+    return D
+
+
+def test_bj_apply_c_twin():
+    # the C block apply inside the oracle's operator == the Python one (pinned
+    # against libm fma), incl. odd order and signed zeros
+    rng = np.random.default_rng(5)
+    for n in (1, 2, 7, 64, 1001):
+        Q = rng.normal(size=((n + 1) // 2, 4))
+        x = rng.normal(size=n)
+        x[rng.random(n) < 0.1] = -0.0
+        Q[rng.random(Q.shape) < 0.1] = 0.0
+        assert np.array_equal(oracle.bj_apply_c(Q, x).view(np.uint64), oracle.bj_apply(Q, x).view(np.uint64))
+
+
+def test_bj_blocks_c_twin():
+    # the C blocks (full-size tests) == block_jacobi_right's, bit for bit
+    for A in (gen.random_banded(1001, seed=6, band=40), gen.stencil(2, 13, 10.0), gen.dense_as_sparse(9, seed=2)):
+        B, M, Mi = oracle.block_jacobi_right(A)
+        M2, Mi2 = oracle.bj_blocks_c(A)
+        assert np.array_equal(M.view(np.uint64), M2.view(np.uint64))
+        assert np.array_equal(Mi.view(np.uint64), Mi2.view(np.uint64))
+    with pytest.raises(ValueError):
+        oracle.bj_blocks_c(gen.from_dense(np.array([[1.0, 2.0], [2.0, 4.0]])))
+
+
+def test_pipelined_bjacobi_operator_products():
+    # after one step: s = B p, z = B s, v = B z, t = B w with B u := spmv(A, bj_apply(M^-1, u))
+    # -- the composition of two pinned routines, right (not left) of A
+    A = gen.random_banded(300, seed=4, band=20)
+    B, M, Mi = oracle.block_jacobi_right(A)
+    S = oracle.PBiCGStab(A, b=A.b, tol=0.0, max_iter=3, minv=Mi)
+    S.step()
+    Bop = lambda u: oracle.spmv(A, oracle.bj_apply(Mi, u))
+    u = lambda a: a.view(np.uint64)
+    assert np.array_equal(u(S.vec("s")), u(Bop(S.vec("p"))))
+    assert np.array_equal(u(S.vec("z")), u(Bop(S.vec("s"))))
+    assert np.array_equal(u(S.vec("v")), u(Bop(S.vec("z"))))
+    assert np.array_equal(u(S.vec("t")), u(Bop(S.vec("w"))))
+    assert not np.array_equal(u(S.vec("z")), u(oracle.bj_apply(Mi, oracle.spmv(A, S.vec("s")))))  # not M^-1 A
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_pipelined_bjacobi_tracks_exact(seed):
+    # exact-rational Algorithm 2 on the matrix A M^-1 (M^-1 = the oracle's
+    # rounded blocks): the fp trajectory agrees to rounding error
+    from a11_cases import alg2_exact
+    n = 10
+    M0, b = _int_system(n, 300 + seed)
+    A = gen.from_dense(M0)
+    B, M, Mi = oracle.block_jacobi_right(A)
+    Mid = np.zeros((n, n))
+    for m in range(Mi.shape[0]):
+        Mid[2 * m:2 * m + 2, 2 * m:2 * m + 2] = Mi[m].reshape(2, 2)
+    P = [[sum(F(M0[i][k]) * F(Mid[k][j]) for k in range(n)) for j in range(n)] for i in range(n)]
+    ex = alg2_exact(P, [F(v) for v in b], 4)
+    S = oracle.PBiCGStab(A, b=b, tol=0.0, max_iter=4, minv=Mi)
+    S.run()
+    H = S.history()
+    for i in range(3):
+        assert math.isclose(H[i + 1, oracle.H_OMEGA], float(ex[i]["omega"]), rel_tol=1e-9), i
+        assert math.isclose(H[i, oracle.H_ALPHA], float(ex[i]["alpha"]), rel_tol=1e-9), i
+        assert math.isclose(H[i + 1, oracle.H_RR], float(ex[i]["rr"]), rel_tol=1e-8), i
+
+
+def test_pipelined_bjacobi_solves():
+    rng = np.random.default_rng(23)
+    for k in range(12):
+        n = int(rng.integers(8, 60))
+        A = gen.dense_as_sparse(n, seed=900 + k, density=0.5)
+        D = _dense(A)
+        b = rng.uniform(-1, 1, n)
+        B, M, Mi = oracle.block_jacobi_right(A)
+        S = oracle.PBiCGStab(A, b=b, tol=1e-10, max_iter=1000, minv=Mi)
+        S.run()
+        assert S.status == oracle.CONVERGED, (k, S.status)
+        x = oracle.bj_apply(Mi, S.vec("x"))
+        xs = np.linalg.solve(D, b)
+        assert np.linalg.norm(x - xs) <= 1e-6 * np.linalg.norm(xs)
+        assert oracle.true_relres(A, b, x)[0] <= 10 * 1e-10
+        # the stored-B arm (R-23) solves the same system; different roundings
+        S2 = oracle.PBiCGStab(B, b=b, tol=1e-10, max_iter=1000)
+        S2.run()
+        assert np.linalg.norm(oracle.bj_apply(Mi, S2.vec("x")) - x) <= 1e-6 * np.linalg.norm(xs)
+
+
+def test_pipelined_bjacobi_block_diagonal():
+    # M = A's blocks: A (M^-1 u) = u up to rounding -> converges in <= 2 iterations
+    rng = np.random.default_rng(8)
+    n = 41
+    D = np.zeros((n, n))
+    for m in range(n // 2):
+        D[2 * m:2 * m + 2, 2 * m:2 * m + 2] = rng.uniform(1, 2, (2, 2)) + 3 * np.eye(2)
+    D[n - 1, n - 1] = 3.0
+    A = gen.from_dense(D)
+    B, M, Mi = oracle.block_jacobi_right(A)
+    b = rng.uniform(-1, 1, n)
+    S = oracle.PBiCGStab(A, b=b, tol=1e-12, max_iter=10, minv=Mi)
+    S.run()
+    assert S.status == oracle.CONVERGED and S.iterations <= 2
+    assert np.allclose(D @ oracle.bj_apply(Mi, S.vec("x")), b, rtol=0, atol=1e-12)
