@@ -1030,6 +1030,12 @@ static constexpr int K2_PPT = PBCG_K2_PPT, K2_ST = PBCG_K2_ST, K3_PPT = PBCG_K3_
 static constexpr int64_t LEAN_ROWS = 8 << 20;
 #define K2SP k2_stream<K2_NH, K2_NC, S_NCW, K2_PPT, K2_ST, K2_NHE, false>
 #define K3SP k3_stream<K3_NH, K3_NC, K3_NCW, K3_PPT, K3_ST, K3_NHE, false>
+// pipelined block Jacobi (R-25): exact (lean cold tier: the z_hat / w_hat
+// work would otherwise spill) and plain dots
+#define K2SX k2_stream<K2_NH, K2_NC - 1, S_NCW, K2_PPT, K2_ST, K2_NHE, true, true>
+#define K3SX k3_stream<K3_NH, K3_NC - 1, S_NCW, K3_PPT, K3_ST, K3_NHE, true, true>  // 7 warps per group: 128 registers
+#define K2SXP k2_stream<K2_NH, K2_NC, S_NCW, K2_PPT, K2_ST, K2_NHE, false, true>
+#define K3SXP k3_stream<K3_NH, K3_NC, K3_NCW, K3_PPT, K3_ST, K3_NHE, false, true>
 #define XDS exdot_stream<X_NH, X_NL, X_NCW, XD_PPT, XD_ST>
 #define XDS2 exdot_stream<X_NH, X_NL, X_NCW, XD_PPT, XD_ST, 2>
 static constexpr size_t ring_bytes(int nv, int ncw, int ppt, int stages) {
@@ -1037,6 +1043,7 @@ static constexpr size_t ring_bytes(int nv, int ncw, int ppt, int stages) {
 }
 static constexpr size_t K2_SMEM = ring_bytes(8, S_NCW, K2_PPT, K2_ST);
 static constexpr size_t K3_SMEM = ring_bytes(7, K3_NCW, K3_PPT, K3_ST);
+static constexpr size_t K3X_SMEM = ring_bytes(7, S_NCW, K3_PPT, K3_ST);  // the pipelined block Jacobi's K3
 static constexpr size_t XD_SMEM = ring_bytes(2, X_NCW, XD_PPT, XD_ST);
 static constexpr int STREAM_THREADS = (X_NCW + 1) * 32;      // exdot: 1 dot group
 static constexpr int KSTREAM_THREADS = (2 * S_NCW + 1) * 32;  // K2: 2 dot groups
@@ -1052,6 +1059,10 @@ static int stream_attrs() {
     CUDA_TRY(cudaFuncSetAttribute((const void *)K2SL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)K3SL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)K3SP, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM));
+    CUDA_TRY(cudaFuncSetAttribute((const void *)K2SX, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM));
+    CUDA_TRY(cudaFuncSetAttribute((const void *)K3SX, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3X_SMEM));
+    CUDA_TRY(cudaFuncSetAttribute((const void *)K2SXP, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM));
+    CUDA_TRY(cudaFuncSetAttribute((const void *)K3SXP, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)XDS, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XD_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)XDS2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XD_SMEM));
     done = 1;
@@ -1081,7 +1092,14 @@ static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     // fin = 1: the last CTA rounds and runs the scalar step; fin = 0: publish only (finalize_kernel follows)
     K2Args a{R.n, R.r, R.rh, R.w(), R.t, R.v, R.p, R.s, R.z(), R.q, R.y, R.sc, R.gacc[1], fin ? R.tickets + 1 : nullptr, R.hist, fin, R.part[1],
              R.pipe ? R.bji : nullptr, R.pipe ? R.zhpad + R.own_off : nullptr, R.rb + R.n == R.ng};
-    if (h->dot_mode == PBCG_DOT_PLAIN) {
+    if (R.pipe) {
+        if (h->dot_mode == PBCG_DOT_PLAIN)
+            launch_ex(K2SXP, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T)), dim3(KSTREAM_THREADS), K2_SMEM, st,
+                      pdl_for(R), a);
+        else
+            launch_ex(K2SX, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T)), dim3(KSTREAM_THREADS), K2_SMEM, st,
+                      pdl_for(R), a);
+    } else if (h->dot_mode == PBCG_DOT_PLAIN) {
         launch_ex(K2SP, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T)), dim3(KSTREAM_THREADS), K2_SMEM, st,
                   pdl_for(R), a);
     } else if (R.n < LEAN_ROWS) {
@@ -1098,7 +1116,14 @@ static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
 static int launch_k3(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
     K3Args a{R.n, R.rh, R.p, R.q, R.y, R.t, R.v, R.x, R.r, R.w(), R.sc, R.gacc[2], fin ? R.tickets + 2 : nullptr, R.hist, fin, R.part[2],
              R.pipe ? R.bji : nullptr, R.pipe ? R.whpad + R.own_off : nullptr, R.rb + R.n == R.ng};
-    if (h->dot_mode == PBCG_DOT_PLAIN) {
+    if (R.pipe) {
+        if (h->dot_mode == PBCG_DOT_PLAIN)
+            launch_ex(K3SXP, dim3(stream_grid(h, R.n, TileGeo<K3_NCW, K3_PPT>::T)), dim3(K3_THREADS), K3_SMEM, st,
+                      pdl_for(R), a);
+        else
+            launch_ex(K3SX, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K3_PPT>::T)), dim3(KSTREAM_THREADS), K3X_SMEM, st,
+                      pdl_for(R), a);
+    } else if (h->dot_mode == PBCG_DOT_PLAIN) {
         launch_ex(K3SP, dim3(stream_grid(h, R.n, TileGeo<K3_NCW, K3_PPT>::T)), dim3(K3_THREADS), K3_SMEM, st,
                   pdl_for(R), a);
     } else if (R.n < LEAN_ROWS) {

@@ -180,8 +180,11 @@ struct K2Op {
     }
 };
 
-// EXACT = false: plain fp64 dots (PlainAcc, dot_mode PBCG_DOT_PLAIN)
-template <int NH, int NL, int W, int PPT, int STAGES, int NHE, bool EXACT = true>
+// EXACT = false: plain fp64 dots (PlainAcc, dot_mode PBCG_DOT_PLAIN).
+// PIPE: the pipelined block Jacobi (R-25) also writes z_hat = M^-1 z (its own
+// instantiation: the extra loads and FMAs would push the plain kernel past
+// its register budget)
+template <int NH, int NL, int W, int PPT, int STAGES, int NHE, bool EXACT = true, bool PIPE = false>
 __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
     using Acc = typename std::conditional<EXACT, ExAccT<NH, NL, NHE>, PlainAcc>::type;
     constexpr int NV = 8;  // r, rh, w, t | p, s, z, v
@@ -264,7 +267,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
                         R.row0(flags, r.y, w.y, t.y, v.y, p.y, ss.y, z.y, q.y, y.y, P[2], P[3]);
                         ((double2 *)a.p)[gp] = p; ((double2 *)a.s)[gp] = ss; ((double2 *)a.z)[gp] = z;
                         ((double2 *)a.q)[gp] = q; ((double2 *)a.y)[gp] = y;
-                        if (a.zh) ((double2 *)a.zh)[gp] = bj_pair(a.minv, gp, z.x, z.y);  // z_hat = M^-1 z (R-25)
+                        if constexpr (PIPE) ((double2 *)a.zh)[gp] = bj_pair(a.minv, gp, z.x, z.y);  // z_hat = M^-1 z (R-25)
                     } else {
                         const double2 rh = B2[1 * TP + j];
                         R.row1(flags, rh.x, w.x, t.x, v.x, ss.x, z.x, P[0], P[1]);
@@ -272,7 +275,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
                     }
                     cascade_batch<4, true>(R.d0, R.d1, P, s0, s1);
                 } else {
-                    double zz[2] = {0.0, 0.0};  // this pair's z (pipelined block Jacobi)
+                    [[maybe_unused]] double zz[2] = {0.0, 0.0};  // this pair's z (pipelined block Jacobi)
                     for (int h = 0; h < 2; ++h) {
                         const int lr = 2 * j + h;  // local row
                         if (lr >= rows) break;
@@ -291,14 +294,14 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
                             if (!first) p = m ? B[4 * T + lr] : a.p[gi];
                             R.row0(flags, r, w, t, v, p, ss, z, q, y, P0, P1);
                             a.p[gi] = p; a.s[gi] = ss; a.z[gi] = z; a.q[gi] = q; a.y[gi] = y;
-                            zz[h] = z;
+                            if constexpr (PIPE) zz[h] = z;
                         } else {
                             R.row1(flags, m ? B[1 * T + lr] : a.rh[gi], w, t, v, ss, z, P0, P1);
                         }
                         cascade_one(R.d0, P0, s0);
                         cascade_one(R.d1, P1, s1);
                     }
-                    if (g == 0 && a.zh && 2 * j < rows) {  // z_hat of the pair; an odd last row is the 1x1 tail block
+                    if (PIPE && g == 0 && 2 * j < rows) {  // z_hat of the pair; an odd last row is the 1x1 tail block
                         const int64_t m0 = (r0 >> 1) + j;
                         if (2 * j + 1 < rows) ((double2 *)a.zh)[m0] = bj_pair(a.minv, m0, zz[0], zz[1]);
                         else a.zh[2 * m0] = __dmul_rn(a.minv[4 * m0], zz[0]);
@@ -370,7 +373,7 @@ struct K3Op {
     }
 };
 
-template <int NH, int NL, int W, int PPT, int STAGES, int NHE, bool EXACT = true>
+template <int NH, int NL, int W, int PPT, int STAGES, int NHE, bool EXACT = true, bool PIPE = false>
 __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
     using Acc = typename std::conditional<EXACT, ExAccT<NH, NL, NHE>, PlainAcc>::type;
     constexpr int NV = 7;  // rh, p, q, y, t, v, x
@@ -455,11 +458,11 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
                         R.row1(flags, rh.x, y.x, t.x, v.x, w.x, P[0]);
                         R.row1(flags, rh.y, y.y, t.y, v.y, w.y, P[1]);
                         ((double2 *)a.w)[gp] = w;
-                        if (a.wh) ((double2 *)a.wh)[gp] = bj_pair(a.minv, gp, w.x, w.y);  // w_hat = M^-1 w (R-25)
+                        if constexpr (PIPE) ((double2 *)a.wh)[gp] = bj_pair(a.minv, gp, w.x, w.y);  // w_hat = M^-1 w (R-25)
                         cascade_batch<2, false>(R.d0, R.d1, P, s0, s1);
                     }
                 } else {
-                    double ww[2] = {0.0, 0.0};  // this pair's w (pipelined block Jacobi)
+                    [[maybe_unused]] double ww[2] = {0.0, 0.0};  // this pair's w (pipelined block Jacobi)
                     for (int h = 0; h < 2; ++h) {
                         const int lr = 2 * j + h;
                         if (lr >= rows) break;
@@ -478,11 +481,11 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
                             Prod P0;
                             R.row1(flags, rh, y, m ? B[4 * T + lr] : a.t[gi], m ? B[5 * T + lr] : a.v[gi], w, P0);
                             a.w[gi] = w;
-                            ww[h] = w;
+                            if constexpr (PIPE) ww[h] = w;
                             cascade_one(R.d0, P0, s0);
                         }
                     }
-                    if (g == 1 && a.wh && 2 * j < rows) {
+                    if (PIPE && g == 1 && 2 * j < rows) {
                         const int64_t m0 = (r0 >> 1) + j;
                         if (2 * j + 1 < rows) ((double2 *)a.wh)[m0] = bj_pair(a.minv, m0, ww[0], ww[1]);
                         else a.wh[2 * m0] = __dmul_rn(a.minv[4 * m0], ww[0]);
