@@ -304,6 +304,11 @@ int pbcg_exec_mode(const pbcg_handle *h, int32_t *mode);
  * superaccumulator deposits.  reset != 0 clears them. */
 int pbcg_debug_counters(uint64_t *out16, int32_t reset);
 
+/* Per-CTA phase timestamps of a -DPBCG_TIMELINE build (tools/timeline.py;
+ * zeros in the release build): 3 kernels (K2, SELL-P SpMV, K3) x 256 CTAs x 8
+ * uint64 globaltimer values; reset != 0 clears them. */
+int pbcg_timeline(uint64_t *out, int32_t reset);
+
 /* ---- host-only planning helpers (no GPU needed; CPU-testable) ------------ */
 
 /* FNV-1a hash of the setup arguments every rank must agree on: ABI version,

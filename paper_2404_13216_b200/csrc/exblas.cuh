@@ -57,6 +57,21 @@ __device__ unsigned long long g_dbg[16];
 #define PBCG_COUNT(i) ((void)0)
 #define PBCG_TS(k) ((void)0)
 #endif
+// Per-CTA timeline (built only with -DPBCG_TIMELINE; tools/timeline.py):
+// globaltimer of thread 0 at phase k of kernel kind (0 K2, 1 SpMV, 2 K3)
+__device__ unsigned long long g_tl[3][256][8];
+#ifdef PBCG_TIMELINE
+#define PBCG_TL(kind, k)                                                               \
+    do {                                                                               \
+        if (threadIdx.x == 0 && blockIdx.x < 256) {                                    \
+            unsigned long long t_;                                                     \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                     \
+            g_tl[(kind)][blockIdx.x][(k)] = t_;                                        \
+        }                                                                              \
+    } while (0)
+#else
+#define PBCG_TL(kind, k) ((void)0)
+#endif
 
 // Programmatic dependent launch: a kernel launched with programmatic stream
 // serialisation may start while the previous kernel of the stream finishes;
@@ -465,6 +480,35 @@ __device__ __forceinline__ void warp_deposit(double v, unsigned long long *sacc)
     }
 }
 
+// The same into words private to this warp (`w`, int64, e.g. a drained ring
+// area): lane 0 adds the warp sums with plain 64-bit adds -- no atomics, and
+// no contention with the other warps of the CTA (their deposits of similar
+// exponents would hit the same few words); the rare wide case deposits per
+// lane with the 32-bit atomics, which only this warp's lanes race on.
+__device__ __forceinline__ void warp_deposit_priv(double v, long long *w) {
+    int i = 0;
+    long long c0 = 0, c1 = 0, c2 = 0;
+    const bool nz = is_nonzero(v) && sacc_split(v, i, c0, c1, c2);
+    const unsigned imin = __reduce_min_sync(0xFFFFFFFFu, nz ? (unsigned)i : 0xFFFFFFFFu);
+    if (imin == 0xFFFFFFFFu) return;
+    const unsigned imax = __reduce_max_sync(0xFFFFFFFFu, nz ? (unsigned)i : 0u);
+    if (imax - imin <= 1u && imin + 3u < (unsigned)SACC_L) {
+        const bool sh = nz && ((unsigned)i != imin);
+        if (!nz) { c0 = 0; c1 = 0; c2 = 0; }
+        const long long d0 = sh ? 0 : c0, d1 = sh ? c0 : c1, d2 = sh ? c1 : c2, d3 = sh ? c2 : 0;
+        const long long s0 = warp_sum_i64(d0), s1 = warp_sum_i64(d1), s2 = warp_sum_i64(d2), s3 = warp_sum_i64(d3);
+        if ((threadIdx.x & 31) == 0) {
+            w[imin] += s0;
+            w[imin + 1] += s1;
+            w[imin + 2] += s2;
+            w[imin + 3] += s3;
+        }
+    } else if (nz) {
+        sacc_deposit((unsigned long long *)w, v);
+    }
+    __syncwarp();
+}
+
 // Two-tier accumulator used by the streaming kernels.  Each product p and its
 // TwoProd error e enter short hot expansions P, E (NH levels each, branch
 // free).  What falls out of them -- values far below this thread's running
@@ -517,6 +561,17 @@ struct ExAccT {
         drain_fpe<NHE>(E, sacc);
         drain_fpe<NC>(CP, sacc);
         drain_fpe<NC>(CE, sacc);
+    }
+    // the same into this warp's private words (warp_deposit_priv)
+    __device__ __forceinline__ void warp_merge_priv(long long *w) {
+#pragma unroll
+        for (int j = 0; j < NH; ++j) warp_deposit_priv(P.a[j], w);
+#pragma unroll
+        for (int j = 0; j < NHE; ++j) warp_deposit_priv(E.a[j], w);
+#pragma unroll
+        for (int j = 0; j < NC; ++j) warp_deposit_priv(CP.a[j], w);
+#pragma unroll
+        for (int j = 0; j < NC; ++j) warp_deposit_priv(CE.a[j], w);
     }
 };
 
@@ -591,6 +646,7 @@ struct PlainAcc {
     __device__ __forceinline__ void zero() { s = 0.0; }
     __device__ __forceinline__ Prod prep(double x, double y, bool, unsigned &) const { return Prod{x, y}; }
     __device__ __forceinline__ void add(const Prod &q) { s = __fma_rn(q.p, q.e, s); }
+    __device__ __forceinline__ void warp_merge_priv(long long *) {}
     // all 32 lanes, converged: lane 0 stores the warp's sum as a double
     __device__ __forceinline__ void warp_merge(unsigned long long *slots) {
         double v = s;

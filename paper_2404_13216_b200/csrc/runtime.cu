@@ -2469,6 +2469,18 @@ extern "C" int pbcg_debug_counters(uint64_t *out16, int32_t reset) {
     return PBCG_OK;
 }
 
+// Per-CTA phase timestamps of a -DPBCG_TIMELINE build (zeros otherwise):
+// out = 3 kinds (K2, SpMV SELL-P, K3) x 256 CTAs x 8 uint64 (globaltimer ns).
+extern "C" int pbcg_timeline(uint64_t *out, int32_t reset) {
+    if (!out) return fail(PBCG_EINVAL, "null");
+    CUDA_TRY(cudaMemcpyFromSymbol(out, g_tl, sizeof(unsigned long long) * 3 * 256 * 8));
+    if (reset) {
+        std::vector<unsigned long long> z(3 * 256 * 8, 0ull);
+        CUDA_TRY(cudaMemcpyToSymbol(g_tl, z.data(), sizeof(unsigned long long) * z.size()));
+    }
+    return PBCG_OK;
+}
+
 // kernel tuning knobs for benchmarks (not part of the numerical contract)
 extern "C" int pbcg_set_chunk(int32_t iters) {
     if (iters < 1) return fail(PBCG_EINVAL, "chunk < 1");

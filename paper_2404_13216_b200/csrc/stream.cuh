@@ -139,6 +139,36 @@ __device__ __forceinline__ size_t stream_smem_bytes() {
     return sizeof(double) * (size_t)STAGES * NV * T + 2 * STAGES * sizeof(uint64_t);
 }
 
+// End of a dot-split stream kernel (exact dots): every consumer warp drains
+// its two accumulators into its own words of the drained ring (plain adds,
+// warp_deposit_priv), then the CTA adds the warps' words into S.w -- the
+// shared-atomic storm of all warps depositing into the same few words of S.w
+// (measured: 6-8 us per launch on C3) is gone.  dot(g, k): the dot of
+// accumulator k of dot group g, or -1.  All threads.
+template <int ND, int NCW, int W, class Acc, class Dot>
+__device__ __forceinline__ void drain_private(CtaSacc<ND> &S, Acc &d0, Acc &d1, long long *ring, Dot dot) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();  // every consumer is done with the ring
+    long long *pw = ring + (size_t)warp * 2 * SACC_L;
+    if (warp < NCW) {
+        for (int i = lane; i < 2 * SACC_L; i += 32) pw[i] = 0;
+        __syncwarp();
+        d0.warp_merge_priv(pw);
+        d1.warp_merge_priv(pw + SACC_L);
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 2 * 2 * SACC_L; idx += blockDim.x) {  // (group, accumulator, word)
+        const int g = idx / (2 * SACC_L), k = (idx / SACC_L) & 1, i = idx % SACC_L;
+        const int d = dot(g, k);
+        if (d < 0) continue;
+        long long t = 0;
+#pragma unroll 4
+        for (int wg = 0; wg < W; ++wg) t += ring[((size_t)(g * W + wg) * 2 + k) * SACC_L + i];
+        if (t) S.w[d][i] += (unsigned long long)t;
+    }
+    __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
 // K2 (Alg. 2 l.70-74) + phase-A dots.  The consumer warps form two dot
 // groups of W warps that see the same tiles: group 0 owns (q,y), (y,y) and
@@ -197,6 +227,14 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
     __shared__ CtaSacc<4> S;
     Scalars *sc = a.sc;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    PBCG_TL(0, 0);
+#ifdef PBCG_TIMELINE
+    if (threadIdx.x == 0 && blockIdx.x < 256) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_tl[0][blockIdx.x][7] = smid;
+    }
+#endif
     cta_sacc_zero<4>(S);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NCW); }
@@ -221,6 +259,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
     }
     if (!run) return;  // the whole CTA: done is the same value for every thread
     PBCG_TS(0);
+    PBCG_TL(0, 1);
     const bool first = (sc->it == 0);
     const int64_t n = a.n;
     unsigned flags = 0;
@@ -243,6 +282,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
         uint32_t ph = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             mbar_wait(&full[st], ph);
+            if (tile == blockIdx.x) PBCG_TL(0, 2);
             const int64_t r0 = tile * T;
             const int rows = (int)min((int64_t)T, n - r0);
             const int rows_even = rows & ~1;
@@ -314,10 +354,19 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
         }
     }
     PBCG_TS(1);
+    PBCG_TL(0, 3);
     __syncwarp();
-    R.d0.warp_merge(s0);
-    R.d1.warp_merge(s1);
+#ifndef PBCG_OLD_DRAIN
+    if constexpr (EXACT) {  // dots 2g, 2g+1 of group g
+        drain_private<4, NCW, W>(S, R.d0, R.d1, (long long *)buf, [](int g, int k) { return 2 * g + k; });
+    } else
+#endif
+    {
+        R.d0.warp_merge(s0);
+        R.d1.warp_merge(s1);
+    }
     PBCG_TS(2);
+    PBCG_TL(0, 4);
     if constexpr (EXACT) {
         if (sc->range_mode == 0) {  // full range (R-24): a flagged CTA corrects its products
             if (flags) atomicOr(&S.flags, flags);
@@ -339,6 +388,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
         }
         const bool last = cta_sacc_publish<4>(S, flags, a.gacc, a.ticket);
         PBCG_TS(3);
+        PBCG_TL(0, 5);
         if (last) {
             last_cta_finish<4>(S, a.gacc, a.ticket, PH_A, a.finalize, sc, a.hist, nullptr, nullptr);
             PBCG_TS(4);
@@ -386,6 +436,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
     __shared__ CtaSacc<3> S;
     Scalars *sc = a.sc;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    PBCG_TL(2, 0);
     cta_sacc_zero<3>(S);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NCW); }
@@ -408,6 +459,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
         run = !sc->done;
     }
     if (!run) return;
+    PBCG_TL(2, 1);
     const int64_t n = a.n;
     unsigned flags = 0;
     K3Op<Acc> R;
@@ -430,6 +482,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
         uint32_t ph = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             mbar_wait(&full[st], ph);
+            if (tile == blockIdx.x) PBCG_TL(2, 2);
             const int64_t r0 = tile * T;
             const int rows = (int)min((int64_t)T, n - r0);
             const int rows_even = rows & ~1;
@@ -497,9 +550,19 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
             if (++st == STAGES) { st = 0; ph ^= 1u; }
         }
     }
+    PBCG_TL(2, 3);
     __syncwarp();
-    R.d0.warp_merge(s0);
-    R.d1.warp_merge(s1);
+#ifndef PBCG_OLD_DRAIN
+    if constexpr (EXACT) {  // group 0: (r0,r') -> 0, (r',r') -> 2; group 1: (r0,w') -> 1
+        drain_private<3, NCW, W>(S, R.d0, R.d1, (long long *)buf,
+                                 [](int g, int k) { return g == 0 ? (k == 0 ? 0 : 2) : (k == 0 ? 1 : -1); });
+    } else
+#endif
+    {
+        R.d0.warp_merge(s0);
+        R.d1.warp_merge(s1);
+    }
+    PBCG_TL(2, 4);
     if constexpr (EXACT) {
         if (sc->range_mode == 0) {  // full range (R-24): a flagged CTA corrects its products
             if (flags) atomicOr(&S.flags, flags);
@@ -519,8 +582,9 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
                         y = d == 1 ? a.w[i] : ri;
                     });
         }
-        if (cta_sacc_publish<3>(S, flags, a.gacc, a.ticket))
-            last_cta_finish<3>(S, a.gacc, a.ticket, PH_B, a.finalize, sc, a.hist, nullptr, nullptr);
+        const bool last = cta_sacc_publish<3>(S, flags, a.gacc, a.ticket);
+        PBCG_TL(2, 5);
+        if (last) last_cta_finish<3>(S, a.gacc, a.ticket, PH_B, a.finalize, sc, a.hist, nullptr, nullptr);
     } else {
         plain_publish<3, W>(S, a.part);
     }
@@ -795,6 +859,7 @@ __global__ void __launch_bounds__((SPS / RPW + 1) * 32, 1)
     uint64_t *full = (uint64_t *)(smem_raw + (size_t)STAGES * STAGE);
     uint64_t *empty = full + STAGES;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    PBCG_TL(1, 0);
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
@@ -813,6 +878,7 @@ __global__ void __launch_bounds__((SPS / RPW + 1) * 32, 1)
     }
     pdl_sync();
     if (sc && sc->done) return;
+    PBCG_TL(1, 1);
     // gathers of a chunk's RPW slices of this warp (stage st)
     auto issue = [&](int64_t c, int st, int (&len)[RPW], double (&xv)[RPW][8]) {
         const unsigned char *sb = smem_raw + (size_t)st * STAGE;
@@ -874,6 +940,7 @@ __global__ void __launch_bounds__((SPS / RPW + 1) * 32, 1)
     double xv[RPW][8];
     for (int64_t c = cbeg + blockIdx.x; c < nchunks; c += gridDim.x) {
         mbar_wait(&full[st], ph);
+        if (c == cbeg + blockIdx.x) PBCG_TL(1, 2);
         issue(c, st, len, xv);
         fold(c, st, len, xv);
         if (++st == STAGES) {
@@ -881,6 +948,7 @@ __global__ void __launch_bounds__((SPS / RPW + 1) * 32, 1)
             ph ^= 1u;
         }
     }
+    PBCG_TL(1, 3);
 }
 
 // ---------------------------------------------------------------------------
