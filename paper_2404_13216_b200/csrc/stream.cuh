@@ -83,6 +83,14 @@ __device__ __forceinline__ void produce(const double *const *src, int nv_act, in
     }
 }
 
+// Ring stages issued before the PDL gate (K2 / K3).  Issuing all of them
+// makes the first tile wait for the whole burst (no priority among bulk
+// copies); fewer stages let the first tiles land sooner after the gate.
+#ifndef PBCG_PREGATE
+#define PBCG_PREGATE 1  // C3: 7,404 (all 5) -> 7,582 iter/s (1), C5 1,111 -> 1,116 (tools/ab_iter.py)
+#endif
+#define PBCG_PREGATE_STAGES(S) ((PBCG_PREGATE) < (S) ? (PBCG_PREGATE) : (S))
+
 // The same, for a kernel launched with PDL: the first STAGES tiles of every
 // vector except `late` (the one the immediately preceding kernel writes) are
 // issued before `gate` (which waits on that kernel and returns false to
@@ -117,7 +125,7 @@ __device__ __forceinline__ bool produce_gated(const double *const *src, int nv_a
         return ok;
     };
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        if (!gated && issued == STAGES && !open_gate()) return false;
+        if (!gated && issued == PBCG_PREGATE_STAGES(STAGES) && !open_gate()) return false;
         mbar_wait(&empty[s], ph ^ 1u);
         const int64_t r0 = tile * T;
         const uint32_t bytes = tile_bytes(tile);
@@ -149,6 +157,7 @@ template <int ND, int NCW, int W, class Acc, class Dot>
 __device__ __forceinline__ void drain_private(CtaSacc<ND> &S, Acc &d0, Acc &d1, long long *ring, Dot dot) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     __syncthreads();  // every consumer is done with the ring
+    PBCG_TL(ND == 4 ? 0 : 2, 6);
     long long *pw = ring + (size_t)warp * 2 * SACC_L;
     if (warp < NCW) {
         for (int i = lane; i < 2 * SACC_L; i += 32) pw[i] = 0;

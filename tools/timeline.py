@@ -1,8 +1,9 @@
 """Per-CTA phase timeline of one iteration (PBCG_TIMELINE build):
 PBCG_LIB=paper_2404_13216_b200/libpbicgstab_tl.so python tools/timeline.py [workload]
 Phases: K2/K3 0 entry, 1 after the PDL wait, 2 first tile landed, 3 tiles
-done, 4 FPEs drained, 5 published; SpMV 0 entry, 1 after the wait, 2 first
-chunk landed, 3 done.  Times in us relative to the earliest K2 entry:
+done (warp 0), 4 FPEs drained, 5 published, 6 every warp done with its tiles; SpMV 0 entry, 1 after the wait, 2 first
+chunk landed, 3 done.  Times in us relative to the earliest release of K2's PDL wait
+(chained graphs: python tools/timeline.py c3_3d128 10, the last iteration):
 min / median / max over CTAs."""
 import sys, os, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -12,19 +13,20 @@ L.pbcg_timeline.argtypes = [ctypes.c_void_p, ctypes.c_int32]
 A = gen.make_config(sys.argv[1] if len(sys.argv) > 1 else "c3_3d128")
 S = pb.Solver(A.row_ptr, A.col, A.val, A.n, history_capacity=16)
 b = torch.from_numpy(A.b).cuda() if A.rhs == "given" else S.spmv(torch.ones(A.n, dtype=torch.float64, device="cuda"))
-S.start(b, tol=0.0, max_iter=200, poll_every=1)
-S.iterate(20)
+CH = int(sys.argv[2]) if len(sys.argv) > 2 else 1  # iterations per graph: the stamps are the last one's
+S.start(b, tol=0.0, max_iter=400, poll_every=CH)
+S.iterate(20 * CH)
 torch.cuda.synchronize()
 buf = np.zeros((3, 256, 8), np.uint64)
 for rep in range(3):
     L.pbcg_timeline(buf.ctypes.data, 1)
-    S.iterate(1)
+    S.iterate(CH)
     torch.cuda.synchronize()
     L.pbcg_timeline(buf.ctypes.data, 1)
     t = buf.astype(np.int64)
-    t0 = t[0, :, 0][t[0, :, 0] > 0].min()
+    t0 = t[0, :, 1][t[0, :, 1] > 0].min()  # K2's PDL wait released
     print(f"--- iteration {rep}")
-    for kind, nm, nph in ((0, "K2", 6), (1, "SpMV", 4), (2, "K3", 6)):
+    for kind, nm, nph in ((0, "K2", 7), (1, "SpMV", 4), (2, "K3", 7)):
         for k in range(nph):
             v = t[kind, :, k]
             v = v[v > 0]
