@@ -562,10 +562,11 @@ struct ExAccT {
         drain_fpe<NC>(CP, sacc);
         drain_fpe<NC>(CE, sacc);
     }
-    // the same into this warp's private words (warp_deposit_priv).  (Cascading
-    // the lane's terms into a fresh 3-term expansion first, to make 3
-    // deposits instead of NH + NHE + 2 NC, ran slower: C3 7,238 vs 7,583
-    // iter/s -- the cascade is one long dependent chain.)
+    // the same into this warp's private words (warp_deposit_priv).  Measured
+    // and rejected: cascading the lane's terms into a fresh 3-term expansion
+    // first (3 deposits instead of NH + NHE + 2 NC: C3 7,238 vs 7,583 iter/s,
+    // one long dependent chain), and batching 2-4 deposits so their REDUX
+    // chains interleave (C3 7,218-7,381 vs 7,585).
     __device__ __forceinline__ void warp_merge_priv(long long *w) {
 #pragma unroll
         for (int j = 0; j < NH; ++j) warp_deposit_priv(P.a[j], w);
