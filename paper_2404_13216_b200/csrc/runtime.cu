@@ -33,6 +33,7 @@
 #include "../../include/pbicgstab.h"
 #include "kernels.cuh"
 #include "small.cuh"
+#include "cluster.cuh"
 #include "stream.cuh"
 
 using namespace pbcg;
@@ -2049,6 +2050,61 @@ static bool small_on(const pbcg_handle *h) {
     const char *e = getenv("PBCG_SMALL");
     return !(e && e[0] == '0') && h->small_grid > 0 && h->method == PBCG_METHOD_PBICGSTAB && h->rr_period == 0;
 }
+// The cluster kernel (cluster.cuh): systems of at most CL x 256 rows that the
+// register-resident fused kernel takes (rows not permuted, <= 8 nonzeros per
+// row), as ONE cluster of CL = 16 CTAs (non-portable; 8 if 16 cannot be
+// scheduled).  0: not available.  PBCG_CLUSTER=0 turns it off (A/B runs).
+static constexpr int CLUSTER_BS = 256;
+static int cluster_size_for(pbcg_handle *h) {
+    const char *e = getenv("PBCG_CLUSTER");
+    if (e && e[0] == '0') return 0;
+    if (h->R.empty()) return 0;
+    const Rank &R = h->R[0];
+    if (!R.h_perm.empty() || R.max_len > 8 || R.n == 0) return 0;
+    static int cached = -1;
+    if (cached < 0) {
+        cached = 0;
+        for (int cl : {16, 8}) {
+            const void *k = (const void *)pbcg_cluster_kernel<CLUSTER_BS, true>;
+            const int dsm = (int)ClusterSmem<CLUSTER_BS>::BYTES;
+            if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm) != cudaSuccess ||
+                cudaFuncSetAttribute((const void *)pbcg_cluster_kernel<CLUSTER_BS, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, dsm) != cudaSuccess) {
+                cudaGetLastError();
+                break;
+            }
+            if (cl > 8) {
+                if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+                    cudaFuncSetAttribute((const void *)pbcg_cluster_kernel<CLUSTER_BS, false>,
+                                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+                    cudaGetLastError();
+                    continue;
+                }
+            }
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(cl);
+            cfg.blockDim = dim3(CLUSTER_BS);
+            cfg.dynamicSmemBytes = ClusterSmem<CLUSTER_BS>::BYTES;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cl;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int nclu = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclu, k, &cfg) == cudaSuccess && nclu >= 1) {
+                cached = cl;
+                break;
+            }
+            cudaGetLastError();
+        }
+    }
+    if (cached == 0) return 0;
+    const int64_t nw = (R.n + 31) / 32;
+    return 32 * ((nw + cached - 1) / cached) <= CLUSTER_BS ? cached : 0;
+}
+
 static int launch_small(pbcg_handle *h, int32_t iters) {
     Rank &R = h->R[0];
     SmallArgs a{};
@@ -2069,6 +2125,23 @@ static int launch_small(pbcg_handle *h, int32_t iters) {
     a.hist = R.hist;
     a.iters = iters;
     void *args[] = {&a};
+    if (const int cl = cluster_size_for(h)) {  // one thread-block cluster (cluster.cuh)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(cl);
+        cfg.blockDim = dim3(CLUSTER_BS);
+        cfg.dynamicSmemBytes = ClusterSmem<CLUSTER_BS>::BYTES;
+        cfg.stream = h->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (h->dot_mode == PBCG_DOT_PLAIN) CUDA_TRY(cudaLaunchKernelEx(&cfg, pbcg_cluster_kernel<CLUSTER_BS, false>, a));
+        else CUDA_TRY(cudaLaunchKernelEx(&cfg, pbcg_cluster_kernel<CLUSTER_BS, true>, a));
+        return PBCG_OK;
+    }
     // register-resident rows (small.cuh) when rows are not permuted, every CTA
     // holds at most SMALL_BS rows and no row more than 8 nonzeros (C1)
     const int64_t nw = (R.n + 31) / 32;

@@ -782,3 +782,40 @@ def test_pipelined_block_jacobi_full_size_and_rejects(pb):
         S.solve(b, method="bicgstab")
     assert e.value.rc == 1
     S.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "2d45", "3d15"])
+def test_cluster_kernel_same_bits(pb, name, monkeypatch):
+    # the one-cluster kernel (csrc/cluster.cuh: 16 CTAs, z/w over DSMEM,
+    # barrier.cluster, dot words summed in CTA 0's shared memory) against the
+    # register-resident fused kernel (PBCG_CLUSTER=0) and the oracle: same
+    # bits, resumed across launches; plain dots deterministic and converging
+    A = {"c1": lambda: gen.make_config("c1_2d64"), "2d45": lambda: gen.stencil(2, 45, 10.0),
+         "3d15": lambda: gen.stencil(3, 15, 100.0)}[name]()
+    got = {}
+    for cl in ("1", "0"):
+        monkeypatch.setenv("PBCG_CLUSTER", cl)
+        S = solver(pb, A, history_capacity=601)
+        b = gpu_b(pb, S, A)
+        S.start(b, tol=1e-10, max_iter=600)
+        assert S.exec_mode() == 1
+        for k in (1, 3, 7, 600):
+            S.iterate(k)
+        x = torch_zeros(A.n)
+        r = S.finish(x)
+        got[cl] = (u64(x.cpu().numpy()), u64(S.history()), r.iterations, r.status)
+        xp, rp = S.solve(b, tol=1e-10, max_iter=600, dot_mode="plain")
+        xp2, rp2 = S.solve(b, tol=1e-10, max_iter=600, dot_mode="plain")
+        assert rp.status == pb.CONVERGED and rp.iterations == rp2.iterations
+        assert np.array_equal(u64(xp.cpu().numpy()), u64(xp2.cpu().numpy()))
+        S.close()
+    assert got["1"][2:] == got["0"][2:]
+    assert np.array_equal(got["1"][0], got["0"][0]) and np.array_equal(got["1"][1], got["0"][1])
+    O = oracle.PBiCGStab(A, tol=1e-10, max_iter=600)
+    O.run()
+    assert np.array_equal(got["1"][1], u64(O.history())) and np.array_equal(got["1"][0], u64(O.vec("x")))
+
+
+def torch_zeros(n):
+    import torch
+    return torch.zeros(n, dtype=torch.float64, device="cuda")
