@@ -308,12 +308,20 @@ static constexpr int PS_SMEM_MAX = 227 * 1024;
 #ifndef PBCG_PV_NCW_G
 #define PBCG_PV_NCW_G 30
 #endif
+#ifndef PBCG_PV_UNR_G
+#define PBCG_PV_UNR_G 3  // C4 SpMV (prefetched, 30 warps): 2: 280, 3: 251, 4: 264, 8 without prefetch: 299 us
+#endif
+#ifndef PBCG_PV_PF_G
+#define PBCG_PV_PF_G 1
+#endif
 #ifndef PBCG_PV_MIN_WIN_STAGES
 #define PBCG_PV_MIN_WIN_STAGES 6
 #endif
+static constexpr int PV_TMA_MAX_WINDOW = 48 * 1024;  // bytes of x window up to which the matrix rides the ring
 static constexpr int PV_NCW = PBCG_PV_NCW, PV_CAP = PBCG_PV_CAP, PV_UNR = PBCG_PV_UNR,
                      PV_MAXSTAGES = PBCG_PV_MAXSTAGES, PV_MIN_WIN_STAGES = PBCG_PV_MIN_WIN_STAGES,
-                     PV_NCW_G = PBCG_PV_NCW_G;
+                     PV_NCW_G = PBCG_PV_NCW_G, PV_UNR_G = PBCG_PV_UNR_G;
+static constexpr bool PV_PF_G = PBCG_PV_PF_G != 0;
 
 struct Rank {
     int id = 0;
@@ -360,7 +368,7 @@ struct Rank {
     int64_t nchunks = 0, blob_cap = 0, blob_bytes = 0;
     std::vector<int32_t> h_cs;
     int32_t *cxlo = nullptr, *cxhi = nullptr;  // SELL-V: x-buffer index range [lo, hi) of each chunk
-    int ps_xr = 0;                             // SELL-V: x-window ring (doubles, power of two)
+    int ps_xr = 0;                             // SELL-V: x-window ring (doubles, a multiple of 64)
     bool pv_gld = false;                       // SELL-V: matrix loaded from global (only headers in the ring)
     unsigned char *blob = nullptr;
     int64_t *blob_off = nullptr;
@@ -867,10 +875,11 @@ static void spmv_dispatch(pbcg_handle *h, const Rank &R, const double *xpad, dou
     }
     if (R.spmv_kind == SPMV_K_TMAV) {
         if (u1 < 0) u1 = R.nchunks;
-        auto *k = R.pv_gld ? spmv_sellv_kernel<MODE, PV_NCW_G, PV_UNR, true> : spmv_sellv_kernel<MODE, PV_NCW, PV_UNR, false>;
+        auto *k = R.pv_gld ? spmv_sellv_kernel<MODE, PV_NCW_G, PV_UNR_G, true, PV_PF_G>
+                           : spmv_sellv_kernel<MODE, PV_NCW, PV_UNR, false>;
         static bool attr = false;
         if (!attr) {
-            cudaFuncSetAttribute((const void *)spmv_sellv_kernel<MODE, PV_NCW_G, PV_UNR, true>,
+            cudaFuncSetAttribute((const void *)spmv_sellv_kernel<MODE, PV_NCW_G, PV_UNR_G, true, PV_PF_G>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, PS_SMEM_MAX);
             cudaFuncSetAttribute((const void *)spmv_sellv_kernel<MODE, PV_NCW, PV_UNR, false>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, PS_SMEM_MAX);
@@ -1338,8 +1347,14 @@ static int build_sellv(pbcg_handle *h, Rank &R) {
             int64_t span = 0;
             for (int64_t c = 0; c < nch; ++c)
                 if (clo[c] != INT32_MAX) span = std::max<int64_t>(span, H[std::min<int64_t>(c + S - 1, nch - 1)] - clo[c]);
-            int64_t xr = 1024;
-            while (xr < span + 4) xr <<= 1;
+            // any multiple of 64 doubles (the consumers reduce i mod XR with one
+            // compare per gather): C4's +-5000 band needs ~85 KB instead of the
+            // 128 KB of a power of two, which leaves room for 6 ring stages
+            const int64_t xr = std::max<int64_t>(1024, (span + 4 + 63) & ~int64_t(63));
+            // the matrix through the ring (gld = false) only for narrow windows:
+            // C4's +-5000 band (85 KB) ran at 356 us that way with 6 stages,
+            // against 299 us with the consumers loading the matrix (gld)
+            if (!gld && 8 * xr > PV_TMA_MAX_WINDOW) continue;
             if ((int64_t)S * R.ps_stage + 8 * xr + 16 * S + 256 <= PS_SMEM_MAX) {
                 R.ps_stages = S;
                 R.ps_xr = (int)xr;
@@ -1352,7 +1367,8 @@ static int build_sellv(pbcg_handle *h, Rank &R) {
     // (PBCG_SELLV_MODE=tma|gld forces one, for A/B runs)
     const char *em = getenv("PBCG_SELLV_MODE");
     bool ok = false;
-    if (!em || strcmp(em, "gld") != 0) ok = plan(PV_CAP, PV_NCW, false, PV_MIN_WIN_STAGES);
+    for (int64_t cap : {(int64_t)PV_CAP, (int64_t)PV_CAP * 5 / 6, (int64_t)PV_CAP * 2 / 3})
+        if (!ok && (!em || strcmp(em, "gld") != 0)) ok = plan(cap, PV_NCW, false, PV_MIN_WIN_STAGES);
     if (!ok && (!em || strcmp(em, "tma") != 0)) ok = plan(INT64_MAX / 4, PV_NCW_G, true, 2);
     if (!ok) {  // x window wider than shared memory (not banded): one row per thread
         cudaFree(d_tmp);

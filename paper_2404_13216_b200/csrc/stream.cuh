@@ -1067,7 +1067,7 @@ __global__ void sellv_xrange_kernel(int64_t n, int64_t nslices, SellMat A, int32
 // The x window.  A CTA folds a contiguous run of chunks (the rows of a banded
 // matrix advance with it), so the x entries its chunks read form a sliding
 // window: the producer streams x into a ring of XR doubles (XR a power of
-// two; entry i at slot i mod XR) ahead of each chunk -- [loaded, hi'_c),
+// of 64; entry i at slot i mod XR) ahead of each chunk -- [loaded, hi'_c),
 // hi'_c = the running maximum of the chunks' upper x indices -- on the same
 // mbarrier as the chunk.  Setup checks that no chunk in flight can see its
 // entries overwritten (hi'_{c+STAGES-1} - lo_c <= XR - 4) with at least
@@ -1078,7 +1078,7 @@ __global__ void sellv_xrange_kernel(int64_t n, int64_t nslices, SellMat A, int32
 // warps cannot cover the gather latency); with C4's +-5000 band the window
 // takes 128 KB and leaves 4 stages: 340 us vs 308 us row-per-thread, so C4
 // stays on the row-per-thread kernel; a +-1000 band: 233 us vs 285 us.
-template <int MODE, int NCW, int UNR, bool GLD>
+template <int MODE, int NCW, int UNR, bool GLD, bool PF = false>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     spmv_sellv_kernel(int64_t n, const unsigned char *__restrict__ blob, const int64_t *__restrict__ blob_off,
                       const int32_t *__restrict__ clo, const int32_t *__restrict__ chi,
@@ -1091,7 +1091,6 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     uint64_t *empty = full + STAGES;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
-    const int XM = XR - 1;
     // this CTA's contiguous run of chunks
     const int64_t U = cend - cbeg;
     const int64_t c0 = cbeg + U * blockIdx.x / gridDim.x, c1 = cbeg + U * (blockIdx.x + 1) / gridDim.x;
@@ -1114,7 +1113,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
             auto need = [&](int64_t c, int ld) { return max(ld, (__ldg(&chi[c]) + 1) & ~1); };
             auto xcopy = [&](int a, int e, uint64_t *bar) {  // x[a, e) -> ring, split at the wrap
                 while (a < e) {
-                    const int sl = a & XM, m = min(e - a, XR - sl);
+                    const int sl = a % XR, m = min(e - a, XR - sl);
                     bulk_g2s(xw + sl, x + a, (uint32_t)m * 8u, bar);
                     a += m;
                 }
@@ -1180,11 +1179,14 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
             const double *vs = (const double *)((GLD ? blob + __ldg(&blob_off[c]) : sb) + sellv_hdr_bytes(ns));
             const int32_t *xs = (const int32_t *)(vs + nval);
             const int64_t pos = ((int64_t)hd[0] + j) * 32 + lane;
-            const int ipos = (int)pos;
+            const int lo = __ldg(&clo[c]);
+            const int ipos = (int)pos - (lo - lo % XR);  // slot of x entry i: i - base, minus XR once if past the ring
             int off = hd[4 + j];
             double acc = 0.0;
-            for (int k = 0; k < W; k += UNR) {
-                double xv[UNR];
+            // slots k..k+UNR-1: this lane's entry ranks (ballots, no data
+            // dependence), their values and column ids, then the x gathers
+            // from the window and the ordered fma chain (R-6, +0.0 start)
+            auto load = [&](int k, int (&cc)[UNR], double (&vv)[UNR]) {
                 int d[UNR];
 #pragma unroll
                 for (int u = 0; u < UNR; ++u) {  // slot k+u: this lane's rank among the active lanes
@@ -1192,20 +1194,43 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                     d[u] = off + __popc(m & lt);
                     off += __popc(m);
                 }
-                double vv[UNR];
-                int cc[UNR];
 #pragma unroll
                 for (int u = 0; u < UNR; ++u)
                     if (k + u < len) {
                         cc[u] = GLD ? __ldcs(xs + d[u]) : xs[d[u]];
                         vv[u] = GLD ? __ldcs(vs + d[u]) : vs[d[u]];
                     }
+            };
+            auto fold = [&](int k, const int (&cc)[UNR], const double (&vv)[UNR]) {
+                double xv[UNR];
 #pragma unroll
                 for (int u = 0; u < UNR; ++u)
-                    if (k + u < len) xv[u] = xw[(ipos + cc[u]) & XM];
+                    if (k + u < len) {
+                        int sl = ipos + cc[u];
+                        if (sl >= XR) sl -= XR;
+                        xv[u] = xw[sl];
+                    }
 #pragma unroll
                 for (int u = 0; u < UNR; ++u)
-                    if (k + u < len) acc = __fma_rn(vv[u], xv[u], acc);  // ordered chain, +0.0 start (R-6)
+                    if (k + u < len) acc = __fma_rn(vv[u], xv[u], acc);
+            };
+            if constexpr (PF) {  // software pipeline: the next slots' loads are in flight during a fold
+                int ca[UNR], cb[UNR];
+                double va[UNR], vb[UNR];
+                if (W > 0) load(0, ca, va);
+                for (int k = 0; k < W; k += 2 * UNR) {
+                    if (k + UNR < W) load(k + UNR, cb, vb);
+                    fold(k, ca, va);
+                    if (k + 2 * UNR < W) load(k + 2 * UNR, ca, va);
+                    if (k + UNR < W) fold(k + UNR, cb, vb);
+                }
+            } else {
+                for (int k = 0; k < W; k += UNR) {
+                    int cc[UNR];
+                    double vv[UNR];
+                    load(k, cc, vv);
+                    fold(k, cc, vv);
+                }
             }
             if (pos < n) {
                 const int64_t row = perm ? (int64_t)__ldg(&perm[pos]) : pos;
