@@ -15,11 +15,11 @@ for it in (0, 10, 50, 100, 200):
     pb.debug_counters(reset=True)
     ms = S.profile(1)
     c = pb.debug_counters(reset=True)
-    print(f"{name} iter {it}: products {7*A.n} warp-batches ~{A.n//64*5} cold-p warp-products {c[1]} cold-e {c[2]} deposits {c[3]} ({c[3]/(7*A.n):.3%})  ms K2 {ms[0]:.3f} K3 {ms[2]:.3f}")
+    print(f"{name} iter {it}: products {7*A.n} c1 {c[1]} ({32*c[1]/(7*A.n):.3%} x32) c2 {c[2]} deposits {c[3]} ({c[3]/(7*A.n):.3%})  ms K2 {ms[0]:.3f} K3 {ms[2]:.3f}")
 if len(sys.argv) > 2:
     n = 1 << 24
     for kind, (x, y) in (("well", (gen.uniform(n, 1), gen.uniform(n, 2))), ("ill", gen.ill_pair(n, seed=3))):
         pb.debug_counters(reset=True)
         pb.exdot(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
         c = pb.debug_counters(reset=True)
-        print(f"exdot {kind}: n {n} lane-overflows {c[2]} ({c[2]/n:.3%}) deposits {c[3]} ({c[3]/n:.3%})")
+        print(f"exdot {kind}: n {n} c1 {c[1]} ({32*c[1]/n:.3%} x32) c2 {c[2]} deposits {c[3]} ({c[3]/n:.3%})")
