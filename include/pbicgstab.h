@@ -140,7 +140,12 @@ typedef struct {
                                  R-21).  0 (default) = never. */
     int32_t x0_zero;          /* 1: start from x0 = 0 without reading x0 (x0 may be NULL in pbicgstab_start;
                                  in pbicgstab_solve x is then the output buffer only): no host->device copy
-                                 of the initial guess.  0 (default): x0 is read. */
+                                 of the initial guess, and no residual SpMV -- r0 = b - A 0 = b bit for bit
+                                 (A is finite), so r0 and r^ are copies of b; a host b of >= 2^20 rows on
+                                 one rank is copied in 16 chunks, the init work of each chunk (copies,
+                                 w0 = A r0, t0 = A w0, its share of the init dots) overlapping the copy.  With NCCL ranks it
+                                 must agree on every rank (it decides whether start exchanges an x halo).
+                                 0 (default): x0 is read. */
     int32_t range_mode;       /* PBCG_RANGE_FULL (0, default): every Algorithm 2 dot is exact over the whole
                                  binary64 range (R-24):
                                  a CTA whose products leave the fast zone (|fl(xy)| < 2^-960 or >= 2^1000)

@@ -24,8 +24,11 @@ enum { H_THETA = 0, H_ETA, H_SIGMA, H_ZETA, H_OMEGA, H_RHO, H_DELTA, H_RR, H_REL
 enum { ST_CONVERGED = 0, ST_MAXITER = 1, ST_BD_INIT = 2, ST_BD_RHO = 3, ST_BD_OMEGA = 4, ST_BD_ALPHA = 5,
        ST_RANGE = 6, ST_RUNNING = -1 };
 enum Phase { PH_INIT = 0, PH_A = 1, PH_B = 2, PH_TRUE = 3, PH_EXDOT = 4,
+             // I2-I4 when x0 = 0, so r0 = r^ = b bit for bit: two dots, (w0,b) = (r^,w0) and (b,b) =
+             // (b,b) = (r^,r0) = (r0,r0)
+             PH_INIT0 = 5,
              // Algorithm 1 (classic BiCGStab, reading R-20)
-             PH1_INIT = 5, PH1_DEN = 6, PH1_QQ = 7, PH1_OM = 8, PH1_R = 9 };
+             PH1_INIT = 6, PH1_DEN = 7, PH1_QQ = 8, PH1_OM = 9, PH1_R = 10 };
 
 // device-resident solver scalars (one copy per rank; identical on all ranks)
 struct Scalars {
@@ -128,8 +131,9 @@ __device__ void phase_finalize(int phase, Scalars *sc, const double *d, unsigned
         sc->relres_true = __ddiv_rn(__dsqrt_rn(d[0]), sc->nb);
         return;
     }
-    if (phase == PH_INIT) {  // lines I2-I4
-        const double bb = d[0], rho = d[1], delta = d[2], rr = d[3];
+    if (phase == PH_INIT || phase == PH_INIT0) {  // lines I2-I4
+        const double bb = phase == PH_INIT ? d[0] : d[1], rho = phase == PH_INIT ? d[1] : d[1],
+                     delta = phase == PH_INIT ? d[2] : d[0], rr = phase == PH_INIT ? d[3] : d[1];
         sc->it = 0;
         sc->nb = __dsqrt_rn(bb);
         if (sc->nb == 0.0) { sc->err = 1; sc->done = 1; sc->status = ST_MAXITER; return; }  // EINVAL
@@ -1191,6 +1195,23 @@ __global__ void sell_halo_flags_kernel(int64_t n, int64_t nslices, const int64_t
         }
         const unsigned any = __ballot_sync(0xFFFFFFFFu, out);
         if (lane == 0) flag[sl] = any ? 1 : 0;
+    }
+}
+
+// per slice: the largest x-buffer index its rows read (-1: no nonzero)
+__global__ void sell_xmax_kernel(int64_t n, int64_t nslices, const int64_t *slice_off, const int32_t *row_len,
+                                 const int32_t *scol, int64_t *xmax) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < nslices; sl += nw) {
+        const int64_t pos = sl * 32 + lane;
+        const int len = pos < n ? row_len[pos] : 0;
+        const int64_t so = slice_off[sl];
+        long long m = -1;
+        for (int k = 0; k < len; ++k) m = max(m, (long long)(pos + scol[so + 32 * k + lane]));
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+        if (lane == 0) xmax[sl] = m;
     }
 }
 

@@ -378,6 +378,10 @@ struct Rank {
     // the SELL-P kernel, slices otherwise) read no halo entry
     bool split = false;
     int64_t in_lo = 0, in_hi = 0;
+    // chunked start (x0 = 0, host b, one rank; plan_start): row boundaries
+    // st_row[0..NCH] of the chunks and the SpMV units st_u[0..NCH] covering
+    // them; chunk k's rows read x rows of chunks <= k + 1 only
+    std::vector<int64_t> st_row, st_u;
     SellMat mat(int64_t p0 = 0, int64_t p1 = -1) const {
         return SellMat{n, slice_off, row_len, sval, scol, h_perm.empty() ? nullptr : perm,
                        use_slots ? slot_rec : nullptr, p0, p1 < 0 ? n : std::min<int64_t>(p1, n)};
@@ -414,6 +418,7 @@ struct pbcg_handle {
     int chunk = 16;                 // iterations per graph chunk (pbcg_opts.poll_every of the last start)
     cudaEvent_t ev[8] = {};
     cudaEvent_t evh[4] = {};  // halo-overlap fork/join (multi-rank)
+    cudaEvent_t evc[16] = {};  // start: chunks of the host copy of b landed (START_NCH)
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     bool started = false;
     int max_iter = 0;
@@ -1531,6 +1536,55 @@ static int plan_split(pbcg_handle *h) {
     return PBCG_OK;
 }
 
+// Chunked start (pbicgstab_start with x0 = 0 and a host b): the copy of b
+// streams in START_NCH chunks and the init work of each chunk -- the scans
+// and copies, w0 = A r0 and t0 = A w0 over its rows, its share of the two
+// init dots -- runs as soon as the chunks it reads have landed (a pipeline
+// lagging one and two chunks).  Planned here: chunk boundaries on SpMV unit
+// boundaries that are also 256-row window boundaries (so a chunk's
+// positions are its rows), and the largest row each chunk's rows read,
+// which must lie in the next chunk at most.  One rank, SELL-P or the slice
+// kernels; otherwise start copies b whole.
+static constexpr int START_NCH = 16;
+static int plan_start(pbcg_handle *h) {
+    if (h->R.size() != 1 || h->comm) return PBCG_OK;
+    Rank &R = h->R[0];
+    R.st_row.clear();
+    R.st_u.clear();
+    if (R.n < (1 << 20) || R.pipe || R.spmv_kind == SPMV_K_TMAV) return PBCG_OK;
+    int64_t *d_x = nullptr;
+    CUDA_TRY(cudaMalloc(&d_x, sizeof(int64_t) * (size_t)R.nslices));
+    const int g = (int)std::min<int64_t>((R.nslices + 7) / 8, 65535);
+    sell_xmax_kernel<<<g, 256, 0, h->stream>>>(R.n, R.nslices, R.slice_off, R.row_len, R.scol, d_x);
+    std::vector<int64_t> xm(R.nslices);
+    cudaError_t ce = cudaGetLastError();
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(xm.data(), d_x, sizeof(int64_t) * R.nslices, cudaMemcpyDeviceToHost, h->stream);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(h->stream);
+    cudaFree(d_x);
+    if (ce != cudaSuccess) return fail(PBCG_ECUDA, "plan_start: %s", cudaGetErrorString(ce));
+    const bool tma = R.spmv_kind == SPMV_K_TMA;
+    const int64_t su = tma ? PS_SPS : 1;                 // slices per unit
+    const int64_t ustep = tma ? 4 : 8;                  // units per 256-row-aligned step (3,840 / 256 rows)
+    const int64_t units = tma ? R.nchunks : R.nslices;
+    std::vector<int64_t> ub(START_NCH + 1), rb(START_NCH + 1);
+    for (int k = 0; k <= START_NCH; ++k) {
+        int64_t u = (units * k / START_NCH) / ustep * ustep;
+        if (k == START_NCH) u = units;
+        ub[k] = u;
+        rb[k] = std::min<int64_t>(R.n, u * su * 32);
+    }
+    for (int k = 0; k < START_NCH; ++k) {
+        if (rb[k + 1] <= rb[k]) return PBCG_OK;  // too few units for the chunks
+        int64_t mx = -1;
+        for (int64_t sl = ub[k] * su; sl < std::min<int64_t>(ub[k + 1] * su, R.nslices); ++sl) mx = std::max(mx, xm[sl]);
+        const int64_t row = mx - R.own_off;  // x-buffer index -> row (one rank: no halo)
+        if (k + 2 <= START_NCH && row >= rb[k + 2]) return PBCG_OK;  // reads beyond the next chunk
+    }
+    R.st_row = rb;
+    R.st_u = ub;
+    return PBCG_OK;
+}
+
 extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void *stream, void *workspace,
                                size_t workspace_bytes, pbcg_handle **out) {
     NvtxRange nvtx_("pbcg.setup");
@@ -1694,6 +1748,7 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
             }
         }
         if (multi(h)) RC_TRY(plan_split(h));
+        RC_TRY(plan_start(h));
     }
     RC_TRY(stream_attrs());
     h->grid_md = grid_for((const void *)multidot_kernel<4, K_NP, K_NE, K_BS, U_MD4>, K_BS, h->nsm);
@@ -1702,6 +1757,7 @@ extern "C" int pbicgstab_setup(const pbcg_csr_local *A, const pbcg_dist *d, void
     CUDA_TRY(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
     for (auto &e : h->ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto &e : h->evh) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto &e : h->evc) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreate(&h->t0));
     CUDA_TRY(cudaEventCreate(&h->t1));
     CUDA_TRY(cudaMallocHost(&h->h_sc, sizeof(Scalars)));
@@ -1720,6 +1776,8 @@ extern "C" void pbicgstab_destroy(pbcg_handle *h) {
     for (auto &e : h->ev)
         if (e) cudaEventDestroy(e);
     for (auto &e : h->evh)
+        if (e) cudaEventDestroy(e);
+    for (auto &e : h->evc)
         if (e) cudaEventDestroy(e);
     if (h->t0) cudaEventDestroy(h->t0);
     if (h->t1) cudaEventDestroy(h->t1);
@@ -1809,7 +1867,8 @@ static void opts_defaults(const pbcg_opts *o, pbcg_opts &e) {
 static int capture_chunk(pbcg_handle *h, int iters, int slot);
 static bool small_on(const pbcg_handle *h);
 static int start_alg1(pbcg_handle *h);
-static int start_alg2_rest(pbcg_handle *h);
+static int start_alg2_rest(pbcg_handle *h, bool r_is_b);
+static int start_chunked(pbcg_handle *h, const double *b);
 static int g_default_chunk = 16;
 
 extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0, const pbcg_opts *o) {
@@ -1850,10 +1909,50 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
         CUDA_TRY(cudaMemsetAsync(R.hist, 0, sizeof(double) * (size_t)h->hist_cap * H_COLS, h->stream));
         CUDA_TRY(cudaMemsetAsync(R.bad, 0, sizeof(int) * 4, h->stream));
     }
-    RC_TRY(scatter_in(h, b, &Rank::b, is_host_ptr(b)));
-    if (op.x0_zero) {
+    // x0 = 0 (x0_zero): r0 = b - A 0 is b bit for bit -- every row's fma
+    // chain over +0 (or, after y0 = M x0, +-0) inputs is +0 since A is finite
+    // (setup checks), and b - (+0) = b -- so the residual SpMV is skipped and
+    // r, r^ are copies of b (I1).  A host b then streams in
+    // chunks on the side stream, each chunk's NaN/Inf scan and copies on the
+    // main stream behind it (the copy overlaps that work).
+    const bool zero_start = op.x0_zero != 0;
+    const bool chunked = zero_start && op.method == PBCG_METHOD_PBICGSTAB && is_host_ptr(b) && h->R.size() == 1 &&
+                         !h->R[0].st_row.empty();
+    if (chunked) {
+        for (auto &R : h->R) CUDA_TRY(cudaMemsetAsync(R.x, 0, sizeof(double) * R.n, h->stream));
+    } else if (zero_start) {
+        const bool hostb = is_host_ptr(b);
+        for (auto &R : h->R) {
+            if (R.n == 0) continue;
+            const int64_t off = h->V > 1 ? R.rb : 0;
+            const int nch = (hostb && h->R.size() == 1 && R.n >= (1 << 20)) ? 8 : 1;
+            const int64_t step = ((R.n + nch - 1) / nch + 63) / 64 * 64;
+            if (nch > 1) {  // the side stream starts after everything enqueued so far
+                CUDA_TRY(cudaEventRecord(h->ev[4], h->stream));
+                CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev[4], 0));
+            }
+            for (int k = 0; k < nch; ++k) {
+                const int64_t c0 = std::min<int64_t>(R.n, k * step), c1 = std::min<int64_t>(R.n, c0 + step);
+                if (c1 <= c0) break;
+                const size_t by = sizeof(double) * (size_t)(c1 - c0);
+                if (nch > 1) {
+                    CUDA_TRY(cudaMemcpyAsync(R.b + c0, b + off + c0, by, cudaMemcpyHostToDevice, h->side));
+                    CUDA_TRY(cudaEventRecord(h->evc[k], h->side));
+                    CUDA_TRY(cudaStreamWaitEvent(h->stream, h->evc[k], 0));
+                } else {
+                    CUDA_TRY(cudaMemcpyAsync(R.b + c0, b + off + c0, by,
+                                             hostb ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, h->stream));
+                }
+                nonfinite_scan_kernel<<<(int)std::min<int64_t>((c1 - c0 + 255) / 256, 4096), 256, 0, h->stream>>>(
+                    c1 - c0, R.b + c0, R.bad);
+                CUDA_TRY(cudaGetLastError());
+                CUDA_TRY(cudaMemcpyAsync(R.r + c0, R.b + c0, by, cudaMemcpyDeviceToDevice, h->stream));
+                CUDA_TRY(cudaMemcpyAsync(R.rh + c0, R.b + c0, by, cudaMemcpyDeviceToDevice, h->stream));
+            }
+        }
         for (auto &R : h->R) CUDA_TRY(cudaMemsetAsync(R.x, 0, sizeof(double) * R.n, h->stream));
     } else {
+        RC_TRY(scatter_in(h, b, &Rank::b, is_host_ptr(b)));
         RC_TRY(scatter_in(h, x0, &Rank::x, is_host_ptr(x0)));
     }
     if (h->precond == PBCG_PRECOND_BJACOBI2 || h->precond == PBCG_PRECOND_BJACOBI2_PIPE)  // y0 := M x0 (R-23, R-25)
@@ -1870,19 +1969,22 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
                     R.n, R.x, R.dg, R.x, 0);
                 CUDA_TRY(cudaGetLastError());
             }
-    for (auto &R : h->R) {
-        if (R.n == 0) continue;
-        const int grid = (int)std::min<int64_t>((R.n + 255) / 256, 4096);
-        nonfinite_scan_kernel<<<grid, 256, 0, h->stream>>>(R.n, R.b, R.bad);
-        nonfinite_scan_kernel<<<grid, 256, 0, h->stream>>>(R.n, R.x, R.bad);
-        CUDA_TRY(cudaGetLastError());
+    if (!zero_start) {
+        for (auto &R : h->R) {
+            if (R.n == 0) continue;
+            const int grid = (int)std::min<int64_t>((R.n + 255) / 256, 4096);
+            nonfinite_scan_kernel<<<grid, 256, 0, h->stream>>>(R.n, R.b, R.bad);
+            nonfinite_scan_kernel<<<grid, 256, 0, h->stream>>>(R.n, R.x, R.bad);
+            CUDA_TRY(cudaGetLastError());
+        }
+        // I1: r0 := b - A x0 ; r^ := r0 ; w0 := A r0 ; t0 := A w0   (R-1)
+        RC_TRY(copy_own_to_pad(h, &Rank::x, 2));
+        RC_TRY(halo(h, 2));
+        for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_RESID, R.xpad, R.r, R.b, R.rh, false, h->stream));
     }
-    // I1: r0 := b - A x0 ; r^ := r0 ; w0 := A r0 ; t0 := A w0   (R-1)
-    RC_TRY(copy_own_to_pad(h, &Rank::x, 2));
-    RC_TRY(halo(h, 2));
-    for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_RESID, R.xpad, R.r, R.b, R.rh, false, h->stream));
     if (h->method == PBCG_METHOD_BICGSTAB) RC_TRY(start_alg1(h));
-    else RC_TRY(start_alg2_rest(h));
+    else if (chunked) RC_TRY(start_chunked(h, b));
+    else RC_TRY(start_alg2_rest(h, zero_start));
     CUDA_TRY(cudaMemcpyAsync(h->h_sc, h->R[0].sc, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
     int bad = 0;
@@ -1901,8 +2003,65 @@ extern "C" int pbicgstab_start(pbcg_handle *h, const double *b, const double *x0
     return PBCG_OK;
 }
 
-// I1 (rest) - I4 of Algorithm 2
-static int start_alg2_rest(pbcg_handle *h) {
+// I1-I4 of Algorithm 2 from x0 = 0 with a host b, chunk by chunk (plan_start):
+// chunk k of b lands (side stream) -> its scan and r = r^ = b copies; then
+// w0 = A r0 over chunk k-1's rows (their x rows lie in chunks <= k), then
+// t0 = A w0 over chunk k-2's rows and its share of (w0,b), (b,b) (the
+// exact dots accumulate over the launches; the last one rounds: PH_INIT0).
+// The same operations as start_alg2_rest, so the same bits.
+static int start_chunked(pbcg_handle *h, const double *b) {
+    Rank &R = h->R[0];
+    const cudaStream_t st = h->stream;
+    CUDA_TRY(cudaEventRecord(h->ev[4], st));  // the side stream starts after the memsets
+    CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev[4], 0));
+    for (int k = 0; k < START_NCH; ++k) {
+        const int64_t c0 = R.st_row[k], c1 = R.st_row[k + 1];
+        CUDA_TRY(cudaMemcpyAsync(R.b + c0, b + c0, sizeof(double) * (size_t)(c1 - c0), cudaMemcpyHostToDevice, h->side));
+        CUDA_TRY(cudaEventRecord(h->evc[k], h->side));
+    }
+    double *x2 = padbuf(R, 2) + R.own_off;  // the SpMV input of w0 = A r0
+    for (int k = 0; k < START_NCH + 2; ++k) {
+        if (k < START_NCH) {
+            const int64_t c0 = R.st_row[k], c1 = R.st_row[k + 1];
+            const size_t by = sizeof(double) * (size_t)(c1 - c0);
+            CUDA_TRY(cudaStreamWaitEvent(st, h->evc[k], 0));
+            nonfinite_scan_kernel<<<(int)std::min<int64_t>((c1 - c0 + 255) / 256, 4096), 256, 0, st>>>(c1 - c0, R.b + c0,
+                                                                                                  R.bad);
+            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(cudaMemcpyAsync(R.r + c0, R.b + c0, by, cudaMemcpyDeviceToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(R.rh + c0, R.b + c0, by, cudaMemcpyDeviceToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(x2 + c0, R.b + c0, by, cudaMemcpyDeviceToDevice, st));
+        }
+        if (k >= 1 && k - 1 < START_NCH) {  // w0 = A r0 over chunk k-1
+            const int j = k - 1;
+            spmv_dispatch<SPMV_PLAIN>(h, R, padbuf(R, 2), R.w(), nullptr, nullptr, nullptr, st, R.st_u[j], R.st_u[j + 1], 0);
+            CUDA_TRY(cudaGetLastError());
+        }
+        if (k >= 2) {  // t0 = A w0 over chunk k-2, and its share of the init dots
+            const int m = k - 2;
+            spmv_dispatch<SPMV_PLAIN>(h, R, padbuf(R, 1), R.t, nullptr, nullptr, nullptr, st, R.st_u[m], R.st_u[m + 1], 0);
+            CUDA_TRY(cudaGetLastError());
+            const int64_t c0 = R.st_row[m], c1 = R.st_row[m + 1];
+            MultiDotArgs a{};
+            a.n = c1 - c0;
+            a.x[0] = R.w() + c0;
+            a.y[0] = R.b + c0;
+            a.x[1] = a.y[1] = R.b + c0;
+            a.sc = R.sc;
+            a.gacc = R.gacc[0];
+            a.ticket = m == START_NCH - 1 ? R.tickets : nullptr;  // the last launch rounds
+            a.hist = R.hist;
+            a.phase = PH_INIT0;
+            a.finalize = 1;
+            RC_TRY(launch_xd2(h, a));
+        }
+    }
+    return PBCG_OK;
+}
+
+// I1 (rest) - I4 of Algorithm 2.  r_is_b: r0 = r^ = b bit for bit (x0 = 0),
+// so the dots read b for all three (the same values, fewer distinct bytes).
+static int start_alg2_rest(pbcg_handle *h, bool r_is_b) {
     RC_TRY(copy_own_to_pad(h, &Rank::r, 2));
     RC_TRY(halo(h, 2));
     for (auto &R : h->R) RC_TRY(launch_spmv(h, R, SPMV_PLAIN, R.xpad, R.w(), nullptr, nullptr, false, h->stream));
@@ -1912,10 +2071,16 @@ static int start_alg2_rest(pbcg_handle *h) {
     // I2-I4: ||b||, rho0 = (r^,r0), delta0 = (r^,w0), (r0,r0); alpha0
     std::vector<const double *> xb, yb, xr, yr, xw, yw, xn, yn;
     for (auto &R : h->R) {
+        const double *r = r_is_b ? R.b : R.r, *rh = r_is_b ? R.b : R.rh;
         xb.push_back(R.b); yb.push_back(R.b);
-        xr.push_back(R.rh); yr.push_back(R.r);
-        xw.push_back(R.rh); yw.push_back(R.w());
-        xn.push_back(R.r); yn.push_back(R.r);
+        xr.push_back(rh); yr.push_back(r);
+        xw.push_back(rh); yw.push_back(R.w());
+        xn.push_back(r); yn.push_back(r);
+    }
+    if (r_is_b) {  // (w0, b) and (b, b) in one pass of the two-dot stream kernel (PH_INIT0)
+        const double *const *xs[4] = {yw.data(), yb.data(), nullptr, nullptr};
+        const double *const *ys[4] = {yb.data(), yb.data(), nullptr, nullptr};
+        return multidot(h, 0, PH_INIT0, 2, xs, ys);
     }
     const double *const *xs[4] = {xb.data(), xr.data(), xw.data(), xn.data()};
     const double *const *ys[4] = {yb.data(), yr.data(), yw.data(), yn.data()};

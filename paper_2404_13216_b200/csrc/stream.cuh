@@ -700,6 +700,25 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a
     __syncwarp();
     acc.warp_merge(S.w[0]);
     if (ND == 2) acc2.warp_merge(s1);
+    if constexpr (ND == 2) {
+        if (phase_full_range(a.phase, a.sc)) {  // Algorithm 2's init with x0 = 0 (PH_INIT0): R-24 as in K2/K3
+            if (flags) atomicOr(&S.flags, flags);
+            flags = 0;
+            __syncthreads();  // the ring is drained: its memory is the scratch
+            if (S.flags & FLAG_RANGE)
+                cta_full_range_nd<2>(S, (unsigned long long *)buf, a.gacc + xs_off(2),
+                    [&](auto f) {
+                        for (int64_t tile = blockIdx.x; tile * T < n; tile += gridDim.x) {
+                            const int64_t e = min(n, tile * T + T);
+                            for (int64_t i = tile * T + threadIdx.x; i < e; i += blockDim.x) f(i);
+                        }
+                    },
+                    [&](int d, int64_t i, double &x, double &y) {  // (x,y), (y,y)
+                        y = a.y[0][i];
+                        x = d == 0 ? a.x[0][i] : y;
+                    });
+        }
+    }
     if constexpr (ND == 1) {
         if (a.phase == PH_EXDOT) {  // standalone dot (single GPU or a rank's slice): a flagged CTA corrects its products (NEXT-4)
             if (flags) atomicOr(&S.flags, flags);

@@ -819,3 +819,44 @@ def test_cluster_kernel_same_bits(pb, name, monkeypatch):
 def torch_zeros(n):
     import torch
     return torch.zeros(n, dtype=torch.float64, device="cuda")
+
+
+@pytest.mark.parametrize("precond,method", [("none", "pbicgstab"), ("jacobi", "pbicgstab"), ("bjacobi2", "pbicgstab"),
+                                            ("bjacobi2_pipe", "pbicgstab"), ("none", "bicgstab")])
+def test_zero_start_chunked_same_bits(pb, precond, method):
+    # x0 = 0 without reading x0 (pbcg_opts.x0_zero): r0 = b - A 0 = b bit for
+    # bit, so start skips the residual SpMV; a pinned host b of >= 2^20 rows
+    # is copied in chunks that overlap the scans and copies.  Same history and
+    # x as an explicit x0 = +0 vector through the residual SpMV.
+    import torch
+    A = gen.stencil(2, 1024, 10.0)  # 2^20 rows: the chunked path
+    S = solver(pb, A, history_capacity=64, precond=precond)
+    b = gpu_b(pb, S, A)
+    b[::1000] = -0.0  # signed zeros in b survive r0 = b - (+0)
+    xa, ra = S.solve(b, x0=torch.zeros(A.n, dtype=torch.float64, device="cuda"), tol=0.0, max_iter=30, method=method)
+    Ha = S.history()
+    out = torch.empty(A.n, dtype=torch.float64).pin_memory()
+    xb, rb = S.solve(b.cpu().pin_memory(), x0=None, out=out, tol=0.0, max_iter=30, method=method)
+    assert ra.iterations == rb.iterations == 30 and ra.status == rb.status
+    assert np.array_equal(u64(Ha), u64(S.history()))
+    assert np.array_equal(u64(xa.cpu().numpy()), u64(out.numpy()))
+    assert ra.relres_true == rb.relres_true
+    S.close()
+
+
+@pytest.mark.parametrize("scale", [2.0 ** -500, 2.0 ** 480])
+def test_zero_start_full_range_init(pb, scale):
+    # the x0 = 0 start's two-dot init kernel (PH_INIT0) corrects products
+    # outside the fast zone like the four-dot init (R-24): a b scaled so that
+    # (b,b) falls below 2^-960 (or reaches 2^960) gives the same history
+    import torch
+    A = gen.stencil(3, 40, 100.0)
+    S = solver(pb, A, history_capacity=16)
+    b = gpu_b(pb, S, A) * scale
+    xa, ra = S.solve(b, x0=torch.zeros(A.n, dtype=torch.float64, device="cuda"), tol=0.0, max_iter=6)
+    Ha = S.history()
+    xb, rb = S.solve(b, x0=None, tol=0.0, max_iter=6)
+    assert ra.status == rb.status and ra.iterations == rb.iterations
+    assert np.array_equal(u64(Ha), u64(S.history()))
+    assert np.array_equal(u64(xa.cpu().numpy()), u64(xb.cpu().numpy()))
+    S.close()

@@ -1,0 +1,5 @@
+O=gpurun_out/s14; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_solver.py -x -q -k "zero_start or x0_zero" > $O/zs.log 2>&1; echo "rc=$?" >> $O/zs.log
+timeout 600 python tools/start_profile.py c5_3d256 finish > $O/start_c5.txt 2>&1
+timeout 600 python tools/e2e_breakdown.py c5_3d256 20 > $O/e2e_c5_k20.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
