@@ -1038,10 +1038,17 @@ static constexpr int K2_PPT = PBCG_K2_PPT, K2_ST = PBCG_K2_ST, K3_PPT = PBCG_K3_
                      XD_PPT = PBCG_XD_PPT, XD_ST = PBCG_XD_ST;
 #define K2S k2_stream<K2_NH, K2_NC, S_NCW, K2_PPT, K2_ST, K2_NHE>
 #define K3S k3_stream<K3_NH, K3_NC, K3_NCW, K3_PPT, K3_ST, K3_NHE>
-// lean variants (one cold level less): less end-of-kernel drain, which is
-// what counts below LEAN_ROWS rows per rank (C1/C3/C4 measured faster, C5 slower)
-#define K2SL k2_stream<K2_NH, K2_NC - 1, S_NCW, K2_PPT, K2_ST, K2_NHE>
-#define K3SL k3_stream<K3_NH, K3_NC - 1, K3_NCW, K3_PPT, K3_ST, K3_NHE>
+// lean variants (one cold level less and, round 3, one hot p level less):
+// less end-of-kernel drain and a shorter hot cascade, which is what counts
+// below LEAN_ROWS rows per rank (C1/C3/C4 measured faster, C5 slower).
+// Hot p levels 3 -> 2 in the lean K2 / K3 (tools/ab_iter.py, iter/s): C3
+// 7,504 -> 7,598 / 7,595 each, C4 1,552 -> 1,559 / 1,558; on C5 (not lean)
+// the same change loses 2.2 % / 0.8 %.
+#ifndef PBCG_LEAN_NH
+#define PBCG_LEAN_NH 2
+#endif
+#define K2SL k2_stream<PBCG_LEAN_NH, K2_NC - 1, S_NCW, K2_PPT, K2_ST, K2_NHE>
+#define K3SL k3_stream<PBCG_LEAN_NH, K3_NC - 1, K3_NCW, K3_PPT, K3_ST, K3_NHE>
 static constexpr int64_t LEAN_ROWS = 8 << 20;
 #define K2SP k2_stream<K2_NH, K2_NC, S_NCW, K2_PPT, K2_ST, K2_NHE, false>
 #define K3SP k3_stream<K3_NH, K3_NC, K3_NCW, K3_PPT, K3_ST, K3_NHE, false>
