@@ -1047,15 +1047,25 @@ static constexpr int K2_PPT = PBCG_K2_PPT, K2_ST = PBCG_K2_ST, K3_PPT = PBCG_K3_
 #ifndef PBCG_LEAN_NH
 #define PBCG_LEAN_NH 2
 #endif
-#define K2SL k2_stream<PBCG_LEAN_NH, K2_NC - 1, S_NCW, K2_PPT, K2_ST, K2_NHE>
-#define K3SL k3_stream<PBCG_LEAN_NH, K3_NC - 1, K3_NCW, K3_PPT, K3_ST, K3_NHE>
+#ifndef PBCG_K2L_NCW
+#define PBCG_K2L_NCW 7
+#endif
+#ifndef PBCG_K3L_NCW
+#define PBCG_K3L_NCW 8
+#endif
+static constexpr int K2L_NCW = PBCG_K2L_NCW, K3L_NCW = PBCG_K3L_NCW;  // lean: warps per dot group
+#define K2SL k2_stream<PBCG_LEAN_NH, K2_NC - 1, K2L_NCW, K2_PPT, K2_ST, K2_NHE>
+#define K3SL k3_stream<PBCG_LEAN_NH, K3_NC - 1, K3L_NCW, K3_PPT, K3_ST, K3_NHE>
 static constexpr int64_t LEAN_ROWS = 8 << 20;
 #define K2SP k2_stream<K2_NH, K2_NC, S_NCW, K2_PPT, K2_ST, K2_NHE, false>
 #define K3SP k3_stream<K3_NH, K3_NC, K3_NCW, K3_PPT, K3_ST, K3_NHE, false>
 // pipelined block Jacobi (R-25): exact (lean cold tier: the z_hat / w_hat
 // work would otherwise spill) and plain dots
-#define K2SX k2_stream<K2_NH, K2_NC - 1, S_NCW, K2_PPT, K2_ST, K2_NHE, true, true>
-#define K3SX k3_stream<K3_NH, K3_NC - 1, S_NCW, K3_PPT, K3_ST, K3_NHE, true, true>  // 7 warps per group: 128 registers
+#ifndef PBCG_PIPE_NH
+#define PBCG_PIPE_NH 3
+#endif
+#define K2SX k2_stream<PBCG_PIPE_NH, K2_NC - 1, S_NCW, K2_PPT, K2_ST, K2_NHE, true, true>
+#define K3SX k3_stream<PBCG_PIPE_NH, K3_NC - 1, S_NCW, K3_PPT, K3_ST, K3_NHE, true, true>  // 7 warps per group: 128 registers
 #define K2SXP k2_stream<K2_NH, K2_NC, S_NCW, K2_PPT, K2_ST, K2_NHE, false, true>
 #define K3SXP k3_stream<K3_NH, K3_NC, K3_NCW, K3_PPT, K3_ST, K3_NHE, false, true>
 #define XDS exdot_stream<X_NH, X_NL, X_NCW, XD_PPT, XD_ST>
@@ -1070,6 +1080,8 @@ static constexpr size_t XD_SMEM = ring_bytes(2, X_NCW, XD_PPT, XD_ST);
 static constexpr int STREAM_THREADS = (X_NCW + 1) * 32;      // exdot: 1 dot group
 static constexpr int KSTREAM_THREADS = (2 * S_NCW + 1) * 32;  // K2: 2 dot groups
 static constexpr int K3_THREADS = (2 * K3_NCW + 1) * 32;       // K3: 2 dot groups
+static constexpr size_t K2L_SMEM = ring_bytes(8, K2L_NCW, K2_PPT, K2_ST), K3L_SMEM = ring_bytes(7, K3L_NCW, K3_PPT, K3_ST);
+static constexpr int K2L_THREADS = (2 * K2L_NCW + 1) * 32, K3L_THREADS = (2 * K3L_NCW + 1) * 32;
 
 
 static int stream_attrs() {
@@ -1078,8 +1090,8 @@ static int stream_attrs() {
     CUDA_TRY(cudaFuncSetAttribute((const void *)K2S, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)K3S, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)K2SP, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM));
-    CUDA_TRY(cudaFuncSetAttribute((const void *)K2SL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM));
-    CUDA_TRY(cudaFuncSetAttribute((const void *)K3SL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM));
+    CUDA_TRY(cudaFuncSetAttribute((const void *)K2SL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2L_SMEM));
+    CUDA_TRY(cudaFuncSetAttribute((const void *)K3SL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3L_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)K3SP, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)K2SX, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K2_SMEM));
     CUDA_TRY(cudaFuncSetAttribute((const void *)K3SX, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3X_SMEM));
@@ -1125,7 +1137,7 @@ static int launch_k2(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
         launch_ex(K2SP, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T)), dim3(KSTREAM_THREADS), K2_SMEM, st,
                   pdl_for(R), a);
     } else if (R.n < LEAN_ROWS) {
-        launch_ex(K2SL, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T)), dim3(KSTREAM_THREADS), K2_SMEM, st,
+        launch_ex(K2SL, dim3(stream_grid(h, R.n, TileGeo<K2L_NCW, K2_PPT>::T)), dim3(K2L_THREADS), K2L_SMEM, st,
                   pdl_for(R), a);
     } else {
         launch_ex(K2S, dim3(stream_grid(h, R.n, TileGeo<S_NCW, K2_PPT>::T)), dim3(KSTREAM_THREADS), K2_SMEM, st,
@@ -1149,7 +1161,7 @@ static int launch_k3(pbcg_handle *h, Rank &R, int fin, cudaStream_t st) {
         launch_ex(K3SP, dim3(stream_grid(h, R.n, TileGeo<K3_NCW, K3_PPT>::T)), dim3(K3_THREADS), K3_SMEM, st,
                   pdl_for(R), a);
     } else if (R.n < LEAN_ROWS) {
-        launch_ex(K3SL, dim3(stream_grid(h, R.n, TileGeo<K3_NCW, K3_PPT>::T)), dim3(K3_THREADS), K3_SMEM, st,
+        launch_ex(K3SL, dim3(stream_grid(h, R.n, TileGeo<K3L_NCW, K3_PPT>::T)), dim3(K3L_THREADS), K3L_SMEM, st,
                   pdl_for(R), a);
     } else {
         launch_ex(K3S, dim3(stream_grid(h, R.n, TileGeo<K3_NCW, K3_PPT>::T)), dim3(K3_THREADS), K3_SMEM, st,

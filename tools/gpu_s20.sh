@@ -1,0 +1,6 @@
+O=gpurun_out/s20; mkdir -p $O
+L=$PWD/paper_2404_13216_b200
+V="$L/libpbicgstab.so $L/libpbicgstab_pnh2.so"
+PRECOND=bjacobi2_pipe timeout 900 python tools/ab_iter.py c5_3d256 200 $V > $O/ab_c5.txt 2>&1
+PRECOND=bjacobi2_pipe timeout 900 python tools/ab_iter.py c3_3d128 400 $V > $O/ab_c3.txt 2>&1
+PRECOND=bjacobi2_pipe timeout 900 python tools/ab_iter.py c4_rand4m 200 $V > $O/ab_c4.txt 2>&1
