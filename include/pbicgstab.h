@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define PBCG_ABI_VERSION 9
+#define PBCG_ABI_VERSION 10
 
 /* return codes of every entry point (never an abort across the ABI) */
 enum pbcg_rc {
@@ -173,6 +173,11 @@ typedef struct {
     double loop_seconds;      /* device time of the iteration loop (CUDA events) */
     int32_t history_rows;     /* rows available via pbicgstab_history */
     int32_t reserved;
+    uint64_t digest;          /* fingerprint of the scalar trajectory: FNV-1a 64 over the
+                                 per-row FNV-1a 64 hashes of history rows 0 .. history_rows-1, each row
+                                 hashed over its 12 doubles' bit patterns as 64-bit words (offset basis
+                                 0xcbf29ce484222325, prime 0x100000001b3).  Bit-identical trajectories --
+                                 at any rank count, any partition -- give the same digest. */
 } pbcg_result;
 
 typedef struct pbcg_handle pbcg_handle;

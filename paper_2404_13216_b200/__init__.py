@@ -68,7 +68,7 @@ class _Opts(ctypes.Structure):
 class _Result(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("iterations", ctypes.c_int32), ("relres_recursive", ctypes.c_double),
                 ("relres_true", ctypes.c_double), ("loop_seconds", ctypes.c_double),
-                ("history_rows", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("history_rows", ctypes.c_int32), ("reserved", ctypes.c_int32), ("digest", ctypes.c_uint64)]
 
 
 _lib = None
@@ -150,6 +150,7 @@ class Result:
     relres_true: float
     loop_seconds: float
     history_rows: int
+    digest: int = 0  # fingerprint of the scalar trajectory (pbcg_result.digest)
 
     @property
     def status_name(self) -> str:
@@ -345,7 +346,8 @@ class Solver:
 
     @staticmethod
     def _result(r: _Result) -> Result:
-        return Result(r.status, r.iterations, r.relres_recursive, r.relres_true, r.loop_seconds, r.history_rows)
+        return Result(r.status, r.iterations, r.relres_recursive, r.relres_true, r.loop_seconds, r.history_rows,
+                      r.digest)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -39,6 +39,7 @@ struct Scalars {
     int32_t hist_cap, err;
     int32_t qconv;  // Alg. 1: converged at the q check, x += alpha p still to apply
     int32_t range_mode;  // Alg. 2 dots: 0 full range (R-24: corrected, only NaN/Inf or overflow stop), 1 fast zone (R-9)
+    unsigned long long digest;  // pbcg_result.digest of the history rows (hist_digest_kernel, at finish)
 };
 
 // ------------------------------------------------------------------------
@@ -1213,6 +1214,27 @@ __global__ void sell_xmax_kernel(int64_t n, int64_t nslices, const int64_t *slic
         for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
         if (lane == 0) xmax[sl] = m;
     }
+}
+
+// pbcg_result.digest: FNV-1a 64 over the per-row FNV-1a 64 hashes of history
+// rows [0, rows) (12 doubles each, bit patterns as 64-bit words).  One warp:
+// the lanes hash rows, lane 0 folds the row hashes in order.
+__global__ void hist_digest_kernel(const double *hist, Scalars *sc) {
+    constexpr unsigned long long B = 0xcbf29ce484222325ull, P = 0x100000001b3ull;
+    const int rows = min(sc->it + 1, sc->hist_cap);
+    const int lane = threadIdx.x & 31;
+    unsigned long long h = B;
+    for (int r0 = 0; r0 < rows; r0 += 32) {
+        const int r = r0 + lane;
+        unsigned long long rh = B;
+        if (r < rows)
+            for (int c = 0; c < H_COLS; ++c) rh = (rh ^ (unsigned long long)__double_as_longlong(hist[(size_t)r * H_COLS + c])) * P;
+        for (int k = 0; k < 32 && r0 + k < rows; ++k) {
+            const unsigned long long v = __shfl_sync(0xFFFFFFFFu, rh, k);
+            h = (h ^ v) * P;
+        }
+    }
+    if (lane == 0) sc->digest = h;
 }
 
 __global__ void nonfinite_scan_kernel(int64_t n, const double *v, int *bad) {

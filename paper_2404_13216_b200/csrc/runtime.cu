@@ -2438,6 +2438,8 @@ extern "C" int pbicgstab_finish(pbcg_handle *h, double *x, pbcg_result *res) {
         }
     }
     if (h->h_sc->err == 0) RC_TRY(true_residual(h));
+    hist_digest_kernel<<<1, 32, 0, h->stream>>>(h->R[0].hist, h->R[0].sc);
+    CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(h->h_sc, h->R[0].sc, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
     if (xs != h->stream) CUDA_TRY(cudaStreamSynchronize(xs));
@@ -2449,6 +2451,7 @@ extern "C" int pbicgstab_finish(pbcg_handle *h, double *x, pbcg_result *res) {
         res->relres_true = s.relres_true;
         res->history_rows = std::min(s.it + 1, h->hist_cap);
         res->loop_seconds = 0.0;
+        res->digest = s.digest;
     }
     return PBCG_OK;
 }

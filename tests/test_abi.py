@@ -32,7 +32,7 @@ def test_library_exports_every_header_symbol():
     assert len(names) >= 15, names
     for nm in names:
         assert hasattr(L, nm), nm
-    assert L.pbcg_abi_version() == 9
+    assert L.pbcg_abi_version() == 10
 
 
 def test_plan_partition_spec_examples():

@@ -116,8 +116,22 @@ def run_both(pb, A, tol, max_iter, steps=None, **kw):
     return S, O, x.cpu().numpy(), r, H
 
 
+def trajectory_digest(H):
+    """pbcg_result.digest (include/pbicgstab.h) of a history array, written
+    out: FNV-1a 64 over the per-row FNV-1a 64 hashes of the rows' bits."""
+    B, P, M = 0xcbf29ce484222325, 0x100000001b3, (1 << 64) - 1
+    h = B
+    for row in u64(np.atleast_2d(H)):
+        rh = B
+        for w in row:
+            rh = ((rh ^ int(w)) * P) & M
+        h = ((h ^ rh) * P) & M
+    return h
+
+
 def assert_same(O, x, r, H, A):
     Ho = O.history()
+    assert r.digest == trajectory_digest(Ho)  # the trajectory fingerprint of the oracle's history
     assert r.iterations == O.iterations, (r.iterations, O.iterations)
     st = O.status if O.status != oracle.RUNNING else oracle.MAXITER
     assert r.status == st, (r.status, O.status)
