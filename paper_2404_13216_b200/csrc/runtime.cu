@@ -2467,11 +2467,13 @@ extern "C" int pbicgstab_solve(pbcg_handle *h, const double *b, double *x, const
     // Polls overlap the next chunk: chunk k+1 is enqueued before the host
     // waits for the scalars copied after chunk k, so the GPU never idles on
     // the round trip (iterations after done are device-side no-ops).
+    // The last chunk is cut to max_iter (its own graph, kept like the full
+    // chunk's): no trailing no-op iterations when the solve runs to max_iter.
     int done_iters = 0, k = 0;
-    while (!h->h_sc->done && done_iters <= op.max_iter) {
-        const int chunk = op.poll_every;
-        RC_TRY(iterate_impl(h, chunk, chunk, op.use_graphs != 0));
-        done_iters += chunk;
+    while (!h->h_sc->done && done_iters < op.max_iter) {
+        const int chunk = op.poll_every, cnt = std::min(chunk, op.max_iter - done_iters);
+        RC_TRY(iterate_impl(h, cnt, chunk, op.use_graphs != 0));
+        done_iters += cnt;
         CUDA_TRY(cudaMemcpyAsync(h->h_poll[k & 1], h->R[0].sc, sizeof(Scalars), cudaMemcpyDeviceToHost, h->stream));
         CUDA_TRY(cudaEventRecord(h->evp[k & 1], h->stream));
         if (k > 0) {  // the previous chunk's scalars
@@ -2479,7 +2481,6 @@ extern "C" int pbicgstab_solve(pbcg_handle *h, const double *b, double *x, const
             *h->h_sc = *h->h_poll[(k - 1) & 1];
         }
         ++k;
-        if (!(done_iters <= op.max_iter)) break;
     }
     CUDA_TRY(cudaStreamSynchronize(h->stream));
     if (k > 0) *h->h_sc = *h->h_poll[(k - 1) & 1];
