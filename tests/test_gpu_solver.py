@@ -874,3 +874,25 @@ def test_zero_start_full_range_init(pb, scale):
     assert np.array_equal(u64(Ha), u64(S.history()))
     assert np.array_equal(u64(xa.cpu().numpy()), u64(xb.cpu().numpy()))
     S.close()
+
+
+@pytest.mark.parametrize("name", ["2d_ragged", "3d_ragged", "short_rows_wide_band", "sellv"])
+def test_zero_start_chunk_plans(pb, name):
+    # the chunked start on ragged sizes (chunk boundaries on 3,840-row unit
+    # steps, a short last chunk), a 3D halo of 10,404 rows, and matrices the
+    # plan rejects (a row reads beyond the next chunk; SELL-V): whole-copy
+    # fallback.  Same history and x as the residual-SpMV path.
+    import torch
+    A = {"2d_ragged": lambda: gen.stencil(2, 1030, 10.0), "3d_ragged": lambda: gen.stencil(3, 102, 100.0),
+         "short_rows_wide_band": lambda: gen.random_banded(1 << 20, lam=4.0, lmin=2, lmax=8, band=400_000),
+         "sellv": lambda: gen.random_banded(1 << 20, lam=12.0, lmin=5, lmax=40, band=3000)}[name]()
+    S = solver(pb, A, history_capacity=32)
+    b = gpu_b(pb, S, A)
+    xa, ra = S.solve(b, x0=torch.zeros(A.n, dtype=torch.float64, device="cuda"), tol=0.0, max_iter=12)
+    Ha = S.history()
+    out = torch.empty(A.n, dtype=torch.float64).pin_memory()
+    xb, rb = S.solve(b.cpu().pin_memory(), x0=None, out=out, tol=0.0, max_iter=12)
+    assert ra.iterations == rb.iterations == 12 and ra.status == rb.status and ra.digest == rb.digest
+    assert np.array_equal(u64(Ha), u64(S.history()))
+    assert np.array_equal(u64(xa.cpu().numpy()), u64(out.numpy()))
+    S.close()
