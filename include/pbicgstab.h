@@ -333,6 +333,11 @@ int pbcg_config_hash(const pbcg_csr_local *A, const pbcg_dist *dist, uint64_t *o
 #define PBCG_RANK_REC 5
 int pbcg_check_ranks(int32_t nranks, const int64_t *records, int64_t n_global, int32_t has_matrix);
 
+/* pbcg_result.digest of a history held in host memory (rows x 12 doubles,
+ * the layout of pbicgstab_history): the host twin of the device kernel, for
+ * comparing trajectories saved from different runs.  rows >= 0. */
+int pbcg_history_digest(const double *history, int32_t rows, uint64_t *out);
+
 /* Balanced contiguous partition of n rows over p ranks (SPEC.md l.148,
  * l.185-187): the first n mod p ranks get one extra row.  begins: p+1 entries. */
 int pbcg_plan_partition(int64_t n, int32_t p, int64_t *begins);

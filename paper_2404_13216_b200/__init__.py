@@ -111,6 +111,7 @@ def lib(build_if_missing: bool = True) -> ctypes.CDLL:
         L.pbcg_get_vector.argtypes = [vp, i32, vp]
         L.pbcg_config_hash.argtypes = [P(_Csr), P(_Dist), P(ctypes.c_uint64)]
         L.pbcg_check_ranks.argtypes = [i32, vp, i64, i32]
+        L.pbcg_history_digest.argtypes = [vp, i32, P(ctypes.c_uint64)]
         _lib = L
     return _lib
 
@@ -446,6 +447,15 @@ def config_hash(n_global: int | None, nranks: int = 1, virtual_ranks: int = 1, p
     out = ctypes.c_uint64(0)
     _check(lib().pbcg_config_hash(ctypes.byref(csr) if n_global is not None else None, ctypes.byref(d),
                                   ctypes.byref(out)))
+    return int(out.value)
+
+
+def history_digest(history) -> int:
+    """pbcg_history_digest of a (rows, 12) float64 history in host memory:
+    the pbcg_result.digest a solve with that trajectory reports."""
+    h = np.ascontiguousarray(np.asarray(history, dtype=np.float64).reshape(-1, 12))
+    out = ctypes.c_uint64(0)
+    _check(lib().pbcg_history_digest(ctypes.c_void_p(h.ctypes.data), h.shape[0], ctypes.byref(out)))
     return int(out.value)
 
 

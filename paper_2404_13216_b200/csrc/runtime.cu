@@ -149,6 +149,23 @@ static int nccl_ctas() {
 // arguments that must agree; setup allgathers (row_begin, row_end, hull,
 // hash) and every rank checks the same records, so all return the same code
 // ----------------------------------------------------------------------------
+extern "C" int pbcg_history_digest(const double *hist, int32_t rows, uint64_t *out) {
+    if (!out || rows < 0 || (rows > 0 && !hist)) return fail(PBCG_EINVAL, "history_digest: bad arguments");
+    constexpr uint64_t B = 0xcbf29ce484222325ull, P = 0x100000001b3ull;  // FNV-1a 64
+    uint64_t h = B;
+    for (int32_t r = 0; r < rows; ++r) {
+        uint64_t rh = B;
+        for (int c = 0; c < H_COLS; ++c) {
+            uint64_t w;
+            memcpy(&w, hist + (size_t)r * H_COLS + c, 8);
+            rh = (rh ^ w) * P;
+        }
+        h = (h ^ rh) * P;
+    }
+    *out = h;
+    return PBCG_OK;
+}
+
 extern "C" int pbcg_config_hash(const pbcg_csr_local *A, const pbcg_dist *d, uint64_t *out) {
     if (!out) return fail(PBCG_EINVAL, "config_hash: out == NULL");
     uint64_t hsh = 1469598103934665603ull;  // FNV-1a 64

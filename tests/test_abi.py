@@ -227,3 +227,32 @@ def test_gloo_world2_setup_contract(mismatch):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert out[0] == out[1] == (1 if mismatch else 0)
+
+
+def test_history_digest_host_twin():
+    # pbcg_result.digest's definition (include/pbicgstab.h), written out in
+    # Python: FNV-1a 64 over the per-row FNV-1a 64 hashes of the rows' bits
+    import paper_2404_13216_b200 as pb
+    B, P, M = 0xcbf29ce484222325, 0x100000001b3, (1 << 64) - 1
+
+    def ref(H):
+        h = B
+        for row in np.ascontiguousarray(H, np.float64).reshape(-1, 12).view(np.uint64):
+            rh = B
+            for w in row:
+                rh = ((rh ^ int(w)) * P) & M
+            h = ((h ^ rh) * P) & M
+        return h
+
+    rng = np.random.default_rng(5)
+    H = rng.standard_normal((9, 12))
+    H[3, 4] = -0.0
+    H[5, :] = np.nan
+    assert pb.history_digest(H) == ref(H)
+    assert pb.history_digest(np.zeros((0, 12))) == B
+    H2 = H.copy()
+    H2[8, 11] = np.nextafter(H2[8, 11], 1.0)  # one ulp anywhere changes it
+    assert pb.history_digest(H2) != pb.history_digest(H)
+    H3 = H.copy()
+    H3[3, 4] = 0.0  # and so does the sign of a zero
+    assert pb.history_digest(H3) != pb.history_digest(H)
