@@ -583,7 +583,7 @@ struct ExAccT {
 // Accumulate a batch of K prepared products with one vote per tier.  Product
 // k goes to d1 when ALT and k is odd, else to d0 (s0/s1: their shared
 // superaccumulators).  All 32 lanes must be active.
-template <int K, bool ALT, class A>
+template <int K, bool ALT, bool SPLIT = false, class A>
 __device__ __forceinline__ void cascade_batch(A &d0, A &d1, const Prod (&P)[K], unsigned long long *s0,
                                               unsigned long long *s1) {
     double rp[K], re[K];
@@ -596,6 +596,50 @@ __device__ __forceinline__ void cascade_batch(A &d0, A &d1, const Prod (&P)[K], 
     }
     // the p and e streams spill independently (e usually more often: it sits
     // 53 bits below p), so each gets its own vote for its cold levels
+    if constexpr (ALT && SPLIT) {  // one vote per (dot, stream): a dot whose residuals are all zero skips its cold levels
+        bool any[4] = {false, false, false, false};  // p0, p1, e0, e1
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            any[k & 1] |= is_nonzero(rp[k]);
+            any[2 + (k & 1)] |= is_nonzero(re[k]);
+        }
+        const unsigned vp0 = __any_sync(0xFFFFFFFFu, any[0]), vp1 = __any_sync(0xFFFFFFFFu, any[1]);
+        const unsigned ve0 = __any_sync(0xFFFFFFFFu, any[2]), ve1 = __any_sync(0xFFFFFFFFu, any[3]);
+        if (vp0 | vp1 | ve0 | ve1) {
+            PBCG_COUNT(1);
+            double cp[K], ce[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                cp[k] = 0.0;
+                ce[k] = 0.0;
+            }
+            if (vp0) {
+#pragma unroll
+                for (int k = 0; k < K; k += 2) cp[k] = d0.CP.add(rp[k]);
+            }
+            if (vp1) {
+#pragma unroll
+                for (int k = 1; k < K; k += 2) cp[k] = d1.CP.add(rp[k]);
+            }
+            if (ve0) {
+#pragma unroll
+                for (int k = 0; k < K; k += 2) ce[k] = d0.CE.add(re[k]);
+            }
+            if (ve1) {
+#pragma unroll
+                for (int k = 1; k < K; k += 2) ce[k] = d1.CE.add(re[k]);
+            }
+            if (__any_sync(0xFFFFFFFFu, any_nonzero(cp, K) | any_nonzero(ce, K))) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    unsigned long long *sk = (k & 1) ? s1 : s0;
+                    if (is_nonzero(cp[k])) sacc_deposit(sk, cp[k]);
+                    if (is_nonzero(ce[k])) sacc_deposit(sk, ce[k]);
+                }
+            }
+        }
+        return;
+    }
     const bool cold_p = __any_sync(0xFFFFFFFFu, any_nonzero(rp, K));
     const bool cold_e = __any_sync(0xFFFFFFFFu, any_nonzero(re, K));
     if (cold_p | cold_e) {
@@ -660,7 +704,7 @@ struct PlainAcc {
     }
 };
 
-template <int K, bool ALT>
+template <int K, bool ALT, bool SPLIT = false>
 __device__ __forceinline__ void cascade_batch(PlainAcc &d0, PlainAcc &d1, const Prod (&P)[K], unsigned long long *,
                                               unsigned long long *) {
 #pragma unroll

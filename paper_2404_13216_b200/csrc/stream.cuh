@@ -16,6 +16,19 @@
 
 #include "kernels.cuh"
 
+// One cold-tier vote per (dot, stream) instead of per stream in the two-dot
+// groups (cascade_batch SPLIT), by kernel and cold depth NL.  On in the
+// non-lean K3 only, whose group 0 pairs a dot that spills often, (r0,r'),
+// with one that rarely does, (r',r'): C5 1,071.5 -> 1,080.4 iter/s at the
+// driver's K = 20 (1,084.5 -> 1,091.6 at K = 200); on in K2 (both pairs
+// spill alike) C5 1,068.7 and C3 7,724 vs 7,770 (tools/ab_iter.py).
+#ifndef PBCG_VSPLIT_K2
+#define PBCG_VSPLIT_K2(nl) false
+#endif
+#ifndef PBCG_VSPLIT_K3
+#define PBCG_VSPLIT_K3(nl) ((nl) >= 2)
+#endif
+
 namespace pbcg {
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -322,7 +335,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
                         R.row1(flags, rh.x, w.x, t.x, v.x, ss.x, z.x, P[0], P[1]);
                         R.row1(flags, rh.y, w.y, t.y, v.y, ss.y, z.y, P[2], P[3]);
                     }
-                    cascade_batch<4, true>(R.d0, R.d1, P, s0, s1);
+                    cascade_batch<4, true, PBCG_VSPLIT_K2(NL)>(R.d0, R.d1, P, s0, s1);
                 } else {
                     [[maybe_unused]] double zz[2] = {0.0, 0.0};  // this pair's z (pipelined block Jacobi)
                     for (int h = 0; h < 2; ++h) {
@@ -512,7 +525,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
                         R.row0(flags, rh.x, p.x, q.x, y.x, x.x, r.x, P[0], P[1]);
                         R.row0(flags, rh.y, p.y, q.y, y.y, x.y, r.y, P[2], P[3]);
                         ((double2 *)a.x)[gp] = x; ((double2 *)a.r)[gp] = r;
-                        cascade_batch<4, true>(R.d0, R.d1, P, s0, s1);
+                        cascade_batch<4, true, PBCG_VSPLIT_K3(NL)>(R.d0, R.d1, P, s0, s1);
                     } else {
                         const double2 t = B2[4 * TP + j], v = B2[5 * TP + j];
                         double2 w;
