@@ -64,6 +64,57 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                  : "memory");
 }
 
+// The same with the L2 evict_first priority: the matrix streams of the SpMV
+// kernels.  A matrix chunk is read once per SpMV and is larger than what the
+// L2 could keep until the next one, so without the hint it only pushes out
+// the vectors the neighbouring kernels re-read (K2's z is the next SpMV's x,
+// v and t are K3's and K2's inputs).  tools/ab_iter.py: C3 (16.8 MB vectors,
+// 134 MB matrix, 126 MB L2) 7,766 -> 8,207 iter/s, C5 1,082 -> 1,090.
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_g2s_stream(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+__device__ __forceinline__ void st_stream_v2(double2 *p, double2 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+// Vectors that K2 / K3 stream through the L2 with the evict_first hint, loads
+// (EFM: bit v = ring vector v) and stores (STM: K2 p,s,z,q,y / K3 x,r,w).
+// Default: s (touched by K2 only) and x (K3 only) -- their next use is a whole
+// iteration away, so they only take the cache from vectors the next kernel
+// reads.  tools/ab_iter.py on top of the matrix hint: C5 1,090.7 -> 1,096.9
+// iter/s, C3 8,213 -> 8,223, C4 unchanged.  Measured and rejected: every
+// load and store (C5 1,076.5, C3 8,061), everything but the SpMV inputs z, w
+// (1,077.9 / 8,150), s, p, r0 / x, p, r0 (1,093.5 / 8,203), stores only
+// (1,089.7 / 8,117), and the loads of the vectors the next kernel overwrites
+// (r, w, v / q, y, t: C3 8,163 vs 8,206 -- their dirty lines then go to DRAM
+// instead of being overwritten in the cache).
+#ifndef PBCG_K2_EFM
+#define PBCG_K2_EFM 0x20u
+#endif
+#ifndef PBCG_K3_EFM
+#define PBCG_K3_EFM 0x40u
+#endif
+#ifndef PBCG_K2_STM
+#define PBCG_K2_STM 0x2u
+#endif
+#ifndef PBCG_K3_STM
+#define PBCG_K3_STM 0x1u
+#endif
+template <unsigned M, int B>
+__device__ __forceinline__ void st_v2(double *base, int64_t gp, double2 v, uint64_t pol) {
+    if constexpr ((M >> B) & 1u) st_stream_v2((double2 *)base + gp, v, pol);
+    else ((double2 *)base)[gp] = v;
+}
+
 // Tile geometry shared by the producer and the consumers.
 template <int NCW, int PPT>
 struct TileGeo {
@@ -111,9 +162,11 @@ __device__ __forceinline__ void produce(const double *const *src, int nv_act, in
 // one launches.  The late vector's copies of those tiles follow the gate
 // (their bytes are already in the barrier's expected count); on abort they
 // are issued anyway and drained, so no copy is in flight at exit.
-template <int NV, int T, int STAGES, class Gate>
+// EFM: bit v set = vector v streams through the L2 (evict_first hint).
+template <int NV, int T, int STAGES, unsigned EFM = 0u, class Gate>
 __device__ __forceinline__ bool produce_gated(const double *const *src, int nv_act, int late, int64_t n, double *buf,
                                               uint64_t *full, uint64_t *empty, Gate gate) {
+    [[maybe_unused]] const uint64_t pol = EFM ? l2_policy_evict_first() : 0ull;
     const int64_t ntiles = (n + T - 1) / T;
     int s = 0, issued = 0;
     uint32_t ph = 0;
@@ -146,8 +199,10 @@ __device__ __forceinline__ bool produce_gated(const double *const *src, int nv_a
         if (bytes) {
 #pragma unroll
             for (int v = 0; v < NV; ++v)  // static indices keep src in registers
-                if (v < nv_act && (gated || v != late))
-                    bulk_g2s(buf + ((size_t)s * NV + v) * T, src[v] + r0, bytes, &full[s]);
+                if (v < nv_act && (gated || v != late)) {
+                    if ((EFM >> v) & 1u) bulk_g2s_stream(buf + ((size_t)s * NV + v) * T, src[v] + r0, bytes, &full[s], pol);
+                    else bulk_g2s(buf + ((size_t)s * NV + v) * T, src[v] + r0, bytes, &full[s]);
+                }
         }
         ++issued;
         if (++s == STAGES) { s = 0; ph ^= 1u; }
@@ -269,7 +324,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
         if (lane == 0) {
             const bool first0 = (sc->it == 0);  // written by the previous finalize: complete (event dependency)
             const double *src[NV] = {a.r, a.rh, a.w, a.t, a.p, a.s, a.z, a.v};
-            ok = produce_gated<NV, T, STAGES>(src, first0 ? 4 : 8, 3, a.n, buf, full, empty, [&]() {
+            ok = produce_gated<NV, T, STAGES, PBCG_K2_EFM>(src, first0 ? 4 : 8, 3, a.n, buf, full, empty, [&]() {
                 pdl_sync();
                 return !sc->done;
             });
@@ -285,6 +340,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
     const bool first = (sc->it == 0);
     const int64_t n = a.n;
     unsigned flags = 0;
+    [[maybe_unused]] const uint64_t stpol = PBCG_K2_STM ? l2_policy_evict_first() : 0ull;
     K2Op<Acc> R;
     R.first = first;
     R.be = sc->beta;
@@ -327,8 +383,9 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
                         if (!first) p = B2[4 * TP + j];
                         R.row0(flags, r.x, w.x, t.x, v.x, p.x, ss.x, z.x, q.x, y.x, P[0], P[1]);
                         R.row0(flags, r.y, w.y, t.y, v.y, p.y, ss.y, z.y, q.y, y.y, P[2], P[3]);
-                        ((double2 *)a.p)[gp] = p; ((double2 *)a.s)[gp] = ss; ((double2 *)a.z)[gp] = z;
-                        ((double2 *)a.q)[gp] = q; ((double2 *)a.y)[gp] = y;
+                        st_v2<PBCG_K2_STM, 0>(a.p, gp, p, stpol); st_v2<PBCG_K2_STM, 1>(a.s, gp, ss, stpol);
+                        st_v2<PBCG_K2_STM, 2>(a.z, gp, z, stpol); st_v2<PBCG_K2_STM, 3>(a.q, gp, q, stpol);
+                        st_v2<PBCG_K2_STM, 4>(a.y, gp, y, stpol);
                         if constexpr (PIPE) ((double2 *)a.zh)[gp] = bj_pair(a.minv, gp, z.x, z.y);  // z_hat = M^-1 z (R-25)
                     } else {
                         const double2 rh = B2[1 * TP + j];
@@ -470,7 +527,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
         bool ok = true;
         if (lane == 0) {
             const double *src[NV] = {a.rh, a.p, a.q, a.y, a.t, a.v, a.x};
-            ok = produce_gated<NV, T, STAGES>(src, NV, 5, a.n, buf, full, empty, [&]() {
+            ok = produce_gated<NV, T, STAGES, PBCG_K3_EFM>(src, NV, 5, a.n, buf, full, empty, [&]() {
                 pdl_sync();
                 return !sc->done;
             });
@@ -484,6 +541,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
     PBCG_TL(2, 1);
     const int64_t n = a.n;
     unsigned flags = 0;
+    [[maybe_unused]] const uint64_t stpol = PBCG_K3_STM ? l2_policy_evict_first() : 0ull;
     K3Op<Acc> R;
     R.al = sc->alpha;
     R.om = sc->omega;
@@ -524,7 +582,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
                         Prod P[4];
                         R.row0(flags, rh.x, p.x, q.x, y.x, x.x, r.x, P[0], P[1]);
                         R.row0(flags, rh.y, p.y, q.y, y.y, x.y, r.y, P[2], P[3]);
-                        ((double2 *)a.x)[gp] = x; ((double2 *)a.r)[gp] = r;
+                        st_v2<PBCG_K3_STM, 0>(a.x, gp, x, stpol); st_v2<PBCG_K3_STM, 1>(a.r, gp, r, stpol);
                         cascade_batch<4, true, PBCG_VSPLIT_K3(NL)>(R.d0, R.d1, P, s0, s1);
                     } else {
                         const double2 t = B2[4 * TP + j], v = B2[5 * TP + j];
@@ -532,7 +590,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
                         Prod P[2];
                         R.row1(flags, rh.x, y.x, t.x, v.x, w.x, P[0]);
                         R.row1(flags, rh.y, y.y, t.y, v.y, w.y, P[1]);
-                        ((double2 *)a.w)[gp] = w;
+                        st_v2<PBCG_K3_STM, 2>(a.w, gp, w, stpol);
                         if constexpr (PIPE) ((double2 *)a.wh)[gp] = bj_pair(a.minv, gp, w.x, w.y);  // w_hat = M^-1 w (R-25)
                         cascade_batch<2, false>(R.d0, R.d1, P, s0, s1);
                     }
@@ -845,6 +903,7 @@ __device__ __forceinline__ void sellp_produce(int64_t cbeg, int64_t nchunks, con
     };
     int issued = 0;
     bool gated = false;
+    const uint64_t pol = l2_policy_evict_first();
     auto pass_gate = [&]() {
         gated = true;
         if (gate()) return true;
@@ -868,7 +927,7 @@ __device__ __forceinline__ void sellp_produce(int64_t cbeg, int64_t nchunks, con
             if (lane == 0) {
                 mbar_wait(&empty[st], ph ^ 1u);
                 mbar_expect_tx(&full[st], (uint32_t)(o1 - o0));
-                bulk_g2s(smem + (size_t)st * STAGE, blob + o0, (uint32_t)(o1 - o0), &full[st]);
+                bulk_g2s_stream(smem + (size_t)st * STAGE, blob + o0, (uint32_t)(o1 - o0), &full[st], pol);
             }
             ++issued;
             if (++st == STAGES) {
@@ -1153,6 +1212,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
             int st = 0, issued = 0;
             uint32_t ph = 0;
             bool ok = true, gated = false;
+            const uint64_t pol = l2_policy_evict_first();
             // the PDL wait, then the x ranges of the `cnt` chunks whose matrix
             // went out before it (their bytes are already expected)
             auto open_gate = [&](int cnt) {
@@ -1176,7 +1236,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                 const int e = need(c, loaded);
                 mbar_wait(&empty[st], ph ^ 1u);
                 mbar_expect_tx(&full[st], (uint32_t)(o1 - o0) + (uint32_t)(e - loaded) * 8u);
-                bulk_g2s(smem_raw + (size_t)st * STAGE, blob + o0, (uint32_t)(o1 - o0), &full[st]);
+                bulk_g2s_stream(smem_raw + (size_t)st * STAGE, blob + o0, (uint32_t)(o1 - o0), &full[st], pol);
                 if (gated) xcopy(loaded, e, &full[st]);
                 loaded = e;
                 ++issued;
