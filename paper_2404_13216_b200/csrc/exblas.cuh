@@ -509,6 +509,67 @@ __device__ __forceinline__ void warp_deposit_priv(double v, long long *w) {
     __syncwarp();
 }
 
+// All NT expansion terms of every lane at once (zeros allowed), into words
+// private to this warp: when the nonzero terms of the warp span at most
+// WIN_W superaccumulator words, every lane adds the digit chunks of its terms
+// into ITS OWN column of a WIN_W x 32 window (`win`: WIN_WORDS int64 of
+// warp-private shared memory; plain read-modify-writes, no atomics, no
+// conflicts between lanes), and lane j then sums row j over the 32 columns
+// and adds it to word lo + j -- 2 REDUX for the whole accumulator instead of
+// 10 per term (warp_deposit_priv), which the drain was bound by.  Wider
+// spreads fall back to one warp_deposit_priv per term.  All 32 lanes active.
+#ifndef PBCG_WIN_W
+#define PBCG_WIN_W 16
+#endif
+constexpr int WIN_W = PBCG_WIN_W;         // window rows (superaccumulator words), at most 32
+constexpr int WIN_LD = 33;                // row stride in int64: 32 columns + 1 (bank skew for the row sums)
+constexpr int WIN_WORDS = WIN_W * WIN_LD;
+template <int NT>
+__device__ __forceinline__ void warp_window_deposit(const double (&v)[NT], long long *w, long long *win) {
+    const int lane = threadIdx.x & 31;
+    unsigned lo = 0xFFFFFFFFu, hi = 0u;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        const unsigned E = (unsigned)(__double_as_longlong(v[t]) >> 52) & 0x7FFu;
+        if (is_nonzero(v[t]) && E != 0x7FFu) {  // NaN/Inf terms are flagged elsewhere and never deposited (sacc_split)
+            const unsigned i = (E ? E - 1u : 0u) >> 5;
+            lo = min(lo, i);
+            hi = max(hi, i);
+        }
+    }
+    lo = __reduce_min_sync(0xFFFFFFFFu, lo);
+    if (lo == 0xFFFFFFFFu) return;  // every term of every lane is zero
+    hi = __reduce_max_sync(0xFFFFFFFFu, hi);
+    if (hi + 3u - lo > (unsigned)WIN_W) {  // a term touches words i, i+1, i+2
+#pragma unroll
+        for (int t = 0; t < NT; ++t) warp_deposit_priv(v[t], w);
+        return;
+    }
+    long long *col = win + lane;
+#pragma unroll
+    for (int k = 0; k < WIN_W; ++k) col[k * WIN_LD] = 0;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        int i;
+        long long c0, c1, c2;
+        if (is_nonzero(v[t]) && sacc_split(v[t], i, c0, c1, c2)) {
+            long long *q = col + (i - (int)lo) * WIN_LD;
+            q[0] += c0;
+            q[WIN_LD] += c1;
+            q[2 * WIN_LD] += c2;
+        }
+    }
+    __syncwarp();
+    if (lane < WIN_W && lo + (unsigned)lane < (unsigned)SACC_L) {
+        const long long *row = win + lane * WIN_LD;
+        long long sum = 0;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) sum += row[k];
+        if (sum) w[lo + lane] += sum;
+    }
+    __syncwarp();
+}
+
 // Two-tier accumulator used by the streaming kernels.  Each product p and its
 // TwoProd error e enter short hot expansions P, E (NH levels each, branch
 // free).  What falls out of them -- values far below this thread's running
@@ -567,6 +628,19 @@ struct ExAccT {
     // first (3 deposits instead of NH + NHE + 2 NC: C3 7,238 vs 7,583 iter/s,
     // one long dependent chain), and batching 2-4 deposits so their REDUX
     // chains interleave (C3 7,218-7,381 vs 7,585).
+    // the same through the per-warp window (warp_window_deposit)
+    __device__ __forceinline__ void warp_merge_win(long long *w, long long *win) {
+        double v[NH + NHE + 2 * NC];
+#pragma unroll
+        for (int j = 0; j < NH; ++j) v[j] = P.a[j];
+#pragma unroll
+        for (int j = 0; j < NHE; ++j) v[NH + j] = E.a[j];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) v[NH + NHE + j] = CP.a[j];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) v[NH + NHE + NC + j] = CE.a[j];
+        warp_window_deposit(v, w, win);
+    }
     __device__ __forceinline__ void warp_merge_priv(long long *w) {
 #pragma unroll
         for (int j = 0; j < NH; ++j) warp_deposit_priv(P.a[j], w);
@@ -695,6 +769,7 @@ struct PlainAcc {
     __device__ __forceinline__ Prod prep(double x, double y, bool, unsigned &) const { return Prod{x, y}; }
     __device__ __forceinline__ void add(const Prod &q) { s = __fma_rn(q.p, q.e, s); }
     __device__ __forceinline__ void warp_merge_priv(long long *) {}
+    __device__ __forceinline__ void warp_merge_win(long long *, long long *) {}
     // all 32 lanes, converged: lane 0 stores the warp's sum as a double
     __device__ __forceinline__ void warp_merge(unsigned long long *slots) {
         double v = s;

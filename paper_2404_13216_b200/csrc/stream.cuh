@@ -221,6 +221,14 @@ __device__ __forceinline__ size_t stream_smem_bytes() {
 // shared-atomic storm of all warps depositing into the same few words of S.w
 // (measured: 6-8 us per launch on C3) is gone.  dot(g, k): the dot of
 // accumulator k of dot group g, or -1.  All threads.
+// The drain goes through a per-warp window (warp_window_deposit) instead of
+// one warp-aggregated deposit per term: tools/ab_iter.py, C3 8,222 -> 8,338
+// iter/s, C4 1,612 -> 1,617, C5 1,097 -> 1,098 (windows of 10 / 16 / 24 words
+// alike).  Ring memory used: drain_ring_words int64.
+#ifndef PBCG_WIN_DRAIN
+#define PBCG_WIN_DRAIN 1
+#endif
+__host__ __device__ constexpr size_t drain_ring_words(int nwarps) { return (size_t)nwarps * (2 * SACC_L + (PBCG_WIN_DRAIN ? WIN_WORDS : 0)); }
 template <int ND, int NCW, int W, class Acc, class Dot>
 __device__ __forceinline__ void drain_private(CtaSacc<ND> &S, Acc &d0, Acc &d1, long long *ring, Dot dot) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -230,8 +238,14 @@ __device__ __forceinline__ void drain_private(CtaSacc<ND> &S, Acc &d0, Acc &d1, 
     if (warp < NCW) {
         for (int i = lane; i < 2 * SACC_L; i += 32) pw[i] = 0;
         __syncwarp();
+#if PBCG_WIN_DRAIN
+        long long *win = ring + (size_t)(NCW + 1) * 2 * SACC_L + (size_t)warp * WIN_WORDS;  // behind every warp's words
+        d0.warp_merge_win(pw, win);
+        d1.warp_merge_win(pw + SACC_L, win);
+#else
         d0.warp_merge_priv(pw);
         d1.warp_merge_priv(pw + SACC_L);
+#endif
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < 2 * 2 * SACC_L; idx += blockDim.x) {  // (group, accumulator, word)
@@ -297,6 +311,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
     constexpr int NV = 8;  // r, rh, w, t | p, s, z, v
     constexpr int NCW = 2 * W;
     constexpr int T = TileGeo<W, PPT>::T;
+    static_assert(drain_ring_words(NCW + 1) <= (size_t)STAGES * NV * T, "the drain's scratch must fit in the ring");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *buf = (double *)smem_raw;
     uint64_t *full = (uint64_t *)(buf + (size_t)STAGES * NV * T);
@@ -508,6 +523,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
     constexpr int NV = 7;  // rh, p, q, y, t, v, x
     constexpr int NCW = 2 * W;
     constexpr int T = TileGeo<W, PPT>::T;
+    static_assert(drain_ring_words(NCW + 1) <= (size_t)STAGES * NV * T, "the drain's scratch must fit in the ring");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *buf = (double *)smem_raw;
     uint64_t *full = (uint64_t *)(buf + (size_t)STAGES * NV * T);
@@ -671,6 +687,9 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
 }
 
 // ---------------------------------------------------------------------------
+#ifndef PBCG_XD_PRIV_DRAIN
+#define PBCG_XD_PRIV_DRAIN 1  // 2^26: WELL 6,517 -> 6,591 GB/s, ILL 4,117 -> 4,172; 2^22 ILL 1,861 -> 1,985 (tools/exdot_bench.py)
+#endif
 // Standalone EXDOT (one dot, x and y 16-byte aligned)
 // ---------------------------------------------------------------------------
 // ND = 2: the dots (x,y) and (y,y) over the same two streams (Alg. 1's
@@ -769,8 +788,14 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1) exdot_stream(MultiDotArgs a
         }
     }
     __syncwarp();
+#if PBCG_XD_PRIV_DRAIN
+    // one dot group of NCW warps: accumulator k -> dot k (acc2 stays zero when ND = 1)
+    static_assert(drain_ring_words(NCW + 1) <= (size_t)STAGES * NV * T, "the drain's scratch must fit in the ring");
+    drain_private<ND, NCW, NCW>(S, acc, acc2, (long long *)buf, [](int g, int k) { return (g == 0 && k < ND) ? k : -1; });
+#else
     acc.warp_merge(S.w[0]);
     if (ND == 2) acc2.warp_merge(s1);
+#endif
     if constexpr (ND == 2) {
         if (phase_full_range(a.phase, a.sc)) {  // Algorithm 2's init with x0 = 0 (PH_INIT0): R-24 as in K2/K3
             if (flags) atomicOr(&S.flags, flags);
