@@ -521,7 +521,7 @@ __device__ __forceinline__ void warp_deposit_priv(double v, long long *w) {
 #ifndef PBCG_WIN_W
 #define PBCG_WIN_W 16
 #endif
-constexpr int WIN_W = PBCG_WIN_W;         // window rows (superaccumulator words), at most 32
+constexpr int WIN_W = PBCG_WIN_W;         // window rows (superaccumulator words), at most 16
 constexpr int WIN_LD = 33;                // row stride in int64: 32 columns + 1 (bank skew for the row sums)
 constexpr int WIN_WORDS = WIN_W * WIN_LD;
 template <int NT>
@@ -545,9 +545,11 @@ __device__ __forceinline__ void warp_window_deposit(const double (&v)[NT], long 
         for (int t = 0; t < NT; ++t) warp_deposit_priv(v[t], w);
         return;
     }
+    const int span = (int)(hi + 3u - lo);  // window rows in use (warp-uniform)
     long long *col = win + lane;
 #pragma unroll
-    for (int k = 0; k < WIN_W; ++k) col[k * WIN_LD] = 0;
+    for (int k = 0; k < WIN_W; ++k)
+        if (k < span) col[k * WIN_LD] = 0;
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
         int i;
@@ -560,13 +562,16 @@ __device__ __forceinline__ void warp_window_deposit(const double (&v)[NT], long 
         }
     }
     __syncwarp();
-    if (lane < WIN_W && lo + (unsigned)lane < (unsigned)SACC_L) {
-        const long long *row = win + lane * WIN_LD;
-        long long sum = 0;
+    static_assert(WIN_W <= 16, "two lanes per window row");
+    const int r = lane & 15;  // lanes r and r + 16 sum the two halves of row r
+    long long sum = 0;
+    if (r < span) {
+        const long long *row = win + r * WIN_LD + (lane & 16);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) sum += row[k];
-        if (sum) w[lo + lane] += sum;
+        for (int k = 0; k < 16; ++k) sum += row[k];
     }
+    sum += __shfl_xor_sync(0xFFFFFFFFu, sum, 16);
+    if (lane < span && lo + (unsigned)lane < (unsigned)SACC_L && sum) w[lo + lane] += sum;
     __syncwarp();
 }
 

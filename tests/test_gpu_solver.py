@@ -189,6 +189,23 @@ def test_full_size_first_iterations(pb, name, steps):
     assert_same(O, x, r, H, A)
 
 
+@pytest.mark.parametrize("V", [1, 3])
+def test_wide_exponent_spread_takes_the_drain_fallback(pb, V):
+    # A diagonal system whose entries span 2^-150 .. 2^150 (shuffled): w0 = A r0, t0 = A w0 and y = w - alpha z
+    # spread the products of (y,y) over ~600 binades inside every warp, more than the 16-word window of the
+    # end-of-kernel drain (exblas.cuh warp_window_deposit), so K2 / K3 take its per-term fallback; every dot is
+    # still the exact sum rounded once, whatever the drain path or the rank count.
+    n = 40_000  # above the fused small-system kernel's 16,384 rows: the six-kernel path
+    e = np.floor(np.linspace(-150, 150, n)).astype(int)[np.random.default_rng(7).permutation(n)]
+    d = np.ldexp(1.0 + gen.uniform(n, 9, 0.0, 1.0), e)
+    A = gen.CSR(n, np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32), d, name="diag_wide", rhs="given",
+                b=gen.uniform(n, 10, 0.5, 1.5))
+    S, O, x, r, H = run_both(pb, A, 0.0, 4, steps=4, virtual_ranks=V)
+    assert_same(O, x, r, H, A)
+    y = O.vec("y")
+    assert np.log2(np.abs(y)).max() - np.log2(np.abs(y[y != 0])).min() > 280  # (y,y) spans > 560 bits: wider than the window
+
+
 def test_diag2_and_breakdowns(pb):
     import torch
     # 1x1 diag(2), b = [2] -> one step, x = [1]
