@@ -103,6 +103,16 @@ __device__ __forceinline__ void st_stream_v2(double2 *p, double2 v, uint64_t pol
 #ifndef PBCG_K3_EFM
 #define PBCG_K3_EFM 0x40u
 #endif
+// Vectors whose K2 / K3 loads carry evict_last (ELM, same bit order as EFM): K2's r0 (the shadow residual, read
+// by K2 and K3 in every iteration and never written), p and z (read here, overwritten in place, re-read by K3 / the
+// SpMV).  tools/ab_iter.py: C3 8,405 -> 8,513 iter/s, C5 1,097.8 -> 1,100.3; r0 alone 8,460, r0 + p 8,504 (C4 1,604
+// -> 1,614), r0 + t 8,457, r0 + t + v 8,460; with K3's p / r0 / both as well 8,504 / 8,480 / 8,435.
+#ifndef PBCG_K2_ELM
+#define PBCG_K2_ELM 0x52u
+#endif
+#ifndef PBCG_K3_ELM
+#define PBCG_K3_ELM 0u
+#endif
 #ifndef PBCG_K2_STM
 #define PBCG_K2_STM 0x2u
 #endif
@@ -151,7 +161,7 @@ __device__ __forceinline__ void produce(const double *const *src, int nv_act, in
 // makes the first tile wait for the whole burst (no priority among bulk
 // copies); fewer stages let the first tiles land sooner after the gate.
 #ifndef PBCG_PREGATE
-#define PBCG_PREGATE 1  // C3: 7,404 (all 5) -> 7,582 iter/s (1), C5 1,111 -> 1,116 (tools/ab_iter.py)
+#define PBCG_PREGATE 2  // C3: 7,404 (all 5) -> 7,582 iter/s (1), C5 1,111 -> 1,116; with the L2 hints 2 stages: C3 8,377 -> 8,410, C5 / C4 +0.1 % (tools/ab_iter.py)
 #endif
 #define PBCG_PREGATE_STAGES(S) ((PBCG_PREGATE) < (S) ? (PBCG_PREGATE) : (S))
 
@@ -163,10 +173,12 @@ __device__ __forceinline__ void produce(const double *const *src, int nv_act, in
 // (their bytes are already in the barrier's expected count); on abort they
 // are issued anyway and drained, so no copy is in flight at exit.
 // EFM: bit v set = vector v streams through the L2 (evict_first hint).
-template <int NV, int T, int STAGES, unsigned EFM = 0u, class Gate>
+template <int NV, int T, int STAGES, unsigned EFM = 0u, unsigned ELM = 0u, class Gate>
 __device__ __forceinline__ bool produce_gated(const double *const *src, int nv_act, int late, int64_t n, double *buf,
                                               uint64_t *full, uint64_t *empty, Gate gate) {
     [[maybe_unused]] const uint64_t pol = EFM ? l2_policy_evict_first() : 0ull;
+    [[maybe_unused]] uint64_t pol_last = 0ull;
+    if constexpr (ELM != 0u) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
     const int64_t ntiles = (n + T - 1) / T;
     int s = 0, issued = 0;
     uint32_t ph = 0;
@@ -201,6 +213,7 @@ __device__ __forceinline__ bool produce_gated(const double *const *src, int nv_a
             for (int v = 0; v < NV; ++v)  // static indices keep src in registers
                 if (v < nv_act && (gated || v != late)) {
                     if ((EFM >> v) & 1u) bulk_g2s_stream(buf + ((size_t)s * NV + v) * T, src[v] + r0, bytes, &full[s], pol);
+                    else if ((ELM >> v) & 1u) bulk_g2s_stream(buf + ((size_t)s * NV + v) * T, src[v] + r0, bytes, &full[s], pol_last);
                     else bulk_g2s(buf + ((size_t)s * NV + v) * T, src[v] + r0, bytes, &full[s]);
                 }
         }
@@ -339,7 +352,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k2_stream(K2Args a) {
         if (lane == 0) {
             const bool first0 = (sc->it == 0);  // written by the previous finalize: complete (event dependency)
             const double *src[NV] = {a.r, a.rh, a.w, a.t, a.p, a.s, a.z, a.v};
-            ok = produce_gated<NV, T, STAGES, PBCG_K2_EFM>(src, first0 ? 4 : 8, 3, a.n, buf, full, empty, [&]() {
+            ok = produce_gated<NV, T, STAGES, PBCG_K2_EFM, PBCG_K2_ELM>(src, first0 ? 4 : 8, 3, a.n, buf, full, empty, [&]() {
                 pdl_sync();
                 return !sc->done;
             });
@@ -543,7 +556,7 @@ __global__ void __launch_bounds__((2 * W + 1) * 32, 1) k3_stream(K3Args a) {
         bool ok = true;
         if (lane == 0) {
             const double *src[NV] = {a.rh, a.p, a.q, a.y, a.t, a.v, a.x};
-            ok = produce_gated<NV, T, STAGES, PBCG_K3_EFM>(src, NV, 5, a.n, buf, full, empty, [&]() {
+            ok = produce_gated<NV, T, STAGES, PBCG_K3_EFM, PBCG_K3_ELM>(src, NV, 5, a.n, buf, full, empty, [&]() {
                 pdl_sync();
                 return !sc->done;
             });
