@@ -106,7 +106,8 @@ __device__ __forceinline__ void st_stream_v2(double2 *p, double2 v, uint64_t pol
 // Vectors whose K2 / K3 loads carry evict_last (ELM, same bit order as EFM): K2's r0 (the shadow residual, read
 // by K2 and K3 in every iteration and never written), p and z (read here, overwritten in place, re-read by K3 / the
 // SpMV).  tools/ab_iter.py: C3 8,405 -> 8,513 iter/s, C5 1,097.8 -> 1,100.3; r0 alone 8,460, r0 + p 8,504 (C4 1,604
-// -> 1,614), r0 + t 8,457, r0 + t + v 8,460; with K3's p / r0 / both as well 8,504 / 8,480 / 8,435.
+// -> 1,614), r0 + t 8,457, r0 + t + v 8,460; with K3's p / r0 / both as well 8,504 / 8,480 / 8,435.  evict_last on
+// STORES loses everywhere (z; z, q, y; K3's w; z and w; p, z: C3 8,457-8,497 vs 8,514, C5 1,080-1,094 vs 1,101).
 #ifndef PBCG_K2_ELM
 #define PBCG_K2_ELM 0x52u
 #endif
