@@ -26,7 +26,7 @@
 #define PBCG_VSPLIT_K2(nl) false
 #endif
 #ifndef PBCG_VSPLIT_K3
-#define PBCG_VSPLIT_K3(nl) ((nl) >= 2)
+#define PBCG_VSPLIT_K3(nl) true  // the lean / pipelined K3 (one cold level) too: C3 8,512 -> 8,536, C4 and the bjacobi2_pipe arm unchanged
 #endif
 
 namespace pbcg {
