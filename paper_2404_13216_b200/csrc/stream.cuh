@@ -17,11 +17,12 @@
 #include "kernels.cuh"
 
 // One cold-tier vote per (dot, stream) instead of per stream in the two-dot
-// groups (cascade_batch SPLIT), by kernel and cold depth NL.  On in the
-// non-lean K3 only, whose group 0 pairs a dot that spills often, (r0,r'),
-// with one that rarely does, (r',r'): C5 1,071.5 -> 1,080.4 iter/s at the
-// driver's K = 20 (1,084.5 -> 1,091.6 at K = 200); on in K2 (both pairs
-// spill alike) C5 1,068.7 and C3 7,724 vs 7,770 (tools/ab_iter.py).
+// groups (cascade_batch SPLIT), by kernel and cold depth NL.  On in K3,
+// whose group 0 pairs a dot that spills often, (r0,r'), with one that rarely
+// does, (r',r'): C5 1,071.5 -> 1,080.4 iter/s at the driver's K = 20
+// (1,084.5 -> 1,091.6 at K = 200); off in K2 (both pairs spill alike: C5
+// 1,068.7, C3 7,724 vs 7,770; lean K2 with it C3 8,491 vs 8,536;
+// tools/ab_iter.py).
 #ifndef PBCG_VSPLIT_K2
 #define PBCG_VSPLIT_K2(nl) false
 #endif
